@@ -1,0 +1,161 @@
+/*
+ * treetrain_b200 — C-ABI of the B200 (sm_100a) DFS prefix-tree forward/backward engine.
+ *
+ * Drop-in boundary for the reference's header-only C++ API in namespace treetrain
+ * (/root/reference/proj/core/include/treetrain/ headers) and for the SPEC-level operations the
+ * reference leaves unshipped. Every entry point:
+ *   - returns TT_OK (0) or a TT_ERR_* status; no exception crosses the ABI;
+ *   - takes plain pointers and sizes (host pointers unless documented otherwise);
+ *   - records a message retrievable with tt_last_error() on failure.
+ * Status -> reference exception mapping (model.hpp:334-343,483-492,647-655; model_io.cpp:60-103):
+ *   TT_ERR_INVALID_ARGUMENT <-> std::invalid_argument, TT_ERR_RUNTIME <-> std::runtime_error,
+ *   TT_ERR_NONFINITE <-> the SPEC's abort on non-finite loss.
+ *
+ * One engine per GPU and per host thread; an engine owns all of its device memory and one
+ * CUDA stream and is not re-entrant. Trees are immutable after build/order and may be shared.
+ */
+#ifndef TREETRAIN_B200_H_
+#define TREETRAIN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_OK 0
+#define TT_ERR_INVALID_ARGUMENT 1
+#define TT_ERR_RUNTIME 2
+#define TT_ERR_OOM 3
+#define TT_ERR_NONFINITE 4
+
+/* ModelConfig (model_config.hpp:19-27). The engine computes in bf16 operands with fp32
+ * accumulation/residual/gradients and fp64 loss, whatever `precision` says; the field is kept so
+ * a reference config round-trips (0 = f32, 1 = f64, model_config.hpp:9). */
+typedef struct tt_model_config {
+  uint64_t vocab_size;
+  uint64_t d_model;
+  uint64_t n_heads;
+  uint64_t n_layers;
+  uint64_t d_ff;
+  uint64_t max_position;
+  int32_t precision;
+  int32_t reserved;
+} tt_model_config;
+
+/* order_children policies. */
+#define TT_ORDER_AS_BUILT 0
+#define TT_ORDER_LEXICOGRAPHIC 1
+#define TT_ORDER_SUBTREE_TOKENS_DESC 2
+#define TT_ORDER_SUBTREE_TOKENS_ASC 3
+
+/* SchedulerConfig plus the B200 sibling-batching switch. */
+typedef struct tt_sched_config {
+  uint64_t chunk_len;          /* SPEC.md:205; 0 = unlimited (whole segment keeps activations) */
+  int32_t leaf_kv_skip;
+  int32_t child_order_policy;  /* informational: the tree passed in is already ordered */
+  int32_t sibling_batch;       /* run each maximal run of consecutive childless siblings as one
+                                  varlen segment batch over the shared prefix (logical DFS order,
+                                  trace and results unchanged up to fp32 summation order) */
+  int32_t reserved;
+  uint64_t batch_token_budget; /* max tokens per sibling batch; 0 = unlimited */
+} tt_sched_config;
+
+/* TrainStepResult counters + device measurements. */
+typedef struct tt_step_result {
+  double total_loss;
+  uint64_t forward_tokens;
+  uint64_t recompute_tokens;
+  uint64_t backward_tokens;
+  uint64_t peak_live_kv_tokens;
+  uint64_t peak_live_activation_tokens;
+  uint64_t num_segments;
+  uint64_t num_chunks;
+  uint64_t rollout_tokens;   /* sum of sequence lengths covered by the step */
+  uint64_t num_batches;      /* executed segment batches (== num_segments without batching) */
+  uint64_t num_launches;     /* device kernel launches issued by the step */
+  uint64_t peak_hbm_bytes;   /* engine static allocations + activation-arena high-water */
+} tt_step_result;
+
+/* ------------------------------------------------------------------ prefix tree */
+typedef struct tt_tree tt_tree;
+
+/* build_prefix_tree. Sequence i occupies tokens[offsets[i], offsets[i+1]) and
+ * weights[...] (per-token loss weights, TokenSequence token_sequence.hpp:15-21); its seq_id is i. */
+int tt_tree_build(const int32_t* tokens, const uint64_t* offsets, const double* weights, uint64_t n_seqs,
+                  tt_tree** out);
+int tt_tree_destroy(tt_tree* tree);
+/* order_children, recursively, stable tie-break by first token ascending. */
+int tt_tree_order_children(tt_tree* tree, int32_t policy);
+/* tree_token_count and companions. */
+int tt_tree_stats(const tt_tree* tree, uint64_t* tree_tokens, uint64_t* num_sequences, uint64_t* num_nodes,
+                  uint64_t* max_path_tokens);
+/* Canonical pre-order text serialisation (bit-exact structure check) and the DFS PUSH/POP trace. */
+int tt_tree_serialize(const tt_tree* tree, char* buf, uint64_t cap, uint64_t* len);
+int tt_tree_dfs_trace(const tt_tree* tree, char* buf, uint64_t cap, uint64_t* len);
+
+/* ------------------------------------------------------------------ partitioner */
+/* lexicographic_sort: order_out[k] = index of the k-th sequence. */
+int tt_lexicographic_sort(const int32_t* tokens, const uint64_t* offsets, uint64_t n_seqs, uint64_t* order_out);
+/* partition_contiguous. group_of_seq[i] in [0,K) for input sequence i;
+ * group_costs[K] = C(T_j); max_cost; duplicated = sum_j C(T_j) - C(combined). */
+int tt_partition_contiguous(const int32_t* tokens, const uint64_t* offsets, uint64_t n_seqs, uint64_t K,
+                            int32_t* group_of_seq, uint64_t* group_costs, uint64_t* max_cost,
+                            uint64_t* duplicated);
+/* greedy_least_loaded; cost_mode 0 = tree_tokens, 1 = raw_tokens. */
+int tt_greedy_least_loaded(const int32_t* tokens, const uint64_t* offsets, uint64_t n_seqs, uint64_t K,
+                           int32_t cost_mode, int32_t* group_of_seq, uint64_t* group_costs, uint64_t* max_cost,
+                           uint64_t* duplicated);
+
+/* ------------------------------------------------------------------ engine */
+typedef struct tt_engine tt_engine;
+
+int tt_param_count(const tt_model_config* cfg, uint64_t* n);
+int tt_engine_create(const tt_model_config* cfg, int32_t device, tt_engine** out);
+int tt_engine_destroy(tt_engine* eng);
+/* cudaStream_t of the engine (for event timing / stream interop by the caller). */
+int tt_engine_stream(tt_engine* eng, void** stream);
+
+/* Parameters in for_each_tensor order (model.hpp:42-59), converted to the device layout. */
+int tt_params_upload_f32(tt_engine* eng, const float* flat, uint64_t n);
+int tt_params_upload_f64(tt_engine* eng, const double* flat, uint64_t n);
+/* Device-side random init: N(0, 0.02) weights, gains 1 (the distribution of model.hpp:119-142;
+ * not bitwise the reference's mt19937_64 stream). */
+int tt_params_init_random(tt_engine* eng, uint64_t seed);
+/* load_parameters (model_io.cpp:73-105): "TTPM" file with f32 or f64 payload. */
+int tt_params_load_ttpm(tt_engine* eng, const char* path);
+
+/* GradientStore (model.hpp:76-81): fp32 flat buffer in for_each_tensor order. */
+int tt_grads_zero(tt_engine* eng); /* zero_gradients, model.hpp:110-117 */
+int tt_grads_download_f32(tt_engine* eng, float* out, uint64_t n);
+int tt_grads_device_ptr(tt_engine* eng, float** dptr, uint64_t* n);
+int tt_grads_accum_count(tt_engine* eng, uint64_t* count);
+
+/* tree_train_step: one DFS push/visit/pop pass over `tree`, gradients added
+ * into the engine's GradientStore, loss in result->total_loss. */
+int tt_tree_train_step(tt_engine* eng, const tt_tree* tree, const tt_sched_config* sched, tt_step_result* result);
+/* dense_train_step: the flat per-sequence baseline on the same engine. */
+int tt_dense_train_step(tt_engine* eng, const int32_t* tokens, const uint64_t* offsets, const double* weights,
+                        uint64_t n_seqs, tt_step_result* result);
+
+/* ------------------------------------------------------------------ segment level (device KV stack)
+ * forward_segment (model.hpp:328-463) continuing from the device stack (KVView of all pushed
+ * segments, start_position = current stack length). logits_out: host [len x V] fp32 or NULL. */
+int tt_segment_push(tt_engine* eng, const int32_t* tokens, uint64_t len, float* logits_out);
+/* backward_segment (model.hpp:474-633) of the top segment. grad_logits: host [len x V] fp32 or NULL
+ * (= zero upstream). grad_new_kv is the dK/dV the popped segment's rows accumulated from segments
+ * popped above it. grad_prefix (returned KVGrad, rows [0,S)) is added into the stack's dK/dV rows of
+ * the ancestors; grad_prefix_out (host, layout [L][2][S][d] fp32, K then V) receives that
+ * contribution when not NULL. */
+int tt_segment_pop(tt_engine* eng, const float* grad_logits, float* grad_prefix_out);
+int tt_stack_reset(tt_engine* eng);
+int tt_stack_depth(tt_engine* eng, uint64_t* segments, uint64_t* tokens);
+
+const char* tt_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TREETRAIN_B200_H_ */

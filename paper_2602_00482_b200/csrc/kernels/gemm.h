@@ -1,0 +1,47 @@
+// Host interface of the sm_100a tcgen05 GEMM (gemm_sm100.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ttb {
+
+// A(m,k) / B(n,k) operand view. K-major: ptr[row*ld + k]; MN-major: ptr[k*ld + row].
+struct GemmOperand {
+  const __nv_bfloat16* ptr = nullptr;
+  long ld = 0;
+  bool mn_major = false;
+};
+
+enum EpiMode : int {
+  EPI_STORE_BF16 = 0,  // out[blk] (bf16) = alpha*acc
+  EPI_STORE_F32 = 1,   // out[blk] (fp32) = alpha*acc
+  EPI_ADD_F32 = 2,     // out[blk] (fp32) += alpha*acc   (residual add / dW accumulate)
+  EPI_SILU = 3,        // out[0] (bf16) = acc, out2 (bf16) = silu(acc)
+  EPI_DSILU = 4,       // out[0] (bf16) = acc * silu'(aux)
+};
+
+// Column blocks of width split_w go to out[n / split_w] (row pitch ldo[...]) so one GEMM can
+// write e.g. q/k/v (or dWq/dWk/dWv) into three separate tensors. split_w = 0: single output.
+struct EpiParams {
+  int mode = EPI_STORE_BF16;
+  int split_w = 0;
+  void* out[3] = {nullptr, nullptr, nullptr};
+  long ldo[3] = {0, 0, 0};
+  void* out2 = nullptr;
+  long ldo2 = 0;
+  const __nv_bfloat16* aux = nullptr;
+  long ld_aux = 0;
+  float alpha = 1.0f;
+  int atomic = 0;
+};
+
+void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
+               cudaStream_t stream);
+int gemm_choose_splits(int M, int N, int K);
+void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                    uint32_t box_inner, uint32_t box_outer);
+
+}  // namespace ttb

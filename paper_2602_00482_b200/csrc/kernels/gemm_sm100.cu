@@ -1,0 +1,399 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a (bf16 operands, fp32 TMEM accumulators).
+//
+//   C[M x N] (op)= A[M x K] * B[N x K]^T
+//
+// A(m,k) is K-major (ptr[m*lda + k]) or MN-major (ptr[k*lda + m]); same for B(n,k).
+// The three transformer GEMM shapes of forward_segment / backward_segment map onto it as
+//   Y  = X W       (matrix.hpp:37-48 `matmul`)            : A K-major,  B MN-major
+//   dX = dY W^T    (matrix.hpp:50-62 `matmul_transposed`)  : A K-major,  B K-major
+//   dW += X^T dY   (matrix.hpp:64-77 `accumulate_outer`)   : A MN-major, B MN-major
+//
+// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
+// warps 2..5 = epilogue (TMEM -> registers -> fused op -> global). Smem ring of STAGES
+// {A,B} tiles (128B swizzle); two TMEM accumulator slots so the epilogue of tile i overlaps
+// the main loop of tile i+1. Split-K partials reduce with red.global.add.v4.f32.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.h"
+#include "sm100.cuh"
+
+namespace ttb {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // two accumulator slots
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float silu_f(float u) { return u / (1.0f + __expf(-u)); }
+__device__ __forceinline__ float silu_grad_f(float u) {
+  const float s = 1.0f / (1.0f + __expf(-u));
+  return s * (1.0f + u * (1.0f - s));
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, int M, int N,
+                int K, int splits, EpiParams epi) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* empty_bar = full_bar + C::kStages;
+  uint64_t* tfull_bar = empty_bar + C::kStages;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = warp_id_sync();
+  const int lane = threadIdx.x & 31;
+
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int kb_total = (K + BK - 1) / BK;
+  const int kb_per = (kb_total + splits - 1) / splits;
+  const int num_tiles = num_m * num_n * splits;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto tile_coords = [&](int t, int& m_blk, int& n_blk, int& kb0, int& kb1) {
+    const int per = num_m * num_n;
+    const int split = t / per;
+    const int rem = t - split * per;
+    n_blk = rem / num_m;
+    m_blk = rem - n_blk * num_m;
+    kb0 = split * kb_per;
+    kb1 = min(kb_total, kb0 + kb_per);
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int m_blk, n_blk, kb0, kb1;
+        tile_coords(t, m_blk, n_blk, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kABytes;
+          mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+          const int k0 = kb * BK;
+          if constexpr (!A_MN) {
+            tma_load_2d(&tmap_a, &full_bar[stage], sa, k0, m_blk * BM);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(&tmap_a, &full_bar[stage], sa + j * 8192, m_blk * BM + j * 64, k0);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(&tmap_b, &full_bar[stage], sb, k0, n_blk * BN);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(&tmap_b, &full_bar[stage], sb + j * 8192, n_blk * BN + j * 64, k0);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int m_blk, n_blk, kb0, kb1;
+      tile_coords(t, m_blk, n_blk, kb0, kb1);
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t da, db;
+            if constexpr (!A_MN) da = make_sdesc_sw128(sa + k * 32, 16, 1024);
+            else da = make_sdesc_sw128(sa + k * 2048, 8192, 1024);
+            if constexpr (!B_MN) db = make_sdesc_sw128(sb + k * 32, 16, 1024);
+            else db = make_sdesc_sw128(sb + k * 2048, 8192, 1024);
+            umma_bf16_ss(d_tmem, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int m_blk, n_blk, kb0, kb1;
+      tile_coords(t, m_blk, n_blk, kb0, kb1);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * BM + quad * 32 + lane;
+      const bool row_ok = row < M;
+      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(t_row + c, r);
+        tmem_ld_wait();
+        const int n = n_blk * BN + c;
+        if (!row_ok || n >= N) continue;
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * epi.alpha;
+        int blk = 0, nc = n;
+        if (epi.split_w > 0) {
+          blk = n / epi.split_w;
+          nc = n - blk * epi.split_w;
+        }
+        const long off = static_cast<long>(row) * epi.ldo[blk] + nc;
+        switch (epi.mode) {
+          case EPI_STORE_BF16: {
+            uint4 w0, w1;
+            w0.x = pack_bf16x2(v[0], v[1]); w0.y = pack_bf16x2(v[2], v[3]);
+            w0.z = pack_bf16x2(v[4], v[5]); w0.w = pack_bf16x2(v[6], v[7]);
+            w1.x = pack_bf16x2(v[8], v[9]); w1.y = pack_bf16x2(v[10], v[11]);
+            w1.z = pack_bf16x2(v[12], v[13]); w1.w = pack_bf16x2(v[14], v[15]);
+            uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[blk]) + off);
+            p[0] = w0;
+            p[1] = w1;
+            break;
+          }
+          case EPI_STORE_F32: {
+            float4* p = reinterpret_cast<float4*>(static_cast<float*>(epi.out[blk]) + off);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            break;
+          }
+          case EPI_ADD_F32: {
+            float* p = static_cast<float*>(epi.out[blk]) + off;
+            if (epi.atomic) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) red_add_v4_f32(p + 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            } else {
+              float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                float4 o = q[i];
+                o.x += v[4 * i]; o.y += v[4 * i + 1]; o.z += v[4 * i + 2]; o.w += v[4 * i + 3];
+                q[i] = o;
+              }
+            }
+            break;
+          }
+          case EPI_SILU: {
+            // out[0] <- h (pre-activation), out2 <- silu(h); both bf16 (model.hpp:443-444).
+            uint4 h0, h1, a0, a1;
+            float hb[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) hb[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+            h0.x = pack_bf16x2(hb[0], hb[1]); h0.y = pack_bf16x2(hb[2], hb[3]);
+            h0.z = pack_bf16x2(hb[4], hb[5]); h0.w = pack_bf16x2(hb[6], hb[7]);
+            h1.x = pack_bf16x2(hb[8], hb[9]); h1.y = pack_bf16x2(hb[10], hb[11]);
+            h1.z = pack_bf16x2(hb[12], hb[13]); h1.w = pack_bf16x2(hb[14], hb[15]);
+            a0.x = pack_bf16x2(silu_f(hb[0]), silu_f(hb[1])); a0.y = pack_bf16x2(silu_f(hb[2]), silu_f(hb[3]));
+            a0.z = pack_bf16x2(silu_f(hb[4]), silu_f(hb[5])); a0.w = pack_bf16x2(silu_f(hb[6]), silu_f(hb[7]));
+            a1.x = pack_bf16x2(silu_f(hb[8]), silu_f(hb[9])); a1.y = pack_bf16x2(silu_f(hb[10]), silu_f(hb[11]));
+            a1.z = pack_bf16x2(silu_f(hb[12]), silu_f(hb[13])); a1.w = pack_bf16x2(silu_f(hb[14]), silu_f(hb[15]));
+            uint4* ph = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
+            uint4* pa = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out2) + static_cast<long>(row) * epi.ldo2 + n);
+            ph[0] = h0; ph[1] = h1;
+            pa[0] = a0; pa[1] = a1;
+            break;
+          }
+          case EPI_DSILU: {
+            // out[0] <- acc * silu'(h) in bf16 (model.hpp:526-528).
+            const uint4* ph = reinterpret_cast<const uint4*>(epi.aux + static_cast<long>(row) * epi.ld_aux + n);
+            uint4 hv[2] = {ph[0], ph[1]};
+            const __nv_bfloat16* hh = reinterpret_cast<const __nv_bfloat16*>(hv);
+            float g[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) g[i] = v[i] * silu_grad_f(__bfloat162float(hh[i]));
+            uint4 w0, w1;
+            w0.x = pack_bf16x2(g[0], g[1]); w0.y = pack_bf16x2(g[2], g[3]);
+            w0.z = pack_bf16x2(g[4], g[5]); w0.w = pack_bf16x2(g[6], g[7]);
+            w1.x = pack_bf16x2(g[8], g[9]); w1.y = pack_bf16x2(g[10], g[11]);
+            w1.z = pack_bf16x2(g[12], g[13]); w1.w = pack_bf16x2(g[14], g[15]);
+            uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + off);
+            p[0] = w0;
+            p[1] = w1;
+            break;
+          }
+          default:
+            break;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem_base, C::kTmemCols);
+}
+
+// ---------------------------------------------------------------- host side
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+}  // namespace
+
+// 2-D bf16 tensor map: inner dimension `inner` (contiguous), outer `outer`, row pitch `ld` elements.
+void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                    uint32_t box_outer) {
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
+namespace {
+
+int g_num_sms = 0;
+
+template <int BN, bool A_MN, bool B_MN>
+void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
+            cudaStream_t stream) {
+  using C = Cfg<BN>;
+  CUtensorMap ta, tb;
+  if (!A_MN) make_tmap_bf16(&ta, A.ptr, K, M, A.ld, 64, BM);
+  else make_tmap_bf16(&ta, A.ptr, M, K, A.ld, 64, 64);
+  if (!B_MN) make_tmap_bf16(&tb, B.ptr, K, N, B.ld, 64, BN);
+  else make_tmap_bf16(&tb, B.ptr, N, K, B.ld, 64, 64);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int kb_total = (K + BK - 1) / BK;
+  if (splits < 1) splits = 1;
+  if (splits > kb_total) splits = kb_total;
+  const int per = (kb_total + splits - 1) / splits;
+  splits = (kb_total + per - 1) / per;  // no empty split
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  EpiParams e = epi;
+  if (splits > 1) e.atomic = 1;
+  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::kSmem, stream>>>(ta, tb, M, N, K, splits, e);
+}
+
+}  // namespace
+
+void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
+               cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  if (N % 16 != 0) throw std::invalid_argument("gemm_bf16: N must be a multiple of 16");
+  if (splits > 1 && epi.mode != EPI_ADD_F32) throw std::invalid_argument("gemm_bf16: split-K needs EPI_ADD_F32");
+  const bool wide = (N % 256 == 0) || N > 4096;
+  const bool amn = A.mn_major, bmn = B.mn_major;
+#define TTB_DISPATCH(BN_)                                             \
+  if (!amn && bmn) return launch<BN_, false, true>(A, B, M, N, K, epi, splits, stream);  \
+  if (!amn && !bmn) return launch<BN_, false, false>(A, B, M, N, K, epi, splits, stream); \
+  if (amn && bmn) return launch<BN_, true, true>(A, B, M, N, K, epi, splits, stream);     \
+  return launch<BN_, true, false>(A, B, M, N, K, epi, splits, stream);
+  if (wide) {
+    TTB_DISPATCH(256)
+  } else {
+    TTB_DISPATCH(128)
+  }
+#undef TTB_DISPATCH
+}
+
+int gemm_choose_splits(int M, int N, int K) {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int bn = ((N % 256 == 0) || N > 4096) ? 256 : 128;
+  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  const int kb = (K + BK - 1) / BK;
+  if (tiles >= g_num_sms || kb < 8) return 1;
+  int s = (g_num_sms + tiles - 1) / tiles;
+  if (s > kb / 4) s = kb / 4;
+  return s < 1 ? 1 : s;
+}
+
+}  // namespace ttb

@@ -1,0 +1,113 @@
+"""Kernel-level checks of the sm_100a CUDA kernels against plain PyTorch fp32 references.
+
+These call the debug entry points of libtreetrain_b200.so with torch device pointers.
+"""
+import ctypes
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2602_00482_b200 import _native
+
+    return _native.lib()
+
+
+EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU = range(5)
+
+
+def _gemm(a, a_mn, b, b_mn, M, N, K, mode, outs, ldo, split_w=0, act=None, aux=None, splits=1):
+    lib = _lib()
+    vp = ctypes.c_void_p
+    o = [vp(t.data_ptr()) if t is not None else vp(0) for t in (outs + [None, None, None])[:3]]
+    rc = lib.tt_debug_gemm(
+        vp(a.data_ptr()), ctypes.c_long(a.stride(0)), a_mn,
+        vp(b.data_ptr()), ctypes.c_long(b.stride(0)), b_mn,
+        M, N, K, mode, o[0], o[1], o[2], ctypes.c_long(ldo), split_w,
+        vp(act.data_ptr()) if act is not None else vp(0),
+        vp(aux.data_ptr()) if aux is not None else vp(0), splits)
+    assert rc == 0, lib.tt_last_error().decode()
+
+
+def _rel(x, y):
+    return ((x.float() - y.float()).norm() / (y.float().norm() + 1e-30)).item()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 384, 192), (1, 512, 256), (300, 896, 896), (129, 4864, 896)])
+def test_gemm_fwd_kmajor_mnmajor(M, N, K):
+    torch.manual_seed(0)
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(K, N, device="cuda").bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _gemm(x, 0, w, 1, M, N, K, EPI_STORE_F32, [out], N)
+    ref = x.float() @ w.float()
+    assert _rel(out, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 256), (77, 896, 4864), (513, 256, 896)])
+def test_gemm_dx_kmajor_kmajor(M, N, K):
+    torch.manual_seed(1)
+    dy = torch.randn(M, K, device="cuda").bfloat16()        # [tokens x N_w]
+    w = torch.randn(N, K, device="cuda").bfloat16()         # [K_w x N_w]
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(dy, 0, w, 0, M, N, K, EPI_STORE_BF16, [out], N)
+    ref = dy.float() @ w.float().t()
+    assert _rel(out, ref) < 1e-2
+
+
+@pytest.mark.parametrize("T,Kw,Nw,splits", [(64, 128, 128, 1), (1000, 256, 384, 1), (2048, 896, 896, 4), (333, 128, 512, 2)])
+def test_gemm_dw_mnmajor_mnmajor(T, Kw, Nw, splits):
+    torch.manual_seed(2)
+    x = torch.randn(T, Kw, device="cuda").bfloat16()
+    dy = torch.randn(T, Nw, device="cuda").bfloat16()
+    g = torch.randn(Kw, Nw, device="cuda")
+    g0 = g.clone()
+    _gemm(x, 1, dy, 1, Kw, Nw, T, EPI_ADD_F32, [g], Nw, splits=splits)
+    ref = g0 + x.float().t() @ dy.float()
+    assert _rel(g, ref) < 1e-5
+
+
+def test_gemm_split_columns_qkv():
+    torch.manual_seed(3)
+    M, d = 200, 256
+    x = torch.randn(M, d, device="cuda").bfloat16()
+    w = torch.randn(d, 3 * d, device="cuda").bfloat16()
+    q, k, v = (torch.empty(M, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    _gemm(x, 0, w, 1, M, 3 * d, d, EPI_STORE_BF16, [q, k, v], d, split_w=d)
+    ref = x.float() @ w.float()
+    assert _rel(torch.cat([q, k, v], 1), ref) < 1e-2
+
+
+def test_gemm_silu_and_dsilu():
+    torch.manual_seed(4)
+    M, K, N = 150, 256, 1024
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = (0.1 * torch.randn(K, N, device="cuda")).bfloat16()
+    h = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    a = torch.empty_like(h)
+    _gemm(x, 0, w, 1, M, N, K, EPI_SILU, [h], N, act=a)
+    href = x.float() @ w.float()
+    assert _rel(h, href) < 1e-2
+    assert _rel(a, torch.nn.functional.silu(h.float())) < 1e-2
+    g = torch.randn(M, K, device="cuda").bfloat16()
+    w2 = torch.randn(N, K, device="cuda").bfloat16()
+    gh = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _gemm(g, 0, w2, 0, M, N, K, EPI_DSILU, [gh], N, aux=h)
+    s = torch.sigmoid(h.float())
+    ref = (g.float() @ w2.float().t()) * s * (1 + h.float() * (1 - s))
+    assert _rel(gh, ref) < 1e-2
+
+
+def test_gemm_large_vocab_head():
+    torch.manual_seed(5)
+    M, K, N = 256, 896, 151936
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = (0.02 * torch.randn(K, N, device="cuda")).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _gemm(x, 0, w, 1, M, N, K, EPI_STORE_F32, [out], N)
+    ref = x.float() @ w.float()
+    assert _rel(out, ref) < 1e-5

@@ -9,20 +9,71 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtreetrain_b200.so")
 _lib = None
 
+c = ctypes
+u64, i32, f64, vp = c.c_uint64, c.c_int32, c.c_double, c.c_void_p
+P = c.POINTER
+
+
+class ModelConfigC(c.Structure):
+    _fields_ = [("vocab_size", u64), ("d_model", u64), ("n_heads", u64), ("n_layers", u64), ("d_ff", u64),
+                ("max_position", u64), ("precision", i32), ("reserved", i32)]
+
+
+class SchedConfigC(c.Structure):
+    _fields_ = [("chunk_len", u64), ("leaf_kv_skip", i32), ("child_order_policy", i32), ("sibling_batch", i32),
+                ("reserved", i32), ("batch_token_budget", u64)]
+
+
+class StepResultC(c.Structure):
+    _fields_ = [("total_loss", f64)] + [(n, u64) for n in (
+        "forward_tokens", "recompute_tokens", "backward_tokens", "peak_live_kv_tokens",
+        "peak_live_activation_tokens", "num_segments", "num_chunks", "rollout_tokens", "num_batches",
+        "num_launches", "peak_hbm_bytes")]
+
+
+EXPORTS = {
+    "tt_tree_build": [P(i32), P(u64), P(f64), u64, P(vp)],
+    "tt_tree_destroy": [vp],
+    "tt_tree_order_children": [vp, i32],
+    "tt_tree_stats": [vp, P(u64), P(u64), P(u64), P(u64)],
+    "tt_tree_serialize": [vp, c.c_char_p, u64, P(u64)],
+    "tt_tree_dfs_trace": [vp, c.c_char_p, u64, P(u64)],
+    "tt_lexicographic_sort": [P(i32), P(u64), u64, P(u64)],
+    "tt_partition_contiguous": [P(i32), P(u64), u64, u64, P(i32), P(u64), P(u64), P(u64)],
+    "tt_greedy_least_loaded": [P(i32), P(u64), u64, u64, i32, P(i32), P(u64), P(u64), P(u64)],
+    "tt_param_count": [P(ModelConfigC), P(u64)],
+    "tt_engine_create": [P(ModelConfigC), i32, P(vp)],
+    "tt_engine_destroy": [vp],
+    "tt_engine_stream": [vp, P(vp)],
+    "tt_params_upload_f32": [vp, P(c.c_float), u64],
+    "tt_params_upload_f64": [vp, P(f64), u64],
+    "tt_params_init_random": [vp, u64],
+    "tt_params_load_ttpm": [vp, c.c_char_p],
+    "tt_grads_zero": [vp],
+    "tt_grads_download_f32": [vp, P(c.c_float), u64],
+    "tt_grads_device_ptr": [vp, P(vp), P(u64)],
+    "tt_grads_accum_count": [vp, P(u64)],
+    "tt_tree_train_step": [vp, vp, P(SchedConfigC), P(StepResultC)],
+    "tt_dense_train_step": [vp, P(i32), P(u64), P(f64), u64, P(StepResultC)],
+    "tt_segment_push": [vp, P(i32), u64, P(c.c_float)],
+    "tt_segment_pop": [vp, P(c.c_float), P(c.c_float)],
+    "tt_stack_reset": [vp],
+    "tt_stack_depth": [vp, P(u64), P(u64)],
+    "tt_last_error": [],
+    "tt_debug_gemm": [vp, c.c_long, c.c_int, vp, c.c_long, c.c_int, c.c_int, c.c_int, c.c_int, c.c_int, vp, vp, vp,
+                      c.c_long, c.c_int, vp, vp, c.c_int],
+}
+
 
 def lib():
     global _lib
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
-        _lib = ctypes.CDLL(LIB_PATH)
-        _declare(_lib)
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in EXPORTS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = c.c_char_p if name == "tt_last_error" else c.c_int
+        _lib = L
     return _lib
-
-
-def _declare(L):
-    c = ctypes
-    L.tt_last_error.restype = c.c_char_p
-    L.tt_debug_gemm.argtypes = [c.c_void_p, c.c_long, c.c_int, c.c_void_p, c.c_long, c.c_int, c.c_int, c.c_int,
-                                c.c_int, c.c_int, c.c_void_p, c.c_void_p, c.c_void_p, c.c_long, c.c_int, c.c_void_p,
-                                c.c_void_p, c.c_int]

@@ -12,6 +12,11 @@ namespace ttb {
 
 void set_last_error(const std::string& msg);
 
+// Non-finite loss: the SPEC's abort-on-divergence.
+struct NonFiniteError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 inline void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -21,6 +26,9 @@ int guarded(F&& f) {
   try {
     f();
     return TT_OK;
+  } catch (const NonFiniteError& e) {
+    set_last_error(e.what());
+    return TT_ERR_NONFINITE;
   } catch (const std::invalid_argument& e) {
     set_last_error(e.what());
     return TT_ERR_INVALID_ARGUMENT;

@@ -1,0 +1,912 @@
+// B200 DFS prefix-tree forward/backward engine. See engine.hpp for the HBM layout.
+//
+//   push  = forward_segment  (model.hpp:328-463)  for a segment batch over the device KV stack
+//   visit = weighted_nll     (model.hpp:643-677)  fused LM head + multi-target CE
+//   pop   = backward_segment (model.hpp:474-633)  with grad_new_kv = the frame's dK/dV stack rows
+//           and grad_prefix added into the ancestors' dK/dV stack rows (KVGrad::add_rows :193-206)
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <stdexcept>
+#include <string>
+
+#include "capi_internal.h"
+#include "kernels/attention.h"
+#include "kernels/elementwise.h"
+#include "kernels/gemm.h"
+#include "ttpm.hpp"
+
+namespace ttb {
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+constexpr int kQBlock = 64;
+constexpr int kQChunk = 1024;  // query rows per backward work item
+
+void ck(cudaError_t e, const char* what) { check_cuda(e, what); }
+
+GemmOperand op(const bf16* p, long ld, bool mn) { return GemmOperand{p, ld, mn}; }
+
+}  // namespace
+
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+
+void DevBuf::ensure(size_t n) {
+  if (n <= bytes) return;
+  if (p) {
+    cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  if (n == 0) return;
+  const cudaError_t e = cudaMalloc(&p, n);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    throw std::bad_alloc();
+  }
+  bytes = n;
+}
+
+Engine::Engine(const tt_model_config& cfg, int device) : cfg_(cfg), device_(device) {
+  if (cfg.vocab_size < 1 || cfg.d_model < 1 || cfg.n_heads < 1 || cfg.n_layers < 1 || cfg.d_ff < 1 ||
+      cfg.max_position < 1)
+    throw std::invalid_argument("ModelConfig: all counts must be >= 1");
+  if (cfg.d_model % cfg.n_heads != 0) throw std::invalid_argument("ModelConfig: d_model must be divisible by n_heads");
+  V_ = cfg.vocab_size;
+  d_ = cfg.d_model;
+  H_ = cfg.n_heads;
+  L_ = cfg.n_layers;
+  F_ = cfg.d_ff;
+  dh_ = d_ / H_;
+  if (dh_ != 64 && dh_ != 128) throw std::invalid_argument("engine: head_dim must be 64 or 128 on sm_100a");
+  if (d_ % 64 || F_ % 64 || V_ % 16)
+    throw std::invalid_argument("engine: d_model and d_ff must be multiples of 64, vocab_size of 16");
+  ck(cudaSetDevice(device_), "cudaSetDevice");
+  ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+
+  // ---- weights (bf16), device layout
+  const size_t n_w = V_ * d_ + L_ * (3 * d_ * d_ + d_ * d_ + 2 * d_ * F_) + d_ * V_;
+  wbuf_.ensure(n_w * sizeof(bf16));
+  bf16* w = wbuf_.as<bf16>();
+  emb_ = w;
+  w += V_ * d_;
+  for (int64_t l = 0; l < L_; ++l) {
+    wqkv_.push_back(w);
+    w += 3 * d_ * d_;
+    wo_.push_back(w);
+    w += d_ * d_;
+    win_.push_back(w);
+    w += d_ * F_;
+    wout_.push_back(w);
+    w += F_ * d_;
+  }
+  head_ = w;
+  gainbuf_.ensure((2 * L_ + 1) * d_ * sizeof(float));
+  float* gp = gainbuf_.as<float>();
+  for (int64_t l = 0; l < L_; ++l) {
+    attn_g_.push_back(gp + 2 * l * d_);
+    mlp_g_.push_back(gp + (2 * l + 1) * d_);
+  }
+  final_g_ = gp + 2 * L_ * d_;
+  k_fill(gp, (2 * L_ + 1) * d_, 1.0f, stream_);
+
+  // ---- sinusoidal PE table, computed like add_positional_encoding (model.hpp:239-248)
+  {
+    std::vector<float> pe(cfg.max_position * d_);
+    for (uint64_t p = 0; p < cfg.max_position; ++p)
+      for (int64_t i = 0; 2 * i < d_; ++i) {
+        const double freq = std::pow(10000.0, -double(2 * i) / double(d_));
+        const double ang = double(p) * freq;
+        pe[p * d_ + 2 * i] = float(std::sin(ang));
+        if (2 * i + 1 < d_) pe[p * d_ + 2 * i + 1] = float(std::cos(ang));
+      }
+    pe_.ensure(pe.size() * sizeof(float));
+    ck(cudaMemcpy(pe_.p, pe.data(), pe.size() * sizeof(float), cudaMemcpyHostToDevice), "upload PE");
+  }
+
+  // ---- GradientStore: flat fp32 in for_each_tensor order
+  n_params_ = 0;
+  for (auto& t : tensor_specs(cfg_)) {
+    uint64_t k = 1;
+    for (auto s : t.second) k *= s;
+    n_params_ += k;
+  }
+  grads_.ensure(n_params_ * sizeof(float));
+  float* g = grads_.as<float>();
+  g_emb_ = g;
+  g += V_ * d_;
+  for (int64_t l = 0; l < L_; ++l) {
+    g_attn_g_.push_back(g);
+    g += d_;
+    g_wq_.push_back(g);
+    g += d_ * d_;
+    g_wk_.push_back(g);
+    g += d_ * d_;
+    g_wv_.push_back(g);
+    g += d_ * d_;
+    g_wo_.push_back(g);
+    g += d_ * d_;
+    g_mlp_g_.push_back(g);
+    g += d_;
+    g_win_.push_back(g);
+    g += d_ * F_;
+    g_wout_.push_back(g);
+    g += F_ * d_;
+  }
+  g_final_g_ = g;
+  g += d_;
+  g_head_ = g;
+  grads_zero();
+  loss_.ensure(sizeof(double));
+  ck(cudaMallocHost(&loss_host_, sizeof(double)), "cudaMallocHost");
+  ck(cudaStreamSynchronize(stream_), "engine init");
+}
+
+Engine::~Engine() {
+  cudaStreamSynchronize(stream_);
+  if (loss_host_) cudaFreeHost(loss_host_);
+  if (meta_host_) cudaFreeHost(meta_host_);
+  cudaStreamDestroy(stream_);
+}
+
+// ----------------------------------------------------------------------------- parameters
+void Engine::upload_params(const float* flat, uint64_t n) {
+  if (n != n_params_) throw std::invalid_argument("params upload: wrong parameter count");
+  DevBuf tmp;
+  size_t maxt = 0;
+  for (auto& t : tensor_specs(cfg_)) {
+    uint64_t k = 1;
+    for (auto s : t.second) k *= s;
+    maxt = std::max<size_t>(maxt, k);
+  }
+  tmp.ensure(maxt * sizeof(float));
+  const float* src = flat;
+  auto put = [&](uint64_t rows, uint64_t cols, bf16* dst, long ldd) {
+    ck(cudaMemcpyAsync(tmp.p, src, rows * cols * sizeof(float), cudaMemcpyHostToDevice, stream_), "params upload");
+    k_f32_to_bf16_2d(tmp.as<float>(), cols, dst, ldd, rows, cols, stream_);
+    ck(cudaStreamSynchronize(stream_), "params upload");
+    src += rows * cols;
+  };
+  auto put_gain = [&](float* dst) {
+    ck(cudaMemcpyAsync(dst, src, d_ * sizeof(float), cudaMemcpyHostToDevice, stream_), "params upload");
+    src += d_;
+  };
+  put(V_, d_, emb_, d_);
+  for (int64_t l = 0; l < L_; ++l) {
+    put_gain(attn_g_[l]);
+    put(d_, d_, wqkv_[l], 3 * d_);           // w_q -> columns [0, d)
+    put(d_, d_, wqkv_[l] + d_, 3 * d_);      // w_k -> columns [d, 2d)
+    put(d_, d_, wqkv_[l] + 2 * d_, 3 * d_);  // w_v -> columns [2d, 3d)
+    put(d_, d_, wo_[l], d_);
+    put_gain(mlp_g_[l]);
+    put(d_, F_, win_[l], F_);
+    put(F_, d_, wout_[l], d_);
+  }
+  put_gain(final_g_);
+  put(d_, V_, head_, V_);
+  ck(cudaStreamSynchronize(stream_), "params upload");
+}
+
+void Engine::init_random(uint64_t seed) {
+  DevBuf tmp;
+  tmp.ensure(std::max<size_t>(V_ * d_, std::max<size_t>(3 * d_ * d_, d_ * F_)) * sizeof(float));
+  uint64_t salt = 0;
+  auto fill = [&](uint64_t rows, uint64_t cols, bf16* dst, long ldd) {
+    k_init_normal(tmp.as<float>(), rows * cols, seed * 1000003ULL + (++salt), 0.02f, stream_);
+    k_f32_to_bf16_2d(tmp.as<float>(), cols, dst, ldd, rows, cols, stream_);
+  };
+  fill(V_, d_, emb_, d_);
+  for (int64_t l = 0; l < L_; ++l) {
+    fill(d_, 3 * d_, wqkv_[l], 3 * d_);
+    fill(d_, d_, wo_[l], d_);
+    fill(d_, F_, win_[l], F_);
+    fill(F_, d_, wout_[l], d_);
+  }
+  fill(d_, V_, head_, V_);
+  k_fill(gainbuf_.as<float>(), (2 * L_ + 1) * d_, 1.0f, stream_);
+  ck(cudaStreamSynchronize(stream_), "init_random");
+}
+
+void Engine::grads_zero() {
+  ck(cudaMemsetAsync(grads_.p, 0, n_params_ * sizeof(float), stream_), "grads_zero");
+  accum_count_ = 0;
+}
+
+void Engine::grads_download(float* out, uint64_t n) {
+  if (n != n_params_) throw std::invalid_argument("grads download: wrong parameter count");
+  ck(cudaMemcpyAsync(out, grads_.p, n * sizeof(float), cudaMemcpyDeviceToHost, stream_), "grads download");
+  ck(cudaStreamSynchronize(stream_), "grads download");
+}
+
+// ----------------------------------------------------------------------------- memory plan
+ActLayout Engine::layout(int64_t n) const {
+  ActLayout a;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t r = o;
+    o += align_up(bytes);
+    return r;
+  };
+  a.x = take(n * d_ * 4);
+  a.inv1 = take(n * 4);
+  a.n1 = take(n * d_ * 2);
+  a.q = take(n * d_ * 2);
+  a.attn = take(n * d_ * 2);
+  a.lse = take(H_ * n * 4);
+  a.xmid = take(n * d_ * 4);
+  a.inv2 = take(n * 4);
+  a.n2 = take(n * d_ * 2);
+  a.h = take(n * F_ * 2);
+  a.act = take(n * F_ * 2);
+  a.per_layer = o;
+  o = a.per_layer * L_;
+  a.final_x = take(n * d_ * 4);
+  a.invf = take(n * 4);
+  a.nf = take(n * d_ * 2);
+  a.total = o;
+  return a;
+}
+
+void Engine::ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, int64_t max_loss_rows) {
+  if (rows > rows_cap_) {
+    if (!seg_stack_.empty()) throw std::runtime_error("engine: KV stack capacity exceeded with a live stack");
+    rows_cap_ = rows;
+    const size_t kvb = static_cast<size_t>(L_) * rows * d_;
+    kst_.ensure(kvb * 2);
+    vst_.ensure(kvb * 2);
+    dkst_.ensure(kvb * 4);
+    dvst_.ensure(kvb * 4);
+    ck(cudaMemsetAsync(dkst_.p, 0, kvb * 4, stream_), "dK stack zero");
+    ck(cudaMemsetAsync(dvst_.p, 0, kvb * 4, stream_), "dV stack zero");
+  }
+  if (arena_bytes > arena_.bytes) {
+    if (!seg_stack_.empty()) throw std::runtime_error("engine: activation arena exceeded with a live stack");
+    arena_.ensure(arena_bytes);
+  }
+  if (max_n > scratch_n_) {
+    scratch_n_ = max_n;
+    const size_t n = max_n;
+    sc_gx_.ensure(n * d_ * 4);
+    sc_gxb_.ensure(n * d_ * 2);
+    sc_gxf_.ensure(n * d_ * 4);
+    sc_gn_.ensure(n * d_ * 4);
+    sc_gh_.ensure(n * F_ * 2);
+    sc_dO_.ensure(n * d_ * 2);
+    sc_D_.ensure(H_ * n * 4);
+    sc_dq_.ensure(n * d_ * 4);
+    sc_dqkv_.ensure(n * 3 * d_ * 2);
+  }
+  // LM-head / CE chunk: ~2 GB of fp32 logits + bf16 dlogits at most
+  const int64_t cap = std::max<int64_t>(128, (int64_t(2) << 30) / (V_ * 6) / 128 * 128);
+  const int64_t chunk = std::min<int64_t>(cap, std::max<int64_t>(max_loss_rows, 1));
+  if (chunk > head_chunk_) {
+    head_chunk_ = chunk;
+    sc_nfl_.ensure(chunk * d_ * 2);
+    sc_logits_.ensure(chunk * V_ * 4);
+    sc_dlog_.ensure(chunk * V_ * 2);
+    sc_gnf_.ensure(chunk * d_ * 4);
+  }
+}
+
+uint64_t Engine::stack_tokens() const {
+  return seg_stack_.empty() ? 0 : static_cast<uint64_t>(seg_stack_.back().S + seg_stack_.back().n);
+}
+
+// Host metadata of one batch: tokens/positions, attention work lists, loss CSR.
+void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
+  auto put = [&](const void* src, size_t bytes) {
+    const size_t off = cursor;
+    cursor = align_up(cursor + bytes);
+    if (host.size() < cursor) host.resize(cursor);
+    if (bytes) std::memcpy(host.data() + off, src, bytes);
+    return off;
+  };
+  b.qblk.clear();
+  b.kvit.clear();
+  b.kvit2.clear();
+  for (size_t i = 0; i < b.seg_off.size(); ++i) {
+    const int64_t so = b.seg_off[i], end = so + b.seg_len[i];
+    for (int64_t q = so; q < end; q += kQBlock) {
+      b.qblk.insert(b.qblk.end(), {int32_t(q), int32_t(std::min<int64_t>(q + kQBlock, end)), int32_t(so), 0});
+    }
+    for (int64_t kv = 0; kv < b.S; kv += 64)  // prefix rows: every query of the member attends
+      for (int64_t q = so; q < end; q += kQChunk) {
+        b.kvit.insert(b.kvit.end(), {int32_t(kv), int32_t(std::min<int64_t>(64, b.S - kv)), int32_t(q),
+                                     int32_t(std::min<int64_t>(q + kQChunk, end))});
+        b.kvit2.insert(b.kvit2.end(), {int32_t(so), 0});
+      }
+    for (int64_t kt = 0; kt < b.seg_len[i]; kt += 64)  // own rows: queries at or after the key
+      for (int64_t q = so + kt; q < end; q += kQChunk) {
+        b.kvit.insert(b.kvit.end(), {int32_t(b.S + so + kt), int32_t(std::min<int64_t>(64, b.seg_len[i] - kt)),
+                                     int32_t(q), int32_t(std::min<int64_t>(q + kQChunk, end))});
+        b.kvit2.insert(b.kvit2.end(), {int32_t(so), 1});
+      }
+  }
+  b.o_tok = put(b.tokens.data(), b.tokens.size() * 4);
+  b.o_pos = put(b.positions.data(), b.positions.size() * 4);
+  b.o_qblk = put(b.qblk.data(), b.qblk.size() * 4);
+  b.o_kvit = put(b.kvit.data(), b.kvit.size() * 4);
+  b.o_kvit2 = put(b.kvit2.data(), b.kvit2.size() * 4);
+  b.o_lrows = put(b.loss_rows.data(), b.loss_rows.size() * 4);
+  b.o_poff = put(b.pair_off.data(), b.pair_off.size() * 4);
+  b.o_ptgt = put(b.pair_tgt.data(), b.pair_tgt.size() * 4);
+  b.o_pw = put(b.pair_w.data(), b.pair_w.size() * 8);
+}
+
+void Engine::upload_meta(std::vector<Batch*>& batches) {
+  std::vector<char> host;
+  size_t cursor = 0;
+  for (Batch* b : batches) build_meta(*b, cursor, host);
+  if (cursor == 0) cursor = kAlign;
+  meta_.ensure(cursor);
+  if (cursor > meta_host_cap_) {
+    ck(cudaStreamSynchronize(stream_), "meta staging");
+    if (meta_host_) cudaFreeHost(meta_host_);
+    ck(cudaMallocHost(&meta_host_, cursor), "cudaMallocHost meta");
+    meta_host_cap_ = cursor;
+  } else {
+    ck(cudaStreamSynchronize(stream_), "meta staging");
+  }
+  std::memcpy(meta_host_, host.data(), host.size());
+  ck(cudaMemcpyAsync(meta_.p, meta_host_, cursor, cudaMemcpyHostToDevice, stream_), "meta upload");
+}
+
+// ----------------------------------------------------------------------------- push (forward_segment)
+void Engine::forward_batch(const Batch& b) {
+  const int n = static_cast<int>(b.n);
+  const int d = static_cast<int>(d_), F = static_cast<int>(F_);
+  const ActLayout lay = layout(b.n);
+  char* base = arena_.as<char>(b.arena_off);
+  auto X = [&](int64_t l) { return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x); };
+  const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
+  const float scale = 1.0f / std::sqrt(static_cast<float>(dh_));  // model.hpp:345
+
+  k_embed_pe(meta<int32_t>(b.o_tok), meta<int32_t>(b.o_pos), emb_, pe_.as<float>(), X(0), n, d, stream_);
+  count();
+  for (int64_t l = 0; l < L_; ++l) {
+    char* Lb = base + l * lay.per_layer;
+    float* inv1 = reinterpret_cast<float*>(Lb + lay.inv1);
+    bf16* n1 = reinterpret_cast<bf16*>(Lb + lay.n1);
+    bf16* q = reinterpret_cast<bf16*>(Lb + lay.q);
+    bf16* attn = reinterpret_cast<bf16*>(Lb + lay.attn);
+    float* lse = reinterpret_cast<float*>(Lb + lay.lse);
+    float* xmid = reinterpret_cast<float*>(Lb + lay.xmid);
+    float* inv2 = reinterpret_cast<float*>(Lb + lay.inv2);
+    bf16* n2 = reinterpret_cast<bf16*>(Lb + lay.n2);
+    bf16* h = reinterpret_cast<bf16*>(Lb + lay.h);
+    bf16* act = reinterpret_cast<bf16*>(Lb + lay.act);
+    bf16* K = kst_.as<bf16>() + l * kv_layer;
+    bf16* Vv = vst_.as<bf16>() + l * kv_layer;
+
+    k_rmsnorm_fwd(X(l), attn_g_[l], inv1, n1, n, d, stream_);  // model.hpp:376-380
+    {  // q,k,v = normed W{q,k,v}; k,v written straight onto the stack rows [S, S+n)
+      EpiParams e;
+      e.mode = EPI_STORE_BF16;
+      e.split_w = d;
+      e.out[0] = q;
+      e.out[1] = K + b.S * d_;
+      e.out[2] = Vv + b.S * d_;
+      e.ldo[0] = e.ldo[1] = e.ldo[2] = d;
+      gemm_bf16(op(n1, d, false), op(wqkv_[l], 3 * d, true), n, 3 * d, d, e, 1, stream_);
+    }
+    {
+      AttnFwdArgs a;
+      a.q = q;
+      a.ldq = d;
+      a.k = K;
+      a.v = Vv;
+      a.ldkv = d;
+      a.o = attn;
+      a.ldo = d;
+      a.lse = lse;
+      a.n = n;
+      a.H = static_cast<int>(H_);
+      a.dh = static_cast<int>(dh_);
+      a.S = static_cast<int>(b.S);
+      a.qblocks = meta<int4>(b.o_qblk);
+      a.nqb = static_cast<int>(b.qblk.size() / 4);
+      a.scale = scale;
+      attn_fwd(a, stream_);
+    }
+    {  // x_mid = x + attn W_o  (model.hpp:410-411,427-428)
+      EpiParams e;
+      e.mode = EPI_RESID_F32;
+      e.out[0] = xmid;
+      e.ldo[0] = d;
+      e.resid = X(l);
+      e.ld_resid = d;
+      gemm_bf16(op(attn, d, false), op(wo_[l], d, true), n, d, d, e, 1, stream_);
+    }
+    k_rmsnorm_fwd(xmid, mlp_g_[l], inv2, n2, n, d, stream_);  // model.hpp:430-434
+    {  // h = normed W_in, act = silu(h)  (model.hpp:435-444)
+      EpiParams e;
+      e.mode = EPI_SILU;
+      e.out[0] = h;
+      e.ldo[0] = F;
+      e.out2 = act;
+      e.ldo2 = F;
+      gemm_bf16(op(n2, d, false), op(win_[l], F, true), n, F, d, e, 1, stream_);
+    }
+    {  // x_out = x_mid + act W_out  (model.hpp:445-448)
+      EpiParams e;
+      e.mode = EPI_RESID_F32;
+      e.out[0] = X(l + 1);
+      e.ldo[0] = d;
+      e.resid = xmid;
+      e.ld_resid = d;
+      gemm_bf16(op(act, F, false), op(wout_[l], d, true), n, d, F, e, 1, stream_);
+    }
+    count(7);
+  }
+  k_rmsnorm_fwd(X(L_), final_g_, reinterpret_cast<float*>(base + lay.invf), reinterpret_cast<bf16*>(base + lay.nf), n, d,
+                stream_);  // model.hpp:451-455
+  count();
+}
+
+// ----------------------------------------------------------------------------- head + loss (visit)
+void Engine::head_backward(const Batch& b, const bf16* nf, const ActLayout& lay, char* base) {
+  (void)lay;
+  (void)base;
+  const int d = static_cast<int>(d_);
+  const long V = V_;
+  float* gxf = sc_gxf_.as<float>();
+  const int64_t m = b.full_logits ? b.n : static_cast<int64_t>(b.loss_rows.size());
+  for (int64_t c0 = 0; c0 < m; c0 += head_chunk_) {
+    const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, m - c0));
+    const bf16* rows = nf + c0 * d_;
+    bf16* dlog = sc_dlog_.as<bf16>();
+    if (!b.full_logits) {
+      bf16* nfl = sc_nfl_.as<bf16>();
+      k_gather_rows_bf16(nf, meta<int32_t>(b.o_lrows) + c0, nfl, cm, d, stream_);
+      rows = nfl;
+      EpiParams e;  // logits = normed_final W_head (model.hpp:460-461), fp32
+      e.mode = EPI_STORE_F32;
+      e.out[0] = sc_logits_.p;
+      e.ldo[0] = V;
+      gemm_bf16(op(rows, d, false), op(head_, V, true), cm, static_cast<int>(V), d, e, 1, stream_);
+      k_ce(sc_logits_.as<float>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt),
+           meta<double>(b.o_pw), dlog, loss_.as<double>(), stream_);
+      count(3);
+    }
+    {  // dW_head += c^T dlogits  (model.hpp:506)
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.out[0] = g_head_;
+      e.ldo[0] = V;
+      gemm_bf16(op(rows, d, true), op(dlog, V, true), d, static_cast<int>(V), cm, e,
+                gemm_choose_splits(d, static_cast<int>(V), cm), stream_);
+    }
+    {  // grad_c = dlogits W_head^T  (model.hpp:507-508)
+      float* gnf = b.full_logits ? gxf + c0 * d_ : sc_gnf_.as<float>();
+      ck(cudaMemsetAsync(gnf, 0, static_cast<size_t>(cm) * d_ * 4, stream_), "memset");
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.out[0] = gnf;
+      e.ldo[0] = d;
+      gemm_bf16(op(dlog, V, false), op(head_, V, false), cm, d, static_cast<int>(V), e,
+                gemm_choose_splits(cm, d, static_cast<int>(V)), stream_);
+      if (!b.full_logits) {
+        k_scatter_rows_f32(gnf, meta<int32_t>(b.o_lrows) + c0, gxf, cm, d, stream_);
+        count();
+      }
+    }
+    count(2);
+  }
+}
+
+// ----------------------------------------------------------------------------- pop (backward_segment)
+void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
+  const int n = static_cast<int>(b.n);
+  const int d = static_cast<int>(d_), F = static_cast<int>(F_);
+  const ActLayout lay = layout(b.n);
+  char* base = arena_.as<char>(b.arena_off);
+  auto X = [&](int64_t l) { return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x); };
+  const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
+  const float scale = 1.0f / std::sqrt(static_cast<float>(dh_));
+  float* gx = sc_gx_.as<float>();
+  bf16* gxb = sc_gxb_.as<bf16>();
+  float* gxf = sc_gxf_.as<float>();
+  float* gn = sc_gn_.as<float>();
+  bf16* gh = sc_gh_.as<bf16>();
+  bf16* dO = sc_dO_.as<bf16>();
+  float* dq = sc_dq_.as<float>();
+  bf16* dqkv = sc_dqkv_.as<bf16>();
+  const bf16* nf = reinterpret_cast<const bf16*>(base + lay.nf);
+
+  ck(cudaMemsetAsync(gxf, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
+  if (b.full_logits) {
+    if (host_grad_logits) {  // caller-provided upstream grad_logits [n x V] (BackwardUpstream, model.hpp:465-469)
+      for (int64_t c0 = 0; c0 < b.n; c0 += head_chunk_) {
+        const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, b.n - c0));
+        ck(cudaMemcpyAsync(sc_logits_.p, host_grad_logits + c0 * V_, static_cast<size_t>(cm) * V_ * 4,
+                           cudaMemcpyHostToDevice, stream_),
+           "grad_logits upload");
+        bf16* dlog = sc_dlog_.as<bf16>();
+        k_f32_to_bf16_2d(sc_logits_.as<float>(), V_, dlog, V_, cm, static_cast<int>(V_), stream_);
+        {  // dW_head += c^T dlogits  (model.hpp:506)
+          EpiParams e;
+          e.mode = EPI_ADD_F32;
+          e.out[0] = g_head_;
+          e.ldo[0] = V_;
+          gemm_bf16(op(nf + c0 * d_, d, true), op(dlog, V_, true), d, static_cast<int>(V_), cm, e,
+                    gemm_choose_splits(d, static_cast<int>(V_), cm), stream_);
+        }
+        {  // grad_c = dlogits W_head^T  (model.hpp:507-508)
+          EpiParams e;
+          e.mode = EPI_ADD_F32;
+          e.out[0] = gxf + c0 * d_;
+          e.ldo[0] = d;
+          gemm_bf16(op(dlog, V_, false), op(head_, V_, false), cm, d, static_cast<int>(V_), e,
+                    gemm_choose_splits(cm, d, static_cast<int>(V_)), stream_);
+        }
+        count(3);
+      }
+    }
+  } else {
+    head_backward(b, nf, lay, base);
+  }
+  // final-norm backward (model.hpp:509-511)
+  k_rmsnorm_bwd(gxf, X(L_), reinterpret_cast<const float*>(base + lay.invf), final_g_, nullptr, gx, gxb, g_final_g_,
+                n, d, stream_);
+  count();
+
+  for (int64_t l = L_ - 1; l >= 0; --l) {
+    char* Lb = base + l * lay.per_layer;
+    const float* inv1 = reinterpret_cast<const float*>(Lb + lay.inv1);
+    const bf16* n1 = reinterpret_cast<const bf16*>(Lb + lay.n1);
+    const bf16* q = reinterpret_cast<const bf16*>(Lb + lay.q);
+    const bf16* attn = reinterpret_cast<const bf16*>(Lb + lay.attn);
+    const float* lse = reinterpret_cast<const float*>(Lb + lay.lse);
+    const float* xmid = reinterpret_cast<const float*>(Lb + lay.xmid);
+    const float* inv2 = reinterpret_cast<const float*>(Lb + lay.inv2);
+    const bf16* n2 = reinterpret_cast<const bf16*>(Lb + lay.n2);
+    const bf16* h = reinterpret_cast<const bf16*>(Lb + lay.h);
+    const bf16* act = reinterpret_cast<const bf16*>(Lb + lay.act);
+    const bf16* K = kst_.as<bf16>() + l * kv_layer;
+    const bf16* Vv = vst_.as<bf16>() + l * kv_layer;
+    float* dK = dkst_.as<float>() + l * kv_layer;
+    float* dV = dvst_.as<float>() + l * kv_layer;
+
+    {  // dW_out += act^T gx  (model.hpp:524)
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.out[0] = g_wout_[l];
+      e.ldo[0] = d;
+      gemm_bf16(op(act, F, true), op(gxb, d, true), F, d, n, e, gemm_choose_splits(F, d, n), stream_);
+    }
+    {  // grad_hidden = (gx W_out^T) * silu'(h)  (model.hpp:525-528)
+      EpiParams e;
+      e.mode = EPI_DSILU;
+      e.out[0] = gh;
+      e.ldo[0] = F;
+      e.aux = h;
+      e.ld_aux = F;
+      gemm_bf16(op(gxb, d, false), op(wout_[l], d, false), n, F, d, e, 1, stream_);
+    }
+    {  // dW_in += normed2^T grad_hidden  (model.hpp:533)
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.out[0] = g_win_[l];
+      e.ldo[0] = F;
+      gemm_bf16(op(n2, d, true), op(gh, F, true), d, F, n, e, gemm_choose_splits(d, F, n), stream_);
+    }
+    {  // grad_normed2 = grad_hidden W_in^T  (model.hpp:535)
+      EpiParams e;
+      e.mode = EPI_STORE_F32;
+      e.out[0] = gn;
+      e.ldo[0] = d;
+      gemm_bf16(op(gh, F, false), op(win_[l], F, false), n, d, F, e, 1, stream_);
+    }
+    // gx_mid = gx + rmsnorm_bwd (model.hpp:536-539)
+    k_rmsnorm_bwd(gn, xmid, inv2, mlp_g_[l], gx, gx, gxb, g_mlp_g_[l], n, d, stream_);
+    {  // dW_o += attn^T gx_mid  (model.hpp:542)
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.out[0] = g_wo_[l];
+      e.ldo[0] = d;
+      gemm_bf16(op(attn, d, true), op(gxb, d, true), d, d, n, e, gemm_choose_splits(d, d, n), stream_);
+    }
+    {  // grad_attn = gx_mid W_o^T  (model.hpp:543-544)
+      EpiParams e;
+      e.mode = EPI_STORE_BF16;
+      e.out[0] = dO;
+      e.ldo[0] = d;
+      gemm_bf16(op(gxb, d, false), op(wo_[l], d, false), n, d, d, e, 1, stream_);
+    }
+    // attention backward (model.hpp:546-604): dQ, and dK/dV added into the stack rows [0, S+n)
+    ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
+    {
+      AttnBwdArgs a;
+      a.q = q;
+      a.dO = dO;
+      a.o = attn;
+      a.ldq = d;
+      a.k = K;
+      a.v = Vv;
+      a.ldkv = d;
+      a.lse = lse;
+      a.D = sc_D_.as<float>();
+      a.dq = dq;
+      a.lddq = d;
+      a.dk = dK;
+      a.dv = dV;
+      a.lddkv = d;
+      a.n = n;
+      a.H = static_cast<int>(H_);
+      a.dh = static_cast<int>(dh_);
+      a.S = static_cast<int>(b.S);
+      a.items = meta<int4>(b.o_kvit);
+      a.items2 = meta<int2>(b.o_kvit2);
+      a.nitems = static_cast<int>(b.kvit.size() / 4);
+      a.scale = scale;
+      attn_bwd(a, stream_);
+    }
+    // pop: consume this batch's dK/dV rows (children + own), zero them for reuse
+    k_pack_dqkv(dq, dK + b.S * d_, dV + b.S * d_, dqkv, n, d, stream_);
+    {  // dW_{q,k,v} += normed1^T [dq | dk | dv]  (model.hpp:610-612)
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.split_w = d;
+      e.out[0] = g_wq_[l];
+      e.out[1] = g_wk_[l];
+      e.out[2] = g_wv_[l];
+      e.ldo[0] = e.ldo[1] = e.ldo[2] = d;
+      gemm_bf16(op(n1, d, true), op(dqkv, 3 * d, true), d, 3 * d, n, e, gemm_choose_splits(d, 3 * d, n), stream_);
+    }
+    {  // grad_normed1 = dq W_q^T + dk W_k^T + dv W_v^T  (model.hpp:613-618)
+      EpiParams e;
+      e.mode = EPI_STORE_F32;
+      e.out[0] = gn;
+      e.ldo[0] = d;
+      gemm_bf16(op(dqkv, 3 * d, false), op(wqkv_[l], 3 * d, false), n, d, 3 * d, e, 1, stream_);
+    }
+    // gx = gx_mid + rmsnorm_bwd (model.hpp:620-624)
+    k_rmsnorm_bwd(gn, X(l), inv1, attn_g_[l], gx, gx, gxb, g_attn_g_[l], n, d, stream_);
+    count(14);
+  }
+  k_embed_grad(gx, meta<int32_t>(b.o_tok), g_emb_, n, d, stream_);  // model.hpp:627-630
+  count();
+  accum_count_ += b.nodes.empty() ? 1 : b.nodes.size();
+}
+
+// ----------------------------------------------------------------------------- tree_train_step
+tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config& sc) {
+  if (!seg_stack_.empty()) throw std::runtime_error("train_step: segment stack is not empty");
+  if (sc.chunk_len != 0) {
+    // chunked backward is not implemented on device yet: only accept chunk_len >= every segment
+    for (auto& nd : tree.nodes)
+      if (nd.tokens.size() > sc.chunk_len)
+        throw std::invalid_argument("tree_train_step: chunk_len smaller than a segment is not supported yet");
+  }
+  if (tree.nodes[0].max_path_below > cfg_.max_position)
+    throw std::invalid_argument("tree_train_step: path exceeds max_position");
+  // ---- plan: batches + PUSH/POP op list in DFS order
+  std::vector<Batch> batches;
+  std::vector<std::pair<int, bool>> ops;  // (batch, is_push)
+  auto make_batch = [&](const std::vector<int32_t>& members, int64_t S) {
+    Batch b;
+    b.S = S;
+    b.nodes = members;
+    int64_t off = 0;
+    for (int32_t u : members) {
+      const auto& nd = tree.nodes[u];
+      b.seg_off.push_back(off);
+      b.seg_len.push_back(static_cast<int64_t>(nd.tokens.size()));
+      for (size_t t = 0; t < nd.tokens.size(); ++t) {
+        b.tokens.push_back(nd.tokens[t]);
+        b.positions.push_back(static_cast<int32_t>(S + t));
+      }
+      LossPairs lp = node_loss_pairs(tree, u, S);
+      // rows within a node are non-decreasing in node_loss_pairs; build the batch CSR
+      for (size_t k = 0; k < lp.rows.size(); ++k) {
+        const int32_t row = static_cast<int32_t>(off + lp.rows[k]);
+        if (b.loss_rows.empty() || b.loss_rows.back() != row) {
+          b.loss_rows.push_back(row);
+          b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
+        }
+        b.pair_tgt.push_back(lp.targets[k]);
+        b.pair_w.push_back(lp.weights[k]);
+      }
+      off += static_cast<int64_t>(nd.tokens.size());
+    }
+    b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
+    b.n = off;
+    batches.push_back(std::move(b));
+    return static_cast<int>(batches.size() - 1);
+  };
+  std::function<void(int32_t, int64_t)> visit = [&](int32_t u, int64_t S) {
+    const auto& ch = tree.nodes[u].children;
+    size_t i = 0;
+    while (i < ch.size()) {
+      const int32_t c = ch[i];
+      if (sc.sibling_batch && tree.nodes[c].children.empty()) {
+        std::vector<int32_t> run = {c};
+        uint64_t tok = tree.nodes[c].tokens.size();
+        size_t j = i + 1;
+        while (j < ch.size() && tree.nodes[ch[j]].children.empty() &&
+               (sc.batch_token_budget == 0 || tok + tree.nodes[ch[j]].tokens.size() <= sc.batch_token_budget)) {
+          tok += tree.nodes[ch[j]].tokens.size();
+          run.push_back(ch[j++]);
+        }
+        const int bi = make_batch(run, S);
+        ops.push_back({bi, true});
+        ops.push_back({bi, false});
+        i = j;
+      } else {
+        const int bi = make_batch({c}, S);
+        ops.push_back({bi, true});
+        visit(c, S + static_cast<int64_t>(tree.nodes[c].tokens.size()));
+        ops.push_back({bi, false});
+        ++i;
+      }
+    }
+  };
+  visit(0, 0);
+
+  // ---- memory plan: LIFO arena offsets, stack rows, scratch sizes
+  tt_step_result res{};
+  int64_t rows = 0, max_n = 0, max_loss = 0;
+  size_t top = 0, peak = 0;
+  uint64_t live_tok = 0, peak_tok = 0;
+  for (auto& [bi, push] : ops) {
+    Batch& b = batches[bi];
+    if (push) {
+      b.arena_off = top;
+      top += align_up(layout(b.n).total);
+      peak = std::max(peak, top);
+      rows = std::max<int64_t>(rows, b.S + b.n);
+      max_n = std::max<int64_t>(max_n, b.n);
+      max_loss = std::max<int64_t>(max_loss, static_cast<int64_t>(b.loss_rows.size()));
+      live_tok += b.n;
+      peak_tok = std::max(peak_tok, live_tok);
+      res.forward_tokens += b.n;
+      res.num_segments += b.nodes.size();
+      res.num_batches += 1;
+    } else {
+      top = b.arena_off;
+      live_tok -= b.n;
+      res.backward_tokens += b.n;
+    }
+  }
+  ensure_capacity(rows, peak, max_n, max_loss);
+  std::vector<Batch*> ptrs;
+  for (auto& b : batches) ptrs.push_back(&b);
+  upload_meta(ptrs);
+  ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
+  const uint64_t launches0 = launches_;
+
+  for (auto& [bi, push] : ops) {
+    if (push) forward_batch(batches[bi]);
+    else backward_batch(batches[bi], nullptr);
+  }
+  ck(cudaGetLastError(), "tree_train_step launch");
+  ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
+  ck(cudaStreamSynchronize(stream_), "tree_train_step");
+  res.total_loss = *loss_host_;
+  res.peak_live_kv_tokens = static_cast<uint64_t>(rows);
+  res.peak_live_activation_tokens = peak_tok;
+  res.num_launches = launches_ - launches0;
+  uint64_t roll = 0;
+  for (auto& s : tree.seq_tokens) roll += s.size();
+  res.rollout_tokens = roll;
+  res.num_chunks = res.num_segments;
+  res.peak_hbm_bytes = wbuf_.bytes + gainbuf_.bytes + pe_.bytes + grads_.bytes + kst_.bytes + vst_.bytes +
+                       dkst_.bytes + dvst_.bytes + peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +
+                       sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes + sc_dq_.bytes + sc_dqkv_.bytes +
+                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + meta_.bytes;
+  arena_peak_ = std::max(arena_peak_, peak);
+  if (!std::isfinite(res.total_loss))
+    throw NonFiniteError("tree_train_step: non-finite loss");
+  return res;
+}
+
+// ----------------------------------------------------------------------------- segment-level API
+void Engine::stack_reset() {
+  ck(cudaStreamSynchronize(stream_), "stack_reset");
+  seg_stack_.clear();
+  arena_top_ = 0;
+  if (dkst_.p) {
+    ck(cudaMemset(dkst_.p, 0, dkst_.bytes), "memset");
+    ck(cudaMemset(dvst_.p, 0, dvst_.bytes), "memset");
+  }
+}
+
+void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out) {
+  if (len == 0) throw std::invalid_argument("forward_segment: empty token list");
+  const int64_t S = static_cast<int64_t>(stack_tokens());
+  if (S + static_cast<int64_t>(len) > static_cast<int64_t>(cfg_.max_position))
+    throw std::invalid_argument("forward_segment: position overflow beyond max_position");
+  for (uint64_t t = 0; t < len; ++t)
+    if (tokens[t] < 0 || static_cast<uint64_t>(tokens[t]) >= cfg_.vocab_size)
+      throw std::invalid_argument("forward_segment: token id out of vocab range");
+  Batch b;
+  b.S = S;
+  b.n = static_cast<int64_t>(len);
+  b.seg_off = {0};
+  b.seg_len = {b.n};
+  b.full_logits = true;
+  for (uint64_t t = 0; t < len; ++t) {
+    b.tokens.push_back(tokens[t]);
+    b.positions.push_back(static_cast<int32_t>(S + t));
+  }
+  b.pair_off = {0};
+  if (seg_stack_.empty()) {
+    // first segment: size the stack for max_position rows and the arena generously
+    size_t arena = 0;
+    arena = align_up(layout(static_cast<int64_t>(cfg_.max_position)).total) + layout(1).total * 64;
+    ensure_capacity(static_cast<int64_t>(cfg_.max_position), arena, static_cast<int64_t>(cfg_.max_position),
+                    static_cast<int64_t>(cfg_.max_position));
+  }
+  b.arena_off = arena_top_;
+  const size_t need = align_up(layout(b.n).total);
+  if (arena_top_ + need > arena_.bytes) throw std::runtime_error("segment_push: activation arena exhausted");
+  arena_top_ += need;
+  // per-segment metadata: its own small meta region appended at the end of meta_
+  std::vector<Batch*> ptrs;
+  for (auto& x : seg_stack_) ptrs.push_back(&x);
+  ptrs.push_back(&b);
+  upload_meta(ptrs);
+  forward_batch(b);
+  if (logits_out) {
+    const ActLayout lay = layout(b.n);
+    const bf16* nf = arena_.as<bf16>(b.arena_off + lay.nf);
+    for (int64_t c0 = 0; c0 < b.n; c0 += head_chunk_) {
+      const int64_t cm = std::min<int64_t>(head_chunk_, b.n - c0);
+      EpiParams e;
+      e.mode = EPI_STORE_F32;
+      e.out[0] = sc_logits_.p;
+      e.ldo[0] = V_;
+      gemm_bf16(op(nf + c0 * d_, d_, false), op(head_, V_, true), static_cast<int>(cm), static_cast<int>(V_),
+                static_cast<int>(d_), e, 1, stream_);
+      ck(cudaMemcpyAsync(logits_out + c0 * V_, sc_logits_.p, cm * V_ * 4, cudaMemcpyDeviceToHost, stream_),
+         "logits download");
+    }
+  }
+  ck(cudaGetLastError(), "segment_push");
+  ck(cudaStreamSynchronize(stream_), "segment_push");
+  seg_stack_.push_back(std::move(b));
+}
+
+void Engine::segment_pop(const float* grad_logits, float* grad_prefix_out) {
+  if (seg_stack_.empty()) throw std::invalid_argument("backward_segment: empty stack");
+  Batch& b = seg_stack_.back();
+  const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
+  std::vector<float> before;
+  const size_t pre = static_cast<size_t>(b.S) * d_;
+  if (grad_prefix_out && b.S > 0) {
+    before.resize(2 * L_ * pre);
+    for (int64_t l = 0; l < L_; ++l) {
+      ck(cudaMemcpyAsync(before.data() + (2 * l) * pre, dkst_.as<float>() + l * kv_layer, pre * 4,
+                         cudaMemcpyDeviceToHost, stream_), "dK download");
+      ck(cudaMemcpyAsync(before.data() + (2 * l + 1) * pre, dvst_.as<float>() + l * kv_layer, pre * 4,
+                         cudaMemcpyDeviceToHost, stream_), "dV download");
+    }
+  }
+  std::vector<Batch*> ptrs;
+  for (auto& x : seg_stack_) ptrs.push_back(&x);
+  upload_meta(ptrs);
+  backward_batch(b, grad_logits);
+  if (grad_prefix_out && b.S > 0) {
+    for (int64_t l = 0; l < L_; ++l) {
+      ck(cudaMemcpyAsync(grad_prefix_out + (2 * l) * pre, dkst_.as<float>() + l * kv_layer, pre * 4,
+                         cudaMemcpyDeviceToHost, stream_), "dK download");
+      ck(cudaMemcpyAsync(grad_prefix_out + (2 * l + 1) * pre, dvst_.as<float>() + l * kv_layer, pre * 4,
+                         cudaMemcpyDeviceToHost, stream_), "dV download");
+    }
+  }
+  ck(cudaGetLastError(), "segment_pop");
+  ck(cudaStreamSynchronize(stream_), "segment_pop");
+  if (grad_prefix_out && b.S > 0)
+    for (size_t i = 0; i < before.size(); ++i) grad_prefix_out[i] -= before[i];
+  arena_top_ = b.arena_off;
+  seg_stack_.pop_back();
+}
+
+}  // namespace ttb

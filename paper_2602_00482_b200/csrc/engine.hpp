@@ -1,0 +1,145 @@
+// B200 DFS prefix-tree forward/backward engine (device side of tree_train_step).
+//
+// HBM layout (one engine per GPU):
+//   weights (bf16): embedding [V x d]; per layer Wqkv [d x 3d] (= [Wq | Wk | Wv] column blocks),
+//                   Wo [d x d], Win [d x F], Wout [F x d]; head [d x V]; gains (fp32)
+//   GradientStore (fp32): one flat buffer in for_each_tensor order (model.hpp:42-59)
+//   KV stack (bf16): per layer K,V [rows_cap x d]; stack row = absolute token position on the path
+//   dKV stack (fp32): per layer dK,dV [rows_cap x d]; a frame's KVGrad lives on its own rows
+//   activation arena: LIFO, one region per pushed segment batch, rewound at pop
+//   scratch: per-pop temporaries (largest batch) + LM-head/CE chunk buffers
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/treetrain_b200.h"
+#include "prefix_tree.hpp"
+
+namespace ttb {
+
+using bf16 = __nv_bfloat16;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf();
+  void ensure(size_t n);  // grow (contents discarded)
+  template <typename T>
+  T* as(size_t byte_off = 0) const {
+    return reinterpret_cast<T*>(static_cast<char*>(p) + byte_off);
+  }
+};
+
+// One executed segment batch: a single tree node, or a run of sibling childless nodes sharing
+// the prefix rows [0, S). Members are laid out contiguously on rows [S, S+n).
+struct Batch {
+  int64_t S = 0, n = 0;
+  std::vector<int32_t> nodes;
+  std::vector<int64_t> seg_off, seg_len;
+  // host-built metadata (uploaded once per step)
+  std::vector<int32_t> tokens, positions;
+  std::vector<int32_t> qblk;   // int4 per query block
+  std::vector<int32_t> kvit;   // int4 per backward item
+  std::vector<int32_t> kvit2;  // int2 per backward item
+  std::vector<int32_t> loss_rows, pair_off, pair_tgt;
+  std::vector<double> pair_w;
+  // device offsets (bytes) into the metadata buffer
+  size_t o_tok = 0, o_pos = 0, o_qblk = 0, o_kvit = 0, o_kvit2 = 0, o_lrows = 0, o_poff = 0, o_ptgt = 0, o_pw = 0;
+  size_t arena_off = 0;
+  bool full_logits = false;  // segment API: head over all rows with caller-provided grad_logits
+};
+
+struct ActLayout {  // byte offsets of one batch's activations inside its arena region
+  size_t per_layer = 0;
+  size_t x, inv1, n1, q, attn, lse, xmid, inv2, n2, h, act;  // within a layer block
+  size_t final_x, invf, nf;                                  // after the layer blocks
+  size_t total = 0;
+};
+
+class Engine {
+ public:
+  Engine(const tt_model_config& cfg, int device);
+  ~Engine();
+
+  const tt_model_config& config() const { return cfg_; }
+  uint64_t param_count() const { return n_params_; }
+  cudaStream_t stream() const { return stream_; }
+
+  void upload_params(const float* flat, uint64_t n);
+  void init_random(uint64_t seed);
+  void grads_zero();
+  void grads_download(float* out, uint64_t n);
+  float* grads_device() const { return grads_.as<float>(); }
+  uint64_t accum_count() const { return accum_count_; }
+
+  tt_step_result train_step(const PrefixTree& tree, const tt_sched_config& sc);
+
+  // segment level (device stack)
+  void segment_push(const int32_t* tokens, uint64_t len, float* logits_out);
+  void segment_pop(const float* grad_logits, float* grad_prefix_out);
+  void stack_reset();
+  uint64_t stack_segments() const { return seg_stack_.size(); }
+  uint64_t stack_tokens() const;
+
+ private:
+  // ---- helpers
+  ActLayout layout(int64_t n) const;
+  void ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, int64_t max_loss_rows);
+  void build_meta(Batch& b, size_t& cursor, std::vector<char>& host);
+  void upload_meta(std::vector<Batch*>& batches);
+  void forward_batch(const Batch& b);
+  void backward_batch(const Batch& b, const float* host_grad_logits);
+  void head_backward(const Batch& b, const bf16* nf, const ActLayout& lay, char* base);
+  template <typename T>
+  const T* meta(size_t off) const {
+    return reinterpret_cast<const T*>(meta_.as<char>() + off);
+  }
+  void count(int k = 1) { launches_ += k; }
+
+  tt_model_config cfg_;
+  int device_ = 0;
+  int64_t V_, d_, H_, L_, F_, dh_;
+  uint64_t n_params_ = 0;
+  cudaStream_t stream_ = nullptr;
+
+  // parameters (device layout) and gradients
+  DevBuf wbuf_;  // all bf16 weights
+  bf16 *emb_ = nullptr, *head_ = nullptr;
+  std::vector<bf16*> wqkv_, wo_, win_, wout_;
+  DevBuf gainbuf_;  // fp32 gains
+  std::vector<float*> attn_g_, mlp_g_;
+  float* final_g_ = nullptr;
+  DevBuf pe_;  // fp32 [max_position x d]
+  DevBuf grads_;
+  // gradient tensor pointers (into grads_)
+  float *g_emb_ = nullptr, *g_final_g_ = nullptr, *g_head_ = nullptr;
+  std::vector<float*> g_attn_g_, g_wq_, g_wk_, g_wv_, g_wo_, g_mlp_g_, g_win_, g_wout_;
+  uint64_t accum_count_ = 0;
+
+  // stacks / arena / scratch
+  int64_t rows_cap_ = 0;
+  DevBuf kst_, vst_, dkst_, dvst_;
+  DevBuf arena_;
+  size_t arena_top_ = 0, arena_peak_ = 0;
+  int64_t scratch_n_ = 0, head_chunk_ = 0;
+  DevBuf sc_gx_, sc_gxb_, sc_gxf_, sc_gn_, sc_gh_, sc_dO_, sc_D_, sc_dq_, sc_dqkv_;
+  DevBuf sc_nfl_, sc_logits_, sc_dlog_, sc_gnf_;
+  DevBuf meta_;
+  DevBuf loss_;
+  double* loss_host_ = nullptr;  // pinned
+  char* meta_host_ = nullptr;    // pinned staging
+  size_t meta_host_cap_ = 0;
+  uint64_t launches_ = 0;
+
+  // segment-level API state
+  std::vector<Batch> seg_stack_;
+};
+
+}  // namespace ttb

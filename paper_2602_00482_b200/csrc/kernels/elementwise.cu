@@ -1,0 +1,320 @@
+// HBM-bound kernels of the push/pop path: embedding + positional encoding, RMSNorm fwd/bwd,
+// fused weighted cross-entropy over a vocab row, stack pop (dK/dV consume + zero), embedding
+// gradient scatter, parameter layout conversion / init. 128-bit coalesced accesses throughout.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "elementwise.h"
+#include "sm100.cuh"
+
+namespace ttb {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffff, v, o));
+  return v;
+}
+// Block-wide sum for blockDim.x == 256; returns the total to every thread.
+__device__ __forceinline__ float block_sum256(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = l < 8 ? red[l] : 0.f;
+  return warp_sum(t);
+}
+
+// x[r] = E[tok[r]] + PE[pos[r]]  (model.hpp:363-369, add_positional_encoding :239-248)
+__global__ void embed_pe_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ pos,
+                                const __nv_bfloat16* __restrict__ emb, const float* __restrict__ pe,
+                                float* __restrict__ x, int d) {
+  const int r = blockIdx.x;
+  const long e0 = static_cast<long>(tok[r]) * d, p0 = static_cast<long>(pos[r]) * d, x0 = static_cast<long>(r) * d;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    const uint2 eb = *reinterpret_cast<const uint2*>(emb + e0 + c);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&eb.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&eb.y));
+    const float4 p = *reinterpret_cast<const float4*>(pe + p0 + c);
+    *reinterpret_cast<float4*>(x + x0 + c) = make_float4(a.x + p.x, a.y + p.y, b.x + p.z, b.y + p.w);
+  }
+}
+
+// inv = 1/sqrt(mean(x^2)+eps); y = x*inv*g (bf16)   (rms_inv model.hpp:250-256; apply :377-380)
+// one warp per row
+__global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain, float* __restrict__ inv,
+                                   __nv_bfloat16* __restrict__ y, int n, int d) {
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const float* xr = x + static_cast<long>(row) * d;
+  float s = 0.f;
+  for (int c = lane * 4; c < d; c += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + c);
+    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  s = warp_sum(s);
+  const float iv = 1.0f / sqrtf(s / static_cast<float>(d) + 1e-6f);
+  if (lane == 0) inv[row] = iv;
+  __nv_bfloat16* yr = y + static_cast<long>(row) * d;
+  for (int c = lane * 4; c < d; c += 128) {
+    const float4 v = *reinterpret_cast<const float4*>(xr + c);
+    const float4 g = *reinterpret_cast<const float4*>(gain + c);
+    uint2 o;
+    o.x = pack_bf16x2(v.x * iv * g.x, v.y * iv * g.y);
+    o.y = pack_bf16x2(v.z * iv * g.z, v.w * iv * g.w);
+    *reinterpret_cast<uint2*>(yr + c) = o;
+  }
+}
+
+// rmsnorm_backward (model.hpp:258-271), rows in blocks of kRows, 256 threads:
+//   gx = gres + gy*g*inv - x*(sum(gy*g*x)*inv^3/d);  ggain += sum_rows gy*x*inv
+constexpr int kNormRows = 16;
+constexpr int kMaxVec = 8;  // d <= 8192
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float* __restrict__ gy, const float* __restrict__ x,
+                                                          const float* __restrict__ inv, const float* __restrict__ gain,
+                                                          const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
+                                                          float* __restrict__ ggain, int n, int d) {
+  __shared__ float red[8];
+  float4 gacc[kMaxVec];
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) gacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int r0 = blockIdx.x * kNormRows;
+  const int r1 = min(n, r0 + kNormRows);
+  for (int r = r0; r < r1; ++r) {
+    const long o = static_cast<long>(r) * d;
+    const float iv = inv[r];
+    float dot = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int c = (threadIdx.x + k * 256) * 4;
+      if (c < d) {
+        const float4 a = *reinterpret_cast<const float4*>(gy + o + c);
+        const float4 b = *reinterpret_cast<const float4*>(x + o + c);
+        const float4 g = *reinterpret_cast<const float4*>(gain + c);
+        dot += a.x * g.x * b.x + a.y * g.y * b.y + a.z * g.z * b.z + a.w * g.w * b.w;
+      }
+    }
+    dot = block_sum256(dot, red);
+    const float scale = dot * iv * iv * iv / static_cast<float>(d);
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int c = (threadIdx.x + k * 256) * 4;
+      if (c < d) {
+        const float4 a = *reinterpret_cast<const float4*>(gy + o + c);
+        const float4 b = *reinterpret_cast<const float4*>(x + o + c);
+        const float4 g = *reinterpret_cast<const float4*>(gain + c);
+        float4 res = gres ? *reinterpret_cast<const float4*>(gres + o + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        res.x += a.x * g.x * iv - b.x * scale;
+        res.y += a.y * g.y * iv - b.y * scale;
+        res.z += a.z * g.z * iv - b.z * scale;
+        res.w += a.w * g.w * iv - b.w * scale;
+        *reinterpret_cast<float4*>(gx + o + c) = res;
+        uint2 pb;
+        pb.x = pack_bf16x2(res.x, res.y);
+        pb.y = pack_bf16x2(res.z, res.w);
+        *reinterpret_cast<uint2*>(gxb + o + c) = pb;
+        gacc[k].x += a.x * b.x * iv;
+        gacc[k].y += a.y * b.y * iv;
+        gacc[k].z += a.z * b.z * iv;
+        gacc[k].w += a.w * b.w * iv;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int c = (threadIdx.x + k * 256) * 4;
+    if (c < d) red_add_v4_f32(ggain + c, gacc[k].x, gacc[k].y, gacc[k].z, gacc[k].w);
+  }
+}
+
+// Weighted NLL over one vocab row with several (target, weight) pairs (weighted_nll,
+// model.hpp:643-677, extended to multi-target rows):
+//   loss += sum_j w_j (lse - l[t_j])  (fp64);  dl = (sum_j w_j) softmax(l) - sum_j w_j onehot(t_j)  (bf16)
+__global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits, long V,
+                                                 const int32_t* __restrict__ pair_off,
+                                                 const int32_t* __restrict__ tgt, const double* __restrict__ w,
+                                                 __nv_bfloat16* __restrict__ dl, double* __restrict__ loss) {
+  __shared__ float red[8];
+  __shared__ float s_lse;
+  const int r = blockIdx.x;
+  const float* lr = logits + static_cast<long>(r) * V;
+  float m = -INFINITY, s = 0.f;
+  for (long c = threadIdx.x * 4; c < V; c += 1024) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    const float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+    if (mx > m) {
+      s *= __expf(m - mx);
+      m = mx;
+    }
+    s += __expf(v.x - m) + __expf(v.y - m) + __expf(v.z - m) + __expf(v.w - m);
+  }
+  // combine (m, s) across the block
+  float gm = warp_max(m);
+  {
+    const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[wi] = gm;
+    __syncthreads();
+    gm = warp_max(l < 8 ? red[l] : -INFINITY);
+    __syncthreads();
+  }
+  s = (m == -INFINITY) ? 0.f : s * __expf(m - gm);
+  s = block_sum256(s, red);
+  if (threadIdx.x == 0) {
+    s_lse = gm + logf(s);
+  }
+  __syncthreads();
+  const float lse = s_lse;
+  const int p0 = pair_off[r], p1 = pair_off[r + 1];
+  float wsum = 0.f;
+  for (int p = p0; p < p1; ++p) wsum += static_cast<float>(w[p]);
+  __nv_bfloat16* dr = dl + static_cast<long>(r) * V;
+  for (long c = threadIdx.x * 4; c < V; c += 1024) {
+    const float4 v = *reinterpret_cast<const float4*>(lr + c);
+    float g[4] = {wsum * __expf(v.x - lse), wsum * __expf(v.y - lse), wsum * __expf(v.z - lse),
+                  wsum * __expf(v.w - lse)};
+    for (int p = p0; p < p1; ++p) {
+      const long t = tgt[p];
+      if (t >= c && t < c + 4) g[t - c] -= static_cast<float>(w[p]);
+    }
+    uint2 o;
+    o.x = pack_bf16x2(g[0], g[1]);
+    o.y = pack_bf16x2(g[2], g[3]);
+    *reinterpret_cast<uint2*>(dr + c) = o;
+  }
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int p = p0; p < p1; ++p) acc += w[p] * (static_cast<double>(lse) - static_cast<double>(lr[tgt[p]]));
+    atomicAdd(loss, acc);
+  }
+}
+
+__global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, const int32_t* __restrict__ idx,
+                                        __nv_bfloat16* __restrict__ dst, int d) {
+  const int i = blockIdx.x;
+  const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<long>(idx[i]) * d);
+  uint4* o = reinterpret_cast<uint4*>(dst + static_cast<long>(i) * d);
+  for (int c = threadIdx.x; c < d / 8; c += blockDim.x) o[c] = s[c];
+}
+
+__global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int32_t* __restrict__ idx,
+                                        float* __restrict__ dst, int d) {
+  const int i = blockIdx.x;
+  const float4* s = reinterpret_cast<const float4*>(src + static_cast<long>(i) * d);
+  float4* o = reinterpret_cast<float4*>(dst + static_cast<long>(idx[i]) * d);
+  for (int c = threadIdx.x; c < d / 4; c += blockDim.x) o[c] = s[c];
+}
+
+// Stack pop of one layer: dqkv[r] = [dQ[r] | dK[r] | dV[r]] (bf16), then zero the consumed
+// dK/dV stack rows (KVGrad::add_rows consumer + frame release, model.hpp:193-206).
+__global__ void pack_dqkv_kernel(const float* __restrict__ dq, float* __restrict__ dk, float* __restrict__ dv,
+                                 __nv_bfloat16* __restrict__ out, int d) {
+  const int r = blockIdx.x;
+  const long o = static_cast<long>(r) * d;
+  __nv_bfloat16* orow = out + static_cast<long>(r) * 3 * d;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    const float4 a = *reinterpret_cast<const float4*>(dq + o + c);
+    const float4 b = *reinterpret_cast<float4*>(dk + o + c);
+    const float4 e = *reinterpret_cast<float4*>(dv + o + c);
+    *reinterpret_cast<uint2*>(orow + c) = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+    *reinterpret_cast<uint2*>(orow + d + c) = make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+    *reinterpret_cast<uint2*>(orow + 2 * d + c) = make_uint2(pack_bf16x2(e.x, e.y), pack_bf16x2(e.z, e.w));
+    *reinterpret_cast<float4*>(dk + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(dv + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// dE[tok[r]] += gx[r]   (model.hpp:627-630)
+__global__ void embed_grad_kernel(const float* __restrict__ gx, const int32_t* __restrict__ tok,
+                                  float* __restrict__ gemb, int d) {
+  const int r = blockIdx.x;
+  const float* s = gx + static_cast<long>(r) * d;
+  float* o = gemb + static_cast<long>(tok[r]) * d;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(s + c);
+    red_add_v4_f32(o + c, v.x, v.y, v.z, v.w);
+  }
+}
+
+__global__ void f32_to_bf16_2d_kernel(const float* __restrict__ src, long lds, __nv_bfloat16* __restrict__ dst,
+                                      long ldd, int rows, int cols) {
+  const long total = static_cast<long>(rows) * cols;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long r = i / cols, c = i % cols;
+    dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// N(0, std) via Box-Muller on a counter hash (seed, element index).
+__global__ void init_normal_kernel(float* __restrict__ out, long n, uint64_t seed, float stdv) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ULL + static_cast<uint64_t>(i));
+    const float u1 = (static_cast<float>(h >> 40) + 1.0f) * (1.0f / 16777217.0f);
+    const float u2 = static_cast<float>((h >> 16) & 0xFFFFFF) * (1.0f / 16777216.0f);
+    out[i] = stdv * sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+  }
+}
+
+__global__ void fill_kernel(float* __restrict__ out, long n, float v) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x)
+    out[i] = v;
+}
+
+}  // namespace
+
+void k_embed_pe(const int32_t* tok, const int32_t* pos, const __nv_bfloat16* emb, const float* pe, float* x, int n,
+                int d, cudaStream_t s) {
+  if (n > 0) embed_pe_kernel<<<n, 128, 0, s>>>(tok, pos, emb, pe, x, d);
+}
+void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16* y, int n, int d, cudaStream_t s) {
+  if (n > 0) rmsnorm_fwd_kernel<<<(n + 7) / 8, 256, 0, s>>>(x, gain, inv, y, n, d);
+}
+void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
+                   __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
+  if (n > 0) rmsnorm_bwd_kernel<<<(n + kNormRows - 1) / kNormRows, 256, 0, s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
+}
+void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
+          __nv_bfloat16* dl, double* loss, cudaStream_t s) {
+  if (m > 0) ce_kernel<<<m, 256, 0, s>>>(logits, V, pair_off, tgt, w, dl, loss);
+}
+void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
+                        cudaStream_t s) {
+  if (m > 0) gather_rows_bf16_kernel<<<m, 128, 0, s>>>(src, idx, dst, d);
+}
+void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m, int d, cudaStream_t s) {
+  if (m > 0) scatter_rows_f32_kernel<<<m, 128, 0, s>>>(src, idx, dst, d);
+}
+void k_pack_dqkv(const float* dq, float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s) {
+  if (n > 0) pack_dqkv_kernel<<<n, 128, 0, s>>>(dq, dk, dv, out, d);
+}
+void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s) {
+  if (n > 0) embed_grad_kernel<<<n, 128, 0, s>>>(gx, tok, gemb, d);
+}
+void k_f32_to_bf16_2d(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s) {
+  const long total = static_cast<long>(rows) * cols;
+  if (total > 0) f32_to_bf16_2d_kernel<<<static_cast<int>(std::min<long>((total + 255) / 256, 148 * 32)), 256, 0, s>>>(src, lds, dst, ldd, rows, cols);
+}
+void k_init_normal(float* out, long n, uint64_t seed, float stdv, cudaStream_t s) {
+  if (n > 0) init_normal_kernel<<<static_cast<int>(std::min<long>((n + 255) / 256, 148 * 32)), 256, 0, s>>>(out, n, seed, stdv);
+}
+void k_fill(float* out, long n, float v, cudaStream_t s) {
+  if (n > 0) fill_kernel<<<static_cast<int>(std::min<long>((n + 255) / 256, 148 * 32)), 256, 0, s>>>(out, n, v);
+}
+
+}  // namespace ttb

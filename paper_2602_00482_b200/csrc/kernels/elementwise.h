@@ -1,0 +1,28 @@
+// HBM-bound kernels of the push/pop path (elementwise.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+namespace ttb {
+
+void k_embed_pe(const int32_t* tok, const int32_t* pos, const __nv_bfloat16* emb, const float* pe, float* x, int n,
+                int d, cudaStream_t s);
+void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16* y, int n, int d, cudaStream_t s);
+// gx = gres + d(rmsnorm)/dx (gres may be null; gx may alias gres), bf16 copy into gxb, gain grad into ggain.
+void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
+                   __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s);
+void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
+          __nv_bfloat16* dl, double* loss, cudaStream_t s);
+void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
+                        cudaStream_t s);
+void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m, int d, cudaStream_t s);
+void k_pack_dqkv(const float* dq, float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s);
+void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s);
+void k_f32_to_bf16_2d(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s);
+void k_init_normal(float* out, long n, uint64_t seed, float stdv, cudaStream_t s);
+void k_fill(float* out, long n, float v, cudaStream_t s);
+
+}  // namespace ttb

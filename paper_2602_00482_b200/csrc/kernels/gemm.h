@@ -21,6 +21,7 @@ enum EpiMode : int {
   EPI_ADD_F32 = 2,     // out[blk] (fp32) += alpha*acc   (residual add / dW accumulate)
   EPI_SILU = 3,        // out[0] (bf16) = acc, out2 (bf16) = silu(acc)
   EPI_DSILU = 4,       // out[0] (bf16) = acc * silu'(aux)
+  EPI_RESID_F32 = 5,   // out[0] (fp32) = resid + alpha*acc   (residual stream, model.hpp:427-428,447-448)
 };
 
 // Column blocks of width split_w go to out[n / split_w] (row pitch ldo[...]) so one GEMM can
@@ -34,6 +35,8 @@ struct EpiParams {
   long ldo2 = 0;
   const __nv_bfloat16* aux = nullptr;
   long ld_aux = 0;
+  const float* resid = nullptr;
+  long ld_resid = 0;
   float alpha = 1.0f;
   int atomic = 0;
 };

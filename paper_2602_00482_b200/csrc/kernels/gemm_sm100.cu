@@ -274,6 +274,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             p[1] = w1;
             break;
           }
+          case EPI_RESID_F32: {
+            const float4* rp = reinterpret_cast<const float4*>(epi.resid + static_cast<long>(row) * epi.ld_resid + n);
+            float4* p = reinterpret_cast<float4*>(static_cast<float*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 r4 = rp[i];
+              p[i] = make_float4(r4.x + v[4 * i], r4.y + v[4 * i + 1], r4.z + v[4 * i + 2], r4.w + v[4 * i + 3]);
+            }
+            break;
+          }
           default:
             break;
         }

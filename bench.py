@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""bench.py — rollout tokens/s of the DFS prefix-tree forward/backward step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c2]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+A step = one DFS tree fwd+bwd pass (push / visit / pop over every prefix tree of the rank's
+shard) + the single NCCL gradient all-reduce (N > 1). Whole prefix trees are sharded across
+ranks with the paper's min-max contiguous partitioner (partition_contiguous),
+N x the per-GPU workload in total ("weak" scaling). Rank 0 prints ONE JSON line.
+
+  value  : device-timed (CUDA events on the engine stream, barrier + synchronize on both sides,
+           max over ranks); the step plan (schedule + metadata) is already resident in HBM.
+  e2e    : the same metric through the public API from host sequences every step: tree build,
+           plan (host->device metadata copy from pinned memory), execute, loss read-back.
+  roofline: the dominant kernel (tcgen05 GEMM) from one profiled step after the timed region
+           (CUDA events around every launch on the engine stream): algorithmic FLOPs / time,
+           against MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step).
+  cpu_baseline: the reference's own model core (oracle/_ref, compiled from /root/reference)
+           timed on this box's host cores on a bounded sample; extrapolated through the FLOP model.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rollout tokens/s (fwd+bwd, DFS tree attn) at 1/2/4/8 B200; peak HBM GB"
+
+# model shapes keep the reference architecture (model.hpp:20-38): MHA, no bias, 2-matrix SiLU MLP,
+# untied head, sinusoidal absolute PE, pre-RMSNorm. (V, d, H, L, d_ff)
+MODELS = {
+    "tiny": (1024, 256, 4, 2, 1024),
+    "qwen2-0.5b-shape": (151936, 896, 14, 24, 4864),
+    "qwen2.5-1.5b-shape": (151936, 1536, 12, 28, 8960),
+    "qwen2.5-7b-shape": (152064, 3584, 28, 28, 18944),
+}
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "c1": dict(model="tiny", prompts=1, group=8, prompt_len=512, resp_len=256,
+               desc="tiny 2-layer d=256 transformer, one prefix tree (512-tok prompt, 8 branches x 256 tok)"),
+    "c2": dict(model="qwen2-0.5b-shape", prompts=64, group=16, prompt_len=1024, resp_len=2048,
+               desc="Qwen2-0.5B-shape random-init, 64 prompts x 16 rollouts, 1K shared prefix / 2K branches, bf16"),
+    "c4": dict(model="qwen2.5-7b-shape", prompts=32, group=16, prompt_len=1024, resp_len=2048,
+               desc="Qwen2.5-7B-shape random-init, 32 trees per GPU (256 on 8 GPUs), load-balanced, NCCL allreduce"),
+}
+
+
+def make_corpus(prompts, group, prompt_len, resp_len, vocab, seed, shared=0):
+    """Rollout groups: a prompt (weights 0) + `group` responses (weights 1) sharing `shared` tokens."""
+    import paper_2602_00482_b200 as tt
+
+    rng = np.random.default_rng(seed)
+    seqs = []
+    for p in range(prompts):
+        prompt = rng.integers(0, vocab, prompt_len, dtype=np.int64)
+        stem = rng.integers(0, vocab, shared, dtype=np.int64)
+        firsts = rng.choice(vocab, size=group, replace=False)
+        for g in range(group):
+            rest = rng.integers(0, vocab, resp_len - shared, dtype=np.int64)
+            rest[0] = firsts[g]
+            toks = np.concatenate([prompt, stem, rest]).astype(np.int32)
+            w = np.concatenate([np.zeros(prompt_len), np.ones(resp_len)])
+            seqs.append(tt.TokenSequence(len(seqs), toks, w))
+    return seqs
+
+
+def step_flops(cfg, tree_nodes):
+    """Algorithmic FLOPs of one fwd+bwd step: sum over nodes of
+    len*6*(L(4d^2+2d*F) + d*V) + sum over queries 12*d*L*(S+t+1). Recompute not counted."""
+    V, d, H, L, F = cfg
+    per_tok = 6.0 * (L * (4 * d * d + 2 * d * F) + d * V)
+    fl = 0.0
+    for S, n in tree_nodes:
+        fl += n * per_tok + 12.0 * d * L * (n * S + n * (n + 1) / 2)
+    return fl
+
+
+def tree_nodes_of(seqs):
+    """(S, len) of every node of the prefix tree over `seqs` (python mirror, for the FLOP model)."""
+    out = []
+    groups = {}
+    for s in seqs:
+        groups.setdefault(tuple(np.asarray(s.tokens[:1]).tolist()), []).append(np.asarray(s.tokens))
+
+    def rec(arrs, S):
+        # longest common extension
+        m = min(len(a) for a in arrs)
+        q = S
+        while q < m and all(a[q] == arrs[0][q] for a in arrs[1:]):
+            q += 1
+        if len(arrs) == 1:
+            q = len(arrs[0])
+        out.append((S, q - S))
+        rest = [a for a in arrs if len(a) > q]
+        by = {}
+        for a in rest:
+            by.setdefault(int(a[q]), []).append(a)
+        for g in by.values():
+            rec(g, q)
+
+    for g in groups.values():
+        rec(g, 0)
+    return out
+
+
+class ClockSampler(threading.Thread):
+    def __init__(self, dev):
+        super().__init__(daemon=True)
+        self.dev, self.samples, self.reasons, self.stop_evt = dev, [], set(), threading.Event()
+        self.max_mhz = None
+
+    def run(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            names = {getattr(nv, k): k for k in dir(nv) if k.startswith("nvmlClocksEventReason") or k.startswith("nvmlClocksThrottleReason")}
+            while not self.stop_evt.is_set():
+                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                for bit, name in names.items():
+                    if isinstance(bit, int) and bit and bit not in (0xFFFFFFFFFFFFFFFF,) and (r & bit) == bit and bit & (bit - 1) == 0:
+                        self.reasons.add(name.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", ""))
+                time.sleep(0.1)
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            self.reasons.add(f"sampler-error:{type(e).__name__}")
+
+    def result(self):
+        self.stop_evt.set()
+        self.join(timeout=2)
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return j.get("bf16_tflops_sustained", 1392.8), j.get("bf16_tflops", 1662.4), j.get("hbm_gbs", 6554.6), "measured"
+    return 1400.0, 1590.0, 6650.0, "fallback"
+
+
+def cuda_array(ptr, n):
+    import torch
+
+    class _A:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
+
+    return torch.as_tensor(_A(), device="cuda")
+
+
+# ----------------------------------------------------------------------------- CPU reference arm
+def cpu_reference_sample(model, S, n_tokens, threads, repeats=1, handle=None):
+    """Reference forward_segment + weighted_nll + backward_segment of n_tokens at prefix S per
+    host thread (T=float, -O3). Returns (seconds per repeat, flops per repeat)."""
+    from oracle import refimpl as R
+    from oracle import treetrain_oracle as O
+
+    V, d, H, L, F = MODELS[model]
+    cfg = O.ModelConfig(V, d, H, L, F, S + n_tokens + 8)
+    m = handle or R.RefModel(cfg, 7)
+    secs = [m.slice(S, n_tokens, threads, seed=11 + i) for i in range(repeats)]
+    fl = threads * step_flops(MODELS[model], [(S, n_tokens)])
+    return secs, fl
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    c = CONFIGS[args.config]
+    model = MODELS[c["model"]]
+    from oracle import refimpl as R
+
+    threads = os.cpu_count() or 1
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libttref.so not built (needs /root/reference at build time)"}))
+        return 0
+    seqs = make_corpus(c["prompts"], c["group"], c["prompt_len"], c["resp_len"], model[0], 3)
+    nodes = tree_nodes_of(seqs)
+    fl_step = step_flops(model, nodes)
+    roll = sum(len(s.tokens) for s in seqs)
+    n_tok = 1 if model[3] > 2 else 64
+    S = c["prompt_len"]
+    secs, fl = cpu_reference_sample(c["model"], S, n_tok, threads, repeats=args.warmup + args.steps)
+    timed = secs[args.warmup:]
+    t = float(np.mean(timed))
+    rate = fl / t
+    value = rate / (fl_step / roll)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rollout tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {c['desc']}", "model": c["model"], "global_batch": len(seqs),
+                   "seq_len": c["prompt_len"] + c["resp_len"], "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "rollout tokens/s", "cores": threads, "kind": "reference",
+                         "sample": f"reference forward_segment+weighted_nll+backward_segment of {n_tok} token(s) at "
+                                   f"prefix S={S} per thread x {threads} threads (T=float), extrapolated to the "
+                                   f"{args.config} step via the FLOP model ({rate / 1e9:.2f} GFLOP/s achieved)"},
+        "e2e": {"value": value, "unit": "rollout tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- B200 arm
+def run_b200(args):
+    import torch
+
+    import paper_2602_00482_b200 as tt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = CONFIGS[args.config]
+    V, d, H, L, F = MODELS[c["model"]]
+    max_pos = c["prompt_len"] + c["resp_len"] + 16
+    cfg = tt.ModelConfig(V, d, H, L, F, max_pos)
+    # whole job: world x per-GPU prompts, sharded by the min-max contiguous partitioner
+    all_seqs = make_corpus(c["prompts"] * world, c["group"], c["prompt_len"], c["resp_len"], V, 3)
+    if world > 1:
+        plan = tt.partition_contiguous(all_seqs, world)
+        mine = set(plan["groups"][rank])
+        seqs = [s for s in all_seqs if s.seq_id in mine]
+    else:
+        seqs = all_seqs
+    eng = tt.Engine(cfg, device=local)
+    eng.init_params_random(7)
+    sched = tt.SchedulerConfig(sibling_batch=not args.no_sibling_batch, batch_token_budget=args.batch_budget)
+    t0 = time.time()
+    tree = tt.build_prefix_tree(seqs)
+    build_s = time.time() - t0
+    st = tree.stats()
+    t0 = time.time()
+    plan = eng.plan(tree, sched)
+    plan_s = time.time() - t0
+    ext = torch.cuda.ExternalStream(eng.stream_ptr)
+    grads = cuda_array(eng.grads_device_ptr(), eng.n_params) if world > 1 else None
+
+    def one_step():
+        eng.zero_gradients()
+        r = plan.execute()
+        if grads is not None:
+            dist.all_reduce(grads)
+            ext.wait_stream(torch.cuda.current_stream())
+        return r
+
+    for _ in range(args.warmup):
+        one_step()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    launches = 0
+    res = None
+    for _ in range(args.steps):
+        res = one_step()
+        launches += res.num_launches
+    e1.record(ext)
+    barrier()
+    clocks = sampler.result()
+    ms = e0.elapsed_time(e1) / args.steps
+    # ---- e2e through the public API from host buffers (tree build + plan upload + execute + loss)
+    e2e_ms = None
+    h2d = 0
+    if not args.no_e2e:
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(ext)
+        for _ in range(args.e2e_steps):
+            eng.zero_gradients()
+            r2 = eng.tree_train_step(tt.build_prefix_tree(seqs), sched)
+            h2d = r2.h2d_bytes
+            if grads is not None:
+                dist.all_reduce(grads)
+                ext.wait_stream(torch.cuda.current_stream())
+        f1.record(ext)
+        barrier()
+        e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
+    # ---- max over ranks
+    t = torch.tensor([ms, e2e_ms or 0.0], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(t[0]), float(t[1])
+    roll_local = sum(len(s.tokens) for s in seqs)
+    roll_total = sum(len(s.tokens) for s in all_seqs)
+    value = roll_total / (ms / 1e3)
+    # ---- profiled step for the roofline (after the timed region)
+    eng.set_profiling(True)
+    eng.zero_gradients()
+    plan.execute()
+    eng.set_profiling(False)
+    prof = eng.profile()
+    sust, burst, hbm, src = measured_peaks()
+    gm = prof["gemm"]
+    gemm_tflops = gm["flops"] / (gm["ms"] / 1e3) / 1e12 if gm["ms"] else 0.0
+    nodes = tree_nodes_of(seqs)
+    fl_step = step_flops((V, d, H, L, F), nodes)
+    prof_total_ms = sum(v["ms"] for v in prof.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": "rollout tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: uniform random tokens (seed 3), prompt weights 0 / response weights 1; random-init N(0,0.02) weights",
+        "config": {"workload": f"{args.config}: {c['desc']}", "model": c["model"], "global_batch": len(all_seqs),
+                   "seq_len": c["prompt_len"] + c["resp_len"], "parallelism": f"dp{world}",
+                   "trees_per_gpu": c["prompts"], "sibling_batch": not args.no_sibling_batch,
+                   "l2": "step working set (weights + activations) >> 126 MB L2; no flush needed"},
+        "e2e": {"value": roll_total / (e2e_ms / 1e3) if e2e_ms else None, "unit": "rollout tokens/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
+                "includes": "host tree build + schedule/metadata upload (pinned) + execute + loss read"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": sust, "unit": "TFLOP/s",
+                     "frac": gemm_tflops / sust if sust else None, "traffic": None,
+                     "kernel": "tcgen05 GEMM (all projection/MLP/LM-head GEMMs of the step)",
+                     "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({src})",
+                     "gemm_share_of_step": gm["ms"] / prof_total_ms if prof_total_ms else None},
+        "step_model_tflops": fl_step / (ms / 1e3) / 1e12 * world,
+        "step_frac_of_peak": fl_step / (ms / 1e3) / 1e12 / sust,
+        "kernel_classes": {k: {"ms": v["ms"], "launches": v["launches"],
+                               "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
+                               "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None}
+                           for k, v in prof.items()},
+        "tree": {"tree_tokens": st["tree_tokens"], "rollout_tokens_per_gpu": roll_local, "nodes": st["num_nodes"],
+                 "duplication_factor": roll_local / st["tree_tokens"], "max_path_tokens": st["max_path_tokens"],
+                 "segment_batches": res.num_batches, "host_tree_build_s": build_s, "host_plan_s": plan_s},
+        "peak_hbm_gb": res.peak_hbm_bytes / 1e9,
+        "device_used_gb": (torch.cuda.mem_get_info()[1] - torch.cuda.mem_get_info()[0]) / 1e9,
+        "clocks": clocks,
+    }
+    # ---- flat per-sequence baseline on the same engine (packed varlen, no prefix sharing)
+    if not args.no_flat and world == 1:
+        eng.zero_gradients()
+        eng.dense_train_step(seqs)  # warm
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(ext)
+        eng.zero_gradients()
+        rf = eng.dense_train_step(seqs)
+        g1.record(ext)
+        torch.cuda.synchronize()
+        fms = g0.elapsed_time(g1)
+        line["flat"] = {"value": roll_total / (fms / 1e3), "unit": "rollout tokens/s", "ms_per_step": fms,
+                        "peak_hbm_gb": rf.peak_hbm_bytes / 1e9, "forward_tokens": rf.forward_tokens,
+                        "note": "same engine, every sequence its own root (no prefix sharing), packed varlen batches"}
+    # ---- CPU baseline (rank 0, N = 1 only)
+    if not args.no_cpu and world == 1 and rank == 0:
+        try:
+            from oracle import refimpl as R
+
+            if R.available():
+                threads = os.cpu_count() or 1
+                n_tok = 1 if L > 2 else 64
+                secs, fl = cpu_reference_sample(c["model"], c["prompt_len"], n_tok, threads)
+                rate = fl / secs[0]
+                cpu_val = rate / (fl_step / roll_local)
+                line["cpu_baseline"] = {
+                    "value": cpu_val, "unit": "rollout tokens/s", "cores": threads, "kind": "reference",
+                    "sample": f"reference forward_segment+weighted_nll+backward_segment (T=float) of {n_tok} token(s) at "
+                              f"prefix S={c['prompt_len']} on each of {threads} threads: {secs[0]:.1f} s, "
+                              f"{rate / 1e9:.2f} GFLOP/s; extrapolated to the step via the FLOP model"}
+            else:
+                line["cpu_baseline"] = {"value": None, "unit": "rollout tokens/s", "cores": 0, "kind": "reference",
+                                        "sample": "oracle/_ref not built"}
+        except Exception as e:  # the baseline is reported, never fatal
+            line["cpu_baseline"] = {"value": None, "unit": "rollout tokens/s", "cores": 0, "kind": "reference",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-flat", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-sibling-batch", action="store_true")
+    ap.add_argument("--batch-budget", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -76,6 +76,8 @@ typedef struct tt_step_result {
   uint64_t num_batches;      /* executed segment batches (== num_segments without batching) */
   uint64_t num_launches;     /* device kernel launches issued by the step */
   uint64_t peak_hbm_bytes;   /* engine static allocations + activation-arena high-water */
+  uint64_t h2d_bytes;        /* host->device bytes of the step (plan metadata: tokens, tables, loss CSR) */
+  uint64_t d2h_bytes;        /* device->host bytes of the step (the loss) */
 } tt_step_result;
 
 /* ------------------------------------------------------------------ prefix tree */
@@ -138,6 +140,23 @@ int tt_tree_train_step(tt_engine* eng, const tt_tree* tree, const tt_sched_confi
 /* dense_train_step: the flat per-sequence baseline on the same engine. */
 int tt_dense_train_step(tt_engine* eng, const int32_t* tokens, const uint64_t* offsets, const double* weights,
                         uint64_t n_seqs, tt_step_result* result);
+
+/* tree_train_step split in two: plan (DFS schedule, sibling batches, memory plan, metadata uploaded
+ * to HBM once) and execute (the device push/visit/pop pass). A plan may be executed many times;
+ * tt_tree_train_step == create + execute + destroy. The plan's logical PUSH/POP trace equals
+ * tt_tree_dfs_trace() of the tree. */
+typedef struct tt_step_plan tt_step_plan;
+int tt_plan_create(tt_engine* eng, const tt_tree* tree, const tt_sched_config* sched, tt_step_plan** out);
+int tt_plan_execute(tt_engine* eng, tt_step_plan* plan, tt_step_result* result);
+int tt_plan_trace(const tt_step_plan* plan, char* buf, uint64_t cap, uint64_t* len);
+int tt_plan_destroy(tt_step_plan* plan);
+
+/* Per-kernel-class device timing (CUDA events around every launch while enabled).
+ * Classes: 0 GEMM (tcgen05), 1 attention fwd, 2 attention bwd, 3 elementwise/stack, 4 CE.
+ * Arrays have TT_NUM_KCLASS entries: accumulated ms, algorithmic FLOPs, algorithmic bytes, launches. */
+#define TT_NUM_KCLASS 5
+int tt_engine_set_profiling(tt_engine* eng, int32_t on);
+int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset);
 
 /* ------------------------------------------------------------------ segment level (device KV stack)
  * forward_segment (model.hpp:328-463) continuing from the device stack (KVView of all pushed

@@ -11,6 +11,8 @@
 #include <treetrain/model.hpp>
 #include <treetrain/model_io.hpp>
 
+#include <algorithm>
+#include <barrier>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -333,19 +335,41 @@ int ttref_run_events_threads(const ttref_cfg* c, const double* params_flat, uint
   });
 }
 
-// CPU baseline at full model shape without a full tree: each of n_threads workers runs
+// CPU baseline at full model shape without a full tree: a model handle holds
+// init_params<float> (made once); each slice call runs, on each of n_threads workers,
 // forward_segment + weighted_nll + backward_segment of `len` tokens over a random prefix KV of
-// S rows, T=float. Returns wall seconds.
-int ttref_slice_bench(const ttref_cfg* c, uint64_t S, uint64_t len, int n_threads, uint64_t seed,
-                      double* seconds_out) {
+// S rows. Per-thread setup (prefix KV fill, GradientStore) happens before a barrier and is not
+// timed; returns the slowest worker's compute seconds.
+struct ttref_model {
+  ModelConfig cfg;
+  Parameters<float> params;
+};
+
+ttref_model* ttref_model_create(const ttref_cfg* c, uint64_t seed) {
+  try {
+    auto* m = new ttref_model;
+    m->cfg = to_cfg(c);
+    m->params = init_params<float>(m->cfg, seed);
+    return m;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ttref_model_destroy(ttref_model* m) { delete m; }
+
+int ttref_model_slice(ttref_model* m, uint64_t S, uint64_t len, int n_threads, uint64_t seed, double* seconds_out) {
   return guard([&] {
-    const ModelConfig cfg = to_cfg(c);
-    const Parameters<float> params = init_params<float>(cfg, seed);
+    const ModelConfig& cfg = m->cfg;
+    if (S + len > cfg.max_position) throw std::invalid_argument("slice exceeds max_position");
     std::vector<std::string> errs(n_threads);
-    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<double> secs(n_threads, 0.0);
+    std::barrier sync(n_threads);
     std::vector<std::thread> th;
     for (int i = 0; i < n_threads; ++i)
       th.emplace_back([&, i] {
+        bool arrived = false;
         try {
           std::mt19937_64 rng(seed + 17 * i + 1);
           std::normal_distribution<double> nd(0.0, 1.0);
@@ -360,26 +384,29 @@ int ttref_slice_bench(const ttref_cfg* c, uint64_t S, uint64_t len, int n_thread
           }
           KVView<float> view;
           view.push(seg);
-          std::vector<TokenId> tok(len);
+          std::vector<TokenId> tok(len), tg(len);
           for (auto& t : tok) t = TokenId(rng() % cfg.vocab_size);
-          ForwardResult<float> r = forward_segment(params, view, std::span<const TokenId>(tok), S, false, true);
-          std::vector<TokenId> tg(len);
-          std::vector<double> w(len, 1.0);
           for (auto& t : tg) t = TokenId(rng() % cfg.vocab_size);
-          LossResult<float> lr = weighted_nll(r.logits, std::span<const TokenId>(tg), std::span<const double>(w));
+          std::vector<double> w(len, 1.0);
           GradientStore<float> g = make_gradient_store<float>(cfg);
+          sync.arrive_and_wait();
+          arrived = true;
+          const auto t0 = std::chrono::steady_clock::now();
+          ForwardResult<float> r = forward_segment(m->params, view, std::span<const TokenId>(tok), S, false, true);
+          LossResult<float> lr = weighted_nll(r.logits, std::span<const TokenId>(tg), std::span<const double>(w));
           BackwardUpstream<float> up;
           up.grad_logits = &lr.grad_logits;
-          backward_segment(params, *r.activations, view, up, g);
+          backward_segment(m->params, *r.activations, view, up, g);
+          secs[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         } catch (const std::exception& e) {
           errs[i] = e.what();
+          if (!arrived) sync.arrive_and_drop();
         }
       });
     for (auto& t : th) t.join();
-    const auto t1 = std::chrono::steady_clock::now();
     for (auto& e : errs)
       if (!e.empty()) throw std::runtime_error(e);
-    *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+    *seconds_out = *std::max_element(secs.begin(), secs.end());
   });
 }
 

@@ -184,8 +184,28 @@ def run_events_threads(cfg, flat, events: EventList, n_threads: int):
     return secs.value, loss.value
 
 
-def slice_bench(cfg, S: int, n: int, threads: int, seed: int = 7) -> float:
-    secs = ctypes.c_double()
-    _check(lib().ttref_slice_bench(ctypes.byref(_cfg(cfg)), ctypes.c_uint64(S), ctypes.c_uint64(n),
-                                   ctypes.c_int(threads), ctypes.c_uint64(seed), ctypes.byref(secs)))
-    return secs.value
+class RefModel:
+    """init_params<float> of the reference held in C++ (made once), for repeated timed slices."""
+
+    def __init__(self, cfg: O.ModelConfig, seed: int = 7):
+        L = lib()
+        L.ttref_model_create.restype = ctypes.c_void_p
+        L.ttref_model_create.argtypes = [ctypes.POINTER(Cfg), ctypes.c_uint64]
+        L.ttref_model_destroy.argtypes = [ctypes.c_void_p]
+        L.ttref_model_slice.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
+                                        ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]
+        self.cfg = cfg
+        self._h = L.ttref_model_create(ctypes.byref(_cfg(cfg)), seed)
+        if not self._h:
+            raise RuntimeError(L.ttref_last_error().decode())
+
+    def slice(self, S: int, n: int, threads: int, seed: int = 7) -> float:
+        """Slowest worker's seconds for forward+NLL+backward of n tokens at prefix S, per thread."""
+        secs = ctypes.c_double()
+        _check(lib().ttref_model_slice(self._h, S, n, threads, seed, ctypes.byref(secs)))
+        return secs.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().ttref_model_destroy(self._h)
+            self._h = None

@@ -125,6 +125,8 @@ class TrainStepResult:
     num_batches: int
     num_launches: int
     peak_hbm_bytes: int
+    h2d_bytes: int
+    d2h_bytes: int
 
     @classmethod
     def _from(cls, r: _native.StepResultC):
@@ -216,6 +218,35 @@ def greedy_least_loaded(seqs: Sequence[TokenSequence], K: int, cost_model: str =
     return _plan(_native.lib().tt_greedy_least_loaded, seqs, K, 1 if cost_model == "raw_tokens" else 0)
 
 
+class StepPlan:
+    """tt_step_plan: a prepared tree step (tt_plan_create / tt_plan_execute)."""
+
+    def __init__(self, eng: "Engine", tree: PrefixTree, sched: SchedulerConfig):
+        self._eng = eng
+        self._tree = tree
+        h = ctypes.c_void_p()
+        _check(_native.lib().tt_plan_create(eng._h, tree._h, ctypes.byref(sched._c()), ctypes.byref(h)))
+        self._h = h
+
+    def execute(self) -> TrainStepResult:
+        r = _native.StepResultC()
+        _check(_native.lib().tt_plan_execute(self._eng._h, self._h, ctypes.byref(r)))
+        return TrainStepResult._from(r)
+
+    def trace(self) -> str:
+        n = ctypes.c_uint64()
+        _check(_native.lib().tt_plan_trace(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _check(_native.lib().tt_plan_trace(self._h, buf, n.value + 1, ctypes.byref(n)))
+        return buf.raw[: n.value].decode()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _native.lib().tt_plan_destroy(h)
+            self._h = None
+
+
 class Engine:
     """One B200 engine (weights, GradientStore, KV/dKV stacks, activation arena, one stream)."""
 
@@ -278,6 +309,24 @@ class Engine:
         r = _native.StepResultC()
         _check(_native.lib().tt_tree_train_step(self._h, tree._h, ctypes.byref(sched._c()), ctypes.byref(r)))
         return TrainStepResult._from(r)
+
+    def plan(self, tree: PrefixTree, sched: Optional[SchedulerConfig] = None) -> "StepPlan":
+        """Prepare a tree step once (schedule + metadata resident in HBM); execute it many times."""
+        return StepPlan(self, tree, sched or SchedulerConfig())
+
+    KCLASSES = ("gemm", "attn_fwd", "attn_bwd", "elementwise", "ce")
+
+    def set_profiling(self, on: bool) -> None:
+        _check(_native.lib().tt_engine_set_profiling(self._h, int(on)))
+
+    def profile(self, reset: bool = True):
+        n = len(self.KCLASSES)
+        ms, fl, by = (np.zeros(n) for _ in range(3))
+        la = np.zeros(n, dtype=np.uint64)
+        _check(_native.lib().tt_engine_profile(self._h, _ptr(ms, ctypes.c_double), _ptr(fl, ctypes.c_double),
+                                               _ptr(by, ctypes.c_double), _ptr(la, ctypes.c_uint64), int(reset)))
+        return {k: dict(ms=float(ms[i]), flops=float(fl[i]), bytes=float(by[i]), launches=int(la[i]))
+                for i, k in enumerate(self.KCLASSES)}
 
     def dense_train_step(self, seqs: Sequence[TokenSequence]) -> TrainStepResult:
         tok, off, w = _csr(seqs)

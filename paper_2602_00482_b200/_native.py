@@ -28,7 +28,7 @@ class StepResultC(c.Structure):
     _fields_ = [("total_loss", f64)] + [(n, u64) for n in (
         "forward_tokens", "recompute_tokens", "backward_tokens", "peak_live_kv_tokens",
         "peak_live_activation_tokens", "num_segments", "num_chunks", "rollout_tokens", "num_batches",
-        "num_launches", "peak_hbm_bytes")]
+        "num_launches", "peak_hbm_bytes", "h2d_bytes", "d2h_bytes")]
 
 
 EXPORTS = {
@@ -55,6 +55,12 @@ EXPORTS = {
     "tt_grads_accum_count": [vp, P(u64)],
     "tt_tree_train_step": [vp, vp, P(SchedConfigC), P(StepResultC)],
     "tt_dense_train_step": [vp, P(i32), P(u64), P(f64), u64, P(StepResultC)],
+    "tt_plan_create": [vp, vp, P(SchedConfigC), P(vp)],
+    "tt_plan_execute": [vp, vp, P(StepResultC)],
+    "tt_plan_trace": [vp, c.c_char_p, u64, P(u64)],
+    "tt_plan_destroy": [vp],
+    "tt_engine_set_profiling": [vp, i32],
+    "tt_engine_profile": [vp, P(f64), P(f64), P(f64), P(u64), i32],
     "tt_segment_push": [vp, P(i32), u64, P(c.c_float)],
     "tt_segment_pop": [vp, P(c.c_float), P(c.c_float)],
     "tt_stack_reset": [vp],

@@ -15,7 +15,9 @@ struct tt_tree {
 };
 struct tt_engine {
   std::unique_ptr<ttb::Engine> e;
-  std::string last_trace;
+};
+struct tt_step_plan {
+  std::unique_ptr<ttb::StepPlan> p;
 };
 
 namespace {
@@ -258,6 +260,59 @@ int tt_dense_train_step(tt_engine* eng, const int32_t* tokens, const uint64_t* o
     sc.batch_token_budget = 65536;
     tt_step_result r = eng->e->train_step(flat, sc);
     if (result) *result = r;
+  });
+}
+
+int tt_plan_create(tt_engine* eng, const tt_tree* tree, const tt_sched_config* sched, tt_step_plan** out) {
+  return ttb::guarded([&] {
+    need(eng, "engine");
+    need(tree, "tree");
+    need(sched, "sched");
+    need(out, "out");
+    auto p = std::make_unique<tt_step_plan>();
+    p->p = eng->e->prepare(tree->t, *sched);
+    *out = p.release();
+  });
+}
+
+int tt_plan_execute(tt_engine* eng, tt_step_plan* plan, tt_step_result* result) {
+  return ttb::guarded([&] {
+    need(eng, "engine");
+    need(plan, "plan");
+    tt_step_result r = eng->e->execute(*plan->p);
+    if (result) *result = r;
+  });
+}
+
+int tt_plan_trace(const tt_step_plan* plan, char* buf, uint64_t cap, uint64_t* len) {
+  return ttb::guarded([&] {
+    need(plan, "plan");
+    copy_out(plan->p->trace, buf, cap, len);
+  });
+}
+
+int tt_plan_destroy(tt_step_plan* plan) {
+  return ttb::guarded([&] { delete plan; });
+}
+
+int tt_engine_set_profiling(tt_engine* eng, int32_t on) {
+  return ttb::guarded([&] {
+    need(eng, "engine");
+    eng->e->set_profiling(on != 0);
+  });
+}
+
+int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset) {
+  return ttb::guarded([&] {
+    need(eng, "engine");
+    const ttb::KStats& k = eng->e->kstats();
+    for (int i = 0; i < TT_NUM_KCLASS; ++i) {
+      if (ms) ms[i] = k.ms[i];
+      if (flops) flops[i] = k.flops[i];
+      if (bytes) bytes[i] = k.bytes[i];
+      if (launches) launches[i] = k.launches[i];
+    }
+    if (reset) eng->e->reset_kstats();
   });
 }
 

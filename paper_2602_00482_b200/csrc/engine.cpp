@@ -340,36 +340,80 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
   b.o_pw = put(b.pair_w.data(), b.pair_w.size() * 8);
 }
 
+
+size_t Engine::upload_staged(const std::vector<char>& host, DevBuf& dst) {
+  const size_t bytes = std::max(host.size(), kAlign);
+  dst.ensure(bytes);
+  ck(cudaStreamSynchronize(stream_), "meta staging");
+  if (bytes > meta_host_cap_) {
+    if (meta_host_) cudaFreeHost(meta_host_);
+    meta_host_ = nullptr;
+    ck(cudaMallocHost(&meta_host_, bytes), "cudaMallocHost meta");
+    meta_host_cap_ = bytes;
+  }
+  if (!host.empty()) {
+    std::memcpy(meta_host_, host.data(), host.size());
+    ck(cudaMemcpyAsync(dst.p, meta_host_, host.size(), cudaMemcpyHostToDevice, stream_), "meta upload");
+  }
+  return host.size();
+}
+
 void Engine::upload_meta(std::vector<Batch*>& batches) {
   std::vector<char> host;
   size_t cursor = 0;
   for (Batch* b : batches) build_meta(*b, cursor, host);
-  if (cursor == 0) cursor = kAlign;
-  meta_.ensure(cursor);
-  if (cursor > meta_host_cap_) {
-    ck(cudaStreamSynchronize(stream_), "meta staging");
-    if (meta_host_) cudaFreeHost(meta_host_);
-    ck(cudaMallocHost(&meta_host_, cursor), "cudaMallocHost meta");
-    meta_host_cap_ = cursor;
-  } else {
-    ck(cudaStreamSynchronize(stream_), "meta staging");
+  upload_staged(host, meta_);
+  cur_meta_ = meta_.as<char>();
+}
+
+cudaEvent_t Engine::event() {
+  if (event_next_ == event_pool_.size()) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    event_pool_.push_back(e);
   }
-  std::memcpy(meta_host_, host.data(), host.size());
-  ck(cudaMemcpyAsync(meta_.p, meta_host_, cursor, cudaMemcpyHostToDevice, stream_), "meta upload");
+  return event_pool_[event_next_++];
+}
+
+void Engine::collect_profile() {
+  for (auto& p : pending_) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, p.a, p.b), "cudaEventElapsedTime");
+    kstats_.ms[p.cls] += ms;
+    kstats_.flops[p.cls] += p.flops;
+    kstats_.bytes[p.cls] += p.bytes;
+    kstats_.launches[p.cls] += 1;
+  }
+  pending_.clear();
+  event_next_ = 0;
+}
+
+// GEMM launch: algorithmic FLOPs 2MNK; algorithmic bytes = operands once + output (x2 if RMW).
+void Engine::gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& e, int splits) {
+  double out_b = 2.0;
+  if (e.mode == EPI_STORE_F32) out_b = 4.0;
+  if (e.mode == EPI_ADD_F32 || e.mode == EPI_RESID_F32) out_b = 8.0;
+  if (e.mode == EPI_SILU || e.mode == EPI_DSILU) out_b = 4.0;
+  const double bytes = 2.0 * (double(M) * K + double(N) * K) + out_b * double(M) * N;
+  run(KC_GEMM, 2.0 * M * N * K, bytes, [&] { gemm_bf16(A, B, M, N, K, e, splits, stream_); });
 }
 
 // ----------------------------------------------------------------------------- push (forward_segment)
 void Engine::forward_batch(const Batch& b) {
   const int n = static_cast<int>(b.n);
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
+  const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);
   char* base = arena_.as<char>(b.arena_off);
-  auto X = [&](int64_t l) { return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x); };
+  auto X = [&](int64_t l) {
+    return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x);
+  };
   const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
   const float scale = 1.0f / std::sqrt(static_cast<float>(dh_));  // model.hpp:345
 
-  k_embed_pe(meta<int32_t>(b.o_tok), meta<int32_t>(b.o_pos), emb_, pe_.as<float>(), X(0), n, d, stream_);
-  count();
+  run(KC_ELEMWISE, 0, nd * 10, [&] {
+    k_embed_pe(meta<int32_t>(b.o_tok), meta<int32_t>(b.o_pos), emb_, pe_.as<float>(), X(0), n, d, stream_);
+  });
   for (int64_t l = 0; l < L_; ++l) {
     char* Lb = base + l * lay.per_layer;
     float* inv1 = reinterpret_cast<float*>(Lb + lay.inv1);
@@ -385,8 +429,8 @@ void Engine::forward_batch(const Batch& b) {
     bf16* K = kst_.as<bf16>() + l * kv_layer;
     bf16* Vv = vst_.as<bf16>() + l * kv_layer;
 
-    k_rmsnorm_fwd(X(l), attn_g_[l], inv1, n1, n, d, stream_);  // model.hpp:376-380
-    {  // q,k,v = normed W{q,k,v}; k,v written straight onto the stack rows [S, S+n)
+    run(KC_ELEMWISE, 0, nd * 6, [&] { k_rmsnorm_fwd(X(l), attn_g_[l], inv1, n1, n, d, stream_); });  // :376-380
+    {  // q,k,v = normed W{q,k,v}; k,v written straight onto the stack rows [S, S+n)  (:381-384)
       EpiParams e;
       e.mode = EPI_STORE_BF16;
       e.split_w = d;
@@ -394,9 +438,9 @@ void Engine::forward_batch(const Batch& b) {
       e.out[1] = K + b.S * d_;
       e.out[2] = Vv + b.S * d_;
       e.ldo[0] = e.ldo[1] = e.ldo[2] = d;
-      gemm_bf16(op(n1, d, false), op(wqkv_[l], 3 * d, true), n, 3 * d, d, e, 1, stream_);
+      gemm(op(n1, d, false), op(wqkv_[l], 3 * d, true), n, 3 * d, d, e, 1);
     }
-    {
+    {  // segment attention over the stack (:386-408)
       AttnFwdArgs a;
       a.q = q;
       a.ldq = d;
@@ -413,91 +457,113 @@ void Engine::forward_batch(const Batch& b) {
       a.qblocks = meta<int4>(b.o_qblk);
       a.nqb = static_cast<int>(b.qblk.size() / 4);
       a.scale = scale;
-      attn_fwd(a, stream_);
+      run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd(a, stream_); });
     }
-    {  // x_mid = x + attn W_o  (model.hpp:410-411,427-428)
+    {  // x_mid = x + attn W_o  (:410-411,427-428)
       EpiParams e;
       e.mode = EPI_RESID_F32;
       e.out[0] = xmid;
       e.ldo[0] = d;
       e.resid = X(l);
       e.ld_resid = d;
-      gemm_bf16(op(attn, d, false), op(wo_[l], d, true), n, d, d, e, 1, stream_);
+      gemm(op(attn, d, false), op(wo_[l], d, true), n, d, d, e, 1);
     }
-    k_rmsnorm_fwd(xmid, mlp_g_[l], inv2, n2, n, d, stream_);  // model.hpp:430-434
-    {  // h = normed W_in, act = silu(h)  (model.hpp:435-444)
+    run(KC_ELEMWISE, 0, nd * 6, [&] { k_rmsnorm_fwd(xmid, mlp_g_[l], inv2, n2, n, d, stream_); });  // :430-434
+    {  // h = normed W_in, act = silu(h)  (:435-444)
       EpiParams e;
       e.mode = EPI_SILU;
       e.out[0] = h;
       e.ldo[0] = F;
       e.out2 = act;
       e.ldo2 = F;
-      gemm_bf16(op(n2, d, false), op(win_[l], F, true), n, F, d, e, 1, stream_);
+      gemm(op(n2, d, false), op(win_[l], F, true), n, F, d, e, 1);
     }
-    {  // x_out = x_mid + act W_out  (model.hpp:445-448)
+    {  // x_out = x_mid + act W_out  (:445-448)
       EpiParams e;
       e.mode = EPI_RESID_F32;
       e.out[0] = X(l + 1);
       e.ldo[0] = d;
       e.resid = xmid;
       e.ld_resid = d;
-      gemm_bf16(op(act, F, false), op(wout_[l], d, true), n, d, F, e, 1, stream_);
+      gemm(op(act, F, false), op(wout_[l], d, true), n, d, F, e, 1);
     }
-    count(7);
   }
-  k_rmsnorm_fwd(X(L_), final_g_, reinterpret_cast<float*>(base + lay.invf), reinterpret_cast<bf16*>(base + lay.nf), n, d,
-                stream_);  // model.hpp:451-455
-  count();
+  run(KC_ELEMWISE, 0, nd * 6, [&] {  // final norm (:451-455)
+    k_rmsnorm_fwd(X(L_), final_g_, reinterpret_cast<float*>(base + lay.invf), reinterpret_cast<bf16*>(base + lay.nf),
+                  n, d, stream_);
+  });
 }
 
-// ----------------------------------------------------------------------------- head + loss (visit)
-void Engine::head_backward(const Batch& b, const bf16* nf, const ActLayout& lay, char* base) {
-  (void)lay;
-  (void)base;
+// ----------------------------------------------------------------------------- visit: LM head + weighted CE
+// For every loss row (compacted): logits = c W_head (fp32), CE -> loss (fp64) and dlogits (bf16),
+// dW_head += c^T dlogits, grad_c = dlogits W_head^T scattered back to the batch rows.
+void Engine::head_backward(const Batch& b, const bf16* nf) {
   const int d = static_cast<int>(d_);
-  const long V = V_;
+  const int V = static_cast<int>(V_);
   float* gxf = sc_gxf_.as<float>();
-  const int64_t m = b.full_logits ? b.n : static_cast<int64_t>(b.loss_rows.size());
+  const int64_t m = static_cast<int64_t>(b.loss_rows.size());
+  bf16* dlog = sc_dlog_.as<bf16>();
+  bf16* nfl = sc_nfl_.as<bf16>();
+  float* gnf = sc_gnf_.as<float>();
   for (int64_t c0 = 0; c0 < m; c0 += head_chunk_) {
     const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, m - c0));
-    const bf16* rows = nf + c0 * d_;
-    bf16* dlog = sc_dlog_.as<bf16>();
-    if (!b.full_logits) {
-      bf16* nfl = sc_nfl_.as<bf16>();
-      k_gather_rows_bf16(nf, meta<int32_t>(b.o_lrows) + c0, nfl, cm, d, stream_);
-      rows = nfl;
+    run(KC_ELEMWISE, 0, 4.0 * cm * d, [&] { k_gather_rows_bf16(nf, meta<int32_t>(b.o_lrows) + c0, nfl, cm, d, stream_); });
+    {
       EpiParams e;  // logits = normed_final W_head (model.hpp:460-461), fp32
       e.mode = EPI_STORE_F32;
       e.out[0] = sc_logits_.p;
       e.ldo[0] = V;
-      gemm_bf16(op(rows, d, false), op(head_, V, true), cm, static_cast<int>(V), d, e, 1, stream_);
-      k_ce(sc_logits_.as<float>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt),
-           meta<double>(b.o_pw), dlog, loss_.as<double>(), stream_);
-      count(3);
+      gemm(op(nfl, d, false), op(head_, V, true), cm, V, d, e, 1);
     }
+    run(KC_CE, 0, 6.0 * cm * V, [&] {  // weighted_nll (model.hpp:643-677), multi-target rows
+      k_ce(sc_logits_.as<float>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt), meta<double>(b.o_pw),
+           dlog, loss_.as<double>(), stream_);
+    });
     {  // dW_head += c^T dlogits  (model.hpp:506)
       EpiParams e;
       e.mode = EPI_ADD_F32;
       e.out[0] = g_head_;
       e.ldo[0] = V;
-      gemm_bf16(op(rows, d, true), op(dlog, V, true), d, static_cast<int>(V), cm, e,
-                gemm_choose_splits(d, static_cast<int>(V), cm), stream_);
+      gemm(op(nfl, d, true), op(dlog, V, true), d, V, cm, e, gemm_choose_splits(d, V, cm));
     }
     {  // grad_c = dlogits W_head^T  (model.hpp:507-508)
-      float* gnf = b.full_logits ? gxf + c0 * d_ : sc_gnf_.as<float>();
       ck(cudaMemsetAsync(gnf, 0, static_cast<size_t>(cm) * d_ * 4, stream_), "memset");
       EpiParams e;
       e.mode = EPI_ADD_F32;
       e.out[0] = gnf;
       e.ldo[0] = d;
-      gemm_bf16(op(dlog, V, false), op(head_, V, false), cm, d, static_cast<int>(V), e,
-                gemm_choose_splits(cm, d, static_cast<int>(V)), stream_);
-      if (!b.full_logits) {
-        k_scatter_rows_f32(gnf, meta<int32_t>(b.o_lrows) + c0, gxf, cm, d, stream_);
-        count();
-      }
+      gemm(op(dlog, V, false), op(head_, V, false), cm, d, V, e, gemm_choose_splits(cm, d, V));
     }
-    count(2);
+    run(KC_ELEMWISE, 0, 8.0 * cm * d, [&] { k_scatter_rows_f32(gnf, meta<int32_t>(b.o_lrows) + c0, gxf, cm, d, stream_); });
+  }
+}
+
+// Segment API: caller-provided upstream grad_logits [n x V] (BackwardUpstream, model.hpp:465-469).
+void Engine::head_backward_dense(const Batch& b, const bf16* nf, const float* host_grad_logits) {
+  const int d = static_cast<int>(d_);
+  const int V = static_cast<int>(V_);
+  float* gxf = sc_gxf_.as<float>();
+  bf16* dlog = sc_dlog_.as<bf16>();
+  for (int64_t c0 = 0; c0 < b.n; c0 += head_chunk_) {
+    const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, b.n - c0));
+    ck(cudaMemcpyAsync(sc_logits_.p, host_grad_logits + c0 * V_, static_cast<size_t>(cm) * V_ * 4,
+                       cudaMemcpyHostToDevice, stream_),
+       "grad_logits upload");
+    run(KC_ELEMWISE, 0, 6.0 * cm * V, [&] { k_f32_to_bf16_2d(sc_logits_.as<float>(), V, dlog, V, cm, V, stream_); });
+    {
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.out[0] = g_head_;
+      e.ldo[0] = V;
+      gemm(op(nf + c0 * d_, d, true), op(dlog, V, true), d, V, cm, e, gemm_choose_splits(d, V, cm));
+    }
+    {
+      EpiParams e;
+      e.mode = EPI_ADD_F32;
+      e.out[0] = gxf + c0 * d_;
+      e.ldo[0] = d;
+      gemm(op(dlog, V, false), op(head_, V, false), cm, d, V, e, gemm_choose_splits(cm, d, V));
+    }
   }
 }
 
@@ -505,9 +571,12 @@ void Engine::head_backward(const Batch& b, const bf16* nf, const ActLayout& lay,
 void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
   const int n = static_cast<int>(b.n);
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
+  const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);
   char* base = arena_.as<char>(b.arena_off);
-  auto X = [&](int64_t l) { return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x); };
+  auto X = [&](int64_t l) {
+    return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x);
+  };
   const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
   const float scale = 1.0f / std::sqrt(static_cast<float>(dh_));
   float* gx = sc_gx_.as<float>();
@@ -522,40 +591,14 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
 
   ck(cudaMemsetAsync(gxf, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
   if (b.full_logits) {
-    if (host_grad_logits) {  // caller-provided upstream grad_logits [n x V] (BackwardUpstream, model.hpp:465-469)
-      for (int64_t c0 = 0; c0 < b.n; c0 += head_chunk_) {
-        const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, b.n - c0));
-        ck(cudaMemcpyAsync(sc_logits_.p, host_grad_logits + c0 * V_, static_cast<size_t>(cm) * V_ * 4,
-                           cudaMemcpyHostToDevice, stream_),
-           "grad_logits upload");
-        bf16* dlog = sc_dlog_.as<bf16>();
-        k_f32_to_bf16_2d(sc_logits_.as<float>(), V_, dlog, V_, cm, static_cast<int>(V_), stream_);
-        {  // dW_head += c^T dlogits  (model.hpp:506)
-          EpiParams e;
-          e.mode = EPI_ADD_F32;
-          e.out[0] = g_head_;
-          e.ldo[0] = V_;
-          gemm_bf16(op(nf + c0 * d_, d, true), op(dlog, V_, true), d, static_cast<int>(V_), cm, e,
-                    gemm_choose_splits(d, static_cast<int>(V_), cm), stream_);
-        }
-        {  // grad_c = dlogits W_head^T  (model.hpp:507-508)
-          EpiParams e;
-          e.mode = EPI_ADD_F32;
-          e.out[0] = gxf + c0 * d_;
-          e.ldo[0] = d;
-          gemm_bf16(op(dlog, V_, false), op(head_, V_, false), cm, d, static_cast<int>(V_), e,
-                    gemm_choose_splits(cm, d, static_cast<int>(V_)), stream_);
-        }
-        count(3);
-      }
-    }
+    if (host_grad_logits) head_backward_dense(b, nf, host_grad_logits);
   } else {
-    head_backward(b, nf, lay, base);
+    head_backward(b, nf);
   }
-  // final-norm backward (model.hpp:509-511)
-  k_rmsnorm_bwd(gxf, X(L_), reinterpret_cast<const float*>(base + lay.invf), final_g_, nullptr, gx, gxb, g_final_g_,
-                n, d, stream_);
-  count();
+  run(KC_ELEMWISE, 0, nd * 14, [&] {  // final-norm backward (model.hpp:509-511)
+    k_rmsnorm_bwd(gxf, X(L_), reinterpret_cast<const float*>(base + lay.invf), final_g_, nullptr, gx, gxb, g_final_g_,
+                  n, d, stream_);
+  });
 
   for (int64_t l = L_ - 1; l >= 0; --l) {
     char* Lb = base + l * lay.per_layer;
@@ -579,7 +622,7 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
       e.mode = EPI_ADD_F32;
       e.out[0] = g_wout_[l];
       e.ldo[0] = d;
-      gemm_bf16(op(act, F, true), op(gxb, d, true), F, d, n, e, gemm_choose_splits(F, d, n), stream_);
+      gemm(op(act, F, true), op(gxb, d, true), F, d, n, e, gemm_choose_splits(F, d, n));
     }
     {  // grad_hidden = (gx W_out^T) * silu'(h)  (model.hpp:525-528)
       EpiParams e;
@@ -588,37 +631,38 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
       e.ldo[0] = F;
       e.aux = h;
       e.ld_aux = F;
-      gemm_bf16(op(gxb, d, false), op(wout_[l], d, false), n, F, d, e, 1, stream_);
+      gemm(op(gxb, d, false), op(wout_[l], d, false), n, F, d, e, 1);
     }
     {  // dW_in += normed2^T grad_hidden  (model.hpp:533)
       EpiParams e;
       e.mode = EPI_ADD_F32;
       e.out[0] = g_win_[l];
       e.ldo[0] = F;
-      gemm_bf16(op(n2, d, true), op(gh, F, true), d, F, n, e, gemm_choose_splits(d, F, n), stream_);
+      gemm(op(n2, d, true), op(gh, F, true), d, F, n, e, gemm_choose_splits(d, F, n));
     }
     {  // grad_normed2 = grad_hidden W_in^T  (model.hpp:535)
       EpiParams e;
       e.mode = EPI_STORE_F32;
       e.out[0] = gn;
       e.ldo[0] = d;
-      gemm_bf16(op(gh, F, false), op(win_[l], F, false), n, d, F, e, 1, stream_);
+      gemm(op(gh, F, false), op(win_[l], F, false), n, d, F, e, 1);
     }
-    // gx_mid = gx + rmsnorm_bwd (model.hpp:536-539)
-    k_rmsnorm_bwd(gn, xmid, inv2, mlp_g_[l], gx, gx, gxb, g_mlp_g_[l], n, d, stream_);
+    run(KC_ELEMWISE, 0, nd * 18, [&] {  // gx_mid = gx + rmsnorm_bwd (model.hpp:536-539)
+      k_rmsnorm_bwd(gn, xmid, inv2, mlp_g_[l], gx, gx, gxb, g_mlp_g_[l], n, d, stream_);
+    });
     {  // dW_o += attn^T gx_mid  (model.hpp:542)
       EpiParams e;
       e.mode = EPI_ADD_F32;
       e.out[0] = g_wo_[l];
       e.ldo[0] = d;
-      gemm_bf16(op(attn, d, true), op(gxb, d, true), d, d, n, e, gemm_choose_splits(d, d, n), stream_);
+      gemm(op(attn, d, true), op(gxb, d, true), d, d, n, e, gemm_choose_splits(d, d, n));
     }
     {  // grad_attn = gx_mid W_o^T  (model.hpp:543-544)
       EpiParams e;
       e.mode = EPI_STORE_BF16;
       e.out[0] = dO;
       e.ldo[0] = d;
-      gemm_bf16(op(gxb, d, false), op(wo_[l], d, false), n, d, d, e, 1, stream_);
+      gemm(op(gxb, d, false), op(wo_[l], d, false), n, d, d, e, 1);
     }
     // attention backward (model.hpp:546-604): dQ, and dK/dV added into the stack rows [0, S+n)
     ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
@@ -646,10 +690,11 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
       a.items2 = meta<int2>(b.o_kvit2);
       a.nitems = static_cast<int>(b.kvit.size() / 4);
       a.scale = scale;
-      attn_bwd(a, stream_);
+      run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] { attn_bwd(a, stream_); });
+      ++launches_;  // the D = rowsum(dO*O) pre-pass inside attn_bwd
     }
-    // pop: consume this batch's dK/dV rows (children + own), zero them for reuse
-    k_pack_dqkv(dq, dK + b.S * d_, dV + b.S * d_, dqkv, n, d, stream_);
+    // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
+    run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.S * d_, dV + b.S * d_, dqkv, n, d, stream_); });
     {  // dW_{q,k,v} += normed1^T [dq | dk | dv]  (model.hpp:610-612)
       EpiParams e;
       e.mode = EPI_ADD_F32;
@@ -658,38 +703,41 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
       e.out[1] = g_wk_[l];
       e.out[2] = g_wv_[l];
       e.ldo[0] = e.ldo[1] = e.ldo[2] = d;
-      gemm_bf16(op(n1, d, true), op(dqkv, 3 * d, true), d, 3 * d, n, e, gemm_choose_splits(d, 3 * d, n), stream_);
+      gemm(op(n1, d, true), op(dqkv, 3 * d, true), d, 3 * d, n, e, gemm_choose_splits(d, 3 * d, n));
     }
     {  // grad_normed1 = dq W_q^T + dk W_k^T + dv W_v^T  (model.hpp:613-618)
       EpiParams e;
       e.mode = EPI_STORE_F32;
       e.out[0] = gn;
       e.ldo[0] = d;
-      gemm_bf16(op(dqkv, 3 * d, false), op(wqkv_[l], 3 * d, false), n, d, 3 * d, e, 1, stream_);
+      gemm(op(dqkv, 3 * d, false), op(wqkv_[l], 3 * d, false), n, d, 3 * d, e, 1);
     }
-    // gx = gx_mid + rmsnorm_bwd (model.hpp:620-624)
-    k_rmsnorm_bwd(gn, X(l), inv1, attn_g_[l], gx, gx, gxb, g_attn_g_[l], n, d, stream_);
-    count(14);
+    run(KC_ELEMWISE, 0, nd * 18, [&] {  // gx = gx_mid + rmsnorm_bwd (model.hpp:620-624)
+      k_rmsnorm_bwd(gn, X(l), inv1, attn_g_[l], gx, gx, gxb, g_attn_g_[l], n, d, stream_);
+    });
   }
-  k_embed_grad(gx, meta<int32_t>(b.o_tok), g_emb_, n, d, stream_);  // model.hpp:627-630
-  count();
+  run(KC_ELEMWISE, 0, nd * 12, [&] { k_embed_grad(gx, meta<int32_t>(b.o_tok), g_emb_, n, d, stream_); });  // :627-630
   accum_count_ += b.nodes.empty() ? 1 : b.nodes.size();
 }
 
 // ----------------------------------------------------------------------------- tree_train_step
-tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config& sc) {
-  if (!seg_stack_.empty()) throw std::runtime_error("train_step: segment stack is not empty");
+std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched_config& sc) {
   if (sc.chunk_len != 0) {
     // chunked backward is not implemented on device yet: only accept chunk_len >= every segment
-    for (auto& nd : tree.nodes)
-      if (nd.tokens.size() > sc.chunk_len)
+    for (size_t u = 1; u < tree.nodes.size(); ++u)
+      if (tree.nodes[u].tokens.size() > sc.chunk_len)
         throw std::invalid_argument("tree_train_step: chunk_len smaller than a segment is not supported yet");
   }
   if (tree.nodes[0].max_path_below > cfg_.max_position)
     throw std::invalid_argument("tree_train_step: path exceeds max_position");
-  // ---- plan: batches + PUSH/POP op list in DFS order
-  std::vector<Batch> batches;
-  std::vector<std::pair<int, bool>> ops;  // (batch, is_push)
+  auto plan = std::make_unique<StepPlan>();
+  auto& batches = plan->batches;
+  auto& ops = plan->ops;
+  const auto pre = preorder(tree);
+  std::vector<int32_t> pid(tree.nodes.size(), -1);
+  for (size_t i = 0; i < pre.size(); ++i) pid[pre[i]] = static_cast<int32_t>(i);
+
+  // ---- batches + PUSH/POP op list in DFS order
   auto make_batch = [&](const std::vector<int32_t>& members, int64_t S) {
     Batch b;
     b.S = S;
@@ -697,14 +745,15 @@ tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config&
     int64_t off = 0;
     for (int32_t u : members) {
       const auto& nd = tree.nodes[u];
+      const int64_t len = static_cast<int64_t>(nd.tokens.size());
       b.seg_off.push_back(off);
-      b.seg_len.push_back(static_cast<int64_t>(nd.tokens.size()));
-      for (size_t t = 0; t < nd.tokens.size(); ++t) {
+      b.seg_len.push_back(len);
+      b.attn_ctx += double(len) * double(S) + 0.5 * double(len) * double(len + 1);
+      for (int64_t t = 0; t < len; ++t) {
         b.tokens.push_back(nd.tokens[t]);
         b.positions.push_back(static_cast<int32_t>(S + t));
       }
-      LossPairs lp = node_loss_pairs(tree, u, S);
-      // rows within a node are non-decreasing in node_loss_pairs; build the batch CSR
+      LossPairs lp = node_loss_pairs(tree, u, S);  // rows are non-decreasing within a node
       for (size_t k = 0; k < lp.rows.size(); ++k) {
         const int32_t row = static_cast<int32_t>(off + lp.rows[k]);
         if (b.loss_rows.empty() || b.loss_rows.back() != row) {
@@ -714,56 +763,59 @@ tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config&
         b.pair_tgt.push_back(lp.targets[k]);
         b.pair_w.push_back(lp.weights[k]);
       }
-      off += static_cast<int64_t>(nd.tokens.size());
+      off += len;
     }
     b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
     b.n = off;
     batches.push_back(std::move(b));
     return static_cast<int>(batches.size() - 1);
   };
+  std::string& trace = plan->trace;
   std::function<void(int32_t, int64_t)> visit = [&](int32_t u, int64_t S) {
     const auto& ch = tree.nodes[u].children;
     size_t i = 0;
     while (i < ch.size()) {
       const int32_t c = ch[i];
       if (sc.sibling_batch && tree.nodes[c].children.empty()) {
-        std::vector<int32_t> run = {c};
+        std::vector<int32_t> run_nodes = {c};
         uint64_t tok = tree.nodes[c].tokens.size();
         size_t j = i + 1;
         while (j < ch.size() && tree.nodes[ch[j]].children.empty() &&
                (sc.batch_token_budget == 0 || tok + tree.nodes[ch[j]].tokens.size() <= sc.batch_token_budget)) {
           tok += tree.nodes[ch[j]].tokens.size();
-          run.push_back(ch[j++]);
+          run_nodes.push_back(ch[j++]);
         }
-        const int bi = make_batch(run, S);
+        const int bi = make_batch(run_nodes, S);
         ops.push_back({bi, true});
         ops.push_back({bi, false});
+        for (int32_t m : run_nodes) trace += "PUSH " + std::to_string(pid[m]) + "\nPOP " + std::to_string(pid[m]) + "\n";
         i = j;
       } else {
         const int bi = make_batch({c}, S);
         ops.push_back({bi, true});
+        trace += "PUSH " + std::to_string(pid[c]) + "\n";
         visit(c, S + static_cast<int64_t>(tree.nodes[c].tokens.size()));
         ops.push_back({bi, false});
+        trace += "POP " + std::to_string(pid[c]) + "\n";
         ++i;
       }
     }
   };
   visit(0, 0);
 
-  // ---- memory plan: LIFO arena offsets, stack rows, scratch sizes
-  tt_step_result res{};
-  int64_t rows = 0, max_n = 0, max_loss = 0;
-  size_t top = 0, peak = 0;
+  // ---- memory plan: LIFO arena offsets, stack rows, scratch sizes, counters
+  tt_step_result& res = plan->counters;
+  size_t top = 0;
   uint64_t live_tok = 0, peak_tok = 0;
   for (auto& [bi, push] : ops) {
     Batch& b = batches[bi];
     if (push) {
       b.arena_off = top;
       top += align_up(layout(b.n).total);
-      peak = std::max(peak, top);
-      rows = std::max<int64_t>(rows, b.S + b.n);
-      max_n = std::max<int64_t>(max_n, b.n);
-      max_loss = std::max<int64_t>(max_loss, static_cast<int64_t>(b.loss_rows.size()));
+      plan->arena_peak = std::max(plan->arena_peak, top);
+      plan->rows = std::max<int64_t>(plan->rows, b.S + b.n);
+      plan->max_n = std::max<int64_t>(plan->max_n, b.n);
+      plan->max_loss = std::max<int64_t>(plan->max_loss, static_cast<int64_t>(b.loss_rows.size()));
       live_tok += b.n;
       peak_tok = std::max(peak_tok, live_tok);
       res.forward_tokens += b.n;
@@ -775,36 +827,51 @@ tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config&
       res.backward_tokens += b.n;
     }
   }
-  ensure_capacity(rows, peak, max_n, max_loss);
-  std::vector<Batch*> ptrs;
-  for (auto& b : batches) ptrs.push_back(&b);
-  upload_meta(ptrs);
+  res.peak_live_kv_tokens = static_cast<uint64_t>(plan->rows);
+  res.peak_live_activation_tokens = peak_tok;
+  res.num_chunks = res.num_segments;
+  for (auto& s : tree.seq_tokens) res.rollout_tokens += s.size();
+  // ---- metadata for every batch, resident in HBM for the plan's lifetime
+  std::vector<char> host;
+  size_t cursor = 0;
+  for (auto& b : batches) build_meta(b, cursor, host);
+  plan->meta_bytes = upload_staged(host, plan->meta);
+  res.h2d_bytes = plan->meta_bytes;
+  ck(cudaStreamSynchronize(stream_), "plan upload");
+  return plan;
+}
+
+tt_step_result Engine::execute(StepPlan& plan) {
+  if (!seg_stack_.empty()) throw std::runtime_error("tree_train_step: segment stack is not empty");
+  ensure_capacity(plan.rows, plan.arena_peak, plan.max_n, plan.max_loss);
+  cur_meta_ = plan.meta.as<char>();
   ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
   const uint64_t launches0 = launches_;
-
-  for (auto& [bi, push] : ops) {
-    if (push) forward_batch(batches[bi]);
-    else backward_batch(batches[bi], nullptr);
+  for (auto& [bi, push] : plan.ops) {
+    if (push) forward_batch(plan.batches[bi]);
+    else backward_batch(plan.batches[bi], nullptr);
   }
   ck(cudaGetLastError(), "tree_train_step launch");
   ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
   ck(cudaStreamSynchronize(stream_), "tree_train_step");
+  collect_profile();
+  tt_step_result res = plan.counters;
   res.total_loss = *loss_host_;
-  res.peak_live_kv_tokens = static_cast<uint64_t>(rows);
-  res.peak_live_activation_tokens = peak_tok;
   res.num_launches = launches_ - launches0;
-  uint64_t roll = 0;
-  for (auto& s : tree.seq_tokens) roll += s.size();
-  res.rollout_tokens = roll;
-  res.num_chunks = res.num_segments;
+  res.d2h_bytes = sizeof(double);
   res.peak_hbm_bytes = wbuf_.bytes + gainbuf_.bytes + pe_.bytes + grads_.bytes + kst_.bytes + vst_.bytes +
-                       dkst_.bytes + dvst_.bytes + peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +
+                       dkst_.bytes + dvst_.bytes + plan.arena_peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +
                        sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes + sc_dq_.bytes + sc_dqkv_.bytes +
-                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + meta_.bytes;
-  arena_peak_ = std::max(arena_peak_, peak);
-  if (!std::isfinite(res.total_loss))
-    throw NonFiniteError("tree_train_step: non-finite loss");
+                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + plan.meta.bytes;
+  arena_peak_ = std::max(arena_peak_, plan.arena_peak);
+  if (!std::isfinite(res.total_loss)) throw NonFiniteError("tree_train_step: non-finite loss");
   return res;
+}
+
+tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config& sc) {
+  auto plan = prepare(tree, sc);
+  last_trace_ = plan->trace;
+  return execute(*plan);
 }
 
 // ----------------------------------------------------------------------------- segment-level API
@@ -832,23 +899,21 @@ void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out
   b.seg_off = {0};
   b.seg_len = {b.n};
   b.full_logits = true;
+  b.attn_ctx = double(b.n) * double(S) + 0.5 * double(b.n) * double(b.n + 1);
   for (uint64_t t = 0; t < len; ++t) {
     b.tokens.push_back(tokens[t]);
     b.positions.push_back(static_cast<int32_t>(S + t));
   }
   b.pair_off = {0};
   if (seg_stack_.empty()) {
-    // first segment: size the stack for max_position rows and the arena generously
-    size_t arena = 0;
-    arena = align_up(layout(static_cast<int64_t>(cfg_.max_position)).total) + layout(1).total * 64;
-    ensure_capacity(static_cast<int64_t>(cfg_.max_position), arena, static_cast<int64_t>(cfg_.max_position),
-                    static_cast<int64_t>(cfg_.max_position));
+    // first segment: size the stack for max_position rows and the arena for a max_position path
+    const int64_t mp = static_cast<int64_t>(cfg_.max_position);
+    ensure_capacity(mp, align_up(layout(mp).total) + 64 * align_up(layout(1).total), mp, mp);
   }
   b.arena_off = arena_top_;
   const size_t need = align_up(layout(b.n).total);
   if (arena_top_ + need > arena_.bytes) throw std::runtime_error("segment_push: activation arena exhausted");
   arena_top_ += need;
-  // per-segment metadata: its own small meta region appended at the end of meta_
   std::vector<Batch*> ptrs;
   for (auto& x : seg_stack_) ptrs.push_back(&x);
   ptrs.push_back(&b);
@@ -863,8 +928,8 @@ void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out
       e.mode = EPI_STORE_F32;
       e.out[0] = sc_logits_.p;
       e.ldo[0] = V_;
-      gemm_bf16(op(nf + c0 * d_, d_, false), op(head_, V_, true), static_cast<int>(cm), static_cast<int>(V_),
-                static_cast<int>(d_), e, 1, stream_);
+      gemm(op(nf + c0 * d_, d_, false), op(head_, V_, true), static_cast<int>(cm), static_cast<int>(V_),
+           static_cast<int>(d_), e, 1);
       ck(cudaMemcpyAsync(logits_out + c0 * V_, sc_logits_.p, cm * V_ * 4, cudaMemcpyDeviceToHost, stream_),
          "logits download");
     }
@@ -880,27 +945,25 @@ void Engine::segment_pop(const float* grad_logits, float* grad_prefix_out) {
   const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
   std::vector<float> before;
   const size_t pre = static_cast<size_t>(b.S) * d_;
+  auto download = [&](float* dst) {
+    for (int64_t l = 0; l < L_; ++l) {
+      ck(cudaMemcpyAsync(dst + (2 * l) * pre, dkst_.as<float>() + l * kv_layer, pre * 4, cudaMemcpyDeviceToHost,
+                         stream_),
+         "dK download");
+      ck(cudaMemcpyAsync(dst + (2 * l + 1) * pre, dvst_.as<float>() + l * kv_layer, pre * 4, cudaMemcpyDeviceToHost,
+                         stream_),
+         "dV download");
+    }
+  };
   if (grad_prefix_out && b.S > 0) {
     before.resize(2 * L_ * pre);
-    for (int64_t l = 0; l < L_; ++l) {
-      ck(cudaMemcpyAsync(before.data() + (2 * l) * pre, dkst_.as<float>() + l * kv_layer, pre * 4,
-                         cudaMemcpyDeviceToHost, stream_), "dK download");
-      ck(cudaMemcpyAsync(before.data() + (2 * l + 1) * pre, dvst_.as<float>() + l * kv_layer, pre * 4,
-                         cudaMemcpyDeviceToHost, stream_), "dV download");
-    }
+    download(before.data());
   }
   std::vector<Batch*> ptrs;
   for (auto& x : seg_stack_) ptrs.push_back(&x);
   upload_meta(ptrs);
   backward_batch(b, grad_logits);
-  if (grad_prefix_out && b.S > 0) {
-    for (int64_t l = 0; l < L_; ++l) {
-      ck(cudaMemcpyAsync(grad_prefix_out + (2 * l) * pre, dkst_.as<float>() + l * kv_layer, pre * 4,
-                         cudaMemcpyDeviceToHost, stream_), "dK download");
-      ck(cudaMemcpyAsync(grad_prefix_out + (2 * l + 1) * pre, dvst_.as<float>() + l * kv_layer, pre * 4,
-                         cudaMemcpyDeviceToHost, stream_), "dV download");
-    }
-  }
+  if (grad_prefix_out && b.S > 0) download(grad_prefix_out);
   ck(cudaGetLastError(), "segment_pop");
   ck(cudaStreamSynchronize(stream_), "segment_pop");
   if (grad_prefix_out && b.S > 0)

@@ -13,10 +13,12 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../include/treetrain_b200.h"
+#include "kernels/gemm.h"
 #include "prefix_tree.hpp"
 
 namespace ttb {
@@ -53,7 +55,30 @@ struct Batch {
   // device offsets (bytes) into the metadata buffer
   size_t o_tok = 0, o_pos = 0, o_qblk = 0, o_kvit = 0, o_kvit2 = 0, o_lrows = 0, o_poff = 0, o_ptgt = 0, o_pw = 0;
   size_t arena_off = 0;
+  double attn_ctx = 0;       // sum over query rows of attended keys (S + t + 1): attention FLOP model
   bool full_logits = false;  // segment API: head over all rows with caller-provided grad_logits
+};
+
+// A prepared tree step: batches, PUSH/POP op list, memory plan, metadata resident in HBM.
+// prepare() once, execute() many times (the timed path with inputs already on the device).
+struct StepPlan {
+  std::vector<Batch> batches;
+  std::vector<std::pair<int, bool>> ops;  // (batch index, is_push) in DFS order
+  int64_t rows = 0, max_n = 0, max_loss = 0;
+  size_t arena_peak = 0;
+  DevBuf meta;
+  size_t meta_bytes = 0;
+  tt_step_result counters{};
+  std::string trace;  // logical DFS trace of the executed schedule
+};
+
+// Per-kernel-class device timing (profiling mode): CUDA events around every launch.
+enum KClass { KC_GEMM = 0, KC_ATTN_FWD = 1, KC_ATTN_BWD = 2, KC_ELEMWISE = 3, KC_CE = 4, KC_NUM = 5 };
+struct KStats {
+  double ms[KC_NUM] = {0, 0, 0, 0, 0};
+  double flops[KC_NUM] = {0, 0, 0, 0, 0};
+  double bytes[KC_NUM] = {0, 0, 0, 0, 0};
+  uint64_t launches[KC_NUM] = {0, 0, 0, 0, 0};
 };
 
 struct ActLayout {  // byte offsets of one batch's activations inside its arena region
@@ -80,6 +105,13 @@ class Engine {
   uint64_t accum_count() const { return accum_count_; }
 
   tt_step_result train_step(const PrefixTree& tree, const tt_sched_config& sc);
+  std::unique_ptr<StepPlan> prepare(const PrefixTree& tree, const tt_sched_config& sc);
+  tt_step_result execute(StepPlan& plan);
+
+  void set_profiling(bool on) { profiling_ = on; }
+  const KStats& kstats() const { return kstats_; }
+  void reset_kstats() { kstats_ = KStats{}; }
+  const std::string& last_trace() const { return last_trace_; }
 
   // segment level (device stack)
   void segment_push(const int32_t* tokens, uint64_t len, float* logits_out);
@@ -96,12 +128,32 @@ class Engine {
   void upload_meta(std::vector<Batch*>& batches);
   void forward_batch(const Batch& b);
   void backward_batch(const Batch& b, const float* host_grad_logits);
-  void head_backward(const Batch& b, const bf16* nf, const ActLayout& lay, char* base);
+  void head_backward(const Batch& b, const bf16* nf);
+  void head_backward_dense(const Batch& b, const bf16* nf, const float* host_grad_logits);
+  void gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& e, int splits);
   template <typename T>
   const T* meta(size_t off) const {
-    return reinterpret_cast<const T*>(meta_.as<char>() + off);
+    return reinterpret_cast<const T*>(cur_meta_ + off);
   }
   void count(int k = 1) { launches_ += k; }
+  // Launch wrapper: counts the launch and, in profiling mode, brackets it with CUDA events.
+  template <typename F>
+  void run(KClass cls, double flops, double bytes, F&& launch) {
+    if (!profiling_) {
+      launch();
+      ++launches_;
+      return;
+    }
+    cudaEvent_t a = event(), b = event();
+    cudaEventRecord(a, stream_);
+    launch();
+    cudaEventRecord(b, stream_);
+    pending_.push_back({cls, a, b, flops, bytes});
+    ++launches_;
+  }
+  cudaEvent_t event();
+  void collect_profile();
+  size_t upload_staged(const std::vector<char>& host, DevBuf& dst);
 
   tt_model_config cfg_;
   int device_ = 0;
@@ -137,6 +189,18 @@ class Engine {
   char* meta_host_ = nullptr;    // pinned staging
   size_t meta_host_cap_ = 0;
   uint64_t launches_ = 0;
+  const char* cur_meta_ = nullptr;
+  std::string last_trace_;
+  bool profiling_ = false;
+  KStats kstats_;
+  struct Pending {
+    KClass cls;
+    cudaEvent_t a, b;
+    double flops, bytes;
+  };
+  std::vector<Pending> pending_;
+  std::vector<cudaEvent_t> event_pool_;
+  size_t event_next_ = 0;
 
   // segment-level API state
   std::vector<Batch> seg_stack_;

@@ -156,6 +156,9 @@ int tt_plan_destroy(tt_step_plan* plan);
  * Arrays have TT_NUM_KCLASS entries: accumulated ms, algorithmic FLOPs, algorithmic bytes, launches. */
 #define TT_NUM_KCLASS 5
 int tt_engine_set_profiling(tt_engine* eng, int32_t on);
+/* Implementation switches for cross-checks and ablations: "attn_fwd_impl" 0 = mma.sync (sm80-style
+ * baseline), 1 = tcgen05/TMEM/TMA (default). */
+int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value);
 int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset);
 
 /* ------------------------------------------------------------------ segment level (device KV stack)

@@ -319,6 +319,9 @@ class Engine:
     def set_profiling(self, on: bool) -> None:
         _check(_native.lib().tt_engine_set_profiling(self._h, int(on)))
 
+    def set_option(self, key: str, value: int) -> None:
+        _check(_native.lib().tt_engine_set_option(self._h, key.encode(), int(value)))
+
     def profile(self, reset: bool = True):
         n = len(self.KCLASSES)
         ms, fl, by = (np.zeros(n) for _ in range(3))

@@ -302,6 +302,14 @@ int tt_engine_set_profiling(tt_engine* eng, int32_t on) {
   });
 }
 
+int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value) {
+  return ttb::guarded([&] {
+    need(eng, "engine");
+    need(key, "key");
+    eng->e->set_option(key, value);
+  });
+}
+
 int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset) {
   return ttb::guarded([&] {
     need(eng, "engine");

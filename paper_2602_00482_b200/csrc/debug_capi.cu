@@ -2,7 +2,12 @@
 // kernel unit tests in tests/test_kernels_gpu.py; the product entry points are in capi.cpp.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
 #include "capi_internal.h"
+#include "kernels/attention.h"
 #include "kernels/gemm.h"
 
 extern "C" {
@@ -28,6 +33,111 @@ int tt_debug_gemm(const void* a, long lda, int a_mn, const void* b, long ldb, in
     ttb::gemm_bf16(A, B, M, N, K, e, splits, nullptr);
     ttb::check_cuda(cudaGetLastError(), "tt_debug_gemm launch");
     ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_gemm sync");
+  });
+}
+
+// Segment attention on one segment of n queries over stack rows [0, S) + own rows [S, S+n)
+// (k/v: [rows_cap x H*dh] bf16). dir 0: forward (impl 0 = mma.sync, 1 = tcgen05) -> o, lse.
+// dir 1: backward (impl 0 = mma.sync) from o, lse, dO -> dq (overwritten), dk/dv (added).
+int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v, void* o, float* lse, const void* dO,
+                  float* D, float* dq, float* dk, float* dv, int n, int S, int H, int dh, long rows_cap) {
+  return ttb::guarded([&] {
+    const int d = H * dh;
+    std::vector<int> q64, q128, it, it2;
+    for (int qs = 0; qs < n; qs += 64) q64.insert(q64.end(), {qs, std::min(qs + 64, n), 0, 0});
+    for (int qs = 0; qs < n; qs += 128) q128.insert(q128.end(), {qs, std::min(qs + 128, n), 0, 0});
+    for (int kv = 0; kv < S; kv += 64) {
+      it.insert(it.end(), {kv, std::min(64, S - kv), 0, n});
+      it2.insert(it2.end(), {0, 0});
+    }
+    for (int kt = 0; kt < n; kt += 64) {
+      it.insert(it.end(), {S + kt, std::min(64, n - kt), kt, n});
+      it2.insert(it2.end(), {0, 1});
+    }
+    auto up = [](const std::vector<int>& h) {
+      void* p = nullptr;
+      ttb::check_cuda(cudaMalloc(&p, std::max<size_t>(16, h.size() * 4)), "cudaMalloc");
+      if (!h.empty()) ttb::check_cuda(cudaMemcpy(p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "memcpy");
+      return p;
+    };
+    void *d64 = up(q64), *d128 = up(q128), *dit = up(it), *dit2 = up(it2);
+    const float scale = 1.0f / std::sqrt(static_cast<float>(dh));
+    if (dir == 0) {
+      ttb::AttnFwdArgs a;
+      a.q = static_cast<const __nv_bfloat16*>(q);
+      a.ldq = d;
+      a.k = static_cast<const __nv_bfloat16*>(k);
+      a.v = static_cast<const __nv_bfloat16*>(v);
+      a.ldkv = d;
+      a.o = static_cast<__nv_bfloat16*>(o);
+      a.ldo = d;
+      a.lse = lse;
+      a.n = n;
+      a.H = H;
+      a.dh = dh;
+      a.S = S;
+      a.scale = scale;
+      if (impl == 1) {
+        a.qblocks = static_cast<const int4*>(d128);
+        a.nqb = static_cast<int>(q128.size() / 4);
+        ttb::attn_fwd_sm100(a, rows_cap, nullptr);
+      } else {
+        a.qblocks = static_cast<const int4*>(d64);
+        a.nqb = static_cast<int>(q64.size() / 4);
+        ttb::attn_fwd(a, nullptr);
+      }
+    } else {
+      ttb::AttnBwdArgs a;
+      a.q = static_cast<const __nv_bfloat16*>(q);
+      a.dO = static_cast<const __nv_bfloat16*>(dO);
+      a.o = static_cast<const __nv_bfloat16*>(o);
+      a.ldq = d;
+      a.k = static_cast<const __nv_bfloat16*>(k);
+      a.v = static_cast<const __nv_bfloat16*>(v);
+      a.ldkv = d;
+      a.lse = lse;
+      a.D = D;
+      a.dq = dq;
+      a.lddq = d;
+      a.dk = dk;
+      a.dv = dv;
+      a.lddkv = d;
+      a.n = n;
+      a.H = H;
+      a.dh = dh;
+      a.S = S;
+      a.items = static_cast<const int4*>(dit);
+      a.items2 = static_cast<const int2*>(dit2);
+      a.nitems = static_cast<int>(it.size() / 4);
+      a.scale = scale;
+      if (impl == 1) {
+        std::vector<int> k128, k128b;
+        for (int kv = 0; kv < S; kv += 128) {
+          k128.insert(k128.end(), {kv, std::min(128, S - kv), 0, n});
+          k128b.insert(k128b.end(), {0, 0});
+        }
+        for (int kt = 0; kt < n; kt += 128) {
+          k128.insert(k128.end(), {S + kt, std::min(128, n - kt), kt, n});
+          k128b.insert(k128b.end(), {0, 1});
+        }
+        void *dk128 = up(k128), *dk128b = up(k128b);
+        ttb::attn_bwd_sm100(a, rows_cap, static_cast<const int4*>(d128), static_cast<int>(q128.size() / 4),
+                            static_cast<const int4*>(dk128), static_cast<const int2*>(dk128b),
+                            static_cast<int>(k128.size() / 4), nullptr);
+        ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_attn sync");
+        cudaFree(dk128);
+        cudaFree(dk128b);
+      } else {
+        ttb::check_cuda(cudaMemset(dq, 0, static_cast<size_t>(n) * d * 4), "memset");
+        ttb::attn_bwd(a, nullptr);
+      }
+    }
+    ttb::check_cuda(cudaGetLastError(), "tt_debug_attn launch");
+    ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_attn sync");
+    cudaFree(d64);
+    cudaFree(d128);
+    cudaFree(dit);
+    cudaFree(dit2);
   });
 }
 

@@ -156,6 +156,18 @@ Engine::~Engine() {
   cudaStreamDestroy(stream_);
 }
 
+void Engine::set_option(const std::string& key, int64_t value) {
+  if (key == "attn_fwd_impl") {
+    if (value != 0 && value != 1) throw std::invalid_argument("attn_fwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
+    attn_fwd_impl_ = static_cast<int>(value);
+  } else if (key == "attn_bwd_impl") {
+    if (value != 0 && value != 1) throw std::invalid_argument("attn_bwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
+    attn_bwd_impl_ = static_cast<int>(value);
+  } else {
+    throw std::invalid_argument("unknown engine option: " + key);
+  }
+}
+
 // ----------------------------------------------------------------------------- parameters
 void Engine::upload_params(const float* flat, uint64_t n) {
   if (n != n_params_) throw std::invalid_argument("params upload: wrong parameter count");
@@ -263,6 +275,8 @@ void Engine::ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, in
     vst_.ensure(kvb * 2);
     dkst_.ensure(kvb * 4);
     dvst_.ensure(kvb * 4);
+    ck(cudaMemsetAsync(kst_.p, 0, kvb * 2, stream_), "K stack zero");
+    ck(cudaMemsetAsync(vst_.p, 0, kvb * 2, stream_), "V stack zero");
     ck(cudaMemsetAsync(dkst_.p, 0, kvb * 4, stream_), "dK stack zero");
     ck(cudaMemsetAsync(dvst_.p, 0, kvb * 4, stream_), "dV stack zero");
   }
@@ -309,12 +323,18 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
     return off;
   };
   b.qblk.clear();
+  b.qblk128.clear();
   b.kvit.clear();
   b.kvit2.clear();
+  b.kvit128.clear();
+  b.kvit128_2.clear();
   for (size_t i = 0; i < b.seg_off.size(); ++i) {
     const int64_t so = b.seg_off[i], end = so + b.seg_len[i];
     for (int64_t q = so; q < end; q += kQBlock) {
       b.qblk.insert(b.qblk.end(), {int32_t(q), int32_t(std::min<int64_t>(q + kQBlock, end)), int32_t(so), 0});
+    }
+    for (int64_t q = so; q < end; q += kFwdBlockQ) {
+      b.qblk128.insert(b.qblk128.end(), {int32_t(q), int32_t(std::min<int64_t>(q + kFwdBlockQ, end)), int32_t(so), 0});
     }
     for (int64_t kv = 0; kv < b.S; kv += 64)  // prefix rows: every query of the member attends
       for (int64_t q = so; q < end; q += kQChunk) {
@@ -328,12 +348,27 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
                                      int32_t(q), int32_t(std::min<int64_t>(q + kQChunk, end))});
         b.kvit2.insert(b.kvit2.end(), {int32_t(so), 1});
       }
+    for (int64_t kv = 0; kv < b.S; kv += kBwdBlockKV)
+      for (int64_t q = so; q < end; q += kQChunk) {
+        b.kvit128.insert(b.kvit128.end(), {int32_t(kv), int32_t(std::min<int64_t>(kBwdBlockKV, b.S - kv)), int32_t(q),
+                                           int32_t(std::min<int64_t>(q + kQChunk, end))});
+        b.kvit128_2.insert(b.kvit128_2.end(), {int32_t(so), 0});
+      }
+    for (int64_t kt = 0; kt < b.seg_len[i]; kt += kBwdBlockKV)
+      for (int64_t q = so + kt; q < end; q += kQChunk) {
+        b.kvit128.insert(b.kvit128.end(), {int32_t(b.S + so + kt), int32_t(std::min<int64_t>(kBwdBlockKV, b.seg_len[i] - kt)),
+                                           int32_t(q), int32_t(std::min<int64_t>(q + kQChunk, end))});
+        b.kvit128_2.insert(b.kvit128_2.end(), {int32_t(so), 1});
+      }
   }
   b.o_tok = put(b.tokens.data(), b.tokens.size() * 4);
   b.o_pos = put(b.positions.data(), b.positions.size() * 4);
   b.o_qblk = put(b.qblk.data(), b.qblk.size() * 4);
+  b.o_qblk128 = put(b.qblk128.data(), b.qblk128.size() * 4);
   b.o_kvit = put(b.kvit.data(), b.kvit.size() * 4);
   b.o_kvit2 = put(b.kvit2.data(), b.kvit2.size() * 4);
+  b.o_kvit128 = put(b.kvit128.data(), b.kvit128.size() * 4);
+  b.o_kvit128_2 = put(b.kvit128_2.data(), b.kvit128_2.size() * 4);
   b.o_lrows = put(b.loss_rows.data(), b.loss_rows.size() * 4);
   b.o_poff = put(b.pair_off.data(), b.pair_off.size() * 4);
   b.o_ptgt = put(b.pair_tgt.data(), b.pair_tgt.size() * 4);
@@ -454,10 +489,16 @@ void Engine::forward_batch(const Batch& b) {
       a.H = static_cast<int>(H_);
       a.dh = static_cast<int>(dh_);
       a.S = static_cast<int>(b.S);
-      a.qblocks = meta<int4>(b.o_qblk);
-      a.nqb = static_cast<int>(b.qblk.size() / 4);
       a.scale = scale;
-      run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd(a, stream_); });
+      if (attn_fwd_impl_ == 1) {
+        a.qblocks = meta<int4>(b.o_qblk128);
+        a.nqb = static_cast<int>(b.qblk128.size() / 4);
+        run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd_sm100(a, rows_cap_, stream_); });
+      } else {
+        a.qblocks = meta<int4>(b.o_qblk);
+        a.nqb = static_cast<int>(b.qblk.size() / 4);
+        run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd(a, stream_); });
+      }
     }
     {  // x_mid = x + attn W_o  (:410-411,427-428)
       EpiParams e;
@@ -665,7 +706,6 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
       gemm(op(gxb, d, false), op(wo_[l], d, false), n, d, d, e, 1);
     }
     // attention backward (model.hpp:546-604): dQ, and dK/dV added into the stack rows [0, S+n)
-    ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
     {
       AttnBwdArgs a;
       a.q = q;
@@ -690,8 +730,18 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
       a.items2 = meta<int2>(b.o_kvit2);
       a.nitems = static_cast<int>(b.kvit.size() / 4);
       a.scale = scale;
-      run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] { attn_bwd(a, stream_); });
-      ++launches_;  // the D = rowsum(dO*O) pre-pass inside attn_bwd
+      if (attn_bwd_impl_ == 1) {
+        run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
+          attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_qblk128), static_cast<int>(b.qblk128.size() / 4),
+                         meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2), static_cast<int>(b.kvit128.size() / 4),
+                         stream_);
+        });
+        launches_ += 2;  // D pre-pass + the dq and dkdv kernels
+      } else {
+        ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
+        run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] { attn_bwd(a, stream_); });
+        ++launches_;  // the D = rowsum(dO*O) pre-pass inside attn_bwd
+      }
     }
     // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
     run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.S * d_, dV + b.S * d_, dqkv, n, d, stream_); });

@@ -47,13 +47,15 @@ struct Batch {
   std::vector<int64_t> seg_off, seg_len;
   // host-built metadata (uploaded once per step)
   std::vector<int32_t> tokens, positions;
-  std::vector<int32_t> qblk;   // int4 per query block
+  std::vector<int32_t> qblk;   // int4 per 64-row query block (mma.sync forward)
+  std::vector<int32_t> qblk128;  // int4 per 128-row query block (tcgen05 forward)
   std::vector<int32_t> kvit;   // int4 per backward item
   std::vector<int32_t> kvit2;  // int2 per backward item
+  std::vector<int32_t> kvit128, kvit128_2;  // 128-row stack blocks (tcgen05 dK/dV kernel)
   std::vector<int32_t> loss_rows, pair_off, pair_tgt;
   std::vector<double> pair_w;
   // device offsets (bytes) into the metadata buffer
-  size_t o_tok = 0, o_pos = 0, o_qblk = 0, o_kvit = 0, o_kvit2 = 0, o_lrows = 0, o_poff = 0, o_ptgt = 0, o_pw = 0;
+  size_t o_tok = 0, o_pos = 0, o_qblk = 0, o_qblk128 = 0, o_kvit = 0, o_kvit2 = 0, o_kvit128 = 0, o_kvit128_2 = 0, o_lrows = 0, o_poff = 0, o_ptgt = 0, o_pw = 0;
   size_t arena_off = 0;
   double attn_ctx = 0;       // sum over query rows of attended keys (S + t + 1): attention FLOP model
   bool full_logits = false;  // segment API: head over all rows with caller-provided grad_logits
@@ -109,6 +111,8 @@ class Engine {
   tt_step_result execute(StepPlan& plan);
 
   void set_profiling(bool on) { profiling_ = on; }
+  // Implementation switches (ablation / cross-checks): attn_{fwd,bwd}_impl 0 = mma.sync, 1 = tcgen05.
+  void set_option(const std::string& key, int64_t value);
   const KStats& kstats() const { return kstats_; }
   void reset_kstats() { kstats_ = KStats{}; }
   const std::string& last_trace() const { return last_trace_; }
@@ -192,6 +196,8 @@ class Engine {
   const char* cur_meta_ = nullptr;
   std::string last_trace_;
   bool profiling_ = false;
+  int attn_fwd_impl_ = 1;
+  int attn_bwd_impl_ = 1;
   KStats kstats_;
   struct Pending {
     KClass cls;

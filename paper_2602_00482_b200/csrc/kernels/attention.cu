@@ -469,9 +469,13 @@ void attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
   }
 }
 
-void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
+void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream) {
   const int warps = a.n * a.H;
   if (warps > 0) attn_bwd_pre_kernel<<<(warps * 32 + 255) / 256, 256, 0, stream>>>(a.dO, a.o, a.ldq, a.D, a.n, a.H, a.dh);
+}
+
+void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {
+  attn_bwd_pre(a, stream);
   if (a.nitems == 0) return;
   dim3 grid(a.nitems, a.H);
   if (a.dh == 64) {

@@ -49,4 +49,18 @@ struct AttnBwdArgs {
 void attn_fwd(const AttnFwdArgs& a, cudaStream_t stream);
 void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream);
 
+// tcgen05/TMEM/TMA forward (attention_sm100.cu): qblocks hold 128-row query blocks; k/v are the
+// layer's stack base pointers with rows_cap rows.
+constexpr int kFwdBlockQ = 128;
+void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream);
+
+// D = rowsum(dO * O) per (head, row) (the softmax-backward correction term).
+void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream);
+// tcgen05 backward (attention_bwd_sm100.cu): dq_blocks are 128-row query blocks (like the forward);
+// kv_items/kv_items2 are 128-row stack blocks {kv_row0, kv_rows, q_lo, q_hi} / {seg_off, is_own}.
+// dq is overwritten; dk/dv are accumulated (red.add) into the fp32 stack rows.
+constexpr int kBwdBlockKV = 128;
+void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
+                    const int2* kv_items2, int n_kv, cudaStream_t stream);
+
 }  // namespace ttb

@@ -1,0 +1,537 @@
+// tcgen05 / TMEM / TMA segment attention backward over the device KV stack (sm_100a).
+//
+// Replaces the attention backward of backward_segment (model.hpp:546-604):
+//   P = softmax(scale Q K^T) (recomputed from the forward LSE), dP = dO V^T,
+//   dS = P * (dP - D) with D = rowsum(dO * O),  dQ = scale dS K,  dK = scale dS^T Q,  dV = P^T dO.
+// Two kernels, both tensor-core only (no atomics on the hot product):
+//   dq kernel   : CTA = (128-query block, head); loops over the block's KV blocks (BKV = 64).
+//                 S, dP double-buffered in TMEM; dS -> swizzled smem; dQ accumulated in TMEM and
+//                 written once (fp32) — the CTA owns its query rows.
+//   dkdv kernel : CTA = (128-key stack block, head, query range); loops over 64-query blocks.
+//                 S^T, dP^T double-buffered in TMEM; P^T, dS^T -> swizzled smem; dK, dV accumulated
+//                 in TMEM, added once into the fp32 dK/dV stack rows (red.add.v4: several query-range
+//                 items and several sibling segments contribute to the same prefix rows).
+// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM alloc + MMA issuer, warps 2..5 one
+// TMEM lane (= query row / key row) per thread.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+
+#include "attention.h"
+#include "gemm.h"
+#include "sm100.cuh"
+
+namespace ttb {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// Writes one thread's row of 64 bf16 values (packed pairs w[32]) into a 128B-swizzled K-major panel.
+__device__ __forceinline__ void st_row_sw128(uint8_t* panel, int row, const uint32_t (&w)[32]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint4* dst = reinterpret_cast<uint4*>(panel + row * 128 + ((c ^ (row & 7)) * 16));
+    *dst = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+  }
+}
+
+// ================================================================================= dQ kernel
+template <int DH, int NS>
+struct DqCfg {
+  static constexpr int BQ = 128, BKV = 64;
+  static constexpr int kQBytes = BQ * DH * 2;
+  static constexpr int kKVBytes = BKV * DH * 2;
+  static constexpr int kDSBytes = BQ * BKV * 2;
+  static constexpr int kOffDO = kQBytes;
+  static constexpr int kOffK = 2 * kQBytes;
+  static constexpr int kOffV = kOffK + NS * kKVBytes;
+  static constexpr int kOffDS = kOffV + NS * kKVBytes;
+  static constexpr int kOffBar = kOffDS + 2 * kDSBytes;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static constexpr int kTmemCols = (4 * BKV + DH) <= 256 ? 256 : 512;
+  static constexpr uint32_t kIdescS = make_idesc_bf16(128, BKV, false, false);
+  static constexpr uint32_t kIdescQ = make_idesc_bf16(128, DH, false, true);
+};
+
+struct BwdParams {
+  const float* lse;  // [H x n]
+  const float* D;    // [H x n]
+  float* dq;         // [n x lddq]
+  long lddq;
+  float* dk;  // stack rows (this layer), fp32
+  float* dv;
+  long lddkv;
+  int n, S, H;
+  const int4* blocks;   // dq: {q_start, q_end, seg_off, 0}; dkdv: {kv_row0, kv_rows, q_lo, q_hi}
+  const int2* blocks2;  // dkdv: {seg_off, is_own}
+  float scale, scale_log2;
+};
+
+template <int DH, int NS>
+__global__ void __launch_bounds__(kThreads, 1)
+    fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                     const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                     BwdParams p) {
+  using C = DqCfg<DH, NS>;
+  constexpr int BKV = C::BKV;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + NS;
+  uint64_t* s_full = kv_empty + NS;  // [2]  S_j and dP_j in TMEM
+  uint64_t* ds_full = s_full + 2;    // [2]  dS_j in smem
+  uint64_t* ds_free = ds_full + 2;   // [2]  dQ MMA consumed dS_j
+  uint64_t* dq_done = ds_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
+
+  const int warp = warp_id_sync();
+  const int lane = threadIdx.x & 31;
+  const int4 blk = p.blocks[blockIdx.x];
+  const int q_start = blk.x, q_end = blk.y, seg_off = blk.z;
+  const int h = blockIdx.y;
+  const int S = p.S;
+  const int n_pre = (S + BKV - 1) / BKV;
+  const int own_rows = q_end - seg_off;
+  const int nblk = n_pre + (own_rows + BKV - 1) / BKV;
+  auto kv_row0 = [&](int j) { return j < n_pre ? j * BKV : S + seg_off + (j - n_pre) * BKV; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&ds_full[s], 4);
+      mbar_init(&ds_free[s], 1);
+    }
+    mbar_init(dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S[2] at [0, 2*BKV), dP[2] at [2*BKV, 4*BKV), dQ at [4*BKV, 4*BKV+DH)
+  const uint32_t t_S = tmem, t_dP = tmem + 2 * BKV, t_dQ = tmem + 4 * BKV;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * C::kQBytes);
+#pragma unroll
+      for (int pn = 0; pn < DH / 64; ++pn) {
+        tma_load_2d(&tm_q, q_full, smem + pn * (128 * 128), h * DH + pn * 64, q_start);
+        tma_load_2d(&tm_do, q_full, smem + C::kOffDO + pn * (128 * 128), h * DH + pn * 64, q_start);
+      }
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % NS;
+        mbar_wait(&kv_empty[st], ((j / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * C::kKVBytes);
+        const int r0 = kv_row0(j);
+#pragma unroll
+        for (int pn = 0; pn < DH / 64; ++pn) {
+          tma_load_2d(&tm_k, &kv_full[st], smem + C::kOffK + st * C::kKVBytes + pn * (BKV * 128), h * DH + pn * 64, r0);
+          tma_load_2d(&tm_v, &kv_full[st], smem + C::kOffV + st * C::kKVBytes + pn * (BKV * 128), h * DH + pn * 64, r0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t q_addr = smem_u32(smem), do_addr = smem_u32(smem + C::kOffDO);
+    auto issue_s = [&](int j) {  // S_j = Q K_j^T ; dP_j = dO V_j^T
+      const int st = j % NS;
+      mbar_wait(&kv_full[st], (j / NS) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t k_addr = smem_u32(smem + C::kOffK + st * C::kKVBytes);
+        const uint32_t v_addr = smem_u32(smem + C::kOffV + st * C::kKVBytes);
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          const uint32_t ao = (k / 4) * (128 * 128) + (k % 4) * 32, bo = (k / 4) * (BKV * 128) + (k % 4) * 32;
+          umma_bf16_ss(t_S + (j & 1) * BKV, make_sdesc_sw128(q_addr + ao, 16, 1024),
+                       make_sdesc_sw128(k_addr + bo, 16, 1024), C::kIdescS, k > 0);
+          umma_bf16_ss(t_dP + (j & 1) * BKV, make_sdesc_sw128(do_addr + ao, 16, 1024),
+                       make_sdesc_sw128(v_addr + bo, 16, 1024), C::kIdescS, k > 0);
+        }
+        umma_commit(&s_full[j & 1]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    issue_s(0);
+    if (nblk > 1) issue_s(1);
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&ds_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {  // dQ += dS_j K_j   (B = K_j read MN-major: N = dh, K = keys)
+        const int st = j % NS;
+        const uint32_t ds_addr = smem_u32(smem + C::kOffDS + (j & 1) * C::kDSBytes);
+        const uint32_t k_addr = smem_u32(smem + C::kOffK + st * C::kKVBytes);
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k)
+          umma_bf16_ss(t_dQ, make_sdesc_sw128(ds_addr + k * 32, 16, 1024),
+                       make_sdesc_sw128(k_addr + k * 2048, BKV * 128, 1024), C::kIdescQ, (j > 0 || k > 0));
+        umma_commit(&kv_empty[st]);
+        umma_commit(&ds_free[j & 1]);
+        if (j == nblk - 1) umma_commit(dq_done);
+      }
+      __syncwarp();
+      if (j + 2 < nblk) issue_s(j + 2);
+    }
+  } else {
+    const int quad = warp & 3;
+    const int rloc = quad * 32 + lane;
+    const int row = q_start + rloc;
+    const int t = row - seg_off;
+    const bool row_ok = row < q_end;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const float lse2 = row_ok ? p.lse[static_cast<long>(h) * p.n + row] * kLog2e : 0.f;
+    const float Dr = row_ok ? p.D[static_cast<long>(h) * p.n + row] : 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      float s[BKV], dp[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV; c += 16) {
+        uint32_t r[16], r2[16];
+        tmem_ld16(t_S + (j & 1) * BKV + c + lane_off, r);
+        tmem_ld16(t_dP + (j & 1) * BKV + c + lane_off, r2);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          s[c + i] = __uint_as_float(r[i]);
+          dp[c + i] = __uint_as_float(r2[i]);
+        }
+      }
+      tmem_ld_wait();
+      const bool pre = j < n_pre;
+      const int base = pre ? j * BKV : (j - n_pre) * BKV;
+      uint32_t w[32];
+#pragma unroll
+      for (int i = 0; i < BKV; i += 2) {
+        float ds2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = row_ok && (pre ? (base + i + e < S) : (base + i + e <= t));
+          const float pv = ok ? exp2f(s[i + e] * p.scale_log2 - lse2) : 0.f;
+          ds2[e] = pv * (dp[i + e] - Dr);
+        }
+        w[i / 2] = pack_bf16x2(ds2[0], ds2[1]);
+      }
+      if (j >= 2) mbar_wait(&ds_free[j & 1], ((j >> 1) + 1) & 1);
+      st_row_sw128(smem + C::kOffDS + (j & 1) * C::kDSBytes, rloc, w);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ds_full[j & 1]);
+    }
+    mbar_wait(dq_done, 0);
+    tc_fence_after();
+#pragma unroll
+    for (int c = 0; c < DH; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(t_dQ + c + lane_off, r);
+      tmem_ld_wait();
+      if (row_ok) {
+        float4* dst = reinterpret_cast<float4*>(p.dq + static_cast<long>(row) * p.lddq + h * DH + c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_float4(__uint_as_float(r[4 * i]) * p.scale, __uint_as_float(r[4 * i + 1]) * p.scale,
+                               __uint_as_float(r[4 * i + 2]) * p.scale, __uint_as_float(r[4 * i + 3]) * p.scale);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
+}
+
+// ================================================================================= dK/dV kernel
+template <int DH, int NS>
+struct DkvCfg {
+  static constexpr int BKV = 128, BQ = 64;
+  static constexpr int kKVBytes = BKV * DH * 2;   // K (or V) block, loaded once
+  static constexpr int kQBytes = BQ * DH * 2;     // Q_i (or dO_i) tile
+  static constexpr int kPBytes = BKV * BQ * 2;    // P^T (or dS^T) tile
+  static constexpr int kOffV = kKVBytes;
+  static constexpr int kOffQ = 2 * kKVBytes;
+  static constexpr int kOffDO = kOffQ + NS * kQBytes;
+  static constexpr int kOffP = kOffDO + NS * kQBytes;   // [2]
+  static constexpr int kOffDS = kOffP + 2 * kPBytes;    // [2]
+  static constexpr int kOffStat = kOffDS + 2 * kPBytes; // [2][2][BQ] floats: lse2, D
+  static constexpr int kOffBar = kOffStat + 2 * 2 * BQ * 4;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static constexpr int kTmemCols = 512;
+  static constexpr uint32_t kIdescS = make_idesc_bf16(128, BQ, false, false);
+  static constexpr uint32_t kIdescKV = make_idesc_bf16(128, DH, false, true);
+};
+
+template <int DH, int NS>
+__global__ void __launch_bounds__(kThreads, 1)
+    fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                       const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                       BwdParams p) {
+  using C = DkvCfg<DH, NS>;
+  constexpr int BQ = C::BQ;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;
+  uint64_t* q_empty = q_full + NS;
+  uint64_t* s_full = q_empty + NS;  // [2]
+  uint64_t* p_full = s_full + 2;    // [2]
+  uint64_t* p_free = p_full + 2;    // [2]
+  uint64_t* acc_done = p_free + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+  float* stat = reinterpret_cast<float*>(smem + C::kOffStat);
+
+  const int warp = warp_id_sync();
+  const int lane = threadIdx.x & 31;
+  const int4 it = p.blocks[blockIdx.x];
+  const int2 it2 = p.blocks2[blockIdx.x];
+  const int kv0 = it.x, kv_rows = it.y, q_lo = it.z, q_hi = it.w;
+  const int seg_off = it2.x;
+  const bool own = it2.y != 0;
+  const int kt_base = own ? kv0 - p.S - seg_off : 0;
+  const int h = blockIdx.y;
+  const int nq = (q_hi - q_lo + BQ - 1) / BQ;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4);
+      mbar_init(&p_free[s], 1);
+    }
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S^T[2] at [0,128), dP^T[2] at [128,256), dK at [256, 256+DH), dV at [384, 384+DH)
+  const uint32_t t_S = tmem, t_dP = tmem + 2 * BQ, t_dK = tmem + 256, t_dV = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::kKVBytes);
+#pragma unroll
+      for (int pn = 0; pn < DH / 64; ++pn) {
+        tma_load_2d(&tm_k, kv_full, smem + pn * (128 * 128), h * DH + pn * 64, kv0);
+        tma_load_2d(&tm_v, kv_full, smem + C::kOffV + pn * (128 * 128), h * DH + pn * 64, kv0);
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int st = i % NS;
+        mbar_wait(&q_empty[st], ((i / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[st], 2 * C::kQBytes);
+        const int q0 = q_lo + i * BQ;
+#pragma unroll
+        for (int pn = 0; pn < DH / 64; ++pn) {
+          tma_load_2d(&tm_q, &q_full[st], smem + C::kOffQ + st * C::kQBytes + pn * (BQ * 128), h * DH + pn * 64, q0);
+          tma_load_2d(&tm_do, &q_full[st], smem + C::kOffDO + st * C::kQBytes + pn * (BQ * 128), h * DH + pn * 64, q0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t k_addr = smem_u32(smem), v_addr = smem_u32(smem + C::kOffV);
+    auto issue_s = [&](int i) {  // S^T_i = K Q_i^T ; dP^T_i = V dO_i^T   (M = 128 keys, N = 64 queries)
+      const int st = i % NS;
+      mbar_wait(&q_full[st], (i / NS) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t q_addr = smem_u32(smem + C::kOffQ + st * C::kQBytes);
+        const uint32_t do_addr = smem_u32(smem + C::kOffDO + st * C::kQBytes);
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          const uint32_t ao = (k / 4) * (128 * 128) + (k % 4) * 32, bo = (k / 4) * (BQ * 128) + (k % 4) * 32;
+          umma_bf16_ss(t_S + (i & 1) * BQ, make_sdesc_sw128(k_addr + ao, 16, 1024),
+                       make_sdesc_sw128(q_addr + bo, 16, 1024), C::kIdescS, k > 0);
+          umma_bf16_ss(t_dP + (i & 1) * BQ, make_sdesc_sw128(v_addr + ao, 16, 1024),
+                       make_sdesc_sw128(do_addr + bo, 16, 1024), C::kIdescS, k > 0);
+        }
+        umma_commit(&s_full[i & 1]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(kv_full, 0);
+    issue_s(0);
+    if (nq > 1) issue_s(1);
+    for (int i = 0; i < nq; ++i) {
+      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {  // dV += P^T dO_i ; dK += dS^T Q_i   (B read MN-major: N = dh, K = queries)
+        const int st = i % NS;
+        const uint32_t pa = smem_u32(smem + C::kOffP + (i & 1) * C::kPBytes);
+        const uint32_t dsa = smem_u32(smem + C::kOffDS + (i & 1) * C::kPBytes);
+        const uint32_t q_addr = smem_u32(smem + C::kOffQ + st * C::kQBytes);
+        const uint32_t do_addr = smem_u32(smem + C::kOffDO + st * C::kQBytes);
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k) {
+          umma_bf16_ss(t_dV, make_sdesc_sw128(pa + k * 32, 16, 1024),
+                       make_sdesc_sw128(do_addr + k * 2048, BQ * 128, 1024), C::kIdescKV, (i > 0 || k > 0));
+          umma_bf16_ss(t_dK, make_sdesc_sw128(dsa + k * 32, 16, 1024),
+                       make_sdesc_sw128(q_addr + k * 2048, BQ * 128, 1024), C::kIdescKV, (i > 0 || k > 0));
+        }
+        umma_commit(&q_empty[st]);
+        umma_commit(&p_free[i & 1]);
+        if (i == nq - 1) umma_commit(acc_done);
+      }
+      __syncwarp();
+      if (i + 2 < nq) issue_s(i + 2);
+    }
+  } else {
+    const int quad = warp & 3;
+    const int krow = quad * 32 + lane;  // key row within the block == TMEM lane
+    const bool key_ok = krow < kv_rows;
+    const int kt = kt_base + krow;      // own: local key index
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int tid = threadIdx.x - 64;   // 0..127
+    for (int i = 0; i < nq; ++i) {
+      const int q0 = q_lo + i * BQ;
+      float* st_lse = stat + (i & 1) * 2 * BQ;
+      float* st_D = st_lse + BQ;
+      if (tid < BQ) {
+        const int q = q0 + tid;
+        const bool ok = q < q_hi;
+        st_lse[tid] = ok ? p.lse[static_cast<long>(h) * p.n + q] * kLog2e : INFINITY;
+        st_D[tid] = ok ? p.D[static_cast<long>(h) * p.n + q] : 0.f;
+      }
+      named_bar_sync(1, 128);
+      mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      tc_fence_after();
+      float s[BQ], dp[BQ];
+#pragma unroll
+      for (int c = 0; c < BQ; c += 16) {
+        uint32_t r[16], r2[16];
+        tmem_ld16(t_S + (i & 1) * BQ + c + lane_off, r);
+        tmem_ld16(t_dP + (i & 1) * BQ + c + lane_off, r2);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          s[c + e] = __uint_as_float(r[e]);
+          dp[c + e] = __uint_as_float(r2[e]);
+        }
+      }
+      tmem_ld_wait();
+      uint32_t wp[32], wd[32];
+#pragma unroll
+      for (int c = 0; c < BQ; c += 2) {
+        float pv[2], dv2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int qi = c + e;
+          bool ok = key_ok;
+          if (own) ok = ok && (kt <= q0 + qi - seg_off);
+          pv[e] = ok ? exp2f(s[qi] * p.scale_log2 - st_lse[qi]) : 0.f;
+          dv2[e] = pv[e] * (dp[qi] - st_D[qi]);
+        }
+        wp[c / 2] = pack_bf16x2(pv[0], pv[1]);
+        wd[c / 2] = pack_bf16x2(dv2[0], dv2[1]);
+      }
+      if (i >= 2) mbar_wait(&p_free[i & 1], ((i >> 1) + 1) & 1);
+      st_row_sw128(smem + C::kOffP + (i & 1) * C::kPBytes, krow, wp);
+      st_row_sw128(smem + C::kOffDS + (i & 1) * C::kPBytes, krow, wd);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[i & 1]);
+    }
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    float* dkr = p.dk + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+    float* dvr = p.dv + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 16) {
+      uint32_t rk[16], rv[16];
+      tmem_ld16(t_dK + c + lane_off, rk);
+      tmem_ld16(t_dV + c + lane_off, rv);
+      tmem_ld_wait();
+      if (key_ok) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          red_add_v4_f32(dkr + c + e, __uint_as_float(rk[e]) * p.scale, __uint_as_float(rk[e + 1]) * p.scale,
+                         __uint_as_float(rk[e + 2]) * p.scale, __uint_as_float(rk[e + 3]) * p.scale);
+          red_add_v4_f32(dvr + c + e, __uint_as_float(rv[e]), __uint_as_float(rv[e + 1]), __uint_as_float(rv[e + 2]),
+                         __uint_as_float(rv[e + 3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
+}
+
+template <int DH>
+void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
+                const int2* kv_items2, int n_kv, cudaStream_t stream) {
+  constexpr int NS = 2;
+  using CQ = DqCfg<DH, NS>;
+  using CK = DkvCfg<DH, NS>;
+  const int d = a.H * DH;
+  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, dq_blocks, nullptr, a.scale,
+              a.scale * kLog2e};
+  if (n_dq > 0) {
+    CUtensorMap tq, tdo, tk, tv;
+    make_tmap_bf16(&tq, a.q, d, a.n, a.ldq, 64, 128);
+    make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, 128);
+    make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, CQ::BKV);
+    make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, CQ::BKV);
+    static bool once = (cudaFuncSetAttribute(fa_bwd_dq_kernel<DH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             CQ::kSmem),
+                        true);
+    (void)once;
+    fa_bwd_dq_kernel<DH, NS><<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
+  }
+  if (n_kv > 0) {
+    CUtensorMap tq, tdo, tk, tv;
+    make_tmap_bf16(&tq, a.q, d, a.n, a.ldq, 64, CK::BQ);
+    make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, CK::BQ);
+    make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, 128);
+    make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, 128);
+    static bool once = (cudaFuncSetAttribute(fa_bwd_dkdv_kernel<DH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             CK::kSmem),
+                        true);
+    (void)once;
+    p.blocks = kv_items;
+    p.blocks2 = kv_items2;
+    fa_bwd_dkdv_kernel<DH, NS><<<dim3(n_kv, a.H), kThreads, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
+  }
+}
+
+}  // namespace
+
+void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
+                    const int2* kv_items2, int n_kv, cudaStream_t stream) {
+  attn_bwd_pre(a, stream);
+  if (a.dh == 64) launch_bwd<64>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
+  else if (a.dh == 128) launch_bwd<128>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
+  else throw std::invalid_argument("attention: head_dim must be 64 or 128");
+}
+
+}  // namespace ttb

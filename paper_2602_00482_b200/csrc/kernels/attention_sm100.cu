@@ -1,0 +1,315 @@
+// tcgen05 / TMEM / TMA segment attention forward over the device KV stack (sm_100a).
+//
+// Replaces detail::attention_probs + the PV loop (model.hpp:298-321, 386-408). One CTA = one
+// (128-query block of one segment, head). Keys are the stack prefix rows [0, S) (full) followed by
+// the segment's own rows (causal); no tree mask is materialised.
+//
+// Roles (192 threads):
+//   warp 0      TMA producer: Q once, then K/V blocks into an NS-stage ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
+//                 S_j = Q K_j^T  (M=128, N=BKV, K=dh)  -> TMEM S[j%2]   (fp32)
+//                 O  += P_j V_j  (M=128, N=dh,  K=BKV) -> TMEM O        (fp32)
+//   warps 2..5  softmax, one query row per thread (TMEM lane): online max/sum in the log2 domain,
+//               P_j (bf16) into 128B-swizzled smem (the UMMA K-major A layout), O rescale in TMEM
+// Barriers: q_full, kv_full/kv_empty[NS], s_full[2], p_full[2], pv_done.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+
+#include "attention.h"
+#include "gemm.h"
+#include "sm100.cuh"
+
+namespace ttb {
+
+namespace {
+
+constexpr int kFwdThreads = 192;
+constexpr int kBQ = 128;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int DH, int BKV, int NS>
+struct FwdCfg {
+  static constexpr int kQBytes = kBQ * DH * 2;
+  static constexpr int kKVBytes = BKV * DH * 2;           // one K (or V) tile
+  static constexpr int kPBytes = kBQ * BKV * 2;           // one P tile
+  static constexpr int kOffK = kQBytes;
+  static constexpr int kOffV = kOffK + NS * kKVBytes;
+  static constexpr int kOffP = kOffV + NS * kKVBytes;
+  static constexpr int kOffBar = kOffP + 2 * kPBytes;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static constexpr int kTmemCols = (2 * BKV + DH) <= 256 ? 256 : 512;
+  static constexpr uint32_t kIdescS = make_idesc_bf16(128, BKV, false, false);
+  static constexpr uint32_t kIdescO = make_idesc_bf16(128, DH, false, true);
+};
+
+struct FwdParams {
+  __nv_bfloat16* o;
+  long ldo;
+  float* lse;
+  int n, S, H;
+  const int4* qblocks;
+  float scale_log2;
+};
+
+template <int DH, int BKV, int NS>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    fa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                  const __grid_constant__ CUtensorMap tm_v, FwdParams p) {
+  using C = FwdCfg<DH, BKV, NS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + NS;
+  uint64_t* s_full = kv_empty + NS;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_done = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+
+  const int warp = warp_id_sync();
+  const int lane = threadIdx.x & 31;
+  const int4 blk = p.qblocks[blockIdx.x];
+  const int q_start = blk.x, q_end = blk.y, seg_off = blk.z;
+  const int h = blockIdx.y;
+  const int S = p.S;
+  const int n_pre = (S + BKV - 1) / BKV;
+  const int own_rows = q_end - seg_off;
+  const int n_own = (own_rows + BKV - 1) / BKV;
+  const int nblk = n_pre + n_own;
+  auto kv_row0 = [&](int j) { return j < n_pre ? j * BKV : S + seg_off + (j - n_pre) * BKV; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4);
+    }
+    mbar_init(pv_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_S = tmem;             // 2 x BKV columns
+  const uint32_t tmem_O = tmem + 2 * BKV;   // DH columns
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, C::kQBytes);
+#pragma unroll
+      for (int pn = 0; pn < DH / 64; ++pn) tma_load_2d(&tm_q, q_full, smem + pn * (kBQ * 128), h * DH + pn * 64, q_start);
+      for (int j = 0; j < nblk; ++j) {
+        const int st = j % NS;
+        const uint32_t ph = (j / NS) & 1;
+        mbar_wait(&kv_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], 2 * C::kKVBytes);
+        const int r0 = kv_row0(j);
+        uint8_t* ks = smem + C::kOffK + st * C::kKVBytes;
+        uint8_t* vs = smem + C::kOffV + st * C::kKVBytes;
+#pragma unroll
+        for (int pn = 0; pn < DH / 64; ++pn) {
+          tma_load_2d(&tm_k, &kv_full[st], ks + pn * (BKV * 128), h * DH + pn * 64, r0);
+          tma_load_2d(&tm_v, &kv_full[st], vs + pn * (BKV * 128), h * DH + pn * 64, r0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    const uint32_t q_addr = smem_u32(smem);
+    auto issue_s = [&](int j) {
+      const int st = j % NS;
+      mbar_wait(&kv_full[st], (j / NS) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t k_addr = smem_u32(smem + C::kOffK + st * C::kKVBytes);
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k) {
+          const uint64_t da = make_sdesc_sw128(q_addr + (k / 4) * (kBQ * 128) + (k % 4) * 32, 16, 1024);
+          const uint64_t db = make_sdesc_sw128(k_addr + (k / 4) * (BKV * 128) + (k % 4) * 32, 16, 1024);
+          umma_bf16_ss(tmem_S + (j & 1) * BKV, da, db, C::kIdescS, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[j & 1]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    issue_s(0);
+    if (nblk > 1) issue_s(1);
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const int st = j % NS;
+        const uint32_t p_addr = smem_u32(smem + C::kOffP + (j & 1) * C::kPBytes);
+        const uint32_t v_addr = smem_u32(smem + C::kOffV + st * C::kKVBytes);
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k) {
+          const uint64_t da = make_sdesc_sw128(p_addr + (k / 4) * (kBQ * 128) + (k % 4) * 32, 16, 1024);
+          const uint64_t db = make_sdesc_sw128(v_addr + k * 2048, BKV * 128, 1024);
+          umma_bf16_ss(tmem_O, da, db, C::kIdescO, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&kv_empty[st]);
+        umma_commit(pv_done);
+      }
+      __syncwarp();
+      if (j + 2 < nblk) issue_s(j + 2);
+    }
+  } else {
+    // ------------------------------------------------------------------ softmax (one row per thread)
+    const int quad = warp & 3;
+    const int rloc = quad * 32 + lane;  // row within the tile == TMEM lane
+    const int row = q_start + rloc;
+    const int t = row - seg_off;        // local query index within the segment
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      float s[BKV];
+#pragma unroll
+      for (int c = 0; c < BKV; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem_S + (j & 1) * BKV + c + lane_off, r);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(r[i]);
+      }
+      tmem_ld_wait();
+      const bool pre = j < n_pre;
+      const int base = pre ? j * BKV : (j - n_pre) * BKV;  // key index of column 0 (prefix row / own local)
+      float mb = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < BKV; ++i) {
+        const bool ok = pre ? (base + i < S) : (base + i <= t);
+        s[i] = ok ? s[i] * p.scale_log2 : -INFINITY;
+        mb = fmaxf(mb, s[i]);
+      }
+      const float m_new = fmaxf(m, mb);
+      const float mref = m_new == -INFINITY ? 0.f : m_new;
+      const float corr = exp2f(m - mref);
+      float rs = 0.f;
+      uint8_t* pbuf = smem + C::kOffP + (j & 1) * C::kPBytes;
+#pragma unroll
+      for (int pn = 0; pn < BKV / 64; ++pn) {
+#pragma unroll
+        for (int cch = 0; cch < 8; ++cch) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a = exp2f(s[pn * 64 + cch * 8 + 2 * e] - mref);
+            const float b = exp2f(s[pn * 64 + cch * 8 + 2 * e + 1] - mref);
+            rs += a + b;
+            w[e] = pack_bf16x2(a, b);
+          }
+          // 128B swizzle: 16B chunk index XOR (row % 8)
+          uint4* dst = reinterpret_cast<uint4*>(pbuf + pn * (kBQ * 128) + rloc * 128 + ((cch ^ (rloc & 7)) * 16));
+          *dst = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      l = l * corr + rs;
+      m = m_new;
+      if (j > 0) {
+        // O (from PV_{j-1}) must be final before it is rescaled and before P_j overwrites P_{j-2}
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffff, corr != 1.0f)) {
+#pragma unroll
+          for (int c = 0; c < DH; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(tmem_O + c + lane_off, r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+            tmem_st16(tmem_O + c + lane_off, r);
+          }
+          tmem_st_wait();
+        }
+      }
+      fence_proxy_async_smem();  // P stores (generic proxy) -> visible to tcgen05.mma (async proxy)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+    }
+    mbar_wait(pv_done, (nblk - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+    if (row < q_end) {
+      __nv_bfloat16* orow = p.o + static_cast<long>(row) * p.ldo + h * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem_O + c + lane_off, r);
+        tmem_ld_wait();
+        uint4 w0, w1;
+        w0.x = pack_bf16x2(__uint_as_float(r[0]) * inv_l, __uint_as_float(r[1]) * inv_l);
+        w0.y = pack_bf16x2(__uint_as_float(r[2]) * inv_l, __uint_as_float(r[3]) * inv_l);
+        w0.z = pack_bf16x2(__uint_as_float(r[4]) * inv_l, __uint_as_float(r[5]) * inv_l);
+        w0.w = pack_bf16x2(__uint_as_float(r[6]) * inv_l, __uint_as_float(r[7]) * inv_l);
+        w1.x = pack_bf16x2(__uint_as_float(r[8]) * inv_l, __uint_as_float(r[9]) * inv_l);
+        w1.y = pack_bf16x2(__uint_as_float(r[10]) * inv_l, __uint_as_float(r[11]) * inv_l);
+        w1.z = pack_bf16x2(__uint_as_float(r[12]) * inv_l, __uint_as_float(r[13]) * inv_l);
+        w1.w = pack_bf16x2(__uint_as_float(r[14]) * inv_l, __uint_as_float(r[15]) * inv_l);
+        *reinterpret_cast<uint4*>(orow + c) = w0;
+        *reinterpret_cast<uint4*>(orow + c + 8) = w1;
+      }
+      p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(l)) * 0.6931471805599453f;
+    } else {
+      // keep the warp-collective TMEM loads convergent
+#pragma unroll
+      for (int c = 0; c < DH; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem_O + c + lane_off, r);
+        tmem_ld_wait();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
+}
+
+template <int DH, int BKV, int NS>
+void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
+  using C = FwdCfg<DH, BKV, NS>;
+  CUtensorMap tq, tk, tv;
+  const int d = a.H * DH;
+  make_tmap_bf16(&tq, a.q, d, a.n, a.ldq, 64, kBQ);
+  make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, BKV);
+  make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, BKV);
+  static bool once = (cudaFuncSetAttribute(fa_fwd_kernel<DH, BKV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           C::kSmem),
+                      true);
+  (void)once;
+  FwdParams p{a.o, a.ldo, a.lse, a.n, a.S, a.H, a.qblocks, a.scale * kLog2e};
+  dim3 grid(a.nqb, a.H);
+  fa_fwd_kernel<DH, BKV, NS><<<grid, kFwdThreads, C::kSmem, stream>>>(tq, tk, tv, p);
+}
+
+}  // namespace
+
+// Forward with 128-query blocks (qblocks built with kFwdBlockQ rows). rows_cap = stack rows.
+void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
+  if (a.nqb == 0) return;
+  if (a.dh == 64) launch_fwd<64, 128, 3>(a, rows_cap, stream);
+  else if (a.dh == 128) launch_fwd<128, 64, 3>(a, rows_cap, stream);
+  else throw std::invalid_argument("attention: head_dim must be 64 or 128");
+}
+
+}  // namespace ttb

@@ -199,3 +199,13 @@ def test_errors_surface_as_exceptions():
     long = [tt.TokenSequence(0, [1] * (cfg.max_position + 1))]
     with pytest.raises(ValueError):
         eng.tree_train_step(tt.build_prefix_tree(long))
+
+
+@pytest.mark.parametrize("fwd_impl,bwd_impl", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_attention_impls_agree_on_tree(fwd_impl, bwd_impl):
+    # mma.sync (sm80-style baseline) and tcgen05 attention give the same step within tolerance
+    cfg, flat, eng = make(SMALL, 12)
+    eng.set_option("attn_fwd_impl", fwd_impl)
+    eng.set_option("attn_bwd_impl", bwd_impl)
+    seqs = O.grouped_corpus(2, 4, 150, 200, cfg.vocab_size, 13, shared_response=20, weight_jitter=True)
+    tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())

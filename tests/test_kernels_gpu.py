@@ -111,3 +111,74 @@ def test_gemm_large_vocab_head():
     _gemm(x, 0, w, 1, M, N, K, EPI_STORE_F32, [out], N)
     ref = x.float() @ w.float()
     assert _rel(out, ref) < 1e-5
+
+
+# ----------------------------------------------------------------------------- segment attention
+def _attn_ref(q, K, V, S, H, dh):
+    """fp32 reference of one segment's attention over stack rows [0,S) + own rows (causal)."""
+    n = q.shape[0]
+    ctx = S + n
+    qh = q.float().view(n, H, dh).transpose(0, 1)
+    kh = K[:ctx].float().view(ctx, H, dh).transpose(0, 1)
+    vh = V[:ctx].float().view(ctx, H, dh).transpose(0, 1)
+    s = qh @ kh.transpose(1, 2) / dh ** 0.5
+    mask = torch.arange(ctx, device=q.device)[None, :] > (S + torch.arange(n, device=q.device))[:, None]
+    s = s.masked_fill(mask[None], float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    p = torch.softmax(s, -1)
+    o = (p @ vh).transpose(0, 1).reshape(n, H * dh)
+    return o, lse
+
+
+def _attn(impl, dirn, q, K, V, o, lse, dO=None, D=None, dq=None, dk=None, dv=None, S=0, H=1, dh=64):
+    lib = _lib()
+    vp = ctypes.c_void_p
+    p = lambda t: vp(t.data_ptr()) if t is not None else vp(0)
+    rc = lib.tt_debug_attn(impl, dirn, p(q), p(K), p(V), p(o), p(lse), p(dO), p(D), p(dq), p(dk), p(dv),
+                           q.shape[0], S, H, dh, ctypes.c_long(K.shape[0]))
+    assert rc == 0, lib.tt_last_error().decode()
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("n,S,H,dh", [(128, 0, 2, 64), (300, 200, 2, 64), (77, 1000, 4, 64), (513, 129, 2, 128),
+                                      (64, 64, 3, 128), (1000, 1024, 1, 64)])
+def test_attention_forward(impl, n, S, H, dh):
+    torch.manual_seed(n + S)
+    d = H * dh
+    rows = S + n + 37
+    q = torch.randn(n, d, device="cuda").bfloat16()
+    K = torch.randn(rows, d, device="cuda").bfloat16()
+    V = torch.randn(rows, d, device="cuda").bfloat16()
+    o = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, n, device="cuda", dtype=torch.float32)
+    _attn(impl, 0, q, K, V, o, lse, S=S, H=H, dh=dh)
+    oref, lref = _attn_ref(q, K, V, S, H, dh)
+    assert _rel(o, oref) < 1e-2, _rel(o, oref)
+    assert (lse - lref).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("n,S,H,dh", [(300, 200, 2, 64), (513, 129, 2, 128), (100, 0, 2, 64), (1200, 1024, 2, 64),
+                                      (64, 300, 1, 128)])
+def test_attention_backward(impl, n, S, H, dh):
+    torch.manual_seed(7 + n)
+    d = H * dh
+    rows = S + n + 11
+    q = torch.randn(n, d, device="cuda").bfloat16()
+    K = torch.randn(rows, d, device="cuda").bfloat16()
+    V = torch.randn(rows, d, device="cuda").bfloat16()
+    dO = torch.randn(n, d, device="cuda").bfloat16()
+    o = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, n, device="cuda", dtype=torch.float32)
+    _attn(1, 0, q, K, V, o, lse, S=S, H=H, dh=dh)
+    D = torch.empty(H, n, device="cuda")
+    dq = torch.empty(n, d, device="cuda")
+    dk = torch.zeros(rows, d, device="cuda")
+    dv = torch.zeros(rows, d, device="cuda")
+    _attn(impl, 1, q, K, V, o, lse, dO, D, dq, dk, dv, S=S, H=H, dh=dh)
+    qf, Kf, Vf = (t.float().requires_grad_() for t in (q, K, V))
+    of, _ = _attn_ref(qf, Kf, Vf, S, H, dh)
+    of.backward(dO.float())
+    assert _rel(dq, qf.grad) < 2e-2
+    assert _rel(dk, Kf.grad) < 2e-2
+    assert _rel(dv, Vf.grad) < 2e-2

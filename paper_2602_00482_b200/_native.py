@@ -62,7 +62,7 @@ EXPORTS = {
     "tt_engine_set_profiling": [vp, i32],
     "tt_engine_set_option": [vp, c.c_char_p, c.c_int64],
     "tt_debug_attn": [c.c_int, c.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, c.c_int, c.c_int, c.c_int, c.c_int,
-                      c.c_long],
+                      c.c_long, c.c_int, P(c.c_float)],
     "tt_engine_profile": [vp, P(f64), P(f64), P(f64), P(u64), i32],
     "tt_segment_push": [vp, P(i32), u64, P(c.c_float)],
     "tt_segment_pop": [vp, P(c.c_float), P(c.c_float)],
@@ -71,6 +71,9 @@ EXPORTS = {
     "tt_last_error": [],
     "tt_debug_gemm": [vp, c.c_long, c.c_int, vp, c.c_long, c.c_int, c.c_int, c.c_int, c.c_int, c.c_int, vp, vp, vp,
                       c.c_long, c.c_int, vp, vp, c.c_int],
+    "tt_debug_gemm_async": [vp, c.c_long, c.c_int, vp, c.c_long, c.c_int, c.c_int, c.c_int, c.c_int, c.c_int, vp, vp,
+                            vp, c.c_long, c.c_int, vp, vp, c.c_int],
+    "tt_debug_gemm_splits": [c.c_int, c.c_int, c.c_int],
 }
 
 

@@ -12,10 +12,10 @@
 
 extern "C" {
 
-// C = A * B^T with the operand majorness flags of ttb::GemmOperand; see gemm.h for modes.
-int tt_debug_gemm(const void* a, long lda, int a_mn, const void* b, long ldb, int b_mn, int M, int N, int K, int mode,
-                  void* out0, void* out1, void* out2, long ldo, int split_w, void* out_act, const void* aux,
-                  int splits) {
+namespace {
+int debug_gemm(bool sync, const void* a, long lda, int a_mn, const void* b, long ldb, int b_mn, int M, int N, int K,
+               int mode, void* out0, void* out1, void* out2, long ldo, int split_w, void* out_act, const void* aux,
+               int splits) {
   return ttb::guarded([&] {
     ttb::GemmOperand A{static_cast<const __nv_bfloat16*>(a), lda, a_mn != 0};
     ttb::GemmOperand B{static_cast<const __nv_bfloat16*>(b), ldb, b_mn != 0};
@@ -30,18 +30,55 @@ int tt_debug_gemm(const void* a, long lda, int a_mn, const void* b, long ldb, in
     e.ldo2 = ldo;
     e.aux = static_cast<const __nv_bfloat16*>(aux);
     e.ld_aux = ldo;
+    e.resid = static_cast<const float*>(aux);  // EPI_RESID_F32: aux is the fp32 residual input
+    e.ld_resid = ldo;
     ttb::gemm_bf16(A, B, M, N, K, e, splits, nullptr);
     ttb::check_cuda(cudaGetLastError(), "tt_debug_gemm launch");
-    ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_gemm sync");
+    if (sync) ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_gemm sync");
   });
 }
+}  // namespace
+
+// C = A * B^T with the operand majorness flags of ttb::GemmOperand; see gemm.h for modes.
+int tt_debug_gemm(const void* a, long lda, int a_mn, const void* b, long ldb, int b_mn, int M, int N, int K, int mode,
+                  void* out0, void* out1, void* out2, long ldo, int split_w, void* out_act, const void* aux,
+                  int splits) {
+  return debug_gemm(true, a, lda, a_mn, b, ldb, b_mn, M, N, K, mode, out0, out1, out2, ldo, split_w, out_act, aux,
+                    splits);
+}
+// Same without the device synchronisation (for timing loops).
+int tt_debug_gemm_async(const void* a, long lda, int a_mn, const void* b, long ldb, int b_mn, int M, int N, int K,
+                        int mode, void* out0, void* out1, void* out2, long ldo, int split_w, void* out_act,
+                        const void* aux, int splits) {
+  return debug_gemm(false, a, lda, a_mn, b, ldb, b_mn, M, N, K, mode, out0, out1, out2, ldo, split_w, out_act, aux,
+                    splits);
+}
+int tt_debug_gemm_splits(int M, int N, int K) { return ttb::gemm_choose_splits(M, N, K); }
 
 // Segment attention on one segment of n queries over stack rows [0, S) + own rows [S, S+n)
 // (k/v: [rows_cap x H*dh] bf16). dir 0: forward (impl 0 = mma.sync, 1 = tcgen05) -> o, lse.
 // dir 1: backward (impl 0 = mma.sync) from o, lse, dO -> dq (overwritten), dk/dv (added).
+// iters > 0: additionally time `iters` back-to-back launches with CUDA events -> *ms_out (per launch).
 int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v, void* o, float* lse, const void* dO,
-                  float* D, float* dq, float* dk, float* dv, int n, int S, int H, int dh, long rows_cap) {
+                  float* D, float* dq, float* dk, float* dv, int n, int S, int H, int dh, long rows_cap, int iters,
+                  float* ms_out) {
   return ttb::guarded([&] {
+    cudaEvent_t e0, e1;
+    ttb::check_cuda(cudaEventCreate(&e0), "event");
+    ttb::check_cuda(cudaEventCreate(&e1), "event");
+    auto timed = [&](auto&& launch) {
+      launch();
+      if (iters > 0 && ms_out) {
+        ttb::check_cuda(cudaDeviceSynchronize(), "sync");
+        cudaEventRecord(e0, nullptr);
+        for (int i = 0; i < iters; ++i) launch();
+        cudaEventRecord(e1, nullptr);
+        ttb::check_cuda(cudaEventSynchronize(e1), "sync");
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *ms_out = ms / iters;
+      }
+    };
     const int d = H * dh;
     std::vector<int> q64, q128, it, it2;
     for (int qs = 0; qs < n; qs += 64) q64.insert(q64.end(), {qs, std::min(qs + 64, n), 0, 0});
@@ -80,11 +117,11 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
       if (impl == 1) {
         a.qblocks = static_cast<const int4*>(d128);
         a.nqb = static_cast<int>(q128.size() / 4);
-        ttb::attn_fwd_sm100(a, rows_cap, nullptr);
+        timed([&] { ttb::attn_fwd_sm100(a, rows_cap, nullptr); });
       } else {
         a.qblocks = static_cast<const int4*>(d64);
         a.nqb = static_cast<int>(q64.size() / 4);
-        ttb::attn_fwd(a, nullptr);
+        timed([&] { ttb::attn_fwd(a, nullptr); });
       }
     } else {
       ttb::AttnBwdArgs a;
@@ -121,15 +158,19 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
           k128b.insert(k128b.end(), {0, 1});
         }
         void *dk128 = up(k128), *dk128b = up(k128b);
-        ttb::attn_bwd_sm100(a, rows_cap, static_cast<const int4*>(d128), static_cast<int>(q128.size() / 4),
-                            static_cast<const int4*>(dk128), static_cast<const int2*>(dk128b),
-                            static_cast<int>(k128.size() / 4), nullptr);
+        timed([&] {
+          ttb::attn_bwd_sm100(a, rows_cap, static_cast<const int4*>(d128), static_cast<int>(q128.size() / 4),
+                              static_cast<const int4*>(dk128), static_cast<const int2*>(dk128b),
+                              static_cast<int>(k128.size() / 4), nullptr);
+        });
         ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_attn sync");
         cudaFree(dk128);
         cudaFree(dk128b);
       } else {
-        ttb::check_cuda(cudaMemset(dq, 0, static_cast<size_t>(n) * d * 4), "memset");
-        ttb::attn_bwd(a, nullptr);
+        timed([&] {
+          cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d * 4, nullptr);
+          ttb::attn_bwd(a, nullptr);
+        });
       }
     }
     ttb::check_cuda(cudaGetLastError(), "tt_debug_attn launch");
@@ -138,6 +179,8 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
     cudaFree(d128);
     cudaFree(dit);
     cudaFree(dit2);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }
 

@@ -34,6 +34,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // Writes one thread's row of 64 bf16 values (packed pairs w[32]) into a 128B-swizzled K-major panel.
 __device__ __forceinline__ void st_row_sw128(uint8_t* panel, int row, const uint32_t (&w)[32]) {
@@ -201,8 +206,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int t = row - seg_off;
     const bool row_ok = row < q_end;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const float lse2 = row_ok ? p.lse[static_cast<long>(h) * p.n + row] * kLog2e : 0.f;
+    // invalid rows: lse2 = +inf -> P = 0 (their dQ rows are never stored)
+    const float lse2 = row_ok ? p.lse[static_cast<long>(h) * p.n + row] * kLog2e : INFINITY;
     const float Dr = row_ok ? p.D[static_cast<long>(h) * p.n + row] : 0.f;
+    const float c2 = p.scale_log2;
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
@@ -221,17 +228,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       const bool pre = j < n_pre;
       const int base = pre ? j * BKV : (j - n_pre) * BKV;
+      const int lim = pre ? (S - base) : (t - base + 1);  // valid key columns [0, lim)
+      if (__any_sync(0xffffffff, lim < BKV)) {
+#pragma unroll
+        for (int i = 0; i < BKV; ++i) s[i] = i < lim ? s[i] : -INFINITY;
+      }
       uint32_t w[32];
 #pragma unroll
       for (int i = 0; i < BKV; i += 2) {
-        float ds2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const bool ok = row_ok && (pre ? (base + i + e < S) : (base + i + e <= t));
-          const float pv = ok ? exp2f(s[i + e] * p.scale_log2 - lse2) : 0.f;
-          ds2[e] = pv * (dp[i + e] - Dr);
-        }
-        w[i / 2] = pack_bf16x2(ds2[0], ds2[1]);
+        const float p0 = ex2_approx(fmaf(s[i], c2, -lse2));
+        const float p1 = ex2_approx(fmaf(s[i + 1], c2, -lse2));
+        w[i / 2] = pack_bf16x2(p0 * (dp[i] - Dr), p1 * (dp[i + 1] - Dr));
       }
       if (j >= 2) mbar_wait(&ds_free[j & 1], ((j >> 1) + 1) & 1);
       st_row_sw128(smem + C::kOffDS + (j & 1) * C::kDSBytes, rloc, w);
@@ -438,20 +445,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tmem_ld_wait();
+      // own rows: key kt sees query t iff kt <= t, i.e. columns qi >= kt - (q0 - seg_off) (invalid
+      // queries beyond q_hi already have lse2 = +inf -> P = 0; invalid keys are never stored)
+      if (own) {
+        const int lo = kt - (q0 - seg_off);
+        if (__any_sync(0xffffffff, lo > 0)) {
+#pragma unroll
+          for (int c = 0; c < BQ; ++c) s[c] = c >= lo ? s[c] : -INFINITY;
+        }
+      }
+      const float c2 = p.scale_log2;
       uint32_t wp[32], wd[32];
 #pragma unroll
-      for (int c = 0; c < BQ; c += 2) {
-        float pv[2], dv2[2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int qi = c + e;
-          bool ok = key_ok;
-          if (own) ok = ok && (kt <= q0 + qi - seg_off);
-          pv[e] = ok ? exp2f(s[qi] * p.scale_log2 - st_lse[qi]) : 0.f;
-          dv2[e] = pv[e] * (dp[qi] - st_D[qi]);
-        }
-        wp[c / 2] = pack_bf16x2(pv[0], pv[1]);
-        wd[c / 2] = pack_bf16x2(dv2[0], dv2[1]);
+      for (int c = 0; c < BQ; c += 4) {
+        const float4 lz = *reinterpret_cast<const float4*>(st_lse + c);
+        const float4 dz = *reinterpret_cast<const float4*>(st_D + c);
+        const float p0 = ex2_approx(fmaf(s[c], c2, -lz.x)), p1 = ex2_approx(fmaf(s[c + 1], c2, -lz.y));
+        const float p2 = ex2_approx(fmaf(s[c + 2], c2, -lz.z)), p3 = ex2_approx(fmaf(s[c + 3], c2, -lz.w));
+        wp[c / 2] = pack_bf16x2(p0, p1);
+        wp[c / 2 + 1] = pack_bf16x2(p2, p3);
+        wd[c / 2] = pack_bf16x2(p0 * (dp[c] - dz.x), p1 * (dp[c + 1] - dz.y));
+        wd[c / 2 + 1] = pack_bf16x2(p2 * (dp[c + 2] - dz.z), p3 * (dp[c + 3] - dz.w));
       }
       if (i >= 2) mbar_wait(&p_free[i & 1], ((i >> 1) + 1) & 1);
       st_row_sw128(smem + C::kOffP + (i & 1) * C::kPBytes, krow, wp);

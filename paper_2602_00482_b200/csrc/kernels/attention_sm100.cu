@@ -33,6 +33,12 @@ constexpr float kLog2e = 1.4426950408889634f;
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: P stays <= 256
 
 template <int DH, int BKV, int NS>
 struct FwdCfg {
@@ -179,7 +185,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int row = q_start + rloc;
     const int t = row - seg_off;        // local query index within the segment
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    float m = -INFINITY, l = 0.f;
+    // m_used: the exponent base actually applied (log2 domain). It only moves when the running max
+    // exceeds it by more than kRescaleThreshold (P <= 2^8 then), so O in TMEM is rescaled rarely.
+    float m_used = -INFINITY, l = 0.f;
+    const float c2 = p.scale_log2;
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
@@ -194,18 +203,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tmem_ld_wait();
       const bool pre = j < n_pre;
       const int base = pre ? j * BKV : (j - n_pre) * BKV;  // key index of column 0 (prefix row / own local)
-      float mb = -INFINITY;
+      // warp-uniform: does any lane of this warp need masking in this block?
+      const int lim = pre ? (S - base) : (t - base + 1);   // valid columns are [0, lim)
+      if (__any_sync(0xffffffff, lim < BKV)) {
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) {
-        const bool ok = pre ? (base + i < S) : (base + i <= t);
-        s[i] = ok ? s[i] * p.scale_log2 : -INFINITY;
-        mb = fmaxf(mb, s[i]);
+        for (int i = 0; i < BKV; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
-      const float m_new = fmaxf(m, mb);
-      const float mref = m_new == -INFINITY ? 0.f : m_new;
-      const float corr = exp2f(m - mref);
+      float mx = s[0];
+#pragma unroll
+      for (int i = 1; i < BKV; ++i) mx = fmaxf(mx, s[i]);
+      const float m_new = fmaxf(m_used, mx * c2);
+      const bool resc = m_new > m_used + kRescaleThreshold;
+      float corr = 1.f;
+      if (resc) {
+        corr = ex2_approx(m_used - m_new);  // 0 on the first block (m_used = -inf)
+        m_used = m_new;
+        l *= corr;
+      }
+      const float mb = m_used == -INFINITY ? 0.f : m_used;
       float rs = 0.f;
-      uint8_t* pbuf = smem + C::kOffP + (j & 1) * C::kPBytes;
+      uint8_t* pbuf = smem + C::kOffP + (j & 1) * C::kPBytes;  // free: S_j's commit covers PV_{j-2}
 #pragma unroll
       for (int pn = 0; pn < BKV / 64; ++pn) {
 #pragma unroll
@@ -213,8 +230,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float a = exp2f(s[pn * 64 + cch * 8 + 2 * e] - mref);
-            const float b = exp2f(s[pn * 64 + cch * 8 + 2 * e + 1] - mref);
+            const float a = ex2_approx(fmaf(s[pn * 64 + cch * 8 + 2 * e], c2, -mb));
+            const float b = ex2_approx(fmaf(s[pn * 64 + cch * 8 + 2 * e + 1], c2, -mb));
             rs += a + b;
             w[e] = pack_bf16x2(a, b);
           }
@@ -223,40 +240,40 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           *dst = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
-      l = l * corr + rs;
-      m = m_new;
-      if (j > 0) {
-        // O (from PV_{j-1}) must be final before it is rescaled and before P_j overwrites P_{j-2}
+      l += rs;
+      if (j > 0 && __any_sync(0xffffffff, resc)) {
+        // O (from PV_{j-1}) must be final before it is rescaled
         mbar_wait(pv_done, (j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffff, corr != 1.0f)) {
 #pragma unroll
-          for (int c = 0; c < DH; c += 16) {
-            uint32_t r[16];
-            tmem_ld16(tmem_O + c + lane_off, r);
-            tmem_ld_wait();
+        for (int c = 0; c < DH; c += 16) {
+          uint32_t r[16];
+          tmem_ld16(tmem_O + c + lane_off, r);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
-            tmem_st16(tmem_O + c + lane_off, r);
-          }
-          tmem_st_wait();
+          for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+          tmem_st16(tmem_O + c + lane_off, r);
         }
+        tmem_st_wait();
       }
       fence_proxy_async_smem();  // P stores (generic proxy) -> visible to tcgen05.mma (async proxy)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
+    const float m = m_used;
     mbar_wait(pv_done, (nblk - 1) & 1);
     tc_fence_after();
     const float inv_l = 1.f / l;
-    if (row < q_end) {
-      __nv_bfloat16* orow = p.o + static_cast<long>(row) * p.ldo + h * DH;
+    // tcgen05.ld is .sync.aligned: every lane executes it (convergently); only valid rows store.
+    const bool row_ok = row < q_end;
+    __nv_bfloat16* orow = p.o + static_cast<long>(row) * p.ldo + h * DH;
 #pragma unroll
-      for (int c = 0; c < DH; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem_O + c + lane_off, r);
-        tmem_ld_wait();
+    for (int c = 0; c < DH; c += 16) {
+      uint32_t r[16];
+      tmem_ld16(tmem_O + c + lane_off, r);
+      tmem_ld_wait();
+      if (row_ok) {
         uint4 w0, w1;
         w0.x = pack_bf16x2(__uint_as_float(r[0]) * inv_l, __uint_as_float(r[1]) * inv_l);
         w0.y = pack_bf16x2(__uint_as_float(r[2]) * inv_l, __uint_as_float(r[3]) * inv_l);
@@ -269,16 +286,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         *reinterpret_cast<uint4*>(orow + c) = w0;
         *reinterpret_cast<uint4*>(orow + c + 8) = w1;
       }
-      p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(l)) * 0.6931471805599453f;
-    } else {
-      // keep the warp-collective TMEM loads convergent
-#pragma unroll
-      for (int c = 0; c < DH; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(tmem_O + c + lane_off, r);
-        tmem_ld_wait();
-      }
     }
+    if (row_ok) p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(l)) * 0.6931471805599453f;
   }
   tc_fence_before();
   __syncthreads();

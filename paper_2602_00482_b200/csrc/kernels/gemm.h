@@ -44,6 +44,7 @@ struct EpiParams {
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
                cudaStream_t stream);
 int gemm_choose_splits(int M, int N, int K);
+int gemm_pick_bn(int N, bool b_mn_major);
 void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
 

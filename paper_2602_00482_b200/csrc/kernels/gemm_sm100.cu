@@ -32,11 +32,11 @@ constexpr int kThreads = 192;
 
 template <int BN>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kStages = BN == 256 ? 4 : (BN == 192 ? 5 : 6);
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // two accumulator slots
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;  // two accumulator slots (power of 2)
   static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -187,10 +187,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row < M;
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(t_row + c, r);
+      for (int c2 = 0; c2 < BN; c2 += 32) {
+        uint32_t rr[2][16];
+        tmem_ld16(t_row + c2, rr[0]);
+        tmem_ld16(t_row + c2 + 16, rr[1]);
         tmem_ld_wait();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+        const int c = c2 + 16 * hh;
+        const uint32_t (&r)[16] = rr[hh];
         const int n = n_blk * BN + c;
         if (!row_ok || n >= N) continue;
         float v[16];
@@ -287,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           default:
             break;
         }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -371,20 +377,38 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
 
 }  // namespace
 
+int gemm_pick_bn(int N, bool b_mn_major) {
+  (void)b_mn_major;  // 128/192/256 are all multiples of the 64-element MN atom
+  // padded columns weighted by the per-tile overhead of narrower tiles (smem operand traffic)
+  int best = 256;
+  double best_cost = 0;
+  for (int bn : {256, 192, 128}) {
+    const double f = bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.10);
+    const double cost = static_cast<double>((N + bn - 1) / bn) * bn * f;
+    if (bn == 256 || cost < best_cost) {
+      best = bn;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
                cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   if (N % 16 != 0) throw std::invalid_argument("gemm_bf16: N must be a multiple of 16");
   if (splits > 1 && epi.mode != EPI_ADD_F32) throw std::invalid_argument("gemm_bf16: split-K needs EPI_ADD_F32");
-  const bool wide = (N % 256 == 0) || N > 4096;
+  const int bn = gemm_pick_bn(N, B.mn_major);
   const bool amn = A.mn_major, bmn = B.mn_major;
 #define TTB_DISPATCH(BN_)                                             \
   if (!amn && bmn) return launch<BN_, false, true>(A, B, M, N, K, epi, splits, stream);  \
   if (!amn && !bmn) return launch<BN_, false, false>(A, B, M, N, K, epi, splits, stream); \
   if (amn && bmn) return launch<BN_, true, true>(A, B, M, N, K, epi, splits, stream);     \
   return launch<BN_, true, false>(A, B, M, N, K, epi, splits, stream);
-  if (wide) {
+  if (bn == 256) {
     TTB_DISPATCH(256)
+  } else if (bn == 192) {
+    TTB_DISPATCH(192)
   } else {
     TTB_DISPATCH(128)
   }
@@ -397,7 +421,7 @@ int gemm_choose_splits(int M, int N, int K) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int bn = ((N % 256 == 0) || N > 4096) ? 256 : 128;
+  const int bn = gemm_pick_bn(N, true);
   const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int kb = (K + BK - 1) / BK;
   if (tiles >= g_num_sms || kb < 8) return 1;

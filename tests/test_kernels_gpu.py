@@ -37,7 +37,8 @@ def _rel(x, y):
     return ((x.float() - y.float()).norm() / (y.float().norm() + 1e-30)).item()
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 384, 192), (1, 512, 256), (300, 896, 896), (129, 4864, 896)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (200, 384, 192), (1, 512, 256), (300, 896, 896), (129, 4864, 896),
+                                   (260, 2688, 896), (64, 576, 128)])
 def test_gemm_fwd_kmajor_mnmajor(M, N, K):
     torch.manual_seed(0)
     x = torch.randn(M, K, device="cuda").bfloat16()
@@ -48,7 +49,7 @@ def test_gemm_fwd_kmajor_mnmajor(M, N, K):
     assert _rel(out, ref) < 1e-5
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 128, 256), (77, 896, 4864), (513, 256, 896)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 256), (77, 896, 4864), (513, 256, 896), (100, 2688, 256)])
 def test_gemm_dx_kmajor_kmajor(M, N, K):
     torch.manual_seed(1)
     dy = torch.randn(M, K, device="cuda").bfloat16()        # [tokens x N_w]
@@ -59,7 +60,8 @@ def test_gemm_dx_kmajor_kmajor(M, N, K):
     assert _rel(out, ref) < 1e-2
 
 
-@pytest.mark.parametrize("T,Kw,Nw,splits", [(64, 128, 128, 1), (1000, 256, 384, 1), (2048, 896, 896, 4), (333, 128, 512, 2)])
+@pytest.mark.parametrize("T,Kw,Nw,splits", [(64, 128, 128, 1), (1000, 256, 384, 1), (2048, 896, 896, 4), (333, 128, 512, 2),
+                                            (700, 896, 2688, 2)])
 def test_gemm_dw_mnmajor_mnmajor(T, Kw, Nw, splits):
     torch.manual_seed(2)
     x = torch.randn(T, Kw, device="cuda").bfloat16()
@@ -135,7 +137,7 @@ def _attn(impl, dirn, q, K, V, o, lse, dO=None, D=None, dq=None, dk=None, dv=Non
     vp = ctypes.c_void_p
     p = lambda t: vp(t.data_ptr()) if t is not None else vp(0)
     rc = lib.tt_debug_attn(impl, dirn, p(q), p(K), p(V), p(o), p(lse), p(dO), p(D), p(dq), p(dk), p(dv),
-                           q.shape[0], S, H, dh, ctypes.c_long(K.shape[0]))
+                           q.shape[0], S, H, dh, ctypes.c_long(K.shape[0]), 0, None)
     assert rc == 0, lib.tt_last_error().decode()
 
 

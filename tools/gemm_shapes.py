@@ -1,0 +1,78 @@
+"""Microbenchmark of the tcgen05 GEMM on the c2 (Qwen2-0.5B-shape) step shapes, timed alone with
+CUDA events (burst roofline: MEASURED_PEAKS.json bf16_tflops). Usage: python tools/gemm_shapes.py"""
+import ctypes
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_00482_b200 import _native  # noqa: E402
+
+EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU, EPI_RESID = range(6)
+n, d, F, V = 32768, 896, 4864, 151936
+SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
+    ("fwd qkv", n, 3 * d, d, 0, 1, EPI_STORE_BF16),
+    ("fwd o", n, d, d, 0, 1, EPI_RESID),
+    ("fwd mlp_in", n, F, d, 0, 1, EPI_SILU),
+    ("fwd mlp_out", n, d, F, 0, 1, EPI_RESID),
+    ("fwd head", 2048, V, d, 0, 1, EPI_STORE_F32),
+    ("dX mlp_out", n, F, d, 0, 0, EPI_DSILU),
+    ("dX mlp_in", n, d, F, 0, 0, EPI_STORE_F32),
+    ("dX o", n, d, d, 0, 0, EPI_STORE_BF16),
+    ("dX qkv", n, d, 3 * d, 0, 0, EPI_STORE_F32),
+    ("dX head", 2048, d, V, 0, 0, EPI_ADD_F32),
+    ("dW mlp_out", F, d, n, 1, 1, EPI_ADD_F32),
+    ("dW mlp_in", d, F, n, 1, 1, EPI_ADD_F32),
+    ("dW o", d, d, n, 1, 1, EPI_ADD_F32),
+    ("dW qkv", d, 3 * d, n, 1, 1, EPI_ADD_F32),
+    ("dW head", d, V, 2048, 1, 1, EPI_ADD_F32),
+]
+
+
+def main():
+    lib = _native.lib()
+    peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json"))) \
+        if os.path.exists("MEASURED_PEAKS.json") else {"bf16_tflops": 1590.0}
+    vp = ctypes.c_void_p
+    out = []
+    for label, M, N, K, amn, bmn, epi in SHAPES:
+        a = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
+        b = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
+        o32 = torch.zeros(M, N, device="cuda")
+        o16 = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        act = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        aux = torch.zeros(M, N, device="cuda", dtype=torch.float32 if epi == EPI_RESID else torch.bfloat16)
+        outp = o32 if epi in (EPI_STORE_F32, EPI_ADD_F32, EPI_RESID) else o16
+        lda = a.stride(0)
+        ldb = b.stride(0)
+        splits = lib.tt_debug_gemm_splits(M, N, K) if epi == EPI_ADD_F32 else 1
+
+        def run():
+            rc = lib.tt_debug_gemm_async(vp(a.data_ptr()), lda, amn, vp(b.data_ptr()), ldb, bmn, M, N, K, epi,
+                                   vp(outp.data_ptr()), vp(0), vp(0), N, 0, vp(act.data_ptr()), vp(aux.data_ptr()),
+                                   splits)
+            assert rc == 0, lib.tt_last_error()
+
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        it = 10
+        e0.record()
+        for _ in range(it):
+            run()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / it
+        tf = 2.0 * M * N * K / (ms / 1e3) / 1e12
+        out.append(dict(shape=label, M=M, N=N, K=K, ms=ms, tflops=tf, frac=tf / peaks["bf16_tflops"], splits=splits))
+        print(f"{label:12s} M={M:6d} N={N:6d} K={K:6d} splits={splits} {ms:8.3f} ms {tf:7.1f} TFLOP/s "
+              f"({100 * tf / peaks['bf16_tflops']:.0f}% of burst peak)", flush=True)
+        del a, b, o32, o16, act, aux
+    json.dump(out, open(os.environ.get("GEMM_SHAPES_OUT", "gpurun_out/gemm_shapes.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

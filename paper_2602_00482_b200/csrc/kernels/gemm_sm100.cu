@@ -28,7 +28,8 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quadrant)
+constexpr int kEpiWarps = 8;
 
 template <int BN>
 struct Cfg {
@@ -40,9 +41,15 @@ struct Cfg {
   static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-__device__ __forceinline__ float silu_f(float u) { return u / (1.0f + __expf(-u)); }
+__device__ __forceinline__ float fast_sigmoid(float u) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * u));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return r;
+}
+__device__ __forceinline__ float silu_f(float u) { return u * fast_sigmoid(u); }
 __device__ __forceinline__ float silu_grad_f(float u) {
-  const float s = 1.0f / (1.0f + __expf(-u));
+  const float s = fast_sigmoid(u);
   return s * (1.0f + u * (1.0f - s));
 }
 
@@ -77,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4);
+      mbar_init(&tempty_bar[s], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -175,7 +182,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int quad = warp & 3;             // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) / 4;       // which half of the BN columns this warp handles
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -186,8 +194,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = m_blk * BM + quad * 32 + lane;
       const bool row_ok = row < M;
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
-#pragma unroll 1
-      for (int c2 = 0; c2 < BN; c2 += 32) {
+#pragma unroll
+      for (int c2 = half * (BN / 2); c2 < (half + 1) * (BN / 2); c2 += 32) {
         uint32_t rr[2][16];
         tmem_ld16(t_row + c2, rr[0]);
         tmem_ld16(t_row + c2 + 16, rr[1]);
@@ -206,7 +214,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           blk = n / epi.split_w;
           nc = n - blk * epi.split_w;
         }
-        const long off = static_cast<long>(row) * epi.ldo[blk] + nc;
+        // select without dynamic indexing into the kernel-parameter arrays (avoids a local copy)
+        void* const outp = blk == 0 ? epi.out[0] : (blk == 1 ? epi.out[1] : epi.out[2]);
+        const long ldo = blk == 0 ? epi.ldo[0] : (blk == 1 ? epi.ldo[1] : epi.ldo[2]);
+        const long off = static_cast<long>(row) * ldo + nc;
         switch (epi.mode) {
           case EPI_STORE_BF16: {
             uint4 w0, w1;
@@ -214,19 +225,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             w0.z = pack_bf16x2(v[4], v[5]); w0.w = pack_bf16x2(v[6], v[7]);
             w1.x = pack_bf16x2(v[8], v[9]); w1.y = pack_bf16x2(v[10], v[11]);
             w1.z = pack_bf16x2(v[12], v[13]); w1.w = pack_bf16x2(v[14], v[15]);
-            uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[blk]) + off);
+            uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + off);
             p[0] = w0;
             p[1] = w1;
             break;
           }
           case EPI_STORE_F32: {
-            float4* p = reinterpret_cast<float4*>(static_cast<float*>(epi.out[blk]) + off);
+            float4* p = reinterpret_cast<float4*>(static_cast<float*>(outp) + off);
 #pragma unroll
             for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
             break;
           }
           case EPI_ADD_F32: {
-            float* p = static_cast<float*>(epi.out[blk]) + off;
+            float* p = static_cast<float*>(outp) + off;
             if (epi.atomic) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) red_add_v4_f32(p + 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);

@@ -27,24 +27,30 @@ namespace ttb {
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9: 2 per TMEM lane quadrant
+constexpr int kSmxWarps = 8;   // softmax-gradient warps; the pair on a quadrant splits the columns
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // Writes one thread's row of 64 bf16 values (packed pairs w[32]) into a 128B-swizzled K-major panel.
 __device__ __forceinline__ void st_row_sw128(uint8_t* panel, int row, const uint32_t (&w)[32]) {
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     uint4* dst = reinterpret_cast<uint4*>(panel + row * 128 + ((c ^ (row & 7)) * 16));
+    *dst = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+  }
+}
+
+// Writes 32 bf16 values (w[16] packed pairs) = chunks [4*half, 4*half+4) of a thread's 128B row.
+__device__ __forceinline__ void st_halfrow_sw128(uint8_t* panel, int row, int half, const uint32_t (&w)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int ch = half * 4 + c;
+    uint4* dst = reinterpret_cast<uint4*>(panel + row * 128 + ((ch ^ (row & 7)) * 16));
     *dst = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
   }
 }
@@ -61,8 +67,11 @@ struct DqCfg {
   static constexpr int kOffV = kOffK + NS * kKVBytes;
   static constexpr int kOffDS = kOffV + NS * kKVBytes;
   static constexpr int kOffBar = kOffDS + 2 * kDSBytes;
-  static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kTmemCols = (4 * BKV + DH) <= 256 ? 256 : 512;
+  // a second co-resident CTA could not get TMEM (it would block in tcgen05.alloc while holding the
+  // SM's warp slots): size smem so that exactly one CTA fits when all 512 columns are needed
+  static constexpr int kSmemUsed = kOffBar + 256 + 1024;
+  static constexpr int kSmem = (kTmemCols == 512 && kSmemUsed < 118 * 1024) ? 118 * 1024 : kSmemUsed;
   static constexpr uint32_t kIdescS = make_idesc_bf16(128, BKV, false, false);
   static constexpr uint32_t kIdescQ = make_idesc_bf16(128, DH, false, true);
 };
@@ -123,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&ds_full[s], 4);
+      mbar_init(&ds_full[s], kSmxWarps);
       mbar_init(&ds_free[s], 1);
     }
     mbar_init(dq_done, 1);
@@ -201,6 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quad = warp & 3;
+    const int half = (warp - 2) / 4;  // key columns [32*half, 32*half+32) of each 64-key block
     const int rloc = quad * 32 + lane;
     const int row = q_start + rloc;
     const int t = row - seg_off;
@@ -210,15 +220,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float lse2 = row_ok ? p.lse[static_cast<long>(h) * p.n + row] * kLog2e : INFINITY;
     const float Dr = row_ok ? p.D[static_cast<long>(h) * p.n + row] : 0.f;
     const float c2 = p.scale_log2;
+    constexpr int HC = BKV / 2;
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      float s[BKV], dp[BKV];
+      float s[HC], dp[HC];
 #pragma unroll
-      for (int c = 0; c < BKV; c += 16) {
+      for (int c = 0; c < HC; c += 16) {
         uint32_t r[16], r2[16];
-        tmem_ld16(t_S + (j & 1) * BKV + c + lane_off, r);
-        tmem_ld16(t_dP + (j & 1) * BKV + c + lane_off, r2);
+        tmem_ld16(t_S + (j & 1) * BKV + half * HC + c + lane_off, r);
+        tmem_ld16(t_dP + (j & 1) * BKV + half * HC + c + lane_off, r2);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           s[c + i] = __uint_as_float(r[i]);
@@ -227,21 +238,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_ld_wait();
       const bool pre = j < n_pre;
-      const int base = pre ? j * BKV : (j - n_pre) * BKV;
-      const int lim = pre ? (S - base) : (t - base + 1);  // valid key columns [0, lim)
-      if (__any_sync(0xffffffff, lim < BKV)) {
+      const int base = (pre ? j * BKV : (j - n_pre) * BKV) + half * HC;
+      const int lim = pre ? (S - base) : (t - base + 1);  // valid key columns [0, lim) of this half
+      if (__any_sync(0xffffffff, lim < HC)) {
 #pragma unroll
-        for (int i = 0; i < BKV; ++i) s[i] = i < lim ? s[i] : -INFINITY;
+        for (int i = 0; i < HC; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
-      uint32_t w[32];
+      uint32_t w[HC / 2];
+      const float2 c22 = make_float2(c2, c2), nl2 = make_float2(-lse2, -lse2), nD2 = make_float2(-Dr, -Dr);
 #pragma unroll
-      for (int i = 0; i < BKV; i += 2) {
-        const float p0 = ex2_approx(fmaf(s[i], c2, -lse2));
-        const float p1 = ex2_approx(fmaf(s[i + 1], c2, -lse2));
-        w[i / 2] = pack_bf16x2(p0 * (dp[i] - Dr), p1 * (dp[i + 1] - Dr));
+      for (int i = 0; i < HC; i += 2) {
+        const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), c22, nl2);
+        const float2 pe = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        const float2 ds = __fmul2_rn(pe, __fadd2_rn(make_float2(dp[i], dp[i + 1]), nD2));
+        w[i / 2] = pack_bf16x2(ds.x, ds.y);
       }
       if (j >= 2) mbar_wait(&ds_free[j & 1], ((j >> 1) + 1) & 1);
-      st_row_sw128(smem + C::kOffDS + (j & 1) * C::kDSBytes, rloc, w);
+      st_halfrow_sw128(smem + C::kOffDS + (j & 1) * C::kDSBytes, rloc, half, w);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
@@ -250,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(dq_done, 0);
     tc_fence_after();
 #pragma unroll
-    for (int c = 0; c < DH; c += 16) {
+    for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
       uint32_t r[16];
       tmem_ld16(t_dQ + c + lane_off, r);
       tmem_ld_wait();
@@ -331,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);
+      mbar_init(&p_full[s], kSmxWarps);
       mbar_init(&p_free[s], 1);
     }
     mbar_init(acc_done, 1);
@@ -414,30 +427,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     const int quad = warp & 3;
+    const int half = (warp - 2) / 4;    // query columns [32*half, 32*half+32) of each 64-query block
     const int krow = quad * 32 + lane;  // key row within the block == TMEM lane
     const bool key_ok = krow < kv_rows;
     const int kt = kt_base + krow;      // own: local key index
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const int tid = threadIdx.x - 64;   // 0..127
+    const int tid = threadIdx.x - 64;   // 0..255
+    constexpr int HC = BQ / 2;
+    // LSE/D of query block i are loaded one block ahead into registers (tid < BQ) and published to
+    // the stat buffer of that block at the start of its iteration (hides the global-load latency)
+    float nl = INFINITY, nd = 0.f;
+    auto fetch = [&](int i) {
+      const int q = q_lo + i * BQ + tid;
+      const bool ok = tid < BQ && i < nq && q < q_hi;
+      nl = ok ? p.lse[static_cast<long>(h) * p.n + q] * kLog2e : INFINITY;
+      nd = ok ? p.D[static_cast<long>(h) * p.n + q] : 0.f;
+    };
+    fetch(0);
     for (int i = 0; i < nq; ++i) {
       const int q0 = q_lo + i * BQ;
       float* st_lse = stat + (i & 1) * 2 * BQ;
       float* st_D = st_lse + BQ;
       if (tid < BQ) {
-        const int q = q0 + tid;
-        const bool ok = q < q_hi;
-        st_lse[tid] = ok ? p.lse[static_cast<long>(h) * p.n + q] * kLog2e : INFINITY;
-        st_D[tid] = ok ? p.D[static_cast<long>(h) * p.n + q] : 0.f;
+        st_lse[tid] = nl;
+        st_D[tid] = nd;
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1, 32 * kSmxWarps);
+      fetch(i + 1);
       mbar_wait(&s_full[i & 1], (i >> 1) & 1);
       tc_fence_after();
-      float s[BQ], dp[BQ];
+      float s[HC], dp[HC];
 #pragma unroll
-      for (int c = 0; c < BQ; c += 16) {
+      for (int c = 0; c < HC; c += 16) {
         uint32_t r[16], r2[16];
-        tmem_ld16(t_S + (i & 1) * BQ + c + lane_off, r);
-        tmem_ld16(t_dP + (i & 1) * BQ + c + lane_off, r2);
+        tmem_ld16(t_S + (i & 1) * BQ + half * HC + c + lane_off, r);
+        tmem_ld16(t_dP + (i & 1) * BQ + half * HC + c + lane_off, r2);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           s[c + e] = __uint_as_float(r[e]);
@@ -448,28 +472,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       // own rows: key kt sees query t iff kt <= t, i.e. columns qi >= kt - (q0 - seg_off) (invalid
       // queries beyond q_hi already have lse2 = +inf -> P = 0; invalid keys are never stored)
       if (own) {
-        const int lo = kt - (q0 - seg_off);
+        const int lo = kt - (q0 - seg_off) - half * HC;
         if (__any_sync(0xffffffff, lo > 0)) {
 #pragma unroll
-          for (int c = 0; c < BQ; ++c) s[c] = c >= lo ? s[c] : -INFINITY;
+          for (int c = 0; c < HC; ++c) s[c] = c >= lo ? s[c] : -INFINITY;
         }
       }
       const float c2 = p.scale_log2;
-      uint32_t wp[32], wd[32];
+      const float* lz_base = st_lse + half * HC;
+      const float* dz_base = st_D + half * HC;
+      uint32_t wp[HC / 2], wd[HC / 2];
 #pragma unroll
-      for (int c = 0; c < BQ; c += 4) {
-        const float4 lz = *reinterpret_cast<const float4*>(st_lse + c);
-        const float4 dz = *reinterpret_cast<const float4*>(st_D + c);
-        const float p0 = ex2_approx(fmaf(s[c], c2, -lz.x)), p1 = ex2_approx(fmaf(s[c + 1], c2, -lz.y));
-        const float p2 = ex2_approx(fmaf(s[c + 2], c2, -lz.z)), p3 = ex2_approx(fmaf(s[c + 3], c2, -lz.w));
-        wp[c / 2] = pack_bf16x2(p0, p1);
-        wp[c / 2 + 1] = pack_bf16x2(p2, p3);
-        wd[c / 2] = pack_bf16x2(p0 * (dp[c] - dz.x), p1 * (dp[c + 1] - dz.y));
-        wd[c / 2 + 1] = pack_bf16x2(p2 * (dp[c + 2] - dz.z), p3 * (dp[c + 3] - dz.w));
+      for (int c = 0; c < HC; c += 4) {
+        const float4 lz = *reinterpret_cast<const float4*>(lz_base + c);
+        const float4 dz = *reinterpret_cast<const float4*>(dz_base + c);
+        const float2 c22 = make_float2(c2, c2);
+        const float2 xa = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, make_float2(-lz.x, -lz.y));
+        const float2 xb = __ffma2_rn(make_float2(s[c + 2], s[c + 3]), c22, make_float2(-lz.z, -lz.w));
+        const float2 pa = make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
+        const float2 pb = make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
+        const float2 da = __fmul2_rn(pa, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-dz.x, -dz.y)));
+        const float2 db = __fmul2_rn(pb, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-dz.z, -dz.w)));
+        wp[c / 2] = pack_bf16x2(pa.x, pa.y);
+        wp[c / 2 + 1] = pack_bf16x2(pb.x, pb.y);
+        wd[c / 2] = pack_bf16x2(da.x, da.y);
+        wd[c / 2 + 1] = pack_bf16x2(db.x, db.y);
       }
       if (i >= 2) mbar_wait(&p_free[i & 1], ((i >> 1) + 1) & 1);
-      st_row_sw128(smem + C::kOffP + (i & 1) * C::kPBytes, krow, wp);
-      st_row_sw128(smem + C::kOffDS + (i & 1) * C::kPBytes, krow, wd);
+      st_halfrow_sw128(smem + C::kOffP + (i & 1) * C::kPBytes, krow, half, wp);
+      st_halfrow_sw128(smem + C::kOffDS + (i & 1) * C::kPBytes, krow, half, wd);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
@@ -480,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* dkr = p.dk + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
     float* dvr = p.dv + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
 #pragma unroll
-    for (int c = 0; c < DH; c += 16) {
+    for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
       uint32_t rk[16], rv[16];
       tmem_ld16(t_dK + c + lane_off, rk);
       tmem_ld16(t_dV + c + lane_off, rv);
@@ -504,9 +535,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int DH>
 void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                 const int2* kv_items2, int n_kv, cudaStream_t stream) {
-  constexpr int NS = 2;
-  using CQ = DqCfg<DH, NS>;
-  using CK = DkvCfg<DH, NS>;
+  // ring depths: loads must run >= 2 blocks ahead of the MMA that frees their stage
+  constexpr int NSQ = DH == 64 ? 4 : 3;  // dq kernel K/V stages
+  constexpr int NSK = DH == 64 ? 4 : 2;  // dkdv kernel Q/dO stages (smem-limited at dh 128)
+  using CQ = DqCfg<DH, NSQ>;
+  using CK = DkvCfg<DH, NSK>;
   const int d = a.H * DH;
   BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, dq_blocks, nullptr, a.scale,
               a.scale * kLog2e};
@@ -516,11 +549,11 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, 128);
     make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, CQ::BKV);
     make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, CQ::BKV);
-    static bool once = (cudaFuncSetAttribute(fa_bwd_dq_kernel<DH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool once = (cudaFuncSetAttribute(fa_bwd_dq_kernel<DH, NSQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              CQ::kSmem),
                         true);
     (void)once;
-    fa_bwd_dq_kernel<DH, NS><<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    fa_bwd_dq_kernel<DH, NSQ><<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
   }
   if (n_kv > 0) {
     CUtensorMap tq, tdo, tk, tv;
@@ -528,13 +561,13 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, CK::BQ);
     make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, 128);
     make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, 128);
-    static bool once = (cudaFuncSetAttribute(fa_bwd_dkdv_kernel<DH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool once = (cudaFuncSetAttribute(fa_bwd_dkdv_kernel<DH, NSK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              CK::kSmem),
                         true);
     (void)once;
     p.blocks = kv_items;
     p.blocks2 = kv_items2;
-    fa_bwd_dkdv_kernel<DH, NS><<<dim3(n_kv, a.H), kThreads, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    fa_bwd_dkdv_kernel<DH, NSK><<<dim3(n_kv, a.H), kThreads, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
   }
 }
 

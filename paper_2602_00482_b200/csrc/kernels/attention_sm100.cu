@@ -26,19 +26,16 @@ namespace ttb {
 
 namespace {
 
-constexpr int kFwdThreads = 192;
+constexpr int kFwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax (2 per TMEM quadrant)
+constexpr int kSmxWarps = 8;
 constexpr int kBQ = 128;
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P stays <= 256
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 template <int DH, int BKV, int NS>
 struct FwdCfg {
@@ -48,7 +45,8 @@ struct FwdCfg {
   static constexpr int kOffK = kQBytes;
   static constexpr int kOffV = kOffK + NS * kKVBytes;
   static constexpr int kOffP = kOffV + NS * kKVBytes;
-  static constexpr int kOffBar = kOffP + 2 * kPBytes;
+  static constexpr int kOffX = kOffP + 2 * kPBytes;   // [2 bufs][2 halves][128 rows] f32: row-max exchange
+  static constexpr int kOffBar = kOffX + 2 * 2 * kBQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kTmemCols = (2 * BKV + DH) <= 256 ? 256 : 512;
   static constexpr uint32_t kIdescS = make_idesc_bf16(128, BKV, false, false);
@@ -103,7 +101,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);
+      mbar_init(&p_full[s], kSmxWarps);
     }
     mbar_init(pv_done, 1);
     fence_barrier_init();
@@ -179,12 +177,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (j + 2 < nblk) issue_s(j + 2);
     }
   } else {
-    // ------------------------------------------------------------------ softmax (one row per thread)
+    // ------------------------------------------------------------------ softmax
+    // One query row per TMEM lane; the two warps on a lane quadrant split the BKV columns (half).
+    // The row max is exchanged through smem (double-buffered, 64-thread named barrier per
+    // quadrant); row sums stay partial per half until the end.
     const int quad = warp & 3;
+    const int half = (warp - 2) / 4;
     const int rloc = quad * 32 + lane;  // row within the tile == TMEM lane
     const int row = q_start + rloc;
     const int t = row - seg_off;        // local query index within the segment
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int bar_id = 2 + quad;
+    float* xch = reinterpret_cast<float*>(smem + C::kOffX);
+    constexpr int HC = BKV / 2;
     // m_used: the exponent base actually applied (log2 domain). It only moves when the running max
     // exceeds it by more than kRescaleThreshold (P <= 2^8 then), so O in TMEM is rescaled rarely.
     float m_used = -INFINITY, l = 0.f;
@@ -192,26 +197,30 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
-      float s[BKV];
+      float s[HC];
 #pragma unroll
-      for (int c = 0; c < BKV; c += 16) {
+      for (int c = 0; c < HC; c += 16) {
         uint32_t r[16];
-        tmem_ld16(tmem_S + (j & 1) * BKV + c + lane_off, r);
+        tmem_ld16(tmem_S + (j & 1) * BKV + half * HC + c + lane_off, r);
 #pragma unroll
         for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(r[i]);
       }
       tmem_ld_wait();
       const bool pre = j < n_pre;
-      const int base = pre ? j * BKV : (j - n_pre) * BKV;  // key index of column 0 (prefix row / own local)
-      // warp-uniform: does any lane of this warp need masking in this block?
+      // key index of this half's column 0 (prefix row / own local)
+      const int base = (pre ? j * BKV : (j - n_pre) * BKV) + half * HC;
       const int lim = pre ? (S - base) : (t - base + 1);   // valid columns are [0, lim)
-      if (__any_sync(0xffffffff, lim < BKV)) {
+      if (__any_sync(0xffffffff, lim < HC)) {
 #pragma unroll
-        for (int i = 0; i < BKV; ++i) s[i] = i < lim ? s[i] : -INFINITY;
+        for (int i = 0; i < HC; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
       float mx = s[0];
 #pragma unroll
-      for (int i = 1; i < BKV; ++i) mx = fmaxf(mx, s[i]);
+      for (int i = 1; i < HC; ++i) mx = fmaxf(mx, s[i]);
+      float* xb = xch + (j & 1) * (2 * kBQ);
+      xb[half * kBQ + rloc] = mx;
+      named_bar_sync(bar_id, 64);
+      mx = fmaxf(mx, xb[(1 - half) * kBQ + rloc]);
       const float m_new = fmaxf(m_used, mx * c2);
       const bool resc = m_new > m_used + kRescaleThreshold;
       float corr = 1.f;
@@ -221,32 +230,35 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         l *= corr;
       }
       const float mb = m_used == -INFINITY ? 0.f : m_used;
-      float rs = 0.f;
-      uint8_t* pbuf = smem + C::kOffP + (j & 1) * C::kPBytes;  // free: S_j's commit covers PV_{j-2}
+      float2 rs2 = make_float2(0.f, 0.f);
+      const float2 c22 = make_float2(c2, c2), nmb2 = make_float2(-mb, -mb);
+      // this half's columns start at key half*HC: panel (half*HC)/64, 16B chunk ((half*HC)%64)/8 of
+      // buffer j%2; the buffer is free since S_j's commit covers PV_{j-2}
+      uint8_t* pbuf = smem + C::kOffP + (j & 1) * C::kPBytes + ((half * HC) / 64) * (kBQ * 128);
+      const int chunk0 = ((half * HC) % 64) / 8;
 #pragma unroll
-      for (int pn = 0; pn < BKV / 64; ++pn) {
+      for (int cch = 0; cch < HC / 8; ++cch) {
+        uint32_t w[4];
 #pragma unroll
-        for (int cch = 0; cch < 8; ++cch) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a = ex2_approx(fmaf(s[pn * 64 + cch * 8 + 2 * e], c2, -mb));
-            const float b = ex2_approx(fmaf(s[pn * 64 + cch * 8 + 2 * e + 1], c2, -mb));
-            rs += a + b;
-            w[e] = pack_bf16x2(a, b);
-          }
-          // 128B swizzle: 16B chunk index XOR (row % 8)
-          uint4* dst = reinterpret_cast<uint4*>(pbuf + pn * (kBQ * 128) + rloc * 128 + ((cch ^ (rloc & 7)) * 16));
-          *dst = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int e = 0; e < 4; ++e) {
+          // paired FP32 (FFMA2 / FADD2): x = s*c - m ; p = 2^x ; row sum += p
+          const float2 x = __ffma2_rn(make_float2(s[cch * 8 + 2 * e], s[cch * 8 + 2 * e + 1]), c22, nmb2);
+          const float2 pe = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          rs2 = __fadd2_rn(rs2, pe);
+          w[e] = pack_bf16x2(pe.x, pe.y);
         }
+        // 128B swizzle: 16B chunk index XOR (row % 8)
+        uint4* dst = reinterpret_cast<uint4*>(pbuf + rloc * 128 + (((chunk0 + cch) ^ (rloc & 7)) * 16));
+        *dst = make_uint4(w[0], w[1], w[2], w[3]);
       }
+      const float rs = rs2.x + rs2.y;
       l += rs;
       if (j > 0 && __any_sync(0xffffffff, resc)) {
-        // O (from PV_{j-1}) must be final before it is rescaled
+        // O (from PV_{j-1}) must be final before it is rescaled; each warp rescales its half of dh
         mbar_wait(pv_done, (j - 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < DH; c += 16) {
+        for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
           uint32_t r[16];
           tmem_ld16(tmem_O + c + lane_off, r);
           tmem_ld_wait();
@@ -261,6 +273,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j & 1]);
     }
+    // combine the two partial row sums
+    float* lb = xch + (nblk & 1) * (2 * kBQ);
+    lb[half * kBQ + rloc] = l;
+    named_bar_sync(bar_id, 64);
+    l += lb[(1 - half) * kBQ + rloc];
     const float m = m_used;
     mbar_wait(pv_done, (nblk - 1) & 1);
     tc_fence_after();
@@ -269,7 +286,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const bool row_ok = row < q_end;
     __nv_bfloat16* orow = p.o + static_cast<long>(row) * p.ldo + h * DH;
 #pragma unroll
-    for (int c = 0; c < DH; c += 16) {
+    for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
       uint32_t r[16];
       tmem_ld16(tmem_O + c + lane_off, r);
       tmem_ld_wait();
@@ -287,7 +304,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         *reinterpret_cast<uint4*>(orow + c + 8) = w1;
       }
     }
-    if (row_ok) p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(l)) * 0.6931471805599453f;
+    if (half == 0 && row_ok) p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(l)) * 0.6931471805599453f;
+
   }
   tc_fence_before();
   __syncthreads();

@@ -160,6 +160,27 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_m
          | ((static_cast<uint32_t>(M) >> 4) << 24);  // m_dim
 }
 
+// ---------------------------------------------------------------- exp2
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = j + f, f in [-0.5, 0.5] via the
+// 1.5*2^23 magic add, cubic minimax 2^f (max rel err 7.5e-5, far below bf16's 3.9e-3), exponent
+// added as an integer. Used for a fraction of the softmax exponentials so the MUFU (16/clk/SM) and
+// FMA (128/clk/SM) pipes share the load. x < -126 (incl. -inf) -> 0.
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -126.0f);
+  const float t = xc + 12582912.0f;  // 0x1.8p23: low mantissa bits = round(xc)
+  const float j = t - 12582912.0f;
+  const float f = xc - j;
+  const float pz = fmaf(fmaf(fmaf(0.05517084f, f, 0.24260935f), f, 0.69326096f), f, 0.99992818f);
+  const int ji = __float_as_int(t) - 0x4B400000;
+  const float r = __int_as_float(__float_as_int(pz) + (ji << 23));
+  return x < -126.0f ? 0.0f : r;
+}
+
 // ---------------------------------------------------------------- misc
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

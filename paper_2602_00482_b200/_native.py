@@ -74,6 +74,7 @@ EXPORTS = {
     "tt_debug_gemm_async": [vp, c.c_long, c.c_int, vp, c.c_long, c.c_int, c.c_int, c.c_int, c.c_int, c.c_int, vp, vp,
                             vp, c.c_long, c.c_int, vp, vp, c.c_int],
     "tt_debug_gemm_splits": [c.c_int, c.c_int, c.c_int],
+    "tt_debug_gemm_set_2cta": [c.c_int],
 }
 
 

@@ -54,6 +54,7 @@ int tt_debug_gemm_async(const void* a, long lda, int a_mn, const void* b, long l
                     splits);
 }
 int tt_debug_gemm_splits(int M, int N, int K) { return ttb::gemm_choose_splits(M, N, K); }
+void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
 
 // Segment attention on one segment of n queries over stack rows [0, S) + own rows [S, S+n)
 // (k/v: [rows_cap x H*dh] bf16). dir 0: forward (impl 0 = mma.sync, 1 = tcgen05) -> o, lse.

@@ -160,6 +160,8 @@ void Engine::set_option(const std::string& key, int64_t value) {
   if (key == "attn_fwd_impl") {
     if (value != 0 && value != 1) throw std::invalid_argument("attn_fwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
     attn_fwd_impl_ = static_cast<int>(value);
+  } else if (key == "gemm_2cta") {
+    gemm_set_2cta(value != 0 ? 1 : 0);
   } else if (key == "attn_bwd_impl") {
     if (value != 0 && value != 1) throw std::invalid_argument("attn_bwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
     attn_bwd_impl_ = static_cast<int>(value);

@@ -36,15 +36,6 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
-// Writes one thread's row of 64 bf16 values (packed pairs w[32]) into a 128B-swizzled K-major panel.
-__device__ __forceinline__ void st_row_sw128(uint8_t* panel, int row, const uint32_t (&w)[32]) {
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint4* dst = reinterpret_cast<uint4*>(panel + row * 128 + ((c ^ (row & 7)) * 16));
-    *dst = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-  }
-}
-
 // Writes 32 bf16 values (w[16] packed pairs) = chunks [4*half, 4*half+4) of a thread's 128B row.
 __device__ __forceinline__ void st_halfrow_sw128(uint8_t* panel, int row, int half, const uint32_t (&w)[16]) {
 #pragma unroll

@@ -8,10 +8,17 @@
 //   dX = dY W^T    (matrix.hpp:50-62 `matmul_transposed`)  : A K-major,  B K-major
 //   dW += X^T dY   (matrix.hpp:64-77 `accumulate_outer`)   : A MN-major, B MN-major
 //
-// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
-// warps 2..5 = epilogue (TMEM -> registers -> fused op -> global). Smem ring of STAGES
-// {A,B} tiles (128B swizzle); two TMEM accumulator slots so the epilogue of tile i overlaps
-// the main loop of tile i+1. Split-K partials reduce with red.global.add.v4.f32.
+// Roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
+// warps 2..9 = epilogue (TMEM -> registers -> fused op -> global; two warps per TMEM lane quadrant
+// split the tile's columns). Smem ring of STAGES {A,B} tiles (128B swizzle); two TMEM accumulator
+// slots so the epilogue of tile i overlaps the main loop of tile i+1. Split-K partials reduce with
+// red.global.add.v4.f32.
+//
+// CG = 2 (M >= 256): a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 issued by the leader CTA: each CTA stages its own 128 rows of A and HALF
+// of B (BN/2), TMA completions of both CTAs land on the leader's full barrier, MMA completions are
+// multicast to both CTAs' barriers, and each CTA's TMEM holds its 128 accumulator rows. Per CTA this
+// halves the B operand traffic through shared memory.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -31,15 +38,80 @@ constexpr int BK = 64;
 constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quadrant)
 constexpr int kEpiWarps = 8;
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 192 ? 5 : 6);
+  static constexpr int BNC = BN / CG;  // B rows (K-major) / columns (MN-major) staged per CTA
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = BNC * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;  // two accumulator slots (power of 2)
   static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(BNC % 64 == 0 || CG == 1, "2-CTA MN-major B needs 64-column halves");
 };
+
+// ---- CTA-pair (cluster of 2) helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// Relaxed remote arrive: these barriers only order TMEM / smem reuse (already fenced by
+// tcgen05.wait + fence::before_thread_sync), not the arriving thread's global stores.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA into this CTA's smem, completion bytes counted on the leader CTA's barrier (cluster address)
+__device__ __forceinline__ void tma_load_2d_2sm(const void* tmap, uint32_t bar_cluster, void* smem_dst, int32_t x,
+                                                int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cluster), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_ss_2cta(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// completion of the pair's MMAs -> arrive on the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma_commit_2cta(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tmem_alloc_cg(uint32_t* smem_result, uint32_t ncols) {
+  if constexpr (CG == 1) {
+    tmem_alloc(smem_result, ncols);
+  } else {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_result)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::);
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) {
+  if constexpr (CG == 1) tmem_dealloc(taddr, ncols);
+  else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
 
 __device__ __forceinline__ float fast_sigmoid(float u) {
   float e, r;
@@ -53,11 +125,15 @@ __device__ __forceinline__ float silu_grad_f(float u) {
   return s * (1.0f + u * (1.0f - s));
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, int CG, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, int M, int N,
                 int K, int splits, EpiParams epi) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
+  constexpr int TM = BM * CG;  // tile rows (per CTA pair when CG = 2)
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;  // cluster id / count
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
@@ -69,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = warp_id_sync();
   const int lane = threadIdx.x & 31;
 
-  const int num_m = (M + BM - 1) / BM;
+  const int num_m = (M + TM - 1) / TM;
   const int num_n = (N + BN - 1) / BN;
   const int kb_total = (K + BK - 1) / BK;
   const int kb_per = (kb_total + splits - 1) / splits;
@@ -79,27 +155,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmap_a);
     tma_prefetch_desc(&tmap_b);
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
+      mbar_init(&full_bar[s], CG);  // leader: its own arrive.expect_tx + the peer's arrive
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], kEpiWarps);
+      mbar_init(&tempty_bar[s], kEpiWarps * CG);  // leader: epilogue warps of both CTAs
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  // Rasterisation: the concurrently running tiles should share the LARGER operand's panels so it
+  // streams from HBM once while the smaller one stays L2-resident: n-fastest when A (M x K) is the
+  // bigger operand (activations x weights), m-fastest otherwise (e.g. the LM head's 150K-wide B).
+  const bool n_fast = static_cast<long>(M) > static_cast<long>(N);
   auto tile_coords = [&](int t, int& m_blk, int& n_blk, int& kb0, int& kb1) {
     const int per = num_m * num_n;
     const int split = t / per;
     const int rem = t - split * per;
-    n_blk = rem / num_m;
-    m_blk = rem - n_blk * num_m;
+    if (n_fast) {
+      m_blk = rem / num_n;
+      n_blk = rem - m_blk * num_n;
+    } else {
+      n_blk = rem / num_m;
+      m_blk = rem - n_blk * num_m;
+    }
     kb0 = split * kb_per;
     kb1 = min(kb_total, kb0 + kb_per);
   };
@@ -109,26 +195,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = cid; t < num_tiles; t += ncl) {
         int m_blk, n_blk, kb0, kb1;
         tile_coords(t, m_blk, n_blk, kb0, kb1);
+        const int m0 = m_blk * TM + static_cast<int>(rank) * BM;         // this CTA's A rows
+        const int n0 = n_blk * BN + static_cast<int>(rank) * C::BNC;     // this CTA's B half
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
-          mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
           const int k0 = kb * BK;
-          if constexpr (!A_MN) {
-            tma_load_2d(&tmap_a, &full_bar[stage], sa, k0, m_blk * BM);
-          } else {
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+            if constexpr (!A_MN) {
+              tma_load_2d(&tmap_a, &full_bar[stage], sa, k0, m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(&tmap_a, &full_bar[stage], sa + j * 8192, m_blk * BM + j * 64, k0);
-          }
-          if constexpr (!B_MN) {
-            tma_load_2d(&tmap_b, &full_bar[stage], sb, k0, n_blk * BN);
-          } else {
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d(&tmap_a, &full_bar[stage], sa + j * 8192, m0 + j * 64, k0);
+            }
+            if constexpr (!B_MN) {
+              tma_load_2d(&tmap_b, &full_bar[stage], sb, k0, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(&tmap_b, &full_bar[stage], sb + j * 8192, n_blk * BN + j * 64, k0);
+              for (int j = 0; j < C::BNC / 64; ++j)
+                tma_load_2d(&tmap_b, &full_bar[stage], sb + j * 8192, n0 + j * 64, k0);
+            }
+          } else {
+            const uint32_t fb = mapa_shared(smem_u32(&full_bar[stage]), 0);  // the leader's full barrier
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
+            else mbar_arrive_remote(fb);
+            if constexpr (!A_MN) {
+              tma_load_2d_2sm(&tmap_a, fb, sa, k0, m0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j) tma_load_2d_2sm(&tmap_a, fb, sa + j * 8192, m0 + j * 64, k0);
+            }
+            if constexpr (!B_MN) {
+              tma_load_2d_2sm(&tmap_b, fb, sb, k0, n0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < C::BNC / 64; ++j) tma_load_2d_2sm(&tmap_b, fb, sb + j * 8192, n0 + j * 64, k0);
+            }
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -138,13 +245,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
+    // ------------------------------------------------------------ MMA issuer (leader CTA only)
+    if (!leader) goto mma_done;
+    {
+    constexpr uint32_t idesc = make_idesc_bf16(TM, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = cid; t < num_tiles; t += ncl) {
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -163,9 +272,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             else da = make_sdesc_sw128(sa + k * 2048, 8192, 1024);
             if constexpr (!B_MN) db = make_sdesc_sw128(sb + k * 32, 16, 1024);
             else db = make_sdesc_sw128(sb + k * 2048, 8192, 1024);
-            umma_bf16_ss(d_tmem, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if constexpr (CG == 1) umma_bf16_ss(d_tmem, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else umma_bf16_ss_2cta(d_tmem, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          if constexpr (CG == 1) umma_commit(&empty_bar[stage]);
+          else umma_commit_2cta(&empty_bar[stage]);
         }
         __syncwarp();
         if (++stage == C::kStages) {
@@ -173,25 +284,30 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      if (lane == 0) umma_commit(&tfull_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) umma_commit(&tfull_bar[acc]);
+        else umma_commit_2cta(&tfull_bar[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    }
+  mma_done:;
   } else {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;             // TMEM lane quadrant this warp may access
     const int half = (warp - 2) / 4;       // which half of the BN columns this warp handles
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = cid; t < num_tiles; t += ncl) {
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * BM + quad * 32 + lane;
+      const int row = m_blk * TM + static_cast<int>(rank) * BM + quad * 32 + lane;
       const bool row_ok = row < M;
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
 #pragma unroll
@@ -307,7 +423,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
+        else mbar_arrive_remote(mapa_shared(smem_u32(&tempty_bar[acc]), 0));  // the leader's slot barrier
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -315,8 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem_base, C::kTmemCols);
+  if constexpr (CG == 2) cluster_sync();  // the peer's MMAs into this CTA's TMEM are complete
+  if (warp == 1) tmem_dealloc_cg<CG>(tmem_base, C::kTmemCols);
 }
 
 // ---------------------------------------------------------------- host side
@@ -355,18 +476,18 @@ namespace {
 
 int g_num_sms = 0;
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, int CG, bool A_MN, bool B_MN>
 void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
             cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   CUtensorMap ta, tb;
   if (!A_MN) make_tmap_bf16(&ta, A.ptr, K, M, A.ld, 64, BM);
   else make_tmap_bf16(&ta, A.ptr, M, K, A.ld, 64, 64);
-  if (!B_MN) make_tmap_bf16(&tb, B.ptr, K, N, B.ld, 64, BN);
+  if (!B_MN) make_tmap_bf16(&tb, B.ptr, K, N, B.ld, 64, C::BNC);
   else make_tmap_bf16(&tb, B.ptr, N, K, B.ld, 64, 64);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(gemm_kernel<BN, CG, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
   if (g_num_sms == 0) {
@@ -379,14 +500,44 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   if (splits > kb_total) splits = kb_total;
   const int per = (kb_total + splits - 1) / splits;
   splits = (kb_total + per - 1) / per;  // no empty split
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * splits;
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int tiles = ((M + BM * CG - 1) / (BM * CG)) * ((N + BN - 1) / BN) * splits;
+  const int max_clusters = g_num_sms / CG;
+  const int grid = (tiles < max_clusters ? tiles : max_clusters) * CG;
   EpiParams e = epi;
   if (splits > 1) e.atomic = 1;
-  gemm_kernel<BN, A_MN, B_MN><<<grid, kThreads, C::kSmem, stream>>>(ta, tb, M, N, K, splits, e);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN>, ta, tb, M, N, K, splits, e);
 }
 
 }  // namespace
+
+int g_gemm_2cta = 1;
+void gemm_set_2cta(int on) { g_gemm_2cta = on; }
+
+// CTA pairs (256-row tiles) unless padding M to 256 wastes more than ~5% (e.g. M = 896)
+bool gemm_use_2cta(int M) {
+  if (!g_gemm_2cta || M < 256) return false;
+  const int padded = (M + 255) / 256 * 256;
+  return (padded - M) * 20 <= M;
+}
+
+// 2-CTA tile width: 256 unless its padding waste outweighs the halved per-CTA B traffic
+int gemm_pick_bn2(int N) {
+  const double c256 = static_cast<double>((N + 255) / 256) * 256;
+  const double c128 = static_cast<double>((N + 127) / 128) * 128 * 1.08;
+  return c256 <= c128 ? 256 : 128;
+}
 
 int gemm_pick_bn(int N, bool b_mn_major) {
   (void)b_mn_major;  // 128/192/256 are all multiples of the 64-element MN atom
@@ -409,19 +560,27 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
   if (M <= 0 || N <= 0 || K <= 0) return;
   if (N % 16 != 0) throw std::invalid_argument("gemm_bf16: N must be a multiple of 16");
   if (splits > 1 && epi.mode != EPI_ADD_F32) throw std::invalid_argument("gemm_bf16: split-K needs EPI_ADD_F32");
-  const int bn = gemm_pick_bn(N, B.mn_major);
   const bool amn = A.mn_major, bmn = B.mn_major;
-#define TTB_DISPATCH(BN_)                                             \
-  if (!amn && bmn) return launch<BN_, false, true>(A, B, M, N, K, epi, splits, stream);  \
-  if (!amn && !bmn) return launch<BN_, false, false>(A, B, M, N, K, epi, splits, stream); \
-  if (amn && bmn) return launch<BN_, true, true>(A, B, M, N, K, epi, splits, stream);     \
-  return launch<BN_, true, false>(A, B, M, N, K, epi, splits, stream);
+#define TTB_DISPATCH(BN_, CG_)                                                                      \
+  if (!amn && bmn) return launch<BN_, CG_, false, true>(A, B, M, N, K, epi, splits, stream);  \
+  if (!amn && !bmn) return launch<BN_, CG_, false, false>(A, B, M, N, K, epi, splits, stream); \
+  if (amn && bmn) return launch<BN_, CG_, true, true>(A, B, M, N, K, epi, splits, stream);     \
+  return launch<BN_, CG_, true, false>(A, B, M, N, K, epi, splits, stream);
+  if (gemm_use_2cta(M)) {
+    // CTA pairs: 256-row tiles; BN 128 or 256 (each CTA stages a 64-aligned half of B)
+    if (gemm_pick_bn2(N) == 256) {
+      TTB_DISPATCH(256, 2)
+    } else {
+      TTB_DISPATCH(128, 2)
+    }
+  }
+  const int bn = gemm_pick_bn(N, B.mn_major);
   if (bn == 256) {
-    TTB_DISPATCH(256)
+    TTB_DISPATCH(256, 1)
   } else if (bn == 192) {
-    TTB_DISPATCH(192)
+    TTB_DISPATCH(192, 1)
   } else {
-    TTB_DISPATCH(128)
+    TTB_DISPATCH(128, 1)
   }
 #undef TTB_DISPATCH
 }
@@ -432,8 +591,9 @@ int gemm_choose_splits(int M, int N, int K) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int bn = gemm_pick_bn(N, true);
-  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  const bool two = gemm_use_2cta(M);
+  const int bn = two ? gemm_pick_bn2(N) : gemm_pick_bn(N, true);
+  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);  // per-CTA tiles (a pair counts as 2)
   const int kb = (K + BK - 1) / BK;
   if (tiles >= g_num_sms || kb < 8) return 1;
   int s = (g_num_sms + tiles - 1) / tiles;

@@ -20,6 +20,14 @@ def _lib():
 EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU = range(5)
 
 
+@pytest.fixture(params=[1, 0], ids=["2cta", "1cta"], autouse=True)
+def gemm_mode(request):
+    """Run every kernel test with the CTA-pair (cta_group::2) GEMM and with the single-CTA GEMM."""
+    _lib().tt_debug_gemm_set_2cta(request.param)
+    yield request.param
+    _lib().tt_debug_gemm_set_2cta(1)
+
+
 def _gemm(a, a_mn, b, b_mn, M, N, K, mode, outs, ldo, split_w=0, act=None, aux=None, splits=1):
     lib = _lib()
     vp = ctypes.c_void_p

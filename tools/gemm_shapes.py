@@ -33,11 +33,15 @@ SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
 
 def main():
     lib = _native.lib()
+    lib.tt_debug_gemm_set_2cta(int(os.environ.get("GEMM_2CTA", "1")))
+    only = os.environ.get("GEMM_ONLY")
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json"))) \
         if os.path.exists("MEASURED_PEAKS.json") else {"bf16_tflops": 1590.0}
     vp = ctypes.c_void_p
     out = []
     for label, M, N, K, amn, bmn, epi in SHAPES:
+        if only and label != only:
+            continue
         a = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
         b = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
         o32 = torch.zeros(M, N, device="cuda")

@@ -160,6 +160,8 @@ int tt_engine_set_profiling(tt_engine* eng, int32_t on);
  * baseline), 1 = tcgen05/TMEM/TMA (default). */
 int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value);
 int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset);
+/* Per-GEMM-shape breakdown of the profiled launches (text, one shape per line, slowest first). */
+int tt_engine_profile_gemm_text(tt_engine* eng, char* buf, uint64_t cap, uint64_t* len);
 
 /* ------------------------------------------------------------------ segment level (device KV stack)
  * forward_segment (model.hpp:328-463) continuing from the device stack (KVView of all pushed

@@ -322,6 +322,13 @@ class Engine:
     def set_option(self, key: str, value: int) -> None:
         _check(_native.lib().tt_engine_set_option(self._h, key.encode(), int(value)))
 
+    def profile_gemm_text(self) -> str:
+        n = ctypes.c_uint64()
+        _check(_native.lib().tt_engine_profile_gemm_text(self._h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        _check(_native.lib().tt_engine_profile_gemm_text(self._h, buf, n.value + 1, ctypes.byref(n)))
+        return buf.raw[: n.value].decode()
+
     def profile(self, reset: bool = True):
         n = len(self.KCLASSES)
         ms, fl, by = (np.zeros(n) for _ in range(3))

@@ -64,6 +64,7 @@ EXPORTS = {
     "tt_debug_attn": [c.c_int, c.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, c.c_int, c.c_int, c.c_int, c.c_int,
                       c.c_long, c.c_int, P(c.c_float)],
     "tt_engine_profile": [vp, P(f64), P(f64), P(f64), P(u64), i32],
+    "tt_engine_profile_gemm_text": [vp, c.c_char_p, u64, P(u64)],
     "tt_segment_push": [vp, P(i32), u64, P(c.c_float)],
     "tt_segment_pop": [vp, P(c.c_float), P(c.c_float)],
     "tt_stack_reset": [vp],

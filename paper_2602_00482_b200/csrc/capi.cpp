@@ -257,7 +257,7 @@ int tt_dense_train_step(tt_engine* eng, const int32_t* tokens, const uint64_t* o
     ttb::PrefixTree flat = ttb::build_flat_forest(views(tokens, offsets, weights, n_seqs));
     tt_sched_config sc{};
     sc.sibling_batch = 1;  // every sequence is its own root-level leaf: packed varlen batches
-    sc.batch_token_budget = 65536;
+    sc.batch_token_budget = 0;  // memory-aware automatic budget
     tt_step_result r = eng->e->train_step(flat, sc);
     if (result) *result = r;
   });
@@ -321,6 +321,13 @@ int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, 
       if (launches) launches[i] = k.launches[i];
     }
     if (reset) eng->e->reset_kstats();
+  });
+}
+
+int tt_engine_profile_gemm_text(tt_engine* eng, char* buf, uint64_t cap, uint64_t* len) {
+  return ttb::guarded([&] {
+    need(eng, "engine");
+    copy_out(eng->e->gemm_profile_text(), buf, cap, len);
   });
 }
 

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -420,9 +421,28 @@ void Engine::collect_profile() {
     kstats_.flops[p.cls] += p.flops;
     kstats_.bytes[p.cls] += p.bytes;
     kstats_.launches[p.cls] += 1;
+    if (!p.tag.empty()) {
+      TagStat& ts = tag_stats_[p.tag];
+      ts.ms += ms;
+      ts.flops += p.flops;
+      ts.n += 1;
+    }
   }
   pending_.clear();
   event_next_ = 0;
+}
+
+std::string Engine::gemm_profile_text() const {
+  std::vector<std::pair<std::string, TagStat>> v(tag_stats_.begin(), tag_stats_.end());
+  std::sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.second.ms > b.second.ms; });
+  std::string out;
+  for (const auto& [tag, st] : v) {
+    char line[256];
+    std::snprintf(line, sizeof(line), "%10.3f ms  n=%6llu  %7.1f TFLOP/s  %s\n", st.ms,
+                  static_cast<unsigned long long>(st.n), st.flops / (st.ms * 1e-3) / 1e12, tag.c_str());
+    out += line;
+  }
+  return out;
 }
 
 // GEMM launch: algorithmic FLOPs 2MNK; algorithmic bytes = operands once + output (x2 if RMW).
@@ -432,16 +452,20 @@ void Engine::gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int 
   if (e.mode == EPI_ADD_F32 || e.mode == EPI_RESID_F32) out_b = 8.0;
   if (e.mode == EPI_SILU || e.mode == EPI_DSILU) out_b = 4.0;
   const double bytes = 2.0 * (double(M) * K + double(N) * K) + out_b * double(M) * N;
+  if (profiling_) {
+    pending_tag_ = std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K) + (A.mn_major ? " A:mn" : " A:k") +
+                   (B.mn_major ? " B:mn" : " B:k") + " epi" + std::to_string(e.mode) + " s" + std::to_string(splits);
+  }
   run(KC_GEMM, 2.0 * M * N * K, bytes, [&] { gemm_bf16(A, B, M, N, K, e, splits, stream_); });
 }
 
 // ----------------------------------------------------------------------------- push (forward_segment)
-void Engine::forward_batch(const Batch& b) {
+void Engine::forward_batch(const Batch& b, size_t arena_off) {
   const int n = static_cast<int>(b.n);
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
   const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);
-  char* base = arena_.as<char>(b.arena_off);
+  char* base = arena_.as<char>(arena_off);
   auto X = [&](int64_t l) {
     return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x);
   };
@@ -611,12 +635,12 @@ void Engine::head_backward_dense(const Batch& b, const bf16* nf, const float* ho
 }
 
 // ----------------------------------------------------------------------------- pop (backward_segment)
-void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
+void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits) {
   const int n = static_cast<int>(b.n);
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
   const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);
-  char* base = arena_.as<char>(b.arena_off);
+  char* base = arena_.as<char>(arena_off);
   auto X = [&](int64_t l) {
     return reinterpret_cast<float*>(l == L_ ? base + lay.final_x : base + l * lay.per_layer + lay.x);
   };
@@ -769,17 +793,38 @@ void Engine::backward_batch(const Batch& b, const float* host_grad_logits) {
     });
   }
   run(KC_ELEMWISE, 0, nd * 12, [&] { k_embed_grad(gx, meta<int32_t>(b.o_tok), g_emb_, n, d, stream_); });  // :627-630
-  accum_count_ += b.nodes.empty() ? 1 : b.nodes.size();
+  accum_count_ += b.accum_inc;
 }
 
 // ----------------------------------------------------------------------------- tree_train_step
-std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched_config& sc) {
-  if (sc.chunk_len != 0) {
-    // chunked backward is not implemented on device yet: only accept chunk_len >= every segment
-    for (size_t u = 1; u < tree.nodes.size(); ++u)
-      if (tree.nodes[u].tokens.size() > sc.chunk_len)
-        throw std::invalid_argument("tree_train_step: chunk_len smaller than a segment is not supported yet");
+// Device bytes one more token of a pushed batch costs: activations (per layer 16d + 4F + 4H + 8,
+// plus the final norm), its K/V (bf16) + dK/dV (fp32) stack rows, and pop scratch.
+double Engine::bytes_per_token() const {
+  const double d = double(d_), F = double(F_), H = double(H_), L = double(L_);
+  const double act = L * (16 * d + 4 * F + 4 * H + 8) + 6 * d + 4;
+  const double stack = 12 * L * d;
+  const double scratch = 26 * d + 2 * F + 4 * H;
+  return act + stack + scratch;
+}
+
+// Sibling-batch token budget that keeps the step inside HBM: what is free now (plus what this
+// engine already holds and can re-purpose) minus the resident path, a head-chunk + safety margin.
+uint64_t Engine::auto_batch_budget(uint64_t path_tokens) const {
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 8192;
   }
+  const double held = double(arena_.bytes + kst_.bytes + vst_.bytes + dkst_.bytes + dvst_.bytes + sc_gx_.bytes +
+                             sc_gxb_.bytes + sc_gxf_.bytes + sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes +
+                             sc_dq_.bytes + sc_dqkv_.bytes);
+  const double per_tok = bytes_per_token();
+  const double avail = 0.85 * (double(free_b) + held) - 6e9 - double(path_tokens) * per_tok;
+  const double tok = avail / per_tok;
+  return tok < 2048 ? 2048 : static_cast<uint64_t>(tok);
+}
+
+std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched_config& sc) {
   if (tree.nodes[0].max_path_below > cfg_.max_position)
     throw std::invalid_argument("tree_train_step: path exceeds max_position");
   auto plan = std::make_unique<StepPlan>();
@@ -819,35 +864,91 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
     }
     b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
     b.n = off;
+    b.accum_inc = static_cast<int>(members.size());
     batches.push_back(std::move(b));
     return static_cast<int>(batches.size() - 1);
   };
   std::string& trace = plan->trace;
+  const uint64_t budget = (sc.batch_token_budget == 0 && sc.sibling_batch)
+                              ? auto_batch_budget(tree.nodes[0].max_path_below)
+                              : sc.batch_token_budget;
+  // chunk [a, b) of node u (S = the node's start): a chained sub-segment (chunked backward,
+  // SPEC.md:234-251); the loss pairs of rows in [a, b) move with it
+  auto make_chunk = [&](int32_t u, int64_t S, int64_t a, int64_t e, int accum_inc) {
+    Batch b;
+    b.S = S + a;
+    b.n = e - a;
+    b.nodes = {u};
+    b.accum_inc = accum_inc;
+    b.seg_off = {0};
+    b.seg_len = {b.n};
+    b.attn_ctx = double(b.n) * double(b.S) + 0.5 * double(b.n) * double(b.n + 1);
+    const auto& nd = tree.nodes[u];
+    for (int64_t t = a; t < e; ++t) {
+      b.tokens.push_back(nd.tokens[t]);
+      b.positions.push_back(static_cast<int32_t>(S + t));
+    }
+    LossPairs lp = node_loss_pairs(tree, u, S);
+    for (size_t k = 0; k < lp.rows.size(); ++k) {
+      if (lp.rows[k] < a || lp.rows[k] >= e) continue;
+      const int32_t row = static_cast<int32_t>(lp.rows[k] - a);
+      if (b.loss_rows.empty() || b.loss_rows.back() != row) {
+        b.loss_rows.push_back(row);
+        b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
+      }
+      b.pair_tgt.push_back(lp.targets[k]);
+      b.pair_w.push_back(lp.weights[k]);
+    }
+    b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
+    batches.push_back(std::move(b));
+    return static_cast<int>(batches.size() - 1);
+  };
+  const uint64_t chunk = sc.chunk_len;
+  auto short_leaf = [&](int32_t c) {
+    return tree.nodes[c].children.empty() && (chunk == 0 || tree.nodes[c].tokens.size() <= chunk);
+  };
   std::function<void(int32_t, int64_t)> visit = [&](int32_t u, int64_t S) {
     const auto& ch = tree.nodes[u].children;
     size_t i = 0;
     while (i < ch.size()) {
       const int32_t c = ch[i];
-      if (sc.sibling_batch && tree.nodes[c].children.empty()) {
+      const int64_t len = static_cast<int64_t>(tree.nodes[c].tokens.size());
+      if (sc.sibling_batch && short_leaf(c)) {
         std::vector<int32_t> run_nodes = {c};
         uint64_t tok = tree.nodes[c].tokens.size();
         size_t j = i + 1;
-        while (j < ch.size() && tree.nodes[ch[j]].children.empty() &&
-               (sc.batch_token_budget == 0 || tok + tree.nodes[ch[j]].tokens.size() <= sc.batch_token_budget)) {
+        while (j < ch.size() && short_leaf(ch[j]) && (budget == 0 || tok + tree.nodes[ch[j]].tokens.size() <= budget)) {
           tok += tree.nodes[ch[j]].tokens.size();
           run_nodes.push_back(ch[j++]);
         }
         const int bi = make_batch(run_nodes, S);
-        ops.push_back({bi, true});
-        ops.push_back({bi, false});
+        batches[bi].leaf_batch = true;
+        ops.push_back({bi, OP_FWD, 0});
+        ops.push_back({bi, OP_BWD, 0});
         for (int32_t m : run_nodes) trace += "PUSH " + std::to_string(pid[m]) + "\nPOP " + std::to_string(pid[m]) + "\n";
         i = j;
-      } else {
+      } else if (chunk == 0 || static_cast<uint64_t>(len) <= chunk) {
         const int bi = make_batch({c}, S);
-        ops.push_back({bi, true});
+        batches[bi].leaf_batch = tree.nodes[c].children.empty();
+        ops.push_back({bi, OP_FWD, 0});
         trace += "PUSH " + std::to_string(pid[c]) + "\n";
-        visit(c, S + static_cast<int64_t>(tree.nodes[c].tokens.size()));
-        ops.push_back({bi, false});
+        visit(c, S + len);
+        ops.push_back({bi, OP_BWD, 0});
+        trace += "POP " + std::to_string(pid[c]) + "\n";
+        ++i;
+      } else {
+        // chunked node: forward every chunk (its K/V stays on the stack), keep activations only for
+        // the newest chunk; at pop recompute + backward the older chunks newest-first
+        std::vector<int> ids;
+        for (int64_t a = 0; a < len; a += static_cast<int64_t>(chunk))
+          ids.push_back(make_chunk(c, S, a, std::min<int64_t>(len, a + static_cast<int64_t>(chunk)), a == 0 ? 1 : 0));
+        for (int id : ids) batches[id].leaf_batch = tree.nodes[c].children.empty();
+        trace += "PUSH " + std::to_string(pid[c]) + "\n";
+        for (size_t k = 0; k + 1 < ids.size(); ++k) ops.push_back({ids[k], OP_FWD_DISCARD, 0});
+        ops.push_back({ids.back(), OP_FWD, 0});
+        visit(c, S + len);
+        ops.push_back({ids.back(), OP_BWD, 0});
+        for (size_t k = ids.size() - 1; k-- > 0;) ops.push_back({ids[k], OP_REFWD_BWD, 0});
         trace += "POP " + std::to_string(pid[c]) + "\n";
         ++i;
       }
@@ -858,30 +959,59 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
   // ---- memory plan: LIFO arena offsets, stack rows, scratch sizes, counters
   tt_step_result& res = plan->counters;
   size_t top = 0;
-  uint64_t live_tok = 0, peak_tok = 0;
-  for (auto& [bi, push] : ops) {
-    Batch& b = batches[bi];
-    if (push) {
-      b.arena_off = top;
-      top += align_up(layout(b.n).total);
-      plan->arena_peak = std::max(plan->arena_peak, top);
+  uint64_t live_tok = 0, peak_tok = 0, peak_kv = 0;
+  std::vector<size_t> fwd_off(batches.size(), 0);
+  for (auto& op : ops) {
+    Batch& b = batches[op.b];
+    const size_t sz = align_up(layout(b.n).total);
+    if (op.code != OP_BWD) {
       plan->rows = std::max<int64_t>(plan->rows, b.S + b.n);
       plan->max_n = std::max<int64_t>(plan->max_n, b.n);
       plan->max_loss = std::max<int64_t>(plan->max_loss, static_cast<int64_t>(b.loss_rows.size()));
-      live_tok += b.n;
-      peak_tok = std::max(peak_tok, live_tok);
-      res.forward_tokens += b.n;
-      res.num_segments += b.nodes.size();
-      res.num_batches += 1;
-    } else {
-      top = b.arena_off;
-      live_tok -= b.n;
-      res.backward_tokens += b.n;
+      // live KV (ledger semantics): childless leaves skip KV storage with leaf_kv_skip
+      const uint64_t kv = static_cast<uint64_t>(b.S) + ((sc.leaf_kv_skip && b.leaf_batch) ? 0 : b.n);
+      peak_kv = std::max(peak_kv, kv);
+    }
+    switch (op.code) {
+      case OP_FWD:
+        op.off = fwd_off[op.b] = top;
+        top += sz;
+        plan->arena_peak = std::max(plan->arena_peak, top);
+        live_tok += b.n;
+        peak_tok = std::max(peak_tok, live_tok);
+        res.forward_tokens += b.n;
+        res.num_segments += b.accum_inc;
+        res.num_batches += 1;
+        break;
+      case OP_FWD_DISCARD:  // forward, activations dropped right after (K/V stay on the stack)
+        op.off = top;
+        plan->arena_peak = std::max(plan->arena_peak, top + sz);
+        peak_tok = std::max(peak_tok, live_tok + b.n);
+        res.forward_tokens += b.n;
+        res.num_batches += 1;
+        break;
+      case OP_BWD:
+        op.off = fwd_off[op.b];
+        top = op.off;
+        live_tok -= b.n;
+        res.backward_tokens += b.n;
+        res.num_chunks += 1;
+        break;
+      case OP_REFWD_BWD:  // recompute the chunk's activations from the stack, then its backward
+        op.off = top;
+        plan->arena_peak = std::max(plan->arena_peak, top + sz);
+        peak_tok = std::max(peak_tok, live_tok + b.n);
+        res.recompute_tokens += b.n;
+        res.backward_tokens += b.n;
+        res.num_chunks += 1;
+        res.num_segments += b.accum_inc;
+        break;
+      default:
+        break;
     }
   }
-  res.peak_live_kv_tokens = static_cast<uint64_t>(plan->rows);
+  res.peak_live_kv_tokens = peak_kv;
   res.peak_live_activation_tokens = peak_tok;
-  res.num_chunks = res.num_segments;
   for (auto& s : tree.seq_tokens) res.rollout_tokens += s.size();
   // ---- metadata for every batch, resident in HBM for the plan's lifetime
   std::vector<char> host;
@@ -899,9 +1029,23 @@ tt_step_result Engine::execute(StepPlan& plan) {
   cur_meta_ = plan.meta.as<char>();
   ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
   const uint64_t launches0 = launches_;
-  for (auto& [bi, push] : plan.ops) {
-    if (push) forward_batch(plan.batches[bi]);
-    else backward_batch(plan.batches[bi], nullptr);
+  for (const auto& op : plan.ops) {
+    const Batch& b = plan.batches[op.b];
+    switch (op.code) {
+      case OP_FWD:
+      case OP_FWD_DISCARD:
+        forward_batch(b, op.off);
+        break;
+      case OP_BWD:
+        backward_batch(b, op.off, nullptr);
+        break;
+      case OP_REFWD_BWD:
+        forward_batch(b, op.off);
+        backward_batch(b, op.off, nullptr);
+        break;
+      default:
+        break;
+    }
   }
   ck(cudaGetLastError(), "tree_train_step launch");
   ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
@@ -970,7 +1114,7 @@ void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out
   for (auto& x : seg_stack_) ptrs.push_back(&x);
   ptrs.push_back(&b);
   upload_meta(ptrs);
-  forward_batch(b);
+  forward_batch(b, b.arena_off);
   if (logits_out) {
     const ActLayout lay = layout(b.n);
     const bf16* nf = arena_.as<bf16>(b.arena_off + lay.nf);
@@ -1014,7 +1158,7 @@ void Engine::segment_pop(const float* grad_logits, float* grad_prefix_out) {
   std::vector<Batch*> ptrs;
   for (auto& x : seg_stack_) ptrs.push_back(&x);
   upload_meta(ptrs);
-  backward_batch(b, grad_logits);
+  backward_batch(b, b.arena_off, grad_logits);
   if (grad_prefix_out && b.S > 0) download(grad_prefix_out);
   ck(cudaGetLastError(), "segment_pop");
   ck(cudaStreamSynchronize(stream_), "segment_pop");

@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -59,13 +60,24 @@ struct Batch {
   size_t arena_off = 0;
   double attn_ctx = 0;       // sum over query rows of attended keys (S + t + 1): attention FLOP model
   bool full_logits = false;  // segment API: head over all rows with caller-provided grad_logits
+  bool leaf_batch = false;   // childless node(s): K/V not kept for descendants (leaf_kv_skip ledger)
+  int accum_inc = 1;         // GradientStore::accum_count increment (nodes completed by this pop)
+};
+
+// Step op codes: push (forward, activations kept), push with activations discarded (older chunks of
+// a chunked node), pop (backward, activations freed), recompute + pop.
+enum OpCode : int { OP_FWD = 0, OP_BWD = 1, OP_FWD_DISCARD = 2, OP_REFWD_BWD = 3 };
+struct PlanOp {
+  int b;       // batch index
+  int code;    // OpCode
+  size_t off;  // arena offset of the batch's activations for this op
 };
 
 // A prepared tree step: batches, PUSH/POP op list, memory plan, metadata resident in HBM.
 // prepare() once, execute() many times (the timed path with inputs already on the device).
 struct StepPlan {
   std::vector<Batch> batches;
-  std::vector<std::pair<int, bool>> ops;  // (batch index, is_push) in DFS order
+  std::vector<PlanOp> ops;  // DFS order
   int64_t rows = 0, max_n = 0, max_loss = 0;
   size_t arena_peak = 0;
   DevBuf meta;
@@ -114,7 +126,11 @@ class Engine {
   // Implementation switches (ablation / cross-checks): attn_{fwd,bwd}_impl 0 = mma.sync, 1 = tcgen05.
   void set_option(const std::string& key, int64_t value);
   const KStats& kstats() const { return kstats_; }
-  void reset_kstats() { kstats_ = KStats{}; }
+  void reset_kstats() {
+    kstats_ = KStats{};
+    tag_stats_.clear();
+  }
+  std::string gemm_profile_text() const;
   const std::string& last_trace() const { return last_trace_; }
 
   // segment level (device stack)
@@ -127,11 +143,13 @@ class Engine {
  private:
   // ---- helpers
   ActLayout layout(int64_t n) const;
+  double bytes_per_token() const;
+  uint64_t auto_batch_budget(uint64_t path_tokens) const;
   void ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, int64_t max_loss_rows);
   void build_meta(Batch& b, size_t& cursor, std::vector<char>& host);
   void upload_meta(std::vector<Batch*>& batches);
-  void forward_batch(const Batch& b);
-  void backward_batch(const Batch& b, const float* host_grad_logits);
+  void forward_batch(const Batch& b, size_t arena_off);
+  void backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits);
   void head_backward(const Batch& b, const bf16* nf);
   void head_backward_dense(const Batch& b, const bf16* nf, const float* host_grad_logits);
   void gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& e, int splits);
@@ -152,7 +170,8 @@ class Engine {
     cudaEventRecord(a, stream_);
     launch();
     cudaEventRecord(b, stream_);
-    pending_.push_back({cls, a, b, flops, bytes});
+    pending_.push_back({cls, a, b, flops, bytes, pending_tag_});
+    pending_tag_.clear();
     ++launches_;
   }
   cudaEvent_t event();
@@ -203,7 +222,14 @@ class Engine {
     KClass cls;
     cudaEvent_t a, b;
     double flops, bytes;
+    std::string tag;  // GEMM shape key (profiling detail)
   };
+  std::string pending_tag_;
+  struct TagStat {
+    double ms = 0, flops = 0;
+    uint64_t n = 0;
+  };
+  std::map<std::string, TagStat> tag_stats_;
   std::vector<Pending> pending_;
   std::vector<cudaEvent_t> event_pool_;
   size_t event_next_ = 0;

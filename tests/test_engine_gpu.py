@@ -209,3 +209,88 @@ def test_attention_impls_agree_on_tree(fwd_impl, bwd_impl):
     eng.set_option("attn_bwd_impl", bwd_impl)
     seqs = O.grouped_corpus(2, 4, 150, 200, cfg.vocab_size, 13, shared_response=20, weight_jitter=True)
     tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
+
+
+@pytest.mark.parametrize("chunk", [37, 64, 1000])
+def test_chunked_backward_vs_oracle(chunk):
+    # chunk_boundaries / chunked_backward: older chunks recomputed from the stack
+    cfg, flat, eng = make(SMALL, 14)
+    seqs = O.grouped_corpus(2, 3, 150, 130, cfg.vocab_size, 15, shared_response=40, weight_jitter=True)
+    r, _ = tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig(chunk_len=chunk))
+    root = O.build_prefix_tree(seqs)
+    longest = max(len(n.tokens) for n in O.preorder(root))
+    if chunk < longest:
+        assert r.recompute_tokens > 0 and r.num_chunks > r.num_segments
+    else:
+        assert r.recompute_tokens == 0
+    assert r.recompute_tokens <= r.forward_tokens
+
+
+def test_chunk_invariance_and_leaf_kv_skip_on_device():
+    # gradients independent of chunk_len and leaf_kv_skip; skip never
+    # increases peak live KV, which stays within the longest path
+    cfg, flat, eng = make(SMALL, 16)
+    seqs = O.grouped_corpus(2, 4, 90, 110, cfg.vocab_size, 17, shared_response=12)
+    tree = tt.build_prefix_tree([tt.TokenSequence(s.seq_id, s.tokens, s.weights) for s in seqs])
+    out = {}
+    for key, sc in (("base", tt.SchedulerConfig(sibling_batch=False)),
+                    ("chunk", tt.SchedulerConfig(sibling_batch=False, chunk_len=29)),
+                    ("skip", tt.SchedulerConfig(sibling_batch=False, leaf_kv_skip=True))):
+        eng.zero_gradients()
+        out[key] = (eng.tree_train_step(tree, sc), eng.gradients().astype(np.float64))
+    base_r, base_g = out["base"]
+    for key in ("chunk", "skip"):
+        r, g = out[key]
+        assert abs(r.total_loss - base_r.total_loss) <= 1e-3 * abs(base_r.total_loss)
+        check_grads(cfg, g, base_g, tol=1e-2, cos_tol=0.9999)
+    assert out["skip"][0].peak_live_kv_tokens <= base_r.peak_live_kv_tokens
+    assert out["skip"][0].peak_live_kv_tokens <= tree.stats()["max_path_tokens"]
+    assert out["skip"][0].recompute_tokens <= base_r.recompute_tokens
+
+
+def _shape_property(cfgt, seqs, chunk=0):
+    """Full-size model: tree step == flat per-sequence step on the device."""
+    eng = tt.Engine(tt.ModelConfig(*cfgt))
+    eng.init_params_random(3)
+    tseqs = [tt.TokenSequence(s.seq_id, s.tokens, s.weights) for s in seqs]
+    eng.zero_gradients()
+    rt = eng.tree_train_step(tt.build_prefix_tree(tseqs), tt.SchedulerConfig(chunk_len=chunk))
+    gt = eng.gradients().astype(np.float64)
+    eng.zero_gradients()
+    rd = eng.dense_train_step(tseqs)
+    gd = eng.gradients().astype(np.float64)
+    assert np.isfinite(rt.total_loss) and abs(rt.total_loss - rd.total_loss) <= 2e-3 * abs(rd.total_loss)
+    cos = float(gt @ gd / (np.linalg.norm(gt) * np.linalg.norm(gd)))
+    rel = float(np.linalg.norm(gt - gd) / np.linalg.norm(gd))
+    assert cos >= 0.9999 and rel <= 2e-2, (cos, rel)
+    assert rd.forward_tokens == sum(len(s.tokens) for s in seqs)
+    return rt, rd
+
+
+def test_c3_shape_deep_tree_tree_equals_flat():
+    # BASELINE configs[2]: 1.5B shape, deep multi-turn tree (4 levels, fan-out 4; 8K path); the
+    # chunked backward bounds activation memory by chunk_len (DFS stack-memory stress)
+    rng = np.random.default_rng(21)
+    V = 151936
+    seqs, sid = [], 0
+
+    def rec(prefix, depth):
+        nonlocal sid
+        if depth == 4:
+            w = [0.0] * 512 + [1.0] * (len(prefix) - 512)
+            seqs.append(O.TokenSequence(sid, prefix, w))
+            sid += 1
+            return
+        firsts = rng.choice(V, size=4 if depth else 1, replace=False)
+        for f in firsts:
+            rec(prefix + [int(f)] + rng.integers(0, V, 2047).tolist(), depth + 1)
+
+    rec([], 0)  # 4 levels of 2048-token nodes -> 64 leaves, 8192-token paths
+    rt, rd = _shape_property((V, 1536, 12, 28, 8960, 8200), seqs, chunk=512)
+    assert rt.recompute_tokens > 0
+
+
+def test_c4_shape_7b_tree_equals_flat():
+    # BASELINE configs[3] model (7B shape) on one rollout group
+    seqs = O.grouped_corpus(1, 4, 512, 768, 152064, 23)
+    _shape_property((152064, 3584, 28, 28, 18944, 1300), seqs)

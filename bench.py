@@ -318,7 +318,7 @@ def run_b200(args):
     eng.zero_gradients()
     plan.execute()
     eng.set_profiling(False)
-    gemm_top = eng.profile_gemm_text().splitlines()[:12]
+    gemm_top = eng.profile_gemm_text().splitlines()[:24]
     prof = eng.profile()
     sust, burst, hbm, src = measured_peaks()
     gm = prof["gemm"]
@@ -350,7 +350,7 @@ def run_b200(args):
                                "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
                                "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] and v["bytes"] else None}
                            for k, v in prof.items()},
-        "gemm_top_shapes": gemm_top,
+        "top_launch_shapes": gemm_top,
         "tree": {"tree_tokens": st["tree_tokens"], "rollout_tokens_per_gpu": roll_local, "nodes": st["num_nodes"],
                  "duplication_factor": roll_local / st["tree_tokens"], "max_path_tokens": st["max_path_tokens"],
                  "segment_batches": res.num_batches, "host_tree_build_s": build_s, "host_plan_s": plan_s},

@@ -8,6 +8,7 @@
 
 #include "capi_internal.h"
 #include "kernels/attention.h"
+#include "kernels/elementwise.h"
 #include "kernels/gemm.h"
 
 extern "C" {
@@ -27,7 +28,7 @@ int debug_gemm(bool sync, const void* a, long lda, int a_mn, const void* b, long
     e.out[2] = out2;
     e.ldo[0] = e.ldo[1] = e.ldo[2] = ldo;
     e.out2 = out_act;
-    e.ldo2 = ldo;
+    e.ldo2 = mode == ttb::EPI_STORE_F32_STATS ? (N + 31) / 32 : ldo;  // stats: float2 per 32-column group
     e.aux = static_cast<const __nv_bfloat16*>(aux);
     e.ld_aux = ldo;
     e.resid = static_cast<const float*>(aux);  // EPI_RESID_F32: aux is the fp32 residual input
@@ -54,6 +55,16 @@ int tt_debug_gemm_async(const void* a, long lda, int a_mn, const void* b, long l
                     splits);
 }
 int tt_debug_gemm_splits(int M, int N, int K) { return ttb::gemm_choose_splits(M, N, K); }
+
+// rmsnorm_backward kernel (model.hpp:258-271) on device buffers; synchronises.
+int tt_debug_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres,
+                         float* gx, void* gxb, float* ggain, int n, int d) {
+  return ttb::guarded([&] {
+    ttb::k_rmsnorm_bwd(gy, x, inv, gain, gres, gx, static_cast<__nv_bfloat16*>(gxb), ggain, n, d, nullptr);
+    ttb::check_cuda(cudaGetLastError(), "tt_debug_rmsnorm_bwd launch");
+    ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_rmsnorm_bwd sync");
+  });
+}
 void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
 
 // Segment attention on one segment of n queries over stack rows [0, S) + own rows [S, S+n)

@@ -69,6 +69,7 @@ Engine::Engine(const tt_model_config& cfg, int device) : cfg_(cfg), device_(devi
   if (dh_ != 64 && dh_ != 128) throw std::invalid_argument("engine: head_dim must be 64 or 128 on sm_100a");
   if (d_ % 64 || F_ % 64 || V_ % 16)
     throw std::invalid_argument("engine: d_model and d_ff must be multiples of 64, vocab_size of 16");
+  if (d_ > 8192) throw std::invalid_argument("engine: d_model must be <= 8192");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
 
@@ -166,6 +167,10 @@ void Engine::set_option(const std::string& key, int64_t value) {
   } else if (key == "attn_bwd_impl") {
     if (value != 0 && value != 1) throw std::invalid_argument("attn_bwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
     attn_bwd_impl_ = static_cast<int>(value);
+  } else if (key == "ce_stats") {
+    // 1: LM-head GEMM epilogue emits per-32-column softmax statistics, CE reads logits once
+    // (default); 0: CE does both passes over the logits row itself
+    ce_stats_ = value != 0;
   } else {
     throw std::invalid_argument("unknown engine option: " + key);
   }
@@ -307,6 +312,7 @@ void Engine::ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, in
     head_chunk_ = chunk;
     sc_nfl_.ensure(chunk * d_ * 2);
     sc_logits_.ensure(chunk * V_ * 4);
+    sc_stats_.ensure(chunk * ((V_ + 31) / 32) * 8);
     sc_dlog_.ensure(chunk * V_ * 2);
     sc_gnf_.ensure(chunk * d_ * 4);
   }
@@ -425,6 +431,7 @@ void Engine::collect_profile() {
       TagStat& ts = tag_stats_[p.tag];
       ts.ms += ms;
       ts.flops += p.flops;
+      ts.bytes += p.bytes;
       ts.n += 1;
     }
   }
@@ -438,8 +445,12 @@ std::string Engine::gemm_profile_text() const {
   std::string out;
   for (const auto& [tag, st] : v) {
     char line[256];
-    std::snprintf(line, sizeof(line), "%10.3f ms  n=%6llu  %7.1f TFLOP/s  %s\n", st.ms,
-                  static_cast<unsigned long long>(st.n), st.flops / (st.ms * 1e-3) / 1e12, tag.c_str());
+    if (st.flops > 0)
+      std::snprintf(line, sizeof(line), "%10.3f ms  n=%6llu  %7.1f TFLOP/s  %s\n", st.ms,
+                    static_cast<unsigned long long>(st.n), st.flops / (st.ms * 1e-3) / 1e12, tag.c_str());
+    else
+      std::snprintf(line, sizeof(line), "%10.3f ms  n=%6llu  %7.1f GB/s     %s\n", st.ms,
+                    static_cast<unsigned long long>(st.n), st.bytes / (st.ms * 1e-3) / 1e9, tag.c_str());
     out += line;
   }
   return out;
@@ -448,7 +459,7 @@ std::string Engine::gemm_profile_text() const {
 // GEMM launch: algorithmic FLOPs 2MNK; algorithmic bytes = operands once + output (x2 if RMW).
 void Engine::gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& e, int splits) {
   double out_b = 2.0;
-  if (e.mode == EPI_STORE_F32) out_b = 4.0;
+  if (e.mode == EPI_STORE_F32 || e.mode == EPI_STORE_F32_STATS) out_b = 4.0;
   if (e.mode == EPI_ADD_F32 || e.mode == EPI_RESID_F32) out_b = 8.0;
   if (e.mode == EPI_SILU || e.mode == EPI_DSILU) out_b = 4.0;
   const double bytes = 2.0 * (double(M) * K + double(N) * K) + out_b * double(M) * N;
@@ -472,6 +483,7 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
   const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
   const float scale = 1.0f / std::sqrt(static_cast<float>(dh_));  // model.hpp:345
 
+  tag("k_embed_pe");
   run(KC_ELEMWISE, 0, nd * 10, [&] {
     k_embed_pe(meta<int32_t>(b.o_tok), meta<int32_t>(b.o_pos), emb_, pe_.as<float>(), X(0), n, d, stream_);
   });
@@ -490,6 +502,7 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
     bf16* K = kst_.as<bf16>() + l * kv_layer;
     bf16* Vv = vst_.as<bf16>() + l * kv_layer;
 
+    tag("k_rmsnorm_fwd");
     run(KC_ELEMWISE, 0, nd * 6, [&] { k_rmsnorm_fwd(X(l), attn_g_[l], inv1, n1, n, d, stream_); });  // :376-380
     {  // q,k,v = normed W{q,k,v}; k,v written straight onto the stack rows [S, S+n)  (:381-384)
       EpiParams e;
@@ -519,10 +532,12 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       if (attn_fwd_impl_ == 1) {
         a.qblocks = meta<int4>(b.o_qblk128);
         a.nqb = static_cast<int>(b.qblk128.size() / 4);
+        tag("attn_fwd_sm100");
         run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd_sm100(a, rows_cap_, stream_); });
       } else {
         a.qblocks = meta<int4>(b.o_qblk);
         a.nqb = static_cast<int>(b.qblk.size() / 4);
+        tag("attn_fwd");
         run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd(a, stream_); });
       }
     }
@@ -535,6 +550,7 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       e.ld_resid = d;
       gemm(op(attn, d, false), op(wo_[l], d, true), n, d, d, e, 1);
     }
+    tag("k_rmsnorm_fwd");
     run(KC_ELEMWISE, 0, nd * 6, [&] { k_rmsnorm_fwd(xmid, mlp_g_[l], inv2, n2, n, d, stream_); });  // :430-434
     {  // h = normed W_in, act = silu(h)  (:435-444)
       EpiParams e;
@@ -555,6 +571,7 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       gemm(op(act, F, false), op(wout_[l], d, true), n, d, F, e, 1);
     }
   }
+  tag("k_rmsnorm_fwd");
   run(KC_ELEMWISE, 0, nd * 6, [&] {  // final norm (:451-455)
     k_rmsnorm_fwd(X(L_), final_g_, reinterpret_cast<float*>(base + lay.invf), reinterpret_cast<bf16*>(base + lay.nf),
                   n, d, stream_);
@@ -574,17 +591,21 @@ void Engine::head_backward(const Batch& b, const bf16* nf) {
   float* gnf = sc_gnf_.as<float>();
   for (int64_t c0 = 0; c0 < m; c0 += head_chunk_) {
     const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, m - c0));
+    tag("k_gather_rows_bf16");
     run(KC_ELEMWISE, 0, 4.0 * cm * d, [&] { k_gather_rows_bf16(nf, meta<int32_t>(b.o_lrows) + c0, nfl, cm, d, stream_); });
     {
-      EpiParams e;  // logits = normed_final W_head (model.hpp:460-461), fp32
-      e.mode = EPI_STORE_F32;
+      EpiParams e;  // logits = normed_final W_head (model.hpp:460-461), fp32, + per-row softmax stats
+      e.mode = ce_stats_ ? EPI_STORE_F32_STATS : EPI_STORE_F32;
       e.out[0] = sc_logits_.p;
       e.ldo[0] = V;
+      e.out2 = sc_stats_.p;
+      e.ldo2 = (V + 31) / 32;
       gemm(op(nfl, d, false), op(head_, V, true), cm, V, d, e, 1);
     }
+    tag("k_ce");
     run(KC_CE, 0, 6.0 * cm * V, [&] {  // weighted_nll (model.hpp:643-677), multi-target rows
       k_ce(sc_logits_.as<float>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt), meta<double>(b.o_pw),
-           dlog, loss_.as<double>(), stream_);
+           dlog, loss_.as<double>(), stream_, ce_stats_ ? sc_stats_.as<float2>() : nullptr, (V + 31) / 32);
     });
     {  // dW_head += c^T dlogits  (model.hpp:506)
       EpiParams e;
@@ -601,6 +622,7 @@ void Engine::head_backward(const Batch& b, const bf16* nf) {
       e.ldo[0] = d;
       gemm(op(dlog, V, false), op(head_, V, false), cm, d, V, e, gemm_choose_splits(cm, d, V));
     }
+    tag("k_scatter_rows_f32");
     run(KC_ELEMWISE, 0, 8.0 * cm * d, [&] { k_scatter_rows_f32(gnf, meta<int32_t>(b.o_lrows) + c0, gxf, cm, d, stream_); });
   }
 }
@@ -616,6 +638,7 @@ void Engine::head_backward_dense(const Batch& b, const bf16* nf, const float* ho
     ck(cudaMemcpyAsync(sc_logits_.p, host_grad_logits + c0 * V_, static_cast<size_t>(cm) * V_ * 4,
                        cudaMemcpyHostToDevice, stream_),
        "grad_logits upload");
+    tag("k_f32_to_bf16_2d");
     run(KC_ELEMWISE, 0, 6.0 * cm * V, [&] { k_f32_to_bf16_2d(sc_logits_.as<float>(), V, dlog, V, cm, V, stream_); });
     {
       EpiParams e;
@@ -662,6 +685,7 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
   } else {
     head_backward(b, nf);
   }
+  tag("k_rmsnorm_bwd");
   run(KC_ELEMWISE, 0, nd * 14, [&] {  // final-norm backward (model.hpp:509-511)
     k_rmsnorm_bwd(gxf, X(L_), reinterpret_cast<const float*>(base + lay.invf), final_g_, nullptr, gx, gxb, g_final_g_,
                   n, d, stream_);
@@ -714,6 +738,7 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       e.ldo[0] = d;
       gemm(op(gh, F, false), op(win_[l], F, false), n, d, F, e, 1);
     }
+    tag("k_rmsnorm_bwd");
     run(KC_ELEMWISE, 0, nd * 18, [&] {  // gx_mid = gx + rmsnorm_bwd (model.hpp:536-539)
       k_rmsnorm_bwd(gn, xmid, inv2, mlp_g_[l], gx, gx, gxb, g_mlp_g_[l], n, d, stream_);
     });
@@ -757,6 +782,7 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       a.nitems = static_cast<int>(b.kvit.size() / 4);
       a.scale = scale;
       if (attn_bwd_impl_ == 1) {
+        tag("attn_bwd_sm100");
         run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
           attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_qblk128), static_cast<int>(b.qblk128.size() / 4),
                          meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2), static_cast<int>(b.kvit128.size() / 4),
@@ -765,11 +791,13 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
         launches_ += 2;  // D pre-pass + the dq and dkdv kernels
       } else {
         ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
+        tag("attn_bwd");
         run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] { attn_bwd(a, stream_); });
         ++launches_;  // the D = rowsum(dO*O) pre-pass inside attn_bwd
       }
     }
     // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
+    tag("k_pack_dqkv");
     run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.S * d_, dV + b.S * d_, dqkv, n, d, stream_); });
     {  // dW_{q,k,v} += normed1^T [dq | dk | dv]  (model.hpp:610-612)
       EpiParams e;
@@ -788,10 +816,12 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       e.ldo[0] = d;
       gemm(op(dqkv, 3 * d, false), op(wqkv_[l], 3 * d, false), n, d, 3 * d, e, 1);
     }
+    tag("k_rmsnorm_bwd");
     run(KC_ELEMWISE, 0, nd * 18, [&] {  // gx = gx_mid + rmsnorm_bwd (model.hpp:620-624)
       k_rmsnorm_bwd(gn, X(l), inv1, attn_g_[l], gx, gx, gxb, g_attn_g_[l], n, d, stream_);
     });
   }
+  tag("k_embed_grad");
   run(KC_ELEMWISE, 0, nd * 12, [&] { k_embed_grad(gx, meta<int32_t>(b.o_tok), g_emb_, n, d, stream_); });  // :627-630
   accum_count_ += b.accum_inc;
 }

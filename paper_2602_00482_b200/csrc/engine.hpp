@@ -158,6 +158,9 @@ class Engine {
     return reinterpret_cast<const T*>(cur_meta_ + off);
   }
   void count(int k = 1) { launches_ += k; }
+  void tag(const char* name) {
+    if (profiling_) pending_tag_ = name;
+  }
   // Launch wrapper: counts the launch and, in profiling mode, brackets it with CUDA events.
   template <typename F>
   void run(KClass cls, double flops, double bytes, F&& launch) {
@@ -205,7 +208,7 @@ class Engine {
   size_t arena_top_ = 0, arena_peak_ = 0;
   int64_t scratch_n_ = 0, head_chunk_ = 0;
   DevBuf sc_gx_, sc_gxb_, sc_gxf_, sc_gn_, sc_gh_, sc_dO_, sc_D_, sc_dq_, sc_dqkv_;
-  DevBuf sc_nfl_, sc_logits_, sc_dlog_, sc_gnf_;
+  DevBuf sc_nfl_, sc_logits_, sc_stats_, sc_dlog_, sc_gnf_;
   DevBuf meta_;
   DevBuf loss_;
   double* loss_host_ = nullptr;  // pinned
@@ -217,6 +220,7 @@ class Engine {
   bool profiling_ = false;
   int attn_fwd_impl_ = 1;
   int attn_bwd_impl_ = 1;
+  bool ce_stats_ = true;
   KStats kstats_;
   struct Pending {
     KClass cls;
@@ -226,7 +230,7 @@ class Engine {
   };
   std::string pending_tag_;
   struct TagStat {
-    double ms = 0, flops = 0;
+    double ms = 0, flops = 0, bytes = 0;
     uint64_t n = 0;
   };
   std::map<std::string, TagStat> tag_stats_;

@@ -1,6 +1,7 @@
 // HBM-bound kernels of the push/pop path: embedding + positional encoding, RMSNorm fwd/bwd,
 // fused weighted cross-entropy over a vocab row, stack pop (dK/dV consume + zero), embedding
 // gradient scatter, parameter layout conversion / init. 128-bit coalesced accesses throughout.
+#include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -74,43 +75,58 @@ __global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __r
   }
 }
 
-// rmsnorm_backward (model.hpp:258-271), rows in blocks of kRows, 256 threads:
+// rmsnorm_backward (model.hpp:258-271), one warp per row, rows warp-strided over a ~2-wave grid:
 //   gx = gres + gy*g*inv - x*(sum(gy*g*x)*inv^3/d);  ggain += sum_rows gy*x*inv
-constexpr int kNormRows = 16;
-constexpr int kMaxVec = 8;  // d <= 8192
+// Each lane owns VPT float4 columns (c = (lane + 32 k) * 4); the row is held in registers when it
+// fits (KEEP), the gain-gradient partial stays in registers for all of the warp's rows, is reduced
+// across the block's warps in shared memory and lands with one red.global.add.v4 per column group.
+template <int VPT>
 __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float* __restrict__ gy, const float* __restrict__ x,
                                                           const float* __restrict__ inv, const float* __restrict__ gain,
                                                           const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
                                                           float* __restrict__ ggain, int n, int d) {
-  __shared__ float red[8];
-  float4 gacc[kMaxVec];
+  constexpr bool KEEP = VPT <= 12;
+  extern __shared__ float gsum[];  // [d]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = threadIdx.x; c < d; c += 256) gsum[c] = 0.f;
+  float4 gacc[VPT];
+  float4 av[KEEP ? VPT : 1], bv[KEEP ? VPT : 1];
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) gacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int r0 = blockIdx.x * kNormRows;
-  const int r1 = min(n, r0 + kNormRows);
-  for (int r = r0; r < r1; ++r) {
+  for (int k = 0; k < VPT; ++k) gacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int nw = gridDim.x * 8;
+  for (int r = blockIdx.x * 8 + warp; r < n; r += nw) {
     const long o = static_cast<long>(r) * d;
     const float iv = inv[r];
     float dot = 0.f;
 #pragma unroll
-    for (int k = 0; k < kMaxVec; ++k) {
-      const int c = (threadIdx.x + k * 256) * 4;
+    for (int k = 0; k < VPT; ++k) {
+      const int c = (lane + k * 32) * 4;
       if (c < d) {
-        const float4 a = *reinterpret_cast<const float4*>(gy + o + c);
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(gy + o + c));
         const float4 b = *reinterpret_cast<const float4*>(x + o + c);
-        const float4 g = *reinterpret_cast<const float4*>(gain + c);
+        const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
         dot += a.x * g.x * b.x + a.y * g.y * b.y + a.z * g.z * b.z + a.w * g.w * b.w;
+        if constexpr (KEEP) {
+          av[k] = a;
+          bv[k] = b;
+        }
       }
     }
-    dot = block_sum256(dot, red);
+    dot = warp_sum(dot);
     const float scale = dot * iv * iv * iv / static_cast<float>(d);
 #pragma unroll
-    for (int k = 0; k < kMaxVec; ++k) {
-      const int c = (threadIdx.x + k * 256) * 4;
+    for (int k = 0; k < VPT; ++k) {
+      const int c = (lane + k * 32) * 4;
       if (c < d) {
-        const float4 a = *reinterpret_cast<const float4*>(gy + o + c);
-        const float4 b = *reinterpret_cast<const float4*>(x + o + c);
-        const float4 g = *reinterpret_cast<const float4*>(gain + c);
+        float4 a, b;
+        if constexpr (KEEP) {
+          a = av[k];
+          b = bv[k];
+        } else {
+          a = *reinterpret_cast<const float4*>(gy + o + c);
+          b = *reinterpret_cast<const float4*>(x + o + c);
+        }
+        const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
         float4 res = gres ? *reinterpret_cast<const float4*>(gres + o + c) : make_float4(0.f, 0.f, 0.f, 0.f);
         res.x += a.x * g.x * iv - b.x * scale;
         res.y += a.y * g.y * iv - b.y * scale;
@@ -128,71 +144,117 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float* __restric
       }
     }
   }
+  __syncthreads();
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int c = (threadIdx.x + k * 256) * 4;
-    if (c < d) red_add_v4_f32(ggain + c, gacc[k].x, gacc[k].y, gacc[k].z, gacc[k].w);
+  for (int k = 0; k < VPT; ++k) {
+    const int c = (lane + k * 32) * 4;
+    if (c < d) {
+      atomicAdd(gsum + c, gacc[k].x);
+      atomicAdd(gsum + c + 1, gacc[k].y);
+      atomicAdd(gsum + c + 2, gacc[k].z);
+      atomicAdd(gsum + c + 3, gacc[k].w);
+    }
   }
+  __syncthreads();
+  for (int c = threadIdx.x * 4; c < d; c += 1024) red_add_v4_f32(ggain + c, gsum[c], gsum[c + 1], gsum[c + 2], gsum[c + 3]);
+}
+
+template <int VPT>
+void launch_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres,
+                        float* gx, __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
+  const int blocks = std::min((n + 7) / 8, 148 * 2);
+  rmsnorm_bwd_kernel<VPT><<<blocks, 256, d * sizeof(float), s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
 }
 
 // Weighted NLL over one vocab row with several (target, weight) pairs (weighted_nll,
 // model.hpp:643-677, extended to multi-target rows):
 //   loss += sum_j w_j (lse - l[t_j])  (fp64);  dl = (sum_j w_j) softmax(l) - sum_j w_j onehot(t_j)  (bf16)
-__global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits, long V,
-                                                 const int32_t* __restrict__ pair_off,
-                                                 const int32_t* __restrict__ tgt, const double* __restrict__ w,
-                                                 __nv_bfloat16* __restrict__ dl, double* __restrict__ loss) {
-  __shared__ float red[8];
+__device__ __forceinline__ float4 ld_evict_last_f4(const float* p, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+// Persistent: one 1024-thread CTA per SM walks rows. Pass 1 streams the row with an L2 evict_last
+// policy (the ~148 rows in flight fit in the 126 MB L2), pass 2 re-reads it from L2 (evict_first)
+// and writes dlogits, so HBM sees each logit once. With `stats` (per-32-column (max, sum) from the
+// LM-head GEMM epilogue) pass 1 reads only the statistics.
+__global__ void __launch_bounds__(1024) ce_kernel(const float* __restrict__ logits, int m, long V,
+                                                  const int32_t* __restrict__ pair_off,
+                                                  const int32_t* __restrict__ tgt, const double* __restrict__ w,
+                                                  __nv_bfloat16* __restrict__ dl, double* __restrict__ loss,
+                                                  const float2* __restrict__ stats, int n_groups) {
+  __shared__ float red[32];
   __shared__ float s_lse;
-  const int r = blockIdx.x;
-  const float* lr = logits + static_cast<long>(r) * V;
-  float m = -INFINITY, s = 0.f;
-  for (long c = threadIdx.x * 4; c < V; c += 1024) {
-    const float4 v = *reinterpret_cast<const float4*>(lr + c);
-    const float mx = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
-    if (mx > m) {
-      s *= __expf(m - mx);
-      m = mx;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  const int wi = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int r = blockIdx.x; r < m; r += gridDim.x) {
+    const float* lr = logits + static_cast<long>(r) * V;
+    float mx = -INFINITY, s = 0.f;
+    if (stats) {
+      const float2* sr = stats + static_cast<long>(r) * n_groups;
+      for (int g = threadIdx.x; g < n_groups; g += 1024) {
+        const float2 ms = sr[g];
+        if (ms.x > mx) {
+          s = s * __expf(mx - ms.x) + ms.y;
+          mx = ms.x;
+        } else {
+          s += ms.y * __expf(ms.x - mx);
+        }
+      }
+    } else {
+      for (long c = threadIdx.x * 4; c < V; c += 4096) {
+        const float4 v = ld_evict_last_f4(lr + c, pol);
+        const float vm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+        if (vm > mx) {
+          s *= __expf(mx - vm);
+          mx = vm;
+        }
+        s += __expf(v.x - mx) + __expf(v.y - mx) + __expf(v.z - mx) + __expf(v.w - mx);
+      }
     }
-    s += __expf(v.x - m) + __expf(v.y - m) + __expf(v.z - m) + __expf(v.w - m);
-  }
-  // combine (m, s) across the block
-  float gm = warp_max(m);
-  {
-    const int wi = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) red[wi] = gm;
+    // combine (max, sum) across the block
+    float gm = warp_max(mx);
+    if (ln == 0) red[wi] = gm;
     __syncthreads();
-    gm = warp_max(l < 8 ? red[l] : -INFINITY);
+    gm = warp_max(red[ln]);
     __syncthreads();
-  }
-  s = (m == -INFINITY) ? 0.f : s * __expf(m - gm);
-  s = block_sum256(s, red);
-  if (threadIdx.x == 0) {
-    s_lse = gm + logf(s);
-  }
-  __syncthreads();
-  const float lse = s_lse;
-  const int p0 = pair_off[r], p1 = pair_off[r + 1];
-  float wsum = 0.f;
-  for (int p = p0; p < p1; ++p) wsum += static_cast<float>(w[p]);
-  __nv_bfloat16* dr = dl + static_cast<long>(r) * V;
-  for (long c = threadIdx.x * 4; c < V; c += 1024) {
-    const float4 v = *reinterpret_cast<const float4*>(lr + c);
-    float g[4] = {wsum * __expf(v.x - lse), wsum * __expf(v.y - lse), wsum * __expf(v.z - lse),
-                  wsum * __expf(v.w - lse)};
-    for (int p = p0; p < p1; ++p) {
-      const long t = tgt[p];
-      if (t >= c && t < c + 4) g[t - c] -= static_cast<float>(w[p]);
+    s = (mx == -INFINITY) ? 0.f : s * __expf(mx - gm);
+    s = warp_sum(s);
+    if (ln == 0) red[wi] = s;
+    __syncthreads();
+    if (wi == 0) {
+      const float t = warp_sum(red[ln]);
+      if (ln == 0) s_lse = gm + logf(t);
     }
-    uint2 o;
-    o.x = pack_bf16x2(g[0], g[1]);
-    o.y = pack_bf16x2(g[2], g[3]);
-    *reinterpret_cast<uint2*>(dr + c) = o;
-  }
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int p = p0; p < p1; ++p) acc += w[p] * (static_cast<double>(lse) - static_cast<double>(lr[tgt[p]]));
-    atomicAdd(loss, acc);
+    __syncthreads();
+    const float lse = s_lse;
+    const int p0 = pair_off[r], p1 = pair_off[r + 1];
+    float wsum = 0.f;
+    for (int p = p0; p < p1; ++p) wsum += static_cast<float>(w[p]);
+    __nv_bfloat16* dr = dl + static_cast<long>(r) * V;
+    for (long c = threadIdx.x * 4; c < V; c += 4096) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(lr + c));
+      float g[4] = {wsum * __expf(v.x - lse), wsum * __expf(v.y - lse), wsum * __expf(v.z - lse),
+                    wsum * __expf(v.w - lse)};
+      for (int p = p0; p < p1; ++p) {
+        const long t = tgt[p];
+        if (t >= c && t < c + 4) g[t - c] -= static_cast<float>(w[p]);
+      }
+      uint2 o;
+      o.x = pack_bf16x2(g[0], g[1]);
+      o.y = pack_bf16x2(g[2], g[3]);
+      *reinterpret_cast<uint2*>(dr + c) = o;
+    }
+    if (threadIdx.x == 0) {
+      double acc = 0.0;
+      for (int p = p0; p < p1; ++p) acc += w[p] * (static_cast<double>(lse) - static_cast<double>(lr[tgt[p]]));
+      atomicAdd(loss, acc);
+    }
+    __syncthreads();  // red / s_lse reuse by the next row
   }
 }
 
@@ -287,11 +349,19 @@ void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16*
 }
 void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
                    __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
-  if (n > 0) rmsnorm_bwd_kernel<<<(n + kNormRows - 1) / kNormRows, 256, 0, s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
+  if (n <= 0) return;
+  const int vpt = (d + 127) / 128;  // float4 column groups per lane
+  if (vpt <= 2) launch_rmsnorm_bwd<2>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 4) launch_rmsnorm_bwd<4>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 7) launch_rmsnorm_bwd<7>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 12) launch_rmsnorm_bwd<12>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 16) launch_rmsnorm_bwd<16>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 28) launch_rmsnorm_bwd<28>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else launch_rmsnorm_bwd<64>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
 }
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
-          __nv_bfloat16* dl, double* loss, cudaStream_t s) {
-  if (m > 0) ce_kernel<<<m, 256, 0, s>>>(logits, V, pair_off, tgt, w, dl, loss);
+          __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {
+  if (m > 0) ce_kernel<<<std::min(m, 148), 1024, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
 }
 void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
                         cudaStream_t s) {

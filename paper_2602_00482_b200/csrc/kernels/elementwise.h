@@ -14,8 +14,10 @@ void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16*
 // gx = gres + d(rmsnorm)/dx (gres may be null; gx may alias gres), bf16 copy into gxb, gain grad into ggain.
 void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
                    __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s);
+// stats: optional per-row (max, sum exp) of 32-column groups from the LM-head GEMM epilogue
+// (EPI_STORE_F32_STATS, n_groups = ceil(V/32) per row); NULL = two passes over the logits row.
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
-          __nv_bfloat16* dl, double* loss, cudaStream_t s);
+          __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats = nullptr, int n_groups = 0);
 void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
                         cudaStream_t s);
 void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m, int d, cudaStream_t s);

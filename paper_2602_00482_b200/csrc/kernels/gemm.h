@@ -22,6 +22,9 @@ enum EpiMode : int {
   EPI_SILU = 3,        // out[0] (bf16) = acc, out2 (bf16) = silu(acc)
   EPI_DSILU = 4,       // out[0] (bf16) = acc * silu'(aux)
   EPI_RESID_F32 = 5,   // out[0] (fp32) = resid + alpha*acc   (residual stream, model.hpp:427-428,447-448)
+  EPI_STORE_F32_STATS = 6,  // out[0] (fp32) = alpha*acc, and out2 (float2, pitch ldo2) gets the per-row
+                            // (max, sum exp(v - max)) of every 32-column group: the softmax statistics
+                            // of LM-head logits, so the CE pass reads each logit row once
 };
 
 // Column blocks of width split_w go to out[n / split_w] (row pitch ldo[...]) so one GEMM can

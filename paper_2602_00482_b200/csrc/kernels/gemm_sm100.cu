@@ -114,15 +114,196 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) 
 }
 
 __device__ __forceinline__ float fast_sigmoid(float u) {
-  float e, r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-1.4426950408889634f * u));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
-  return r;
+  // sigmoid(u) = 0.5 tanh(u/2) + 0.5: one MUFU op (tanh.approx, max rel err ~2^-11 < bf16 ulp)
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * u));
+  return fmaf(0.5f, t, 0.5f);
 }
 __device__ __forceinline__ float silu_f(float u) { return u * fast_sigmoid(u); }
 __device__ __forceinline__ float silu_grad_f(float u) {
   const float s = fast_sigmoid(u);
   return s * (1.0f + u * (1.0f - s));
+}
+
+// ---- epilogue helpers (one thread = one accumulator row; 32 columns per call)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// tcgen05.wait::ld that also names the destination registers of the pending load, so no use of
+// them can be scheduled above the wait
+__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+// Output pointer / element offset of column n of `row` (column blocks of split_w go to out[n/split_w]).
+// Selects without dynamic indexing into the kernel-parameter arrays (avoids a local copy).
+__device__ __forceinline__ void epi_target(const EpiParams& epi, int row, int n, void*& outp, long& off) {
+  int blk = 0, nc = n;
+  if (epi.split_w > 0) {
+    blk = n / epi.split_w;
+    nc = n - blk * epi.split_w;
+  }
+  outp = blk == 0 ? epi.out[0] : (blk == 1 ? epi.out[1] : epi.out[2]);
+  const long ldo = blk == 0 ? epi.ldo[0] : (blk == 1 ? epi.ldo[1] : epi.ldo[2]);
+  off = static_cast<long>(row) * ldo + nc;
+}
+
+// Global operands of a 32-column chunk (independent of the accumulator): issued before the TMEM wait.
+__device__ __forceinline__ void epi_preload(const EpiParams& epi, bool row_ok, int row, int n0, int N,
+                                            uint4 (&pre)[2][4]) {
+  if (!row_ok) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int n = n0 + 16 * h;
+    if (n >= N) continue;
+    if (epi.mode == EPI_RESID_F32) {
+      const uint4* rp = reinterpret_cast<const uint4*>(epi.resid + static_cast<long>(row) * epi.ld_resid + n);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pre[h][i] = rp[i];
+    } else if (epi.mode == EPI_DSILU) {
+      const uint4* ph = reinterpret_cast<const uint4*>(epi.aux + static_cast<long>(row) * epi.ld_aux + n);
+      pre[h][0] = ph[0];
+      pre[h][1] = ph[1];
+    } else if (epi.mode == EPI_ADD_F32 && !epi.atomic) {
+      void* outp;
+      long off;
+      epi_target(epi, row, n, outp, off);
+      const uint4* q = reinterpret_cast<const uint4*>(static_cast<float*>(outp) + off);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pre[h][i] = q[i];
+    }
+  }
+}
+
+// One thread = one accumulator row; 32 columns (two 16-column halves) per call.
+__device__ __forceinline__ void epi_chunk32(const EpiParams& epi, const uint32_t (&r)[32], const uint4 (&pre)[2][4],
+                                            bool row_ok, int row, int n0, int N) {
+  if (!row_ok) return;
+  float st_m = -INFINITY, st_s = 0.f;  // EPI_STORE_F32_STATS: (max, sum exp) of this 32-column group
+#pragma unroll
+  for (int hh = 0; hh < 2; ++hh) {
+    const int n = n0 + 16 * hh;
+    if (n >= N) continue;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[16 * hh + i]) * epi.alpha;
+    void* outp;
+    long off;
+    epi_target(epi, row, n, outp, off);
+    switch (epi.mode) {
+      case EPI_STORE_BF16: {
+        uint4 w0, w1;
+        w0.x = pack_bf16x2(v[0], v[1]); w0.y = pack_bf16x2(v[2], v[3]);
+        w0.z = pack_bf16x2(v[4], v[5]); w0.w = pack_bf16x2(v[6], v[7]);
+        w1.x = pack_bf16x2(v[8], v[9]); w1.y = pack_bf16x2(v[10], v[11]);
+        w1.z = pack_bf16x2(v[12], v[13]); w1.w = pack_bf16x2(v[14], v[15]);
+        uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + off);
+        p[0] = w0;
+        p[1] = w1;
+        break;
+      }
+      case EPI_STORE_F32: {
+        float4* p = reinterpret_cast<float4*>(static_cast<float*>(outp) + off);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        break;
+      }
+      case EPI_STORE_F32_STATS: {
+        float4* p = reinterpret_cast<float4*>(static_cast<float*>(outp) + off);
+        float mx = v[0];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          mx = fmaxf(mx, fmaxf(fmaxf(v[4 * i], v[4 * i + 1]), fmaxf(v[4 * i + 2], v[4 * i + 3])));
+        }
+        const float nm = fmaxf(st_m, mx);
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sum += __expf(v[i] - nm);
+        st_s = st_s * __expf(st_m - nm) + sum;
+        st_m = nm;
+        break;
+      }
+      case EPI_ADD_F32: {
+        float* p = static_cast<float*>(outp) + off;
+        if (epi.atomic) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) red_add_v4_f32(p + 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+          float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 o = *reinterpret_cast<const float4*>(&pre[hh][i]);
+            q[i] = make_float4(o.x + v[4 * i], o.y + v[4 * i + 1], o.z + v[4 * i + 2], o.w + v[4 * i + 3]);
+          }
+        }
+        break;
+      }
+      case EPI_SILU: {
+        // out[0] <- h (pre-activation), out2 <- silu(h); both bf16 (model.hpp:443-444).
+        uint4 h0, h1, a0, a1;
+        float hb[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) hb[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+        h0.x = pack_bf16x2(hb[0], hb[1]); h0.y = pack_bf16x2(hb[2], hb[3]);
+        h0.z = pack_bf16x2(hb[4], hb[5]); h0.w = pack_bf16x2(hb[6], hb[7]);
+        h1.x = pack_bf16x2(hb[8], hb[9]); h1.y = pack_bf16x2(hb[10], hb[11]);
+        h1.z = pack_bf16x2(hb[12], hb[13]); h1.w = pack_bf16x2(hb[14], hb[15]);
+        a0.x = pack_bf16x2(silu_f(hb[0]), silu_f(hb[1])); a0.y = pack_bf16x2(silu_f(hb[2]), silu_f(hb[3]));
+        a0.z = pack_bf16x2(silu_f(hb[4]), silu_f(hb[5])); a0.w = pack_bf16x2(silu_f(hb[6]), silu_f(hb[7]));
+        a1.x = pack_bf16x2(silu_f(hb[8]), silu_f(hb[9])); a1.y = pack_bf16x2(silu_f(hb[10]), silu_f(hb[11]));
+        a1.z = pack_bf16x2(silu_f(hb[12]), silu_f(hb[13])); a1.w = pack_bf16x2(silu_f(hb[14]), silu_f(hb[15]));
+        uint4* ph = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
+        uint4* pa = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out2) + static_cast<long>(row) * epi.ldo2 + n);
+        ph[0] = h0; ph[1] = h1;
+        pa[0] = a0; pa[1] = a1;
+        break;
+      }
+      case EPI_DSILU: {
+        // out[0] <- acc * silu'(h) in bf16 (model.hpp:526-528).
+        const __nv_bfloat16* hh_ = reinterpret_cast<const __nv_bfloat16*>(&pre[hh][0]);
+        float g[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) g[i] = v[i] * silu_grad_f(__bfloat162float(hh_[i]));
+        uint4 w0, w1;
+        w0.x = pack_bf16x2(g[0], g[1]); w0.y = pack_bf16x2(g[2], g[3]);
+        w0.z = pack_bf16x2(g[4], g[5]); w0.w = pack_bf16x2(g[6], g[7]);
+        w1.x = pack_bf16x2(g[8], g[9]); w1.y = pack_bf16x2(g[10], g[11]);
+        w1.z = pack_bf16x2(g[12], g[13]); w1.w = pack_bf16x2(g[14], g[15]);
+        uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + off);
+        p[0] = w0;
+        p[1] = w1;
+        break;
+      }
+      case EPI_RESID_F32: {
+        float4* p = reinterpret_cast<float4*>(static_cast<float*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 r4 = *reinterpret_cast<const float4*>(&pre[hh][i]);
+          p[i] = make_float4(r4.x + v[4 * i], r4.y + v[4 * i + 1], r4.z + v[4 * i + 2], r4.w + v[4 * i + 3]);
+        }
+        break;
+      }
+      default:
+        break;
+    }
+  }
+  if (epi.mode == EPI_STORE_F32_STATS && n0 < N)
+    reinterpret_cast<float2*>(epi.out2)[static_cast<long>(row) * epi.ldo2 + n0 / 32] = make_float2(st_m, st_s);
 }
 
 template <int BN, int CG, bool A_MN, bool B_MN>
@@ -298,134 +479,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   mma_done:;
   } else {
     // ------------------------------------------------------------ epilogue
+    // Each warp drains 32 TMEM lanes (rows) x BN/2 columns in 32-column chunks, software-pipelined:
+    // the TMEM load of chunk c+1 and the global operand loads (residual / aux / RMW target) of chunk
+    // c are in flight while chunk c is converted and stored; the accumulator slot is handed back to
+    // the MMA warp as soon as its last chunk is in registers.
     const int quad = warp & 3;             // TMEM lane quadrant this warp may access
     const int half = (warp - 2) / 4;       // which half of the BN columns this warp handles
+    constexpr int CW = BN / 2;
+    constexpr int NCH = CW / 32;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < num_tiles; t += ncl) {
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
       const int row = m_blk * TM + static_cast<int>(rank) * BM + quad * 32 + lane;
       const bool row_ok = row < M;
-      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(quad * 32) << 16);
+      const int n_base = n_blk * BN + half * CW;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + acc * BN + half * CW + (static_cast<uint32_t>(quad * 32) << 16);
+      uint32_t rr[2][32];
+      tmem_ld32(t_row, rr[0]);
 #pragma unroll
-      for (int c2 = half * (BN / 2); c2 < (half + 1) * (BN / 2); c2 += 32) {
-        uint32_t rr[2][16];
-        tmem_ld16(t_row + c2, rr[0]);
-        tmem_ld16(t_row + c2 + 16, rr[1]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-        const int c = c2 + 16 * hh;
-        const uint32_t (&r)[16] = rr[hh];
-        const int n = n_blk * BN + c;
-        if (!row_ok || n >= N) continue;
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * epi.alpha;
-        int blk = 0, nc = n;
-        if (epi.split_w > 0) {
-          blk = n / epi.split_w;
-          nc = n - blk * epi.split_w;
+      for (int ch = 0; ch < NCH; ++ch) {
+        const int n0 = n_base + ch * 32;
+        uint4 pre[2][4];
+        epi_preload(epi, row_ok, row, n0, N, pre);
+        tmem_ld_wait_regs(rr[ch & 1]);
+        if (ch + 1 < NCH) {
+          tmem_ld32(t_row + (ch + 1) * 32, rr[(ch + 1) & 1]);
+        } else {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
+            else mbar_arrive_remote(mapa_shared(smem_u32(&tempty_bar[acc]), 0));  // the leader's slot barrier
+          }
         }
-        // select without dynamic indexing into the kernel-parameter arrays (avoids a local copy)
-        void* const outp = blk == 0 ? epi.out[0] : (blk == 1 ? epi.out[1] : epi.out[2]);
-        const long ldo = blk == 0 ? epi.ldo[0] : (blk == 1 ? epi.ldo[1] : epi.ldo[2]);
-        const long off = static_cast<long>(row) * ldo + nc;
-        switch (epi.mode) {
-          case EPI_STORE_BF16: {
-            uint4 w0, w1;
-            w0.x = pack_bf16x2(v[0], v[1]); w0.y = pack_bf16x2(v[2], v[3]);
-            w0.z = pack_bf16x2(v[4], v[5]); w0.w = pack_bf16x2(v[6], v[7]);
-            w1.x = pack_bf16x2(v[8], v[9]); w1.y = pack_bf16x2(v[10], v[11]);
-            w1.z = pack_bf16x2(v[12], v[13]); w1.w = pack_bf16x2(v[14], v[15]);
-            uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + off);
-            p[0] = w0;
-            p[1] = w1;
-            break;
-          }
-          case EPI_STORE_F32: {
-            float4* p = reinterpret_cast<float4*>(static_cast<float*>(outp) + off);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            break;
-          }
-          case EPI_ADD_F32: {
-            float* p = static_cast<float*>(outp) + off;
-            if (epi.atomic) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i) red_add_v4_f32(p + 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            } else {
-              float4* q = reinterpret_cast<float4*>(p);
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                float4 o = q[i];
-                o.x += v[4 * i]; o.y += v[4 * i + 1]; o.z += v[4 * i + 2]; o.w += v[4 * i + 3];
-                q[i] = o;
-              }
-            }
-            break;
-          }
-          case EPI_SILU: {
-            // out[0] <- h (pre-activation), out2 <- silu(h); both bf16 (model.hpp:443-444).
-            uint4 h0, h1, a0, a1;
-            float hb[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) hb[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-            h0.x = pack_bf16x2(hb[0], hb[1]); h0.y = pack_bf16x2(hb[2], hb[3]);
-            h0.z = pack_bf16x2(hb[4], hb[5]); h0.w = pack_bf16x2(hb[6], hb[7]);
-            h1.x = pack_bf16x2(hb[8], hb[9]); h1.y = pack_bf16x2(hb[10], hb[11]);
-            h1.z = pack_bf16x2(hb[12], hb[13]); h1.w = pack_bf16x2(hb[14], hb[15]);
-            a0.x = pack_bf16x2(silu_f(hb[0]), silu_f(hb[1])); a0.y = pack_bf16x2(silu_f(hb[2]), silu_f(hb[3]));
-            a0.z = pack_bf16x2(silu_f(hb[4]), silu_f(hb[5])); a0.w = pack_bf16x2(silu_f(hb[6]), silu_f(hb[7]));
-            a1.x = pack_bf16x2(silu_f(hb[8]), silu_f(hb[9])); a1.y = pack_bf16x2(silu_f(hb[10]), silu_f(hb[11]));
-            a1.z = pack_bf16x2(silu_f(hb[12]), silu_f(hb[13])); a1.w = pack_bf16x2(silu_f(hb[14]), silu_f(hb[15]));
-            uint4* ph = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
-            uint4* pa = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out2) + static_cast<long>(row) * epi.ldo2 + n);
-            ph[0] = h0; ph[1] = h1;
-            pa[0] = a0; pa[1] = a1;
-            break;
-          }
-          case EPI_DSILU: {
-            // out[0] <- acc * silu'(h) in bf16 (model.hpp:526-528).
-            const uint4* ph = reinterpret_cast<const uint4*>(epi.aux + static_cast<long>(row) * epi.ld_aux + n);
-            uint4 hv[2] = {ph[0], ph[1]};
-            const __nv_bfloat16* hh = reinterpret_cast<const __nv_bfloat16*>(hv);
-            float g[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) g[i] = v[i] * silu_grad_f(__bfloat162float(hh[i]));
-            uint4 w0, w1;
-            w0.x = pack_bf16x2(g[0], g[1]); w0.y = pack_bf16x2(g[2], g[3]);
-            w0.z = pack_bf16x2(g[4], g[5]); w0.w = pack_bf16x2(g[6], g[7]);
-            w1.x = pack_bf16x2(g[8], g[9]); w1.y = pack_bf16x2(g[10], g[11]);
-            w1.z = pack_bf16x2(g[12], g[13]); w1.w = pack_bf16x2(g[14], g[15]);
-            uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + off);
-            p[0] = w0;
-            p[1] = w1;
-            break;
-          }
-          case EPI_RESID_F32: {
-            const float4* rp = reinterpret_cast<const float4*>(epi.resid + static_cast<long>(row) * epi.ld_resid + n);
-            float4* p = reinterpret_cast<float4*>(static_cast<float*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float4 r4 = rp[i];
-              p[i] = make_float4(r4.x + v[4 * i], r4.y + v[4 * i + 1], r4.z + v[4 * i + 2], r4.w + v[4 * i + 3]);
-            }
-            break;
-          }
-          default:
-            break;
-        }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
-        else mbar_arrive_remote(mapa_shared(smem_u32(&tempty_bar[acc]), 0));  // the leader's slot barrier
+        epi_chunk32(epi, rr[ch & 1], pre, row_ok, row, n0, N);
       }
       if (++acc == 2) {
         acc = 0;

@@ -211,6 +211,16 @@ def test_attention_impls_agree_on_tree(fwd_impl, bwd_impl):
     tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
 
 
+@pytest.mark.parametrize("ce_stats", [0, 1])
+def test_lm_head_ce_variants_vs_oracle(ce_stats):
+    # weighted_nll (model.hpp:643-677): CE from the GEMM-epilogue softmax statistics (1) or from
+    # its own two passes over the logits row (0) — same step against the oracle
+    cfg, flat, eng = make(SMALL, 18)
+    eng.set_option("ce_stats", ce_stats)
+    seqs = O.grouped_corpus(2, 4, 150, 200, cfg.vocab_size, 19, shared_response=20, weight_jitter=True)
+    tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
+
+
 @pytest.mark.parametrize("chunk", [37, 64, 1000])
 def test_chunked_backward_vs_oracle(chunk):
     # chunk_boundaries / chunked_backward: older chunks recomputed from the stack

@@ -17,7 +17,7 @@ def _lib():
     return _native.lib()
 
 
-EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU = range(5)
+EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU, EPI_RESID_F32, EPI_STORE_F32_STATS = range(7)
 
 
 @pytest.fixture(params=[1, 0], ids=["2cta", "1cta"], autouse=True)
@@ -121,6 +121,58 @@ def test_gemm_large_vocab_head():
     _gemm(x, 0, w, 1, M, N, K, EPI_STORE_F32, [out], N)
     ref = x.float() @ w.float()
     assert _rel(out, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N", [(256, 151936), (77, 1024), (300, 4864), (130, 1040)])
+def test_gemm_logits_with_softmax_stats(M, N):
+    """EPI_STORE_F32_STATS: fp32 logits plus (max, sum exp) per row and 32-column group."""
+    torch.manual_seed(6)
+    K = 896
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = (0.05 * torch.randn(K, N, device="cuda")).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    G = (N + 31) // 32
+    stats = torch.full((M, G, 2), float("nan"), device="cuda")
+    _gemm(x, 0, w, 1, M, N, K, EPI_STORE_F32_STATS, [out], N, act=stats)
+    ref = x.float() @ w.float()
+    assert _rel(out, ref) < 1e-5
+    pad = torch.full((M, G * 32), float("-inf"), device="cuda")
+    pad[:, :N] = out
+    grp = pad.view(M, G, 32)
+    mx = grp.max(-1).values
+    se = torch.exp(grp - mx[..., None]).sum(-1)
+    assert torch.allclose(stats[..., 0], mx)
+    assert torch.allclose(stats[..., 1], se, rtol=1e-5)
+    # combined log-sum-exp equals the row's
+    lse = stats[..., 0].max(-1).values
+    lse = lse + torch.log((stats[..., 1] * torch.exp(stats[..., 0] - lse[:, None])).sum(-1))
+    assert torch.allclose(lse, torch.logsumexp(out, -1), atol=1e-5)
+
+
+@pytest.mark.parametrize("n,d", [(1, 256), (37, 896), (4099, 896), (300, 1536), (129, 3584)])
+def test_rmsnorm_bwd_matches_torch(n, d):
+    torch.manual_seed(7)
+    lib = _lib()
+    vp = ctypes.c_void_p
+    gy = torch.randn(n, d, device="cuda")
+    x = torch.randn(n, d, device="cuda")
+    g = torch.rand(d, device="cuda") + 0.5
+    inv = 1.0 / torch.sqrt((x * x).mean(-1) + 1e-6)
+    gres = torch.randn(n, d, device="cuda")
+    gx = torch.empty(n, d, device="cuda")
+    gxb = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    gg = torch.randn(d, device="cuda")
+    gg0 = gg.clone()
+    rc = lib.tt_debug_rmsnorm_bwd(vp(gy.data_ptr()), vp(x.data_ptr()), vp(inv.data_ptr()), vp(g.data_ptr()),
+                                  vp(gres.data_ptr()), vp(gx.data_ptr()), vp(gxb.data_ptr()), vp(gg.data_ptr()), n, d)
+    assert rc == 0, lib.tt_last_error().decode()
+    xr = x.clone().requires_grad_(True)
+    gr = g.clone().requires_grad_(True)
+    y = xr * torch.rsqrt((xr * xr).mean(-1, keepdim=True) + 1e-6) * gr
+    y.backward(gy)
+    assert _rel(gx, gres + xr.grad) < 1e-5
+    assert _rel(gxb, gres + xr.grad) < 1e-2
+    assert _rel(gg, gg0 + gr.grad) < 1e-5
 
 
 # ----------------------------------------------------------------------------- segment attention

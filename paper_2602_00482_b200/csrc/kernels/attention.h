@@ -54,6 +54,10 @@ void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream);
 constexpr int kFwdBlockQ = 128;
 void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream);
 
+// Softmax exponentials taken on the FMA pipe per 4 element pairs (0..2; default 1). Tuning knob:
+// env TT_ATTN_POLY, read once.
+int attn_poly_pairs();
+
 // D = rowsum(dO * O) per (head, row) (the softmax-backward correction term).
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream);
 // tcgen05 backward (attention_bwd_sm100.cu): dq_blocks are 128-row query blocks (like the forward);

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include "attention.h"
@@ -50,6 +51,7 @@ __device__ __forceinline__ void st_halfrow_sw128(uint8_t* panel, int row, int ha
 template <int DH, int NS>
 struct DqCfg {
   static constexpr int BQ = 128, BKV = 64;
+  static constexpr int NB = 3;  // S/dP TMEM buffers: the MMA warp runs NB-1 blocks ahead of softmax
   static constexpr int kQBytes = BQ * DH * 2;
   static constexpr int kKVBytes = BKV * DH * 2;
   static constexpr int kDSBytes = BQ * BKV * 2;
@@ -58,7 +60,8 @@ struct DqCfg {
   static constexpr int kOffV = kOffK + NS * kKVBytes;
   static constexpr int kOffDS = kOffV + NS * kKVBytes;
   static constexpr int kOffBar = kOffDS + 2 * kDSBytes;
-  static constexpr int kTmemCols = (4 * BKV + DH) <= 256 ? 256 : 512;
+  static constexpr int kTmemCols = (2 * NB * BKV + DH) <= 256 ? 256 : 512;
+  static_assert(2 * NB * BKV + DH <= 512 && NS >= NB, "dq kernel: TMEM / K-V ring too small");
   // a second co-resident CTA could not get TMEM (it would block in tcgen05.alloc while holding the
   // SM's warp slots): size smem so that exactly one CTA fits when all 512 columns are needed
   static constexpr int kSmemUsed = kOffBar + 256 + 1024;
@@ -81,21 +84,23 @@ struct BwdParams {
   float scale, scale_log2;
 };
 
-template <int DH, int NS>
+// DBG (timing experiments only, TT_ATTN_DBG): 1 = softmax warps skip TMEM loads + math (MMA/TMA
+// pipeline alone), 2 = softmax warps do not wait for S (softmax alone).
+template <int DH, int NS, int POLY, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                      BwdParams p) {
   using C = DqCfg<DH, NS>;
   constexpr int BKV = C::BKV;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + NS;
-  uint64_t* s_full = kv_empty + NS;  // [2]  S_j and dP_j in TMEM
-  uint64_t* ds_full = s_full + 2;    // [2]  dS_j in smem
+  uint64_t* s_full = kv_empty + NS;  // [NB] S_j and dP_j in TMEM
+  uint64_t* ds_full = s_full + C::NB;  // [2]  dS_j in smem
   uint64_t* ds_free = ds_full + 2;   // [2]  dQ MMA consumed dS_j
   uint64_t* dq_done = ds_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
@@ -121,8 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
+    for (int s = 0; s < C::NB; ++s) mbar_init(&s_full[s], 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&s_full[s], 1);
       mbar_init(&ds_full[s], kSmxWarps);
       mbar_init(&ds_free[s], 1);
     }
@@ -134,8 +139,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: S[2] at [0, 2*BKV), dP[2] at [2*BKV, 4*BKV), dQ at [4*BKV, 4*BKV+DH)
-  const uint32_t t_S = tmem, t_dP = tmem + 2 * BKV, t_dQ = tmem + 4 * BKV;
+  // TMEM columns: S[NB] at [0, NB*BKV), dP[NB] at [NB*BKV, 2*NB*BKV), dQ at [2*NB*BKV, +DH)
+  constexpr int NB = C::NB;
+  const uint32_t t_S = tmem, t_dP = tmem + NB * BKV, t_dQ = tmem + 2 * NB * BKV;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -158,46 +164,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t q_addr = smem_u32(smem), do_addr = smem_u32(smem + C::kOffDO);
+    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);         // K-major tiles
+    const uint64_t dKmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // K_j read MN-major
     auto issue_s = [&](int j) {  // S_j = Q K_j^T ; dP_j = dO V_j^T
       const int st = j % NS;
       mbar_wait(&kv_full[st], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t k_addr = smem_u32(smem + C::kOffK + st * C::kKVBytes);
-        const uint32_t v_addr = smem_u32(smem + C::kOffV + st * C::kKVBytes);
+        const uint32_t k_off = C::kOffK + st * C::kKVBytes, v_off = C::kOffV + st * C::kKVBytes;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
           const uint32_t ao = (k / 4) * (128 * 128) + (k % 4) * 32, bo = (k / 4) * (BKV * 128) + (k % 4) * 32;
-          umma_bf16_ss(t_S + (j & 1) * BKV, make_sdesc_sw128(q_addr + ao, 16, 1024),
-                       make_sdesc_sw128(k_addr + bo, 16, 1024), C::kIdescS, k > 0);
-          umma_bf16_ss(t_dP + (j & 1) * BKV, make_sdesc_sw128(do_addr + ao, 16, 1024),
-                       make_sdesc_sw128(v_addr + bo, 16, 1024), C::kIdescS, k > 0);
+          umma_bf16_ss(t_S + (j % NB) * BKV, sdesc_add(d16, ao), sdesc_add(sdesc_add(d16, k_off), bo), C::kIdescS, k > 0);
+          umma_bf16_ss(t_dP + (j % NB) * BKV, sdesc_add(d16, C::kOffDO + ao), sdesc_add(sdesc_add(d16, v_off), bo), C::kIdescS,
+                       k > 0);
         }
-        umma_commit(&s_full[j & 1]);
+        umma_commit(&s_full[j % NB]);
       }
       __syncwarp();
     };
     mbar_wait(q_full, 0);
-    issue_s(0);
-    if (nblk > 1) issue_s(1);
+    for (int j = 0; j < NB && j < nblk; ++j) issue_s(j);
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&ds_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {  // dQ += dS_j K_j   (B = K_j read MN-major: N = dh, K = keys)
         const int st = j % NS;
-        const uint32_t ds_addr = smem_u32(smem + C::kOffDS + (j & 1) * C::kDSBytes);
-        const uint32_t k_addr = smem_u32(smem + C::kOffK + st * C::kKVBytes);
+        const uint32_t ds_off = C::kOffDS + (j & 1) * C::kDSBytes, k_off = C::kOffK + st * C::kKVBytes;
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          umma_bf16_ss(t_dQ, make_sdesc_sw128(ds_addr + k * 32, 16, 1024),
-                       make_sdesc_sw128(k_addr + k * 2048, BKV * 128, 1024), C::kIdescQ, (j > 0 || k > 0));
+          umma_bf16_ss(t_dQ, sdesc_add(sdesc_add(d16, ds_off), k * 32), sdesc_add(sdesc_add(dKmn, k_off), k * 2048), C::kIdescQ,
+                       (j > 0 || k > 0));
         umma_commit(&kv_empty[st]);
         umma_commit(&ds_free[j & 1]);
         if (j == nblk - 1) umma_commit(dq_done);
       }
       __syncwarp();
-      if (j + 2 < nblk) issue_s(j + 2);
+      if (j + NB < nblk) issue_s(j + NB);
     }
   } else {
     const int quad = warp & 3;
@@ -213,14 +216,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float c2 = p.scale_log2;
     constexpr int HC = BKV / 2;
     for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      if (DBG != 2) mbar_wait(&s_full[j % NB], (j / NB) & 1);
       tc_fence_after();
+      if (DBG == 1) {
+        if (j >= 2) mbar_wait(&ds_free[j & 1], ((j >> 1) + 1) & 1);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[j & 1]);
+        continue;
+      }
       float s[HC], dp[HC];
 #pragma unroll
       for (int c = 0; c < HC; c += 16) {
         uint32_t r[16], r2[16];
-        tmem_ld16(t_S + (j & 1) * BKV + half * HC + c + lane_off, r);
-        tmem_ld16(t_dP + (j & 1) * BKV + half * HC + c + lane_off, r2);
+        tmem_ld16(t_S + (j % NB) * BKV + half * HC + c + lane_off, r);
+        tmem_ld16(t_dP + (j % NB) * BKV + half * HC + c + lane_off, r2);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           s[c + i] = __uint_as_float(r[i]);
@@ -240,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int i = 0; i < HC; i += 2) {
         const float2 x = __ffma2_rn(make_float2(s[i], s[i + 1]), c22, nl2);
-        const float2 pe = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        const float2 pe = ((i / 2) & 3) < POLY ? ex2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
         const float2 ds = __fmul2_rn(pe, __fadd2_rn(make_float2(dp[i], dp[i + 1]), nD2));
         w[i / 2] = pack_bf16x2(ds.x, ds.y);
       }
@@ -276,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int DH, int NS>
 struct DkvCfg {
   static constexpr int BKV = 128, BQ = 64;
+  static constexpr int NB = DH == 64 ? 3 : 2;  // S^T/dP^T TMEM buffers (TMEM: 2*NB*BQ + 2*DH <= 512)
   static constexpr int kKVBytes = BKV * DH * 2;   // K (or V) block, loaded once
   static constexpr int kQBytes = BQ * DH * 2;     // Q_i (or dO_i) tile
   static constexpr int kPBytes = BKV * BQ * 2;    // P^T (or dS^T) tile
@@ -288,25 +300,26 @@ struct DkvCfg {
   static constexpr int kOffBar = kOffStat + 2 * 2 * BQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kTmemCols = 512;
+  static_assert(2 * NB * BQ + 2 * DH <= 512 && NS >= NB, "dkdv kernel: TMEM / Q ring too small");
   static constexpr uint32_t kIdescS = make_idesc_bf16(128, BQ, false, false);
   static constexpr uint32_t kIdescKV = make_idesc_bf16(128, DH, false, true);
 };
 
-template <int DH, int NS>
+template <int DH, int NS, int POLY>
 __global__ void __launch_bounds__(kThreads, 1)
     fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        BwdParams p) {
   using C = DkvCfg<DH, NS>;
   constexpr int BQ = C::BQ;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;
   uint64_t* q_empty = q_full + NS;
-  uint64_t* s_full = q_empty + NS;  // [2]
-  uint64_t* p_full = s_full + 2;    // [2]
+  uint64_t* s_full = q_empty + NS;    // [NB]
+  uint64_t* p_full = s_full + C::NB;  // [2]
   uint64_t* p_free = p_full + 2;    // [2]
   uint64_t* acc_done = p_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
@@ -333,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
+    for (int s = 0; s < C::NB; ++s) mbar_init(&s_full[s], 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSmxWarps);
       mbar_init(&p_free[s], 1);
     }
@@ -346,8 +359,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: S^T[2] at [0,128), dP^T[2] at [128,256), dK at [256, 256+DH), dV at [384, 384+DH)
-  const uint32_t t_S = tmem, t_dP = tmem + 2 * BQ, t_dK = tmem + 256, t_dV = tmem + 384;
+  // TMEM columns: S^T[NB] at [0, NB*BQ), dP^T[NB] at [NB*BQ, 2*NB*BQ), then dK and dV (DH each)
+  constexpr int NB = C::NB;
+  const uint32_t t_S = tmem, t_dP = tmem + NB * BQ, t_dK = tmem + 2 * NB * BQ, t_dV = t_dK + DH;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -370,51 +384,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t k_addr = smem_u32(smem), v_addr = smem_u32(smem + C::kOffV);
+    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);        // K-major tiles
+    const uint64_t dmn = make_sdesc_sw128(smem_u32(smem), BQ * 128, 1024);  // Q_i / dO_i read MN-major
     auto issue_s = [&](int i) {  // S^T_i = K Q_i^T ; dP^T_i = V dO_i^T   (M = 128 keys, N = 64 queries)
       const int st = i % NS;
       mbar_wait(&q_full[st], (i / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t q_addr = smem_u32(smem + C::kOffQ + st * C::kQBytes);
-        const uint32_t do_addr = smem_u32(smem + C::kOffDO + st * C::kQBytes);
+        const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
           const uint32_t ao = (k / 4) * (128 * 128) + (k % 4) * 32, bo = (k / 4) * (BQ * 128) + (k % 4) * 32;
-          umma_bf16_ss(t_S + (i & 1) * BQ, make_sdesc_sw128(k_addr + ao, 16, 1024),
-                       make_sdesc_sw128(q_addr + bo, 16, 1024), C::kIdescS, k > 0);
-          umma_bf16_ss(t_dP + (i & 1) * BQ, make_sdesc_sw128(v_addr + ao, 16, 1024),
-                       make_sdesc_sw128(do_addr + bo, 16, 1024), C::kIdescS, k > 0);
+          umma_bf16_ss(t_S + (i % NB) * BQ, sdesc_add(d16, ao), sdesc_add(sdesc_add(d16, q_off), bo), C::kIdescS, k > 0);
+          umma_bf16_ss(t_dP + (i % NB) * BQ, sdesc_add(d16, C::kOffV + ao), sdesc_add(sdesc_add(d16, do_off), bo), C::kIdescS,
+                       k > 0);
         }
-        umma_commit(&s_full[i & 1]);
+        umma_commit(&s_full[i % NB]);
       }
       __syncwarp();
     };
     mbar_wait(kv_full, 0);
-    issue_s(0);
-    if (nq > 1) issue_s(1);
+    for (int i = 0; i < NB && i < nq; ++i) issue_s(i);
     for (int i = 0; i < nq; ++i) {
       mbar_wait(&p_full[i & 1], (i >> 1) & 1);
       tc_fence_after();
       if (lane == 0) {  // dV += P^T dO_i ; dK += dS^T Q_i   (B read MN-major: N = dh, K = queries)
         const int st = i % NS;
-        const uint32_t pa = smem_u32(smem + C::kOffP + (i & 1) * C::kPBytes);
-        const uint32_t dsa = smem_u32(smem + C::kOffDS + (i & 1) * C::kPBytes);
-        const uint32_t q_addr = smem_u32(smem + C::kOffQ + st * C::kQBytes);
-        const uint32_t do_addr = smem_u32(smem + C::kOffDO + st * C::kQBytes);
+        const uint32_t p_off = C::kOffP + (i & 1) * C::kPBytes, ds_off = C::kOffDS + (i & 1) * C::kPBytes;
+        const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k) {
-          umma_bf16_ss(t_dV, make_sdesc_sw128(pa + k * 32, 16, 1024),
-                       make_sdesc_sw128(do_addr + k * 2048, BQ * 128, 1024), C::kIdescKV, (i > 0 || k > 0));
-          umma_bf16_ss(t_dK, make_sdesc_sw128(dsa + k * 32, 16, 1024),
-                       make_sdesc_sw128(q_addr + k * 2048, BQ * 128, 1024), C::kIdescKV, (i > 0 || k > 0));
+          umma_bf16_ss(t_dV, sdesc_add(sdesc_add(d16, p_off), k * 32), sdesc_add(sdesc_add(dmn, do_off), k * 2048), C::kIdescKV,
+                       (i > 0 || k > 0));
+          umma_bf16_ss(t_dK, sdesc_add(sdesc_add(d16, ds_off), k * 32), sdesc_add(sdesc_add(dmn, q_off), k * 2048), C::kIdescKV,
+                       (i > 0 || k > 0));
         }
         umma_commit(&q_empty[st]);
         umma_commit(&p_free[i & 1]);
         if (i == nq - 1) umma_commit(acc_done);
       }
       __syncwarp();
-      if (i + 2 < nq) issue_s(i + 2);
+      if (i + NB < nq) issue_s(i + NB);
     }
   } else {
     const int quad = warp & 3;
@@ -431,7 +441,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto fetch = [&](int i) {
       const int q = q_lo + i * BQ + tid;
       const bool ok = tid < BQ && i < nq && q < q_hi;
-      nl = ok ? p.lse[static_cast<long>(h) * p.n + q] * kLog2e : INFINITY;
+      // raw values only: the log2e scaling happens at the smem store one iteration later, so no
+      // instruction consumes the global load until its latency is hidden
+      nl = ok ? p.lse[static_cast<long>(h) * p.n + q] : INFINITY;
       nd = ok ? p.D[static_cast<long>(h) * p.n + q] : 0.f;
     };
     fetch(0);
@@ -440,19 +452,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* st_lse = stat + (i & 1) * 2 * BQ;
       float* st_D = st_lse + BQ;
       if (tid < BQ) {
-        st_lse[tid] = nl;
+        st_lse[tid] = nl * kLog2e;
         st_D[tid] = nd;
       }
       named_bar_sync(1, 32 * kSmxWarps);
       fetch(i + 1);
-      mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      mbar_wait(&s_full[i % NB], (i / NB) & 1);
       tc_fence_after();
       float s[HC], dp[HC];
 #pragma unroll
       for (int c = 0; c < HC; c += 16) {
         uint32_t r[16], r2[16];
-        tmem_ld16(t_S + (i & 1) * BQ + half * HC + c + lane_off, r);
-        tmem_ld16(t_dP + (i & 1) * BQ + half * HC + c + lane_off, r2);
+        tmem_ld16(t_S + (i % NB) * BQ + half * HC + c + lane_off, r);
+        tmem_ld16(t_dP + (i % NB) * BQ + half * HC + c + lane_off, r2);
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           s[c + e] = __uint_as_float(r[e]);
@@ -480,8 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 c22 = make_float2(c2, c2);
         const float2 xa = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, make_float2(-lz.x, -lz.y));
         const float2 xb = __ffma2_rn(make_float2(s[c + 2], s[c + 3]), c22, make_float2(-lz.z, -lz.w));
-        const float2 pa = make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
-        const float2 pb = make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
+        const float2 pa = ((c / 2) & 3) < POLY ? ex2_poly2(xa) : make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
+        const float2 pb = ((c / 2 + 1) & 3) < POLY ? ex2_poly2(xb) : make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
         const float2 da = __fmul2_rn(pa, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-dz.x, -dz.y)));
         const float2 db = __fmul2_rn(pb, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-dz.z, -dz.w)));
         wp[c / 2] = pack_bf16x2(pa.x, pa.y);
@@ -523,12 +535,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 
-template <int DH>
+template <int DH, int POLY>
 void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                 const int2* kv_items2, int n_kv, cudaStream_t stream) {
   // ring depths: loads must run >= 2 blocks ahead of the MMA that frees their stage
-  constexpr int NSQ = DH == 64 ? 4 : 3;  // dq kernel K/V stages
-  constexpr int NSK = DH == 64 ? 4 : 2;  // dkdv kernel Q/dO stages (smem-limited at dh 128)
+  // Ring depths: a stage is held until the LAST MMA reading it completes (dQ_j reads K_j; dV/dK_i
+  // read Q_i/dO_i), so the refill of the stage NS blocks ahead only starts then. The ring must cover
+  // that plus the L2/HBM TMA latency (~1-2 us under load), i.e. several block periods.
+  constexpr int NSQ = DH == 64 ? 8 : 4;  // dq kernel K/V stages (smem: 192 KB / 224 KB)
+  constexpr int NSK = DH == 64 ? 7 : 2;  // dkdv kernel Q/dO stages (smem-limited at dh 128)
   using CQ = DqCfg<DH, NSQ>;
   using CK = DkvCfg<DH, NSK>;
   const int d = a.H * DH;
@@ -540,11 +555,21 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, 128);
     make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, CQ::BKV);
     make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, CQ::BKV);
-    static bool once = (cudaFuncSetAttribute(fa_bwd_dq_kernel<DH, NSQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool once = (cudaFuncSetAttribute(fa_bwd_dq_kernel<DH, NSQ, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              CQ::kSmem),
                         true);
     (void)once;
-    fa_bwd_dq_kernel<DH, NSQ><<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    static const int dbg = [] {
+      const char* e = std::getenv("TT_ATTN_DBG");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (dbg == 1 || dbg == 2) {
+      auto kfn = dbg == 1 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 1> : fa_bwd_dq_kernel<DH, NSQ, POLY, 2>;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CQ::kSmem);
+      kfn<<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    } else {
+      fa_bwd_dq_kernel<DH, NSQ, POLY><<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    }
   }
   if (n_kv > 0) {
     CUtensorMap tq, tdo, tk, tv;
@@ -552,13 +577,13 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, CK::BQ);
     make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, 128);
     make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, 128);
-    static bool once = (cudaFuncSetAttribute(fa_bwd_dkdv_kernel<DH, NSK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool once = (cudaFuncSetAttribute(fa_bwd_dkdv_kernel<DH, NSK, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              CK::kSmem),
                         true);
     (void)once;
     p.blocks = kv_items;
     p.blocks2 = kv_items2;
-    fa_bwd_dkdv_kernel<DH, NSK><<<dim3(n_kv, a.H), kThreads, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreads, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
   }
 }
 
@@ -567,9 +592,16 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
 void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                     const int2* kv_items2, int n_kv, cudaStream_t stream) {
   attn_bwd_pre(a, stream);
-  if (a.dh == 64) launch_bwd<64>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
-  else if (a.dh == 128) launch_bwd<128>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
-  else throw std::invalid_argument("attention: head_dim must be 64 or 128");
+#define TT_BWD(P)                                                                                          \
+  if (a.dh == 64) return launch_bwd<64, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream); \
+  if (a.dh == 128) return launch_bwd<128, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
+  switch (attn_poly_pairs()) {
+    case 0: TT_BWD(0) break;
+    case 2: TT_BWD(2) break;
+    default: TT_BWD(1) break;
+  }
+#undef TT_BWD
+  throw std::invalid_argument("attention: head_dim must be 64 or 128");
 }
 
 }  // namespace ttb

@@ -16,6 +16,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include "attention.h"
@@ -39,16 +40,19 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("ba
 
 template <int DH, int BKV, int NS>
 struct FwdCfg {
+  static constexpr int NB = 3;  // S (TMEM) and P (smem) buffers: the MMA warp runs NB-1 blocks ahead
   static constexpr int kQBytes = kBQ * DH * 2;
   static constexpr int kKVBytes = BKV * DH * 2;           // one K (or V) tile
   static constexpr int kPBytes = kBQ * BKV * 2;           // one P tile
   static constexpr int kOffK = kQBytes;
   static constexpr int kOffV = kOffK + NS * kKVBytes;
   static constexpr int kOffP = kOffV + NS * kKVBytes;
-  static constexpr int kOffX = kOffP + 2 * kPBytes;   // [2 bufs][2 halves][128 rows] f32: row-max exchange
+  static constexpr int kOffX = kOffP + NB * kPBytes;   // [2 bufs][2 halves][128 rows] f32: row-max exchange
   static constexpr int kOffBar = kOffX + 2 * 2 * kBQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
-  static constexpr int kTmemCols = (2 * BKV + DH) <= 256 ? 256 : 512;
+  static constexpr int kOCol = (NB * BKV + DH - 1) / DH * DH;
+  static constexpr int kTmemCols = (kOCol + DH) <= 256 ? 256 : 512;
+  static_assert(kOCol + DH <= 512 && NS >= NB, "fwd kernel: TMEM / K-V ring too small");
   static constexpr uint32_t kIdescS = make_idesc_bf16(128, BKV, false, false);
   static constexpr uint32_t kIdescO = make_idesc_bf16(128, DH, false, true);
 };
@@ -62,21 +66,29 @@ struct FwdParams {
   float scale_log2;
 };
 
-template <int DH, int BKV, int NS>
+// POLY: of every 4 element pairs, how many take 2^x on the FMA pipe (ex2_poly2) instead of MUFU:
+// at dh=64 one exponential per 4*dh MMA FLOPs makes the MUFU (16/clk/SM) the bottleneck.
+template <int DH, int BKV, int NS, int POLY>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     fa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                   const __grid_constant__ CUtensorMap tm_v, FwdParams p) {
   using C = FwdCfg<DH, BKV, NS>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + NS;
-  uint64_t* s_full = kv_empty + NS;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* pv_done = p_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  // separate K and V rings: a K slot frees when S_j completes, a V slot when PV_j does, so the
+  // loads for S_{j+NB} never wait on the PV MMA just issued
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + NS;
+  uint64_t* v_full = k_empty + NS;
+  uint64_t* v_empty = v_full + NS;
+  uint64_t* s_full = v_empty + NS;  // [NB]
+  uint64_t* p_full = s_full + C::NB;  // [NB]
+  // PV_j completion -> pv_done[j % NB]: per-buffer barriers keep the parity waits unambiguous (the
+  // softmax may run up to NB-1 PV MMAs ahead of their completion)
+  uint64_t* pv_done = p_full + C::NB;  // [NB]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + C::NB);
 
   const int warp = warp_id_sync();
   const int lane = threadIdx.x & 31;
@@ -96,14 +108,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     tma_prefetch_desc(&tm_v);
     mbar_init(q_full, 1);
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::NB; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSmxWarps);
+      mbar_init(&pv_done[s], 1);
     }
-    mbar_init(pv_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
@@ -111,8 +125,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_S = tmem;             // 2 x BKV columns
-  const uint32_t tmem_O = tmem + 2 * BKV;   // DH columns
+  constexpr int NB = C::NB;
+  const uint32_t tmem_S = tmem;              // NB x BKV columns
+  // O (N = DH) at a DH-aligned column (dh 128: 256, not 192)
+  const uint32_t tmem_O = tmem + C::kOCol;
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -123,58 +139,62 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int j = 0; j < nblk; ++j) {
         const int st = j % NS;
         const uint32_t ph = (j / NS) & 1;
-        mbar_wait(&kv_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], 2 * C::kKVBytes);
         const int r0 = kv_row0(j);
         uint8_t* ks = smem + C::kOffK + st * C::kKVBytes;
         uint8_t* vs = smem + C::kOffV + st * C::kKVBytes;
+        mbar_wait(&k_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], C::kKVBytes);
 #pragma unroll
-        for (int pn = 0; pn < DH / 64; ++pn) {
-          tma_load_2d(&tm_k, &kv_full[st], ks + pn * (BKV * 128), h * DH + pn * 64, r0);
-          tma_load_2d(&tm_v, &kv_full[st], vs + pn * (BKV * 128), h * DH + pn * 64, r0);
-        }
+        for (int pn = 0; pn < DH / 64; ++pn) tma_load_2d(&tm_k, &k_full[st], ks + pn * (BKV * 128), h * DH + pn * 64, r0);
+        mbar_wait(&v_empty[st], ph ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], C::kKVBytes);
+#pragma unroll
+        for (int pn = 0; pn < DH / 64; ++pn) tma_load_2d(&tm_v, &v_full[st], vs + pn * (BKV * 128), h * DH + pn * 64, r0);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    const uint32_t q_addr = smem_u32(smem);
+    // descriptors = one base (smem start) + byte offsets: keeps the single-thread issue path short
+    const uint64_t dK16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);         // K-major tiles
+    const uint64_t dVmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // V read MN-major
     auto issue_s = [&](int j) {
       const int st = j % NS;
-      mbar_wait(&kv_full[st], (j / NS) & 1);
+      mbar_wait(&k_full[st], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t k_addr = smem_u32(smem + C::kOffK + st * C::kKVBytes);
+        const uint32_t k_off = C::kOffK + st * C::kKVBytes;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
-          const uint64_t da = make_sdesc_sw128(q_addr + (k / 4) * (kBQ * 128) + (k % 4) * 32, 16, 1024);
-          const uint64_t db = make_sdesc_sw128(k_addr + (k / 4) * (BKV * 128) + (k % 4) * 32, 16, 1024);
-          umma_bf16_ss(tmem_S + (j & 1) * BKV, da, db, C::kIdescS, k > 0 ? 1u : 0u);
+          const uint64_t da = sdesc_add(dK16, (k / 4) * (kBQ * 128) + (k % 4) * 32);
+          const uint64_t db = sdesc_add(sdesc_add(dK16, k_off), (k / 4) * (BKV * 128) + (k % 4) * 32);
+          umma_bf16_ss(tmem_S + (j % NB) * BKV, da, db, C::kIdescS, k > 0 ? 1u : 0u);
         }
-        umma_commit(&s_full[j & 1]);
+        umma_commit(&s_full[j % NB]);
+        umma_commit(&k_empty[st]);
       }
       __syncwarp();
     };
     mbar_wait(q_full, 0);
-    issue_s(0);
-    if (nblk > 1) issue_s(1);
+    for (int j = 0; j < NB && j < nblk; ++j) issue_s(j);
     for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&p_full[j % NB], (j / NB) & 1);
+      mbar_wait(&v_full[j % NS], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
         const int st = j % NS;
-        const uint32_t p_addr = smem_u32(smem + C::kOffP + (j & 1) * C::kPBytes);
-        const uint32_t v_addr = smem_u32(smem + C::kOffV + st * C::kKVBytes);
+        const uint32_t p_off = C::kOffP + (j % NB) * C::kPBytes;
+        const uint32_t v_off = C::kOffV + st * C::kKVBytes;
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k) {
-          const uint64_t da = make_sdesc_sw128(p_addr + (k / 4) * (kBQ * 128) + (k % 4) * 32, 16, 1024);
-          const uint64_t db = make_sdesc_sw128(v_addr + k * 2048, BKV * 128, 1024);
+          const uint64_t da = sdesc_add(sdesc_add(dK16, p_off), (k / 4) * (kBQ * 128) + (k % 4) * 32);
+          const uint64_t db = sdesc_add(sdesc_add(dVmn, v_off), k * 2048);
           umma_bf16_ss(tmem_O, da, db, C::kIdescO, (j > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(&kv_empty[st]);
-        umma_commit(pv_done);
+        umma_commit(&v_empty[st]);
+        umma_commit(&pv_done[j % NB]);
       }
       __syncwarp();
-      if (j + 2 < nblk) issue_s(j + 2);
+      if (j + NB < nblk) issue_s(j + NB);
     }
   } else {
     // ------------------------------------------------------------------ softmax
@@ -195,13 +215,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float m_used = -INFINITY, l = 0.f;
     const float c2 = p.scale_log2;
     for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&s_full[j % NB], (j / NB) & 1);
       tc_fence_after();
       float s[HC];
 #pragma unroll
       for (int c = 0; c < HC; c += 16) {
         uint32_t r[16];
-        tmem_ld16(tmem_S + (j & 1) * BKV + half * HC + c + lane_off, r);
+        tmem_ld16(tmem_S + (j % NB) * BKV + half * HC + c + lane_off, r);
 #pragma unroll
         for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(r[i]);
       }
@@ -214,9 +234,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int i = 0; i < HC; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
-      float mx = s[0];
+      float mx = fmax3f(s[0], s[1], s[2]);
 #pragma unroll
-      for (int i = 1; i < HC; ++i) mx = fmaxf(mx, s[i]);
+      for (int i = 3; i + 1 < HC; i += 2) mx = fmax3f(mx, s[i], s[i + 1]);
+      if ((HC - 3) % 2) mx = fmaxf(mx, s[HC - 1]);
       float* xb = xch + (j & 1) * (2 * kBQ);
       xb[half * kBQ + rloc] = mx;
       named_bar_sync(bar_id, 64);
@@ -233,8 +254,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       float2 rs2 = make_float2(0.f, 0.f);
       const float2 c22 = make_float2(c2, c2), nmb2 = make_float2(-mb, -mb);
       // this half's columns start at key half*HC: panel (half*HC)/64, 16B chunk ((half*HC)%64)/8 of
-      // buffer j%2; the buffer is free since S_j's commit covers PV_{j-2}
-      uint8_t* pbuf = smem + C::kOffP + (j & 1) * C::kPBytes + ((half * HC) / 64) * (kBQ * 128);
+      // buffer j%NB; the buffer is free since S_j (issued after PV_{j-NB}) has completed
+      uint8_t* pbuf = smem + C::kOffP + (j % NB) * C::kPBytes + ((half * HC) / 64) * (kBQ * 128);
       const int chunk0 = ((half * HC) % 64) / 8;
 #pragma unroll
       for (int cch = 0; cch < HC / 8; ++cch) {
@@ -243,7 +264,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int e = 0; e < 4; ++e) {
           // paired FP32 (FFMA2 / FADD2): x = s*c - m ; p = 2^x ; row sum += p
           const float2 x = __ffma2_rn(make_float2(s[cch * 8 + 2 * e], s[cch * 8 + 2 * e + 1]), c22, nmb2);
-          const float2 pe = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          const float2 pe = e < POLY ? ex2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
           rs2 = __fadd2_rn(rs2, pe);
           w[e] = pack_bf16x2(pe.x, pe.y);
         }
@@ -255,7 +276,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       l += rs;
       if (j > 0 && __any_sync(0xffffffff, resc)) {
         // O (from PV_{j-1}) must be final before it is rescaled; each warp rescales its half of dh
-        mbar_wait(pv_done, (j - 1) & 1);
+        mbar_wait(&pv_done[(j - 1) % NB], ((j - 1) / NB) & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
@@ -271,7 +292,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       fence_proxy_async_smem();  // P stores (generic proxy) -> visible to tcgen05.mma (async proxy)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[j & 1]);
+      if (lane == 0) mbar_arrive(&p_full[j % NB]);
     }
     // combine the two partial row sums
     float* lb = xch + (nblk & 1) * (2 * kBQ);
@@ -279,7 +300,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     named_bar_sync(bar_id, 64);
     l += lb[(1 - half) * kBQ + rloc];
     const float m = m_used;
-    mbar_wait(pv_done, (nblk - 1) & 1);
+    mbar_wait(&pv_done[(nblk - 1) % NB], ((nblk - 1) / NB) & 1);
     tc_fence_after();
     const float inv_l = 1.f / l;
     // tcgen05.ld is .sync.aligned: every lane executes it (convergently); only valid rows store.
@@ -312,7 +333,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 
-template <int DH, int BKV, int NS>
+template <int DH, int BKV, int NS, int POLY>
 void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
   using C = FwdCfg<DH, BKV, NS>;
   CUtensorMap tq, tk, tv;
@@ -320,23 +341,44 @@ void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
   make_tmap_bf16(&tq, a.q, d, a.n, a.ldq, 64, kBQ);
   make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, BKV);
   make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, BKV);
-  static bool once = (cudaFuncSetAttribute(fa_fwd_kernel<DH, BKV, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static bool once = (cudaFuncSetAttribute(fa_fwd_kernel<DH, BKV, NS, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            C::kSmem),
                       true);
   (void)once;
   FwdParams p{a.o, a.ldo, a.lse, a.n, a.S, a.H, a.qblocks, a.scale * kLog2e};
   dim3 grid(a.nqb, a.H);
-  fa_fwd_kernel<DH, BKV, NS><<<grid, kFwdThreads, C::kSmem, stream>>>(tq, tk, tv, p);
+  fa_fwd_kernel<DH, BKV, NS, POLY><<<grid, kFwdThreads, C::kSmem, stream>>>(tq, tk, tv, p);
 }
 
 }  // namespace
 
+int attn_poly_pairs() {
+  static const int v = [] {
+    const char* e = std::getenv("TT_ATTN_POLY");
+    const int x = e ? std::atoi(e) : 1;
+    return x < 0 ? 0 : (x > 2 ? 2 : x);
+  }();
+  return v;
+}
+
 // Forward with 128-query blocks (qblocks built with kFwdBlockQ rows). rows_cap = stack rows.
 void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
   if (a.nqb == 0) return;
-  if (a.dh == 64) launch_fwd<64, 128, 3>(a, rows_cap, stream);
-  else if (a.dh == 128) launch_fwd<128, 64, 3>(a, rows_cap, stream);
-  else throw std::invalid_argument("attention: head_dim must be 64 or 128");
+  switch (attn_poly_pairs()) {
+    case 0:
+      if (a.dh == 64) return launch_fwd<64, 128, 3, 0>(a, rows_cap, stream);
+      if (a.dh == 128) return launch_fwd<128, 64, 3, 0>(a, rows_cap, stream);
+      break;
+    case 2:
+      if (a.dh == 64) return launch_fwd<64, 128, 3, 2>(a, rows_cap, stream);
+      if (a.dh == 128) return launch_fwd<128, 64, 3, 2>(a, rows_cap, stream);
+      break;
+    default:
+      if (a.dh == 64) return launch_fwd<64, 128, 3, 1>(a, rows_cap, stream);
+      if (a.dh == 128) return launch_fwd<128, 64, 3, 1>(a, rows_cap, stream);
+      break;
+  }
+  throw std::invalid_argument("attention: head_dim must be 64 or 128");
 }
 
 }  // namespace ttb

@@ -315,8 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;  // cluster id / count
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;  // [2]

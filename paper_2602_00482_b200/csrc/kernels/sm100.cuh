@@ -14,6 +14,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 1024-byte aligned base of the dynamic shared memory (the SWIZZLE_128B atom alignment). Pointer
+// arithmetic on the __shared__ array (not a uintptr_t round trip) keeps the shared address space
+// visible to the compiler, so accesses through it compile to LDS/STS rather than generic LD/ST.
+__device__ __forceinline__ uint8_t* align_smem_1024(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -149,6 +156,11 @@ __device__ __forceinline__ uint64_t make_sdesc_sw128(uint32_t smem_addr, uint32_
   return d;
 }
 
+// Descriptor of (the address of desc) + off bytes: the start-address field holds addr >> 4 in its low
+// 14 bits and shared-memory addresses stay below 2^18, so a plain add never carries out of it. Lets
+// an MMA issuer build every descriptor from one precomputed base with a single integer add.
+__device__ __forceinline__ uint64_t sdesc_add(uint64_t desc, uint32_t off_bytes) { return desc + (off_bytes >> 4); }
+
 // Instruction descriptor, kind::f16: A,B bf16, D fp32.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4)                                   // c_format = F32
@@ -179,6 +191,28 @@ __device__ __forceinline__ float ex2_poly(float x) {
   const int ji = __float_as_int(t) - 0x4B400000;
   const float r = __int_as_float(__float_as_int(pz) + (ji << 23));
   return x < -126.0f ? 0.0f : r;
+}
+
+// Paired variant on FFMA2/FADD2 (two exponentials per issue of each step). x is clamped to
+// [-126, +inf) so masked (-inf) inputs give ~2^-126 instead of 0 — below every bf16/fp32 sum they
+// enter. The exponent add uses (t_bits << 23): the 1.5*2^23 bias bits vanish mod 2^32.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.0f, -1.0f), x);
+  float2 pz = __ffma2_rn(make_float2(0.05517084f, 0.05517084f), f, make_float2(0.24260935f, 0.24260935f));
+  pz = __ffma2_rn(pz, f, make_float2(0.69326096f, 0.69326096f));
+  pz = __ffma2_rn(pz, f, make_float2(0.99992818f, 0.99992818f));
+  return make_float2(__int_as_float(__float_as_int(pz.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(pz.y) + (__float_as_int(t.y) << 23)));
+}
+// 3-input max (FMNMX3, sm_100+).
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
 }
 
 // ---------------------------------------------------------------- misc

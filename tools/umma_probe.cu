@@ -1,0 +1,85 @@
+// Microbenchmark: issue rate of tcgen05.mma kind::f16 (cta_group::1, M = 128) for several N, with
+// both operands in shared memory (SS) or A in TMEM (TS), and the cost of a commit -> mbarrier ->
+// wake-up round trip. One CTA per SM on all SMs; clock64 deltas measured by the issuing thread.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2602_00482_b200/csrc/kernels \
+//        tools/umma_probe.cu -o tools/umma_probe && tools/umma_probe
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "sm100.cuh"
+
+using namespace ttb;
+
+template <int N, bool TS>
+__global__ void __launch_bounds__(128, 1) probe(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&slot, 512);
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = make_idesc_bf16(128, N, false, false);
+    const uint32_t a = smem_u32(smem), b = smem_u32(smem + 32768);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (TS) umma_bf16_ts(tmem + 256, tmem + 384 + k * 8, make_sdesc_sw128(b + k * 32, 16, 1024), idesc, 1);
+        else umma_bf16_ss(tmem, make_sdesc_sw128(a + k * 32, 16, 1024), make_sdesc_sw128(b + k * 32, 16, 1024), idesc, 1);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    // round trip: one tiny MMA, commit, wait
+    long long t2 = clock64();
+    for (int it = 0; it < 16; ++it) {
+      umma_bf16_ss(tmem, make_sdesc_sw128(a, 16, 1024), make_sdesc_sw128(b, 16, 1024), idesc, 1);
+      umma_commit(&bar);
+      mbar_wait(&bar, (it + 1) & 1);
+    }
+    long long t3 = clock64();
+    if (blockIdx.x == 0) {
+      out[0] = t1 - t0;
+      out[1] = (t3 - t2) / 16;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int N, bool TS>
+void run(long long* d, int iters) {
+  cudaFuncSetAttribute(probe<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
+  probe<N, TS><<<148, 128, 70000>>>(d, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[2];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  const double per = double(h[0]) / (iters * 4.0);
+  const double flop = 2.0 * 128 * N * 16;
+  printf("M=128 N=%3d K=16 %s: %7.1f clk/MMA -> %6.0f FLOP/clk/SM ; commit->wait round trip %lld clk  %s\n", N,
+         TS ? "TS" : "SS", per, flop / per, h[1], cudaGetErrorString(e));
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 64);
+  run<64, false>(d, 2000);
+  run<128, false>(d, 2000);
+  run<256, false>(d, 2000);
+  run<64, true>(d, 2000);
+  run<128, true>(d, 2000);
+  return 0;
+}

@@ -67,6 +67,9 @@ int tt_debug_rmsnorm_bwd(const float* gy, const float* x, const float* inv, cons
 }
 void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
 
+// clock64 trace of the TT_ATTN_DBG=3 attention dq kernel (timing experiments only)
+int tt_debug_attn_trace(long long* out, int n) { return ttb::attn_debug_trace(out, n); }
+
 // Segment attention on one segment of n queries over stack rows [0, S) + own rows [S, S+n)
 // (k/v: [rows_cap x H*dh] bf16). dir 0: forward (impl 0 = mma.sync, 1 = tcgen05) -> o, lse.
 // dir 1: backward (impl 0 = mma.sync) from o, lse, dO -> dq (overwritten), dk/dv (added).

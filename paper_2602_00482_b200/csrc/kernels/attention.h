@@ -58,6 +58,10 @@ void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream);
 // env TT_ATTN_POLY, read once.
 int attn_poly_pairs();
 
+// Copies the clock64 trace of the TT_ATTN_DBG=3 dq kernel (4 x 256: MMA ds_full wake, MMA issue
+// done, softmax s_full wake, softmax arrive). Returns the count copied or -1.
+int attn_debug_trace(long long* host, int n);
+
 // D = rowsum(dO * O) per (head, row) (the softmax-backward correction term).
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream);
 // tcgen05 backward (attention_bwd_sm100.cu): dq_blocks are 128-row query blocks (like the forward);

@@ -85,7 +85,9 @@ struct BwdParams {
 };
 
 // DBG (timing experiments only, TT_ATTN_DBG): 1 = softmax warps skip TMEM loads + math (MMA/TMA
-// pipeline alone), 2 = softmax warps do not wait for S (softmax alone).
+// pipeline alone), 2 = softmax warps do not wait for S (softmax alone), 3 = normal + clock64 trace of
+// one mid-grid CTA into g_attn_trace (tt_debug_attn_trace).
+__device__ long long g_attn_trace[6][256];
 template <int DH, int NS, int POLY, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
@@ -101,8 +103,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_empty = kv_full + NS;
   uint64_t* s_full = kv_empty + NS;  // [NB] S_j and dP_j in TMEM
   uint64_t* ds_full = s_full + C::NB;  // [2]  dS_j in smem
-  uint64_t* ds_free = ds_full + 2;   // [2]  dQ MMA consumed dS_j
-  uint64_t* dq_done = ds_free + 2;
+  // kv_empty[j % NS] completes when dQ_j (the last reader of K_j and of dS_j) is done: it frees the
+  // K/V stage for the producer AND the dS buffer for the softmax warps (one commit, two waiters)
+  uint64_t* dq_done = ds_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = warp_id_sync();
@@ -129,7 +132,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::NB; ++s) mbar_init(&s_full[s], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&ds_full[s], kSmxWarps);
-      mbar_init(&ds_free[s], 1);
     }
     mbar_init(dq_done, 1);
     fence_barrier_init();
@@ -166,9 +168,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);         // K-major tiles
     const uint64_t dKmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // K_j read MN-major
+    const bool trace = DBG == 3 && lane == 0 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     auto issue_s = [&](int j) {  // S_j = Q K_j^T ; dP_j = dO V_j^T
       const int st = j % NS;
+      if (trace && j >= NB && j - NB < 256) g_attn_trace[4][j - NB] = clock64();
       mbar_wait(&kv_full[st], (j / NS) & 1);
+      if (trace && j >= NB && j - NB < 256) g_attn_trace[5][j - NB] = clock64();
       tc_fence_after();
       if (lane == 0) {
         const uint32_t k_off = C::kOffK + st * C::kKVBytes, v_off = C::kOffV + st * C::kKVBytes;
@@ -187,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < NB && j < nblk; ++j) issue_s(j);
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&ds_full[j & 1], (j >> 1) & 1);
+      if (trace && j < 256) g_attn_trace[0][j] = clock64();
       tc_fence_after();
       if (lane == 0) {  // dQ += dS_j K_j   (B = K_j read MN-major: N = dh, K = keys)
         const int st = j % NS;
@@ -196,11 +202,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_bf16_ss(t_dQ, sdesc_add(sdesc_add(d16, ds_off), k * 32), sdesc_add(sdesc_add(dKmn, k_off), k * 2048), C::kIdescQ,
                        (j > 0 || k > 0));
         umma_commit(&kv_empty[st]);
-        umma_commit(&ds_free[j & 1]);
         if (j == nblk - 1) umma_commit(dq_done);
       }
       __syncwarp();
       if (j + NB < nblk) issue_s(j + NB);
+      if (trace && j < 256) g_attn_trace[1][j] = clock64();
     }
   } else {
     const int quad = warp & 3;
@@ -215,11 +221,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float Dr = row_ok ? p.D[static_cast<long>(h) * p.n + row] : 0.f;
     const float c2 = p.scale_log2;
     constexpr int HC = BKV / 2;
+    const bool trace = DBG == 3 && threadIdx.x == 64 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     for (int j = 0; j < nblk; ++j) {
       if (DBG != 2) mbar_wait(&s_full[j % NB], (j / NB) & 1);
+      if (trace && j < 256) g_attn_trace[2][j] = clock64();
       tc_fence_after();
       if (DBG == 1) {
-        if (j >= 2) mbar_wait(&ds_free[j & 1], ((j >> 1) + 1) & 1);
+        if (j >= 2) mbar_wait(&kv_empty[(j - 2) % NS], ((j - 2) / NS) & 1);
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
@@ -255,12 +263,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 ds = __fmul2_rn(pe, __fadd2_rn(make_float2(dp[i], dp[i + 1]), nD2));
         w[i / 2] = pack_bf16x2(ds.x, ds.y);
       }
-      if (j >= 2) mbar_wait(&ds_free[j & 1], ((j >> 1) + 1) & 1);
+      if (j >= 2) mbar_wait(&kv_empty[(j - 2) % NS], ((j - 2) / NS) & 1);  // dQ_{j-2} done: dS buffer free
       st_halfrow_sw128(smem + C::kOffDS + (j & 1) * C::kDSBytes, rloc, half, w);
       fence_proxy_async_smem();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ds_full[j & 1]);
+      if (trace && j < 256) g_attn_trace[3][j] = clock64();
     }
     mbar_wait(dq_done, 0);
     tc_fence_after();
@@ -320,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_empty = q_full + NS;
   uint64_t* s_full = q_empty + NS;    // [NB]
   uint64_t* p_full = s_full + C::NB;  // [2]
-  uint64_t* p_free = p_full + 2;    // [2]
-  uint64_t* acc_done = p_free + 2;
+  // q_empty[i % NS] completes when dV/dK_i are done: frees the Q/dO stage AND the P/dS buffers
+  uint64_t* acc_done = p_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
   float* stat = reinterpret_cast<float*>(smem + C::kOffStat);
 
@@ -349,7 +358,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < C::NB; ++s) mbar_init(&s_full[s], 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&p_full[s], kSmxWarps);
-      mbar_init(&p_free[s], 1);
     }
     mbar_init(acc_done, 1);
     fence_barrier_init();
@@ -420,7 +428,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                        (i > 0 || k > 0));
         }
         umma_commit(&q_empty[st]);
-        umma_commit(&p_free[i & 1]);
         if (i == nq - 1) umma_commit(acc_done);
       }
       __syncwarp();
@@ -501,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         wd[c / 2] = pack_bf16x2(da.x, da.y);
         wd[c / 2 + 1] = pack_bf16x2(db.x, db.y);
       }
-      if (i >= 2) mbar_wait(&p_free[i & 1], ((i >> 1) + 1) & 1);
+      if (i >= 2) mbar_wait(&q_empty[(i - 2) % NS], ((i - 2) / NS) & 1);  // dV/dK_{i-2} done: P/dS free
       st_halfrow_sw128(smem + C::kOffP + (i & 1) * C::kPBytes, krow, half, wp);
       st_halfrow_sw128(smem + C::kOffDS + (i & 1) * C::kPBytes, krow, half, wd);
       fence_proxy_async_smem();
@@ -563,8 +570,9 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
       const char* e = std::getenv("TT_ATTN_DBG");
       return e ? std::atoi(e) : 0;
     }();
-    if (dbg == 1 || dbg == 2) {
-      auto kfn = dbg == 1 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 1> : fa_bwd_dq_kernel<DH, NSQ, POLY, 2>;
+    if (dbg == 1 || dbg == 2 || dbg == 3) {
+      auto kfn = dbg == 1 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 1>
+                          : (dbg == 2 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 2> : fa_bwd_dq_kernel<DH, NSQ, POLY, 3>);
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CQ::kSmem);
       kfn<<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
     } else {
@@ -588,6 +596,11 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
 }
 
 }  // namespace
+
+int attn_debug_trace(long long* host, int n) {
+  const int m = n < 6 * 256 ? n : 6 * 256;
+  return cudaMemcpyFromSymbol(host, g_attn_trace, m * sizeof(long long)) == cudaSuccess ? m : -1;
+}
 
 void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                     const int2* kv_items2, int n_kv, cudaStream_t stream) {

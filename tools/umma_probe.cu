@@ -60,6 +60,90 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int iters) {
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// The dq-kernel issue pattern: per block, S (Q x K_st) and dP (dO x V_st) interleaved into two TMEM
+// accumulators, then dQ (dS x K_st, B MN-major); stages cycle over NS K/V tiles of 8 KB.
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) probe_dq(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  __shared__ uint64_t bar, cbar[8];
+  __shared__ uint32_t slot;
+  __shared__ int stop;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&cbar[i], 1);
+    stop = 0;
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&slot, 512);
+  for (int i = threadIdx.x; i < 196608 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idS = make_idesc_bf16(128, 64, false, false), idQ = make_idesc_bf16(128, 64, false, true);
+    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024), dmn = make_sdesc_sw128(smem_u32(smem), 8192, 1024);
+    long long t0 = clock64();
+    for (int j = 0; j < iters; ++j) {
+      const uint32_t st = j % 8, k_off = 32768 + st * 8192, v_off = 98304 + st * 8192, ds_off = 163840 + (j & 1) * 16384;
+      if (MODE != 1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          umma_bf16_ss(tmem + (j % 3) * 64, sdesc_add(d16, k * 32), sdesc_add(sdesc_add(d16, k_off), k * 32), idS, k > 0);
+          umma_bf16_ss(tmem + 192 + (j % 3) * 64, sdesc_add(d16, 16384 + k * 32), sdesc_add(sdesc_add(d16, v_off), k * 32), idS, k > 0);
+        }
+      }
+      if (MODE >= 3) umma_commit(&cbar[j % 3]);
+      if (MODE != 2) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16_ss(tmem + 384, sdesc_add(sdesc_add(d16, ds_off), k * 32), sdesc_add(sdesc_add(dmn, k_off), k * 2048), idQ, 1);
+      }
+      if (MODE >= 3) {
+        umma_commit(&cbar[3 + (j & 1)]);
+        umma_commit(&cbar[5 + (j & 1)]);
+      }
+    }
+    umma_commit(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (blockIdx.x == 0) out[0] = t1 - t0;
+    *reinterpret_cast<volatile int*>(&stop) = 1;
+  } else if (MODE == 4 && threadIdx.x >= 32) {
+    // other warps: stream tcgen05.ld of their TMEM lane quadrant (like the softmax warps reading S/dP)
+    const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
+    float acc = 0;
+    while (!*reinterpret_cast<volatile int*>(&stop)) {
+      uint32_t r[16], r2[16];
+      tmem_ld16(tmem + lane_off, r);
+      tmem_ld16(tmem + 192 + lane_off, r2);
+      tmem_ld_wait();
+      for (int i = 0; i < 16; ++i) acc += __uint_as_float(r[i]) + __uint_as_float(r2[i]);
+    }
+    if (acc == 12345.f) out[1] = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int MODE>
+void run_dq(long long* d, int iters) {
+  cudaFuncSetAttribute(probe_dq<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200000);
+  probe_dq<MODE><<<148, 128, 200000>>>(d, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[1];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  const int per = (MODE == 0 || MODE >= 3) ? 12 : (MODE == 1 ? 4 : 8);
+  const char* names[] = {"S+dP+dQ", "dQ only (B MN-major)", "S+dP only", "S+dP+dQ + 3 commits/block",
+                         "S+dP+dQ + commits + 3 warps streaming tcgen05.ld"};
+  printf("dq pattern mode %d (%s): %7.1f clk/block, %6.1f clk/MMA  %s\n", MODE, names[MODE], double(h[0]) / iters,
+         double(h[0]) / (iters * per), cudaGetErrorString(e));
+}
+
 template <int N, bool TS>
 void run(long long* d, int iters) {
   cudaFuncSetAttribute(probe<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
@@ -81,5 +165,10 @@ int main() {
   run<256, false>(d, 2000);
   run<64, true>(d, 2000);
   run<128, true>(d, 2000);
+  run_dq<0>(d, 1000);
+  run_dq<1>(d, 1000);
+  run_dq<2>(d, 1000);
+  run_dq<3>(d, 1000);
+  run_dq<4>(d, 1000);
   return 0;
 }

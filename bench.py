@@ -50,9 +50,51 @@ CONFIGS = {
                desc="tiny 2-layer d=256 transformer, one prefix tree (512-tok prompt, 8 branches x 256 tok)"),
     "c2": dict(model="qwen2-0.5b-shape", prompts=64, group=16, prompt_len=1024, resp_len=2048,
                desc="Qwen2-0.5B-shape random-init, 64 prompts x 16 rollouts, 1K shared prefix / 2K branches, bf16"),
+    "c3": dict(model="qwen2.5-1.5b-shape", prompts=2, deep=(4, 4, 2048), prompt_len=2048, resp_len=6144,
+               desc="deep multi-turn agent trees (4 levels, fan-out 4, 2048-token turns: 85 nodes, 64 leaves, "
+                    "8K paths), Qwen2.5-1.5B-shape random-init, 2 trees per GPU, DFS stack-memory stress"),
     "c4": dict(model="qwen2.5-7b-shape", prompts=32, group=16, prompt_len=1024, resp_len=2048,
                desc="Qwen2.5-7B-shape random-init, 32 trees per GPU (256 on 8 GPUs), load-balanced, NCCL allreduce"),
+    # c5: prefix-share sweep point (--share r): 16 rollouts of 4096 tokens sharing a prefix of r*4096
+    "c5": dict(model="qwen2-0.5b-shape", prompts=64, group=16, seq_len=4096,
+               desc="prefix-share sweep point: Qwen2-0.5B-shape, 64 prompts x 16 rollouts of 4096 tokens sharing "
+                    "a prefix of r*4096 tokens"),
 }
+
+
+def make_deep_corpus(trees, levels, fanout, node_len, vocab, seed):
+    """Multi-turn agent trees: a root turn (weights 0) then `levels`-1 levels of `fanout` branches of
+    node_len-token turns (weights 1); every root-to-leaf path is one rollout (levels * node_len tokens)."""
+    import paper_2602_00482_b200 as tt
+
+    rng = np.random.default_rng(seed)
+    seqs = []
+
+    def rec(prefix, w, depth):
+        if depth == levels:
+            seqs.append(tt.TokenSequence(len(seqs), np.asarray(prefix, dtype=np.int32), np.asarray(w)))
+            return
+        n = fanout if depth else 1
+        firsts = rng.choice(vocab, size=n, replace=False)
+        for f0 in firsts:
+            turn = rng.integers(0, vocab, node_len).tolist()
+            turn[0] = int(f0)
+            rec(prefix + turn, w + [0.0 if depth == 0 else 1.0] * node_len, depth + 1)
+
+    for _ in range(trees):
+        rec([], [], 0)
+    return seqs
+
+
+def config_corpus(c, n_prompts, vocab, share=0.0):
+    """The config's synthetic rollouts for n_prompts prompts (trees)."""
+    if "deep" in c:
+        lv, fo, nl = c["deep"]
+        return make_deep_corpus(n_prompts, lv, fo, nl, vocab, 3)
+    if "seq_len" in c:  # c5: shared prefix of share * seq_len tokens
+        p = int(round(share * c["seq_len"]))
+        return make_corpus(n_prompts, c["group"], p, c["seq_len"] - p, vocab, 3)
+    return make_corpus(n_prompts, c["group"], c["prompt_len"], c["resp_len"], vocab, 3)
 
 
 def make_corpus(prompts, group, prompt_len, resp_len, vocab, seed, shared=0):
@@ -183,7 +225,9 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.prompts:
+        c["prompts"] = args.prompts
     model = MODELS[c["model"]]
     from oracle import refimpl as R
 
@@ -191,12 +235,12 @@ def run_reference(args):
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libttref.so not built (needs /root/reference at build time)"}))
         return 0
-    seqs = make_corpus(c["prompts"], c["group"], c["prompt_len"], c["resp_len"], model[0], 3)
+    seqs = config_corpus(c, c["prompts"], model[0], args.share)
     nodes = tree_nodes_of(seqs)
     fl_step = step_flops(model, nodes)
     roll = sum(len(s.tokens) for s in seqs)
     n_tok = 1 if model[3] > 2 else 64
-    S = c["prompt_len"]
+    S = c["prompt_len"] if "prompt_len" in c else int(round(args.share * c["seq_len"]))
     secs, fl = cpu_reference_sample(c["model"], S, n_tok, threads, repeats=args.warmup + args.steps)
     timed = secs[args.warmup:]
     t = float(np.mean(timed))
@@ -207,7 +251,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {c['desc']}", "model": c["model"], "global_batch": len(seqs),
-                   "seq_len": c["prompt_len"] + c["resp_len"], "parallelism": "host threads"},
+                   "seq_len": c.get("seq_len") or c["prompt_len"] + c["resp_len"], "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": "rollout tokens/s", "cores": threads, "kind": "reference",
                          "sample": f"reference forward_segment+weighted_nll+backward_segment of {n_tok} token(s) at "
                                    f"prefix S={S} per thread x {threads} threads (T=float), extrapolated to the "
@@ -233,12 +277,15 @@ def run_b200(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.prompts:
+        c["prompts"] = args.prompts
     V, d, H, L, F = MODELS[c["model"]]
-    max_pos = c["prompt_len"] + c["resp_len"] + 16
+    seq_len = c.get("seq_len") or c["prompt_len"] + c["resp_len"]
+    max_pos = seq_len + 16
     cfg = tt.ModelConfig(V, d, H, L, F, max_pos)
     # whole job: world x per-GPU prompts, sharded by the min-max contiguous partitioner
-    all_seqs = make_corpus(c["prompts"] * world, c["group"], c["prompt_len"], c["resp_len"], V, 3)
+    all_seqs = config_corpus(c, c["prompts"] * world, V, args.share)
     if world > 1:
         plan = tt.partition_contiguous(all_seqs, world)
         mine = set(plan["groups"][rank])
@@ -247,7 +294,8 @@ def run_b200(args):
         seqs = all_seqs
     eng = tt.Engine(cfg, device=local)
     eng.init_params_random(7)
-    sched = tt.SchedulerConfig(sibling_batch=not args.no_sibling_batch, batch_token_budget=args.batch_budget)
+    sched = tt.SchedulerConfig(sibling_batch=not args.no_sibling_batch, batch_token_budget=args.batch_budget,
+                               chunk_len=args.chunk_len)
     t0 = time.time()
     tree = tt.build_prefix_tree(seqs)
     build_s = time.time() - t0
@@ -332,7 +380,7 @@ def run_b200(args):
         "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic: uniform random tokens (seed 3), prompt weights 0 / response weights 1; random-init N(0,0.02) weights",
         "config": {"workload": f"{args.config}: {c['desc']}", "model": c["model"], "global_batch": len(all_seqs),
-                   "seq_len": c["prompt_len"] + c["resp_len"], "parallelism": f"dp{world}",
+                   "seq_len": seq_len, "parallelism": f"dp{world}",
                    "trees_per_gpu": c["prompts"], "sibling_batch": not args.no_sibling_batch,
                    "l2": "step working set (weights + activations) >> 126 MB L2; no flush needed"},
         "e2e": {"value": roll_total / (e2e_ms / 1e3) if e2e_ms else None, "unit": "rollout tokens/s",
@@ -381,13 +429,14 @@ def run_b200(args):
             if R.available():
                 threads = os.cpu_count() or 1
                 n_tok = 1 if L > 2 else 64
-                secs, fl = cpu_reference_sample(c["model"], c["prompt_len"], n_tok, threads)
+                S0 = c["prompt_len"] if "prompt_len" in c else int(round(args.share * c["seq_len"]))
+                secs, fl = cpu_reference_sample(c["model"], S0, n_tok, threads)
                 rate = fl / secs[0]
                 cpu_val = rate / (fl_step / roll_local)
                 line["cpu_baseline"] = {
                     "value": cpu_val, "unit": "rollout tokens/s", "cores": threads, "kind": "reference",
                     "sample": f"reference forward_segment+weighted_nll+backward_segment (T=float) of {n_tok} token(s) at "
-                              f"prefix S={c['prompt_len']} on each of {threads} threads: {secs[0]:.1f} s, "
+                              f"prefix S={S0} on each of {threads} threads: {secs[0]:.1f} s, "
                               f"{rate / 1e9:.2f} GFLOP/s; extrapolated to the step via the FLOP model"}
             else:
                 line["cpu_baseline"] = {"value": None, "unit": "rollout tokens/s", "cores": 0, "kind": "reference",
@@ -415,6 +464,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-sibling-batch", action="store_true")
     ap.add_argument("--batch-budget", type=int, default=0)
+    ap.add_argument("--prompts", type=int, default=0, help="override the config's prompts per GPU (quick profiling only)")
+    ap.add_argument("--share", type=float, default=0.5, help="c5: shared-prefix fraction r of the 4096-token rollouts")
+    ap.add_argument("--chunk-len", type=int, default=0, help="chunked backward (SPEC.md:234-251); 0 = off")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -84,9 +84,11 @@ EXPORTS = {
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise RuntimeError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
-        L = ctypes.CDLL(LIB_PATH)
+        # TT_LIB_PATH: an alternative build of the same library (A/B kernel timing in tools/ only)
+        path = os.environ.get("TT_LIB_PATH", LIB_PATH)
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(path)
         for name, args in EXPORTS.items():
             fn = getattr(L, name)
             fn.argtypes = args

@@ -181,7 +181,10 @@ __device__ __forceinline__ float4 ld_evict_last_f4(const float* p, uint64_t pol)
 // policy (the ~148 rows in flight fit in the 126 MB L2), pass 2 re-reads it from L2 (evict_first)
 // and writes dlogits, so HBM sees each logit once. With `stats` (per-32-column (max, sum) from the
 // LM-head GEMM epilogue) pass 1 reads only the statistics.
-__global__ void __launch_bounds__(1024) ce_kernel(const float* __restrict__ logits, int m, long V,
+// 512 threads, 4 CTAs (rows) per SM; the write pass keeps 4 float4 loads per thread in flight
+// (64 KB per SM) — one float4 per thread is far too little memory-level parallelism for HBM.
+constexpr int kCeThreads = 512;
+__global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restrict__ logits, int m, long V,
                                                   const int32_t* __restrict__ pair_off,
                                                   const int32_t* __restrict__ tgt, const double* __restrict__ w,
                                                   __nv_bfloat16* __restrict__ dl, double* __restrict__ loss,
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(1024) ce_kernel(const float* __restrict__ logi
     float mx = -INFINITY, s = 0.f;
     if (stats) {
       const float2* sr = stats + static_cast<long>(r) * n_groups;
-      for (int g = threadIdx.x; g < n_groups; g += 1024) {
+      for (int g = threadIdx.x; g < n_groups; g += kCeThreads) {
         const float2 ms = sr[g];
         if (ms.x > mx) {
           s = s * __expf(mx - ms.x) + ms.y;
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(1024) ce_kernel(const float* __restrict__ logi
         }
       }
     } else {
-      for (long c = threadIdx.x * 4; c < V; c += 4096) {
+      for (long c = threadIdx.x * 4; c < V; c += 4 * kCeThreads) {
         const float4 v = ld_evict_last_f4(lr + c, pol);
         const float vm = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
         if (vm > mx) {
@@ -220,14 +223,14 @@ __global__ void __launch_bounds__(1024) ce_kernel(const float* __restrict__ logi
     float gm = warp_max(mx);
     if (ln == 0) red[wi] = gm;
     __syncthreads();
-    gm = warp_max(red[ln]);
+    gm = warp_max(ln < kCeThreads / 32 ? red[ln] : -INFINITY);
     __syncthreads();
     s = (mx == -INFINITY) ? 0.f : s * __expf(mx - gm);
     s = warp_sum(s);
     if (ln == 0) red[wi] = s;
     __syncthreads();
     if (wi == 0) {
-      const float t = warp_sum(red[ln]);
+      const float t = warp_sum(ln < kCeThreads / 32 ? red[ln] : 0.f);
       if (ln == 0) s_lse = gm + logf(t);
     }
     __syncthreads();
@@ -236,18 +239,30 @@ __global__ void __launch_bounds__(1024) ce_kernel(const float* __restrict__ logi
     float wsum = 0.f;
     for (int p = p0; p < p1; ++p) wsum += static_cast<float>(w[p]);
     __nv_bfloat16* dr = dl + static_cast<long>(r) * V;
-    for (long c = threadIdx.x * 4; c < V; c += 4096) {
-      const float4 v = __ldcs(reinterpret_cast<const float4*>(lr + c));
-      float g[4] = {wsum * __expf(v.x - lse), wsum * __expf(v.y - lse), wsum * __expf(v.z - lse),
-                    wsum * __expf(v.w - lse)};
-      for (int p = p0; p < p1; ++p) {
-        const long t = tgt[p];
-        if (t >= c && t < c + 4) g[t - c] -= static_cast<float>(w[p]);
+    constexpr int U = 4;
+    constexpr long kStep = 4L * kCeThreads;
+    for (long c0 = threadIdx.x * 4; c0 < V; c0 += U * kStep) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long c = c0 + u * kStep;
+        v[u] = c < V ? __ldcs(reinterpret_cast<const float4*>(lr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      uint2 o;
-      o.x = pack_bf16x2(g[0], g[1]);
-      o.y = pack_bf16x2(g[2], g[3]);
-      *reinterpret_cast<uint2*>(dr + c) = o;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long c = c0 + u * kStep;
+        if (c >= V) break;
+        float g[4] = {wsum * __expf(v[u].x - lse), wsum * __expf(v[u].y - lse), wsum * __expf(v[u].z - lse),
+                      wsum * __expf(v[u].w - lse)};
+        for (int p = p0; p < p1; ++p) {
+          const long t = tgt[p];
+          if (t >= c && t < c + 4) g[t - c] -= static_cast<float>(w[p]);
+        }
+        uint2 o;
+        o.x = pack_bf16x2(g[0], g[1]);
+        o.y = pack_bf16x2(g[2], g[3]);
+        *reinterpret_cast<uint2*>(dr + c) = o;
+      }
     }
     if (threadIdx.x == 0) {
       double acc = 0.0;
@@ -361,7 +376,7 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
 }
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
           __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {
-  if (m > 0) ce_kernel<<<std::min(m, 148), 1024, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
+  if (m > 0) ce_kernel<<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
 }
 void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
                         cudaStream_t s) {

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
@@ -44,9 +45,12 @@ struct Cfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BNC * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (196 * 1024) / kStageBytes > 8 ? 8 : (196 * 1024) / kStageBytes;
+  static constexpr int kStages = (160 * 1024) / kStageBytes > 8 ? 8 : (160 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;  // two accumulator slots (power of 2)
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kOffBar = kStages * kStageBytes;
+  static constexpr int kOffStage = kOffBar + 1024;  // epilogue staging: kEpiWarps x 2 slots x 4 KB
+  static constexpr int kSmem = kOffStage + kEpiWarps * 2 * 4096 + 1024 /*align*/;
+  static_assert(kSmem <= 227 * 1024, "GEMM smem budget");
   static_assert(BNC % 64 == 0 || CG == 1, "2-CTA MN-major B needs 64-column halves");
 };
 
@@ -149,166 +153,121 @@ __device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
                : "memory");
 }
 
-// Output pointer / element offset of column n of `row` (column blocks of split_w go to out[n/split_w]).
-// Selects without dynamic indexing into the kernel-parameter arrays (avoids a local copy).
-__device__ __forceinline__ void epi_target(const EpiParams& epi, int row, int n, void*& outp, long& off) {
-  int blk = 0, nc = n;
-  if (epi.split_w > 0) {
-    blk = n / epi.split_w;
-    nc = n - blk * epi.split_w;
-  }
-  outp = blk == 0 ? epi.out[0] : (blk == 1 ? epi.out[1] : epi.out[2]);
-  const long ldo = blk == 0 ? epi.ldo[0] : (blk == 1 ? epi.ldo[1] : epi.ldo[2]);
-  off = static_cast<long>(row) * ldo + nc;
+// ---- TMA-store epilogue
+// Each epilogue warp drains its 32 accumulator rows in 32-column chunks: the chunk is written (one
+// row per thread) into a per-warp shared-memory slot in the swizzled layout of an output tensor map
+// and written back by ONE cp.async.bulk.tensor store (or cp.reduce.async.bulk .add for accumulating
+// modes), so the LSU never issues the 32-rows-by-16-bytes scattered stores that capped the direct
+// epilogue at ~16 B/clk/SM. Operands the epilogue reads (residual, SiLU input) arrive by TMA into the
+// same slot. Two slots per warp: the store of chunk c drains while chunk c+1 is being produced.
+// fp32 chunk: 32 rows x 128 B, SWIZZLE_128B (16-byte unit u of row r at u ^ (r & 7));
+// bf16 chunk: 32 rows x 64 B, SWIZZLE_64B (unit u of row r at u ^ ((r >> 1) & 3)).
+__device__ __forceinline__ uint32_t sw128_off(int r, int u) { return r * 128 + ((u ^ (r & 7)) << 4); }
+__device__ __forceinline__ uint32_t sw64_off(int r, int u) { return r * 64 + ((u ^ ((r >> 1) & 3)) << 4); }
+
+__device__ __forceinline__ void tma_store_2d(const void* tmap, const void* smem_src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(smem_src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* smem_src, int32_t x, int32_t y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(smem_src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ bool epi_f32_out(int mode) {
+  return mode == EPI_STORE_F32 || mode == EPI_STORE_F32_STATS || mode == EPI_ADD_F32 || mode == EPI_RESID_F32;
 }
 
-// Global operands of a 32-column chunk (independent of the accumulator): issued before the TMEM wait.
-__device__ __forceinline__ void epi_preload(const EpiParams& epi, bool row_ok, int row, int n0, int N,
-                                            uint4 (&pre)[2][4]) {
-  if (!row_ok) return;
+// This thread's row (lane) of a 32-column chunk -> the warp's staging slot `buf`.
+__device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (&r)[32], uint8_t* buf, int lane,
+                                          int row, int M, int n0, int N) {
+  const float alpha = epi.alpha;
+  float v[32];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int n = n0 + 16 * h;
-    if (n >= N) continue;
-    if (epi.mode == EPI_RESID_F32) {
-      const uint4* rp = reinterpret_cast<const uint4*>(epi.resid + static_cast<long>(row) * epi.ld_resid + n);
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * alpha;
+  switch (epi.mode) {
+    case EPI_STORE_F32_STATS:
+      if (row < M) {
+        // per-row (max, sum exp) of this 32-column group (columns >= N excluded)
+        float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) pre[h][i] = rp[i];
-    } else if (epi.mode == EPI_DSILU) {
-      const uint4* ph = reinterpret_cast<const uint4*>(epi.aux + static_cast<long>(row) * epi.ld_aux + n);
-      pre[h][0] = ph[0];
-      pre[h][1] = ph[1];
-    } else if (epi.mode == EPI_ADD_F32 && !epi.atomic) {
-      void* outp;
-      long off;
-      epi_target(epi, row, n, outp, off);
-      const uint4* q = reinterpret_cast<const uint4*>(static_cast<float*>(outp) + off);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) pre[h][i] = q[i];
-    }
-  }
-}
-
-// One thread = one accumulator row; 32 columns (two 16-column halves) per call.
-__device__ __forceinline__ void epi_chunk32(const EpiParams& epi, const uint32_t (&r)[32], const uint4 (&pre)[2][4],
-                                            bool row_ok, int row, int n0, int N) {
-  if (!row_ok) return;
-  float st_m = -INFINITY, st_s = 0.f;  // EPI_STORE_F32_STATS: (max, sum exp) of this 32-column group
-#pragma unroll
-  for (int hh = 0; hh < 2; ++hh) {
-    const int n = n0 + 16 * hh;
-    if (n >= N) continue;
-    float v[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[16 * hh + i]) * epi.alpha;
-    void* outp;
-    long off;
-    epi_target(epi, row, n, outp, off);
-    switch (epi.mode) {
-      case EPI_STORE_BF16: {
-        uint4 w0, w1;
-        w0.x = pack_bf16x2(v[0], v[1]); w0.y = pack_bf16x2(v[2], v[3]);
-        w0.z = pack_bf16x2(v[4], v[5]); w0.w = pack_bf16x2(v[6], v[7]);
-        w1.x = pack_bf16x2(v[8], v[9]); w1.y = pack_bf16x2(v[10], v[11]);
-        w1.z = pack_bf16x2(v[12], v[13]); w1.w = pack_bf16x2(v[14], v[15]);
-        uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(outp) + off);
-        p[0] = w0;
-        p[1] = w1;
-        break;
-      }
-      case EPI_STORE_F32: {
-        float4* p = reinterpret_cast<float4*>(static_cast<float*>(outp) + off);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        break;
-      }
-      case EPI_STORE_F32_STATS: {
-        float4* p = reinterpret_cast<float4*>(static_cast<float*>(outp) + off);
-        float mx = v[0];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-          mx = fmaxf(mx, fmaxf(fmaxf(v[4 * i], v[4 * i + 1]), fmaxf(v[4 * i + 2], v[4 * i + 3])));
-        }
-        const float nm = fmaxf(st_m, mx);
+        for (int i = 0; i < 32; ++i)
+          if (n0 + i < N) mx = fmaxf(mx, v[i]);
         float sum = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) sum += __expf(v[i] - nm);
-        st_s = st_s * __expf(st_m - nm) + sum;
-        st_m = nm;
-        break;
+        for (int i = 0; i < 32; ++i)
+          if (n0 + i < N) sum += __expf(v[i] - mx);
+        reinterpret_cast<float2*>(epi.out2)[static_cast<long>(row) * epi.ldo2 + n0 / 32] = make_float2(mx, sum);
       }
-      case EPI_ADD_F32: {
-        float* p = static_cast<float*>(outp) + off;
-        if (epi.atomic) {
+      [[fallthrough]];
+    case EPI_STORE_F32:
+    case EPI_ADD_F32:
 #pragma unroll
-          for (int i = 0; i < 4; ++i) red_add_v4_f32(p + 4 * i, v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        } else {
-          float4* q = reinterpret_cast<float4*>(p);
+      for (int u = 0; u < 8; ++u)
+        *reinterpret_cast<float4*>(buf + sw128_off(lane, u)) =
+            make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+      break;
+    case EPI_RESID_F32:  // out = resid + acc (model.hpp:427-428,447-448); resid chunk already in buf
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 o = *reinterpret_cast<const float4*>(&pre[hh][i]);
-            q[i] = make_float4(o.x + v[4 * i], o.y + v[4 * i + 1], o.z + v[4 * i + 2], o.w + v[4 * i + 3]);
-          }
-        }
-        break;
+      for (int u = 0; u < 8; ++u) {
+        float4* p = reinterpret_cast<float4*>(buf + sw128_off(lane, u));
+        const float4 o = *p;
+        *p = make_float4(o.x + v[4 * u], o.y + v[4 * u + 1], o.z + v[4 * u + 2], o.w + v[4 * u + 3]);
       }
-      case EPI_SILU: {
-        // out[0] <- h (pre-activation), out2 <- silu(h); both bf16 (model.hpp:443-444).
-        uint4 h0, h1, a0, a1;
-        float hb[16];
+      break;
+    case EPI_STORE_BF16:
 #pragma unroll
-        for (int i = 0; i < 16; ++i) hb[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-        h0.x = pack_bf16x2(hb[0], hb[1]); h0.y = pack_bf16x2(hb[2], hb[3]);
-        h0.z = pack_bf16x2(hb[4], hb[5]); h0.w = pack_bf16x2(hb[6], hb[7]);
-        h1.x = pack_bf16x2(hb[8], hb[9]); h1.y = pack_bf16x2(hb[10], hb[11]);
-        h1.z = pack_bf16x2(hb[12], hb[13]); h1.w = pack_bf16x2(hb[14], hb[15]);
-        a0.x = pack_bf16x2(silu_f(hb[0]), silu_f(hb[1])); a0.y = pack_bf16x2(silu_f(hb[2]), silu_f(hb[3]));
-        a0.z = pack_bf16x2(silu_f(hb[4]), silu_f(hb[5])); a0.w = pack_bf16x2(silu_f(hb[6]), silu_f(hb[7]));
-        a1.x = pack_bf16x2(silu_f(hb[8]), silu_f(hb[9])); a1.y = pack_bf16x2(silu_f(hb[10]), silu_f(hb[11]));
-        a1.z = pack_bf16x2(silu_f(hb[12]), silu_f(hb[13])); a1.w = pack_bf16x2(silu_f(hb[14]), silu_f(hb[15]));
-        uint4* ph = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
-        uint4* pa = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out2) + static_cast<long>(row) * epi.ldo2 + n);
-        ph[0] = h0; ph[1] = h1;
-        pa[0] = a0; pa[1] = a1;
-        break;
-      }
-      case EPI_DSILU: {
-        // out[0] <- acc * silu'(h) in bf16 (model.hpp:526-528).
-        const __nv_bfloat16* hh_ = reinterpret_cast<const __nv_bfloat16*>(&pre[hh][0]);
-        float g[16];
+      for (int u = 0; u < 4; ++u)
+        *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) =
+            make_uint4(pack_bf16x2(v[8 * u], v[8 * u + 1]), pack_bf16x2(v[8 * u + 2], v[8 * u + 3]),
+                       pack_bf16x2(v[8 * u + 4], v[8 * u + 5]), pack_bf16x2(v[8 * u + 6], v[8 * u + 7]));
+      break;
+    case EPI_SILU: {  // h (bf16) -> buf, silu(h) (bf16) -> buf + 2048 (model.hpp:443-444)
 #pragma unroll
-        for (int i = 0; i < 16; ++i) g[i] = v[i] * silu_grad_f(__bfloat162float(hh_[i]));
-        uint4 w0, w1;
-        w0.x = pack_bf16x2(g[0], g[1]); w0.y = pack_bf16x2(g[2], g[3]);
-        w0.z = pack_bf16x2(g[4], g[5]); w0.w = pack_bf16x2(g[6], g[7]);
-        w1.x = pack_bf16x2(g[8], g[9]); w1.y = pack_bf16x2(g[10], g[11]);
-        w1.z = pack_bf16x2(g[12], g[13]); w1.w = pack_bf16x2(g[14], g[15]);
-        uint4* p = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(epi.out[0]) + off);
-        p[0] = w0;
-        p[1] = w1;
-        break;
-      }
-      case EPI_RESID_F32: {
-        float4* p = reinterpret_cast<float4*>(static_cast<float*>(epi.out[0]) + static_cast<long>(row) * epi.ldo[0] + n);
+      for (int u = 0; u < 4; ++u) {
+        float h[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 r4 = *reinterpret_cast<const float4*>(&pre[hh][i]);
-          p[i] = make_float4(r4.x + v[4 * i], r4.y + v[4 * i + 1], r4.z + v[4 * i + 2], r4.w + v[4 * i + 3]);
-        }
-        break;
+        for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(v[8 * u + i]));
+        *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) =
+            make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]),
+                       pack_bf16x2(h[6], h[7]));
+        *reinterpret_cast<uint4*>(buf + 2048 + sw64_off(lane, u)) =
+            make_uint4(pack_bf16x2(silu_f(h[0]), silu_f(h[1])), pack_bf16x2(silu_f(h[2]), silu_f(h[3])),
+                       pack_bf16x2(silu_f(h[4]), silu_f(h[5])), pack_bf16x2(silu_f(h[6]), silu_f(h[7])));
       }
-      default:
-        break;
+      break;
     }
+    case EPI_DSILU:  // out = acc * silu'(h) (model.hpp:526-528); h chunk (bf16) already in buf
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint4* p = reinterpret_cast<uint4*>(buf + sw64_off(lane, u));
+        const uint4 hw = *p;
+        const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hw);
+        float g[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) g[i] = v[8 * u + i] * silu_grad_f(__bfloat162float(hb[i]));
+        *p = make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
+                        pack_bf16x2(g[6], g[7]));
+      }
+      break;
+    default:
+      break;
   }
-  if (epi.mode == EPI_STORE_F32_STATS && n0 < N)
-    reinterpret_cast<float2*>(epi.out2)[static_cast<long>(row) * epi.ldo2 + n0 / 32] = make_float2(st_m, st_s);
 }
 
 template <int BN, int CG, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, int M, int N,
+    gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
+                const __grid_constant__ CUtensorMap tm_o2, const __grid_constant__ CUtensorMap tm_x, int M, int N,
                 int K, int splits, EpiParams epi) {
   using C = Cfg<BN, CG>;
   constexpr int TM = BM * CG;  // tile rows (per CTA pair when CG = 2)
@@ -317,11 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;  // cluster id / count
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* ld_bar = tempty_bar + 2;  // [kEpiWarps][2]: TMA loads of epilogue operands into the slots
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ld_bar + 2 * kEpiWarps);
 
   const int warp = warp_id_sync();
   const int lane = threadIdx.x & 31;
@@ -343,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], kEpiWarps * CG);  // leader: epilogue warps of both CTAs
     }
+    for (int s = 0; s < 2 * kEpiWarps; ++s) mbar_init(&ld_bar[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, C::kTmemCols);
@@ -479,21 +440,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   mma_done:;
   } else {
     // ------------------------------------------------------------ epilogue
-    // Each warp drains 32 TMEM lanes (rows) x BN/2 columns in 32-column chunks, software-pipelined:
-    // the TMEM load of chunk c+1 and the global operand loads (residual / aux / RMW target) of chunk
-    // c are in flight while chunk c is converted and stored; the accumulator slot is handed back to
-    // the MMA warp as soon as its last chunk is in registers.
+    // Each warp drains 32 TMEM lanes (rows) x BN/2 columns in 32-column chunks. The TMEM load of
+    // chunk c+1 is in flight while chunk c is staged; the accumulator slot is handed back to the MMA
+    // warp as soon as its last chunk is in registers; stores drain asynchronously (TMA).
     const int quad = warp & 3;             // TMEM lane quadrant this warp may access
     const int half = (warp - 2) / 4;       // which half of the BN columns this warp handles
     constexpr int CW = BN / 2;
     constexpr int NCH = CW / 32;
+    const int ew = warp - 2;
+    uint8_t* stg = smem + C::kOffStage + ew * 8192;
+    uint64_t* wld = ld_bar + 2 * ew;
+    const int mode = epi.mode;
+    const bool need_ld = mode == EPI_RESID_F32 || mode == EPI_DSILU;
+    const uint32_t ld_bytes = epi_f32_out(mode) ? 4096u : 2048u;
+    uint32_t gc = 0;        // chunks staged by this warp: slot = gc & 1
+    uint32_t ld_phase = 0;  // per-slot parity of the operand-load barriers
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < num_tiles; t += ncl) {
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
-      const int row = m_blk * TM + static_cast<int>(rank) * BM + quad * 32 + lane;
-      const bool row_ok = row < M;
+      const int row0 = m_blk * TM + static_cast<int>(rank) * BM + quad * 32;  // this warp's first row
       const int n_base = n_blk * BN + half * CW;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -503,8 +470,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
         const int n0 = n_base + ch * 32;
-        uint4 pre[2][4];
-        epi_preload(epi, row_ok, row, n0, N, pre);
+        const bool active = n0 < N;  // warp-uniform
+        const int slot = gc & 1;
+        uint8_t* buf = stg + slot * 4096;
+        int blk = 0, xc = n0;
+        if (epi.split_w > 0) {
+          blk = n0 / epi.split_w;
+          xc = n0 - blk * epi.split_w;
+        }
+        if (active) {
+          if (lane == 0) bulk_wait_read1();  // the store issued from this slot two chunks ago has read it
+          __syncwarp();
+          if (need_ld && lane == 0) {
+            mbar_arrive_expect_tx(&wld[slot], ld_bytes);
+            tma_load_2d(&tm_x, &wld[slot], buf, n0, row0);
+          }
+        }
         tmem_ld_wait_regs(rr[ch & 1]);
         if (ch + 1 < NCH) {
           tmem_ld32(t_row + (ch + 1) * 32, rr[(ch + 1) & 1]);
@@ -516,13 +497,30 @@ __global__ void __launch_bounds__(kThreads, 1)
             else mbar_arrive_remote(mapa_shared(smem_u32(&tempty_bar[acc]), 0));  // the leader's slot barrier
           }
         }
-        epi_chunk32(epi, rr[ch & 1], pre, row_ok, row, n0, N);
+        if (active) {
+          if (need_ld) {
+            mbar_wait(&wld[slot], (ld_phase >> slot) & 1);
+            ld_phase ^= 1u << slot;
+          }
+          epi_stage(epi, rr[ch & 1], buf, lane, row0 + lane, M, n0, N);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const CUtensorMap* tm = blk == 0 ? &tm_o0 : (blk == 1 ? &tm_o1 : &tm_o2);
+            if (mode == EPI_ADD_F32) tma_reduce_add_2d(tm, buf, xc, row0);
+            else tma_store_2d(tm, buf, xc, row0);
+            if (mode == EPI_SILU) tma_store_2d(&tm_x, buf + 2048, n0, row0);
+            bulk_commit();
+          }
+          ++gc;
+        }
       }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait_all();  // stores complete before the CTA (and its smem) retires
   }
 
   tc_fence_before();
@@ -567,6 +565,24 @@ namespace {
 
 int g_num_sms = 0;
 
+// Output / epilogue-operand tensor map: [rows x width] elements (fp32 or bf16), row pitch ld elements,
+// 32 x 32 boxes in the swizzled staging layout of the epilogue (128B rows fp32, 64B rows bf16).
+void make_tmap_epi(CUtensorMap* map, const void* ptr, bool f32, uint64_t width, uint64_t rows, uint64_t ld) {
+  const uint64_t esz = f32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * esz) % 16 != 0)
+    throw std::invalid_argument("gemm epilogue: output pointer / pitch must be 16-byte aligned");
+  cuuint64_t dims[2] = {width, rows};
+  cuuint64_t strides[1] = {ld * esz};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                               const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (epilogue) failed (" + std::to_string(int(r)) + ")");
+}
+
 template <int BN, int CG, bool A_MN, bool B_MN>
 void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
             cudaStream_t stream) {
@@ -596,6 +612,21 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   const int grid = (tiles < max_clusters ? tiles : max_clusters) * CG;
   EpiParams e = epi;
   if (splits > 1) e.atomic = 1;
+  // output tensor maps (and the epilogue operand map: silu output / dsilu input / residual input)
+  const bool f32 = e.mode == EPI_STORE_F32 || e.mode == EPI_STORE_F32_STATS || e.mode == EPI_ADD_F32 ||
+                   e.mode == EPI_RESID_F32;
+  if (e.split_w > 0 && (e.split_w % 32 != 0 || e.mode == EPI_SILU || e.mode == EPI_DSILU || e.mode == EPI_RESID_F32))
+    throw std::invalid_argument("gemm epilogue: split_w must be a multiple of 32 (store / add modes only)");
+  CUtensorMap to[3], tx;
+  std::memset(to, 0, sizeof(to));
+  std::memset(&tx, 0, sizeof(tx));
+  const uint64_t width = e.split_w > 0 ? static_cast<uint64_t>(e.split_w) : static_cast<uint64_t>(N);
+  const int nout = e.split_w > 0 ? (N + e.split_w - 1) / e.split_w : 1;
+  if (nout > 3) throw std::invalid_argument("gemm epilogue: at most 3 column blocks");
+  for (int i = 0; i < nout; ++i) make_tmap_epi(&to[i], e.out[i], f32, width, M, e.ldo[i]);
+  if (e.mode == EPI_SILU) make_tmap_epi(&tx, e.out2, false, N, M, e.ldo2);
+  if (e.mode == EPI_DSILU) make_tmap_epi(&tx, e.aux, false, N, M, e.ld_aux);
+  if (e.mode == EPI_RESID_F32) make_tmap_epi(&tx, e.resid, true, N, M, e.ld_resid);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -608,7 +639,7 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN>, ta, tb, M, N, K, splits, e);
+  cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN>, ta, tb, to[0], to[1], to[2], tx, M, N, K, splits, e);
 }
 
 }  // namespace

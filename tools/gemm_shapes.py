@@ -39,7 +39,12 @@ def main():
         if os.path.exists("MEASURED_PEAKS.json") else {"bf16_tflops": 1590.0}
     vp = ctypes.c_void_p
     out = []
-    for label, M, N, K, amn, bmn, epi in SHAPES:
+    shapes = list(SHAPES)
+    if os.environ.get("GEMM_EXTRA"):  # "M,N,K" plain bf16-store GEMM (A K-major, B MN-major)
+        M_, N_, K_ = (int(x) for x in os.environ["GEMM_EXTRA"].split(","))
+        shapes.append(("extra", M_, N_, K_, 0, 1, EPI_STORE_BF16))
+        only = only or "extra"
+    for label, M, N, K, amn, bmn, epi in shapes:
         if only and label != only:
             continue
         a = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()

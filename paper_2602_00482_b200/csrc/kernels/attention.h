@@ -54,8 +54,8 @@ void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream);
 constexpr int kFwdBlockQ = 128;
 void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream);
 
-// Softmax exponentials taken on the FMA pipe per 4 element pairs (0..2; default 1). Tuning knob:
-// env TT_ATTN_POLY, read once.
+// Forward softmax exponentials taken on the FMA pipe per 4 element pairs (0..2; default 1). Tuning
+// knob: env TT_ATTN_POLY, read once.
 int attn_poly_pairs();
 
 // Copies the clock64 trace of the TT_ATTN_DBG=3 dq kernel (4 x 256: MMA ds_full wake, MMA issue

@@ -605,15 +605,9 @@ int attn_debug_trace(long long* host, int n) {
 void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                     const int2* kv_items2, int n_kv, cudaStream_t stream) {
   attn_bwd_pre(a, stream);
-#define TT_BWD(P)                                                                                          \
-  if (a.dh == 64) return launch_bwd<64, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream); \
-  if (a.dh == 128) return launch_bwd<128, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
-  switch (attn_poly_pairs()) {
-    case 0: TT_BWD(0) break;
-    case 2: TT_BWD(2) break;
-    default: TT_BWD(1) break;
-  }
-#undef TT_BWD
+  // exponentials stay on MUFU here (measured: the FMA-pipe polynomial only pays in the forward)
+  if (a.dh == 64) return launch_bwd<64, 0>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
+  if (a.dh == 128) return launch_bwd<128, 0>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
   throw std::invalid_argument("attention: head_dim must be 64 or 128");
 }
 

@@ -112,6 +112,16 @@ __global__ void __launch_bounds__(128, 1) probe_dq(long long* out, int iters) {
     long long t1 = clock64();
     if (blockIdx.x == 0) out[0] = t1 - t0;
     *reinterpret_cast<volatile int*>(&stop) = 1;
+  } else if (MODE == 5 && threadIdx.x >= 32) {
+    // other warps: stream 16-byte shared-memory stores (like TMA fills + softmax dS stores)
+    uint4* p = reinterpret_cast<uint4*>(smem + 180224);
+    const uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+    int i = threadIdx.x;
+    while (!*reinterpret_cast<volatile int*>(&stop)) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) p[(i + k * 96) & 1023] = v;
+      i += 7;
+    }
   } else if (MODE == 4 && threadIdx.x >= 32) {
     // other warps: stream tcgen05.ld of their TMEM lane quadrant (like the softmax warps reading S/dP)
     const uint32_t lane_off = static_cast<uint32_t>((warp & 3) * 32) << 16;
@@ -139,7 +149,7 @@ void run_dq(long long* d, int iters) {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   const int per = (MODE == 0 || MODE >= 3) ? 12 : (MODE == 1 ? 4 : 8);
   const char* names[] = {"S+dP+dQ", "dQ only (B MN-major)", "S+dP only", "S+dP+dQ + 3 commits/block",
-                         "S+dP+dQ + commits + 3 warps streaming tcgen05.ld"};
+                         "S+dP+dQ + commits + 3 warps streaming tcgen05.ld", "S+dP+dQ + commits + 3 warps streaming STS.128"};
   printf("dq pattern mode %d (%s): %7.1f clk/block, %6.1f clk/MMA  %s\n", MODE, names[MODE], double(h[0]) / iters,
          double(h[0]) / (iters * per), cudaGetErrorString(e));
 }
@@ -170,5 +180,6 @@ int main() {
   run_dq<2>(d, 1000);
   run_dq<3>(d, 1000);
   run_dq<4>(d, 1000);
+  run_dq<5>(d, 1000);
   return 0;
 }

@@ -3,6 +3,7 @@
 // gradient scatter, parameter layout conversion / init. 128-bit coalesced accesses throughout.
 #include <algorithm>
 #include <cuda_bf16.h>
+#include <stdexcept>
 #include <cuda_runtime.h>
 
 #include "elementwise.h"
@@ -50,28 +51,37 @@ __global__ void embed_pe_kernel(const int32_t* __restrict__ tok, const int32_t* 
 
 // inv = 1/sqrt(mean(x^2)+eps); y = x*inv*g (bf16)   (rms_inv model.hpp:250-256; apply :377-380)
 // one warp per row
-__global__ void rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain, float* __restrict__ inv,
-                                   __nv_bfloat16* __restrict__ y, int n, int d) {
+// One warp per row; VPT float4 column groups per lane held in registers, so x is read from HBM once.
+template <int VPT>
+__global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                                          float* __restrict__ inv, __nv_bfloat16* __restrict__ y, int n,
+                                                          int d) {
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (row >= n) return;
   const float* xr = x + static_cast<long>(row) * d;
+  float4 v[VPT];
   float s = 0.f;
-  for (int c = lane * 4; c < d; c += 128) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int c = (lane + 32 * k) * 4;
+    v[k] = c < d ? __ldcs(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
   }
   s = warp_sum(s);
   const float iv = 1.0f / sqrtf(s / static_cast<float>(d) + 1e-6f);
   if (lane == 0) inv[row] = iv;
   __nv_bfloat16* yr = y + static_cast<long>(row) * d;
-  for (int c = lane * 4; c < d; c += 128) {
-    const float4 v = *reinterpret_cast<const float4*>(xr + c);
-    const float4 g = *reinterpret_cast<const float4*>(gain + c);
-    uint2 o;
-    o.x = pack_bf16x2(v.x * iv * g.x, v.y * iv * g.y);
-    o.y = pack_bf16x2(v.z * iv * g.z, v.w * iv * g.w);
-    *reinterpret_cast<uint2*>(yr + c) = o;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int c = (lane + 32 * k) * 4;
+    if (c < d) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
+      uint2 o;
+      o.x = pack_bf16x2(v[k].x * iv * g.x, v[k].y * iv * g.y);
+      o.y = pack_bf16x2(v[k].z * iv * g.z, v[k].w * iv * g.w);
+      *reinterpret_cast<uint2*>(yr + c) = o;
+    }
   }
 }
 
@@ -360,7 +370,15 @@ void k_embed_pe(const int32_t* tok, const int32_t* pos, const __nv_bfloat16* emb
   if (n > 0) embed_pe_kernel<<<n, 128, 0, s>>>(tok, pos, emb, pe, x, d);
 }
 void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16* y, int n, int d, cudaStream_t s) {
-  if (n > 0) rmsnorm_fwd_kernel<<<(n + 7) / 8, 256, 0, s>>>(x, gain, inv, y, n, d);
+  if (n <= 0) return;
+  const int vpt = (d + 127) / 128;
+  const int blocks = (n + 7) / 8;
+  if (vpt <= 2) rmsnorm_fwd_kernel<2><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
+  else if (vpt <= 4) rmsnorm_fwd_kernel<4><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
+  else if (vpt <= 8) rmsnorm_fwd_kernel<8><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
+  else if (vpt <= 16) rmsnorm_fwd_kernel<16><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
+  else if (vpt <= 32) rmsnorm_fwd_kernel<32><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
+  else throw std::invalid_argument("rmsnorm: d_model > 4096");
 }
 void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
                    __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {

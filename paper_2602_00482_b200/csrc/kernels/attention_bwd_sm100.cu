@@ -85,8 +85,8 @@ struct BwdParams {
 };
 
 // DBG (timing experiments only, TT_ATTN_DBG): 1 = softmax warps skip TMEM loads + math (MMA/TMA
-// pipeline alone), 2 = softmax warps do not wait for S (softmax alone), 3 = normal + clock64 trace of
-// one mid-grid CTA into g_attn_trace (tt_debug_attn_trace).
+// pipeline alone), 2 = softmax warps do not wait for S (softmax alone), 4 = + clock64 trace of one
+// mid-grid CTA into g_attn_trace (tt_debug_attn_trace). TT_ATTN_DBG=3 -> trace, 5 -> skip + trace.
 __device__ long long g_attn_trace[6][256];
 template <int DH, int NS, int POLY, int DBG = 0>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);         // K-major tiles
     const uint64_t dKmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // K_j read MN-major
-    const bool trace = DBG == 3 && lane == 0 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
+    const bool trace = (DBG & 4) && lane == 0 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     auto issue_s = [&](int j) {  // S_j = Q K_j^T ; dP_j = dO V_j^T
       const int st = j % NS;
       if (trace && j >= NB && j - NB < 256) g_attn_trace[4][j - NB] = clock64();
@@ -221,12 +221,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float Dr = row_ok ? p.D[static_cast<long>(h) * p.n + row] : 0.f;
     const float c2 = p.scale_log2;
     constexpr int HC = BKV / 2;
-    const bool trace = DBG == 3 && threadIdx.x == 64 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
+    const bool trace = (DBG & 4) && threadIdx.x == 64 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     for (int j = 0; j < nblk; ++j) {
       if (DBG != 2) mbar_wait(&s_full[j % NB], (j / NB) & 1);
       if (trace && j < 256) g_attn_trace[2][j] = clock64();
       tc_fence_after();
-      if (DBG == 1) {
+      if ((DBG & 1)) {
         if (j >= 2) mbar_wait(&kv_empty[(j - 2) % NS], ((j - 2) / NS) & 1);
         fence_proxy_async_smem();
         tc_fence_before();
@@ -570,9 +570,10 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
       const char* e = std::getenv("TT_ATTN_DBG");
       return e ? std::atoi(e) : 0;
     }();
-    if (dbg == 1 || dbg == 2 || dbg == 3) {
+    if (dbg == 1 || dbg == 2 || dbg == 3 || dbg == 5) {
       auto kfn = dbg == 1 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 1>
-                          : (dbg == 2 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 2> : fa_bwd_dq_kernel<DH, NSQ, POLY, 3>);
+                          : (dbg == 2 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 2>
+                                      : (dbg == 3 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 4> : fa_bwd_dq_kernel<DH, NSQ, POLY, 5>));
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CQ::kSmem);
       kfn<<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
     } else {

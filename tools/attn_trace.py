@@ -10,7 +10,7 @@ from paper_2602_00482_b200 import _native  # noqa: E402
 
 
 def main():
-    assert os.environ.get("TT_ATTN_DBG") == "3"
+    assert os.environ.get("TT_ATTN_DBG") in ("3", "5")
     subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "attn_bench.py"), "1", "1"] + sys.argv[1:],
                    check=True)
     # attn_bench ran in a child process; rerun one bwd here to fill the trace

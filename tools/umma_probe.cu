@@ -77,7 +77,14 @@ __global__ void __launch_bounds__(128, 1) probe_dq(long long* out, int iters) {
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(&slot, 512);
-  for (int i = threadIdx.x; i < 196608 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = threadIdx.x; i < 196608 / 4; i += blockDim.x) {
+    // MODE 6: random bf16 operands (|x| ~ 1) instead of zeros (data-dependent MMA power/throughput?)
+    uint32_t h = (i + 1) * 2654435761u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    const uint32_t lo = 0x3f80u ^ (h & 0x807fu), hi = 0x3f80u ^ ((h >> 16) & 0x807fu);
+    reinterpret_cast<uint32_t*>(smem)[i] = MODE == 6 ? (lo | (hi << 16)) : 0u;
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
@@ -149,7 +156,7 @@ void run_dq(long long* d, int iters) {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   const int per = (MODE == 0 || MODE >= 3) ? 12 : (MODE == 1 ? 4 : 8);
   const char* names[] = {"S+dP+dQ", "dQ only (B MN-major)", "S+dP only", "S+dP+dQ + 3 commits/block",
-                         "S+dP+dQ + commits + 3 warps streaming tcgen05.ld", "S+dP+dQ + commits + 3 warps streaming STS.128"};
+                         "S+dP+dQ + commits + 3 warps streaming tcgen05.ld", "S+dP+dQ + commits + 3 warps streaming STS.128", "S+dP+dQ + commits, random operands"};
   printf("dq pattern mode %d (%s): %7.1f clk/block, %6.1f clk/MMA  %s\n", MODE, names[MODE], double(h[0]) / iters,
          double(h[0]) / (iters * per), cudaGetErrorString(e));
 }
@@ -181,5 +188,6 @@ int main() {
   run_dq<3>(d, 1000);
   run_dq<4>(d, 1000);
   run_dq<5>(d, 1000);
+  run_dq<6>(d, 1000);
   return 0;
 }

@@ -62,17 +62,32 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int iters) {
 
 // The dq-kernel issue pattern: per block, S (Q x K_st) and dP (dO x V_st) interleaved into two TMEM
 // accumulators, then dQ (dS x K_st, B MN-major); stages cycle over NS K/V tiles of 8 KB.
+__device__ __forceinline__ void mbar_wait_test(uint64_t* bar, uint32_t parity) {
+  // non-blocking mbarrier.test_wait spin (vs the potentially-blocking try_wait)
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\tselp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(128, 1) probe_dq(long long* out, int iters) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
-  __shared__ uint64_t bar, cbar[8];
+  __shared__ uint64_t bar, cbar[8], done_bar;
   __shared__ uint32_t slot;
   __shared__ int stop;
   const int warp = threadIdx.x / 32;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     for (int i = 0; i < 8; ++i) mbar_init(&cbar[i], 1);
+    mbar_init(&done_bar, 1);
+    mbar_arrive(&done_bar);  // phase 0 complete
     stop = 0;
     fence_barrier_init();
   }
@@ -96,6 +111,9 @@ __global__ void __launch_bounds__(128, 1) probe_dq(long long* out, int iters) {
     long long t0 = clock64();
     for (int j = 0; j < iters; ++j) {
       const uint32_t st = j % 8, k_off = 32768 + st * 8192, v_off = 98304 + st * 8192, ds_off = 163840 + (j & 1) * 16384;
+      if (MODE == 7 || MODE == 8) mbar_wait(&done_bar, 0);  // the kernel's pattern: (complete) mbarrier wait
+      if (MODE == 10) mbar_wait_test(&done_bar, 0);
+      if (MODE == 7 || MODE == 9) tc_fence_after();         // + tcgen05 fence per group
       if (MODE != 1) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -104,6 +122,9 @@ __global__ void __launch_bounds__(128, 1) probe_dq(long long* out, int iters) {
         }
       }
       if (MODE >= 3) umma_commit(&cbar[j % 3]);
+      if (MODE == 7 || MODE == 8) mbar_wait(&done_bar, 0);
+      if (MODE == 10) mbar_wait_test(&done_bar, 0);
+      if (MODE == 7 || MODE == 9) tc_fence_after();
       if (MODE != 2) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -156,7 +177,7 @@ void run_dq(long long* d, int iters) {
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
   const int per = (MODE == 0 || MODE >= 3) ? 12 : (MODE == 1 ? 4 : 8);
   const char* names[] = {"S+dP+dQ", "dQ only (B MN-major)", "S+dP only", "S+dP+dQ + 3 commits/block",
-                         "S+dP+dQ + commits + 3 warps streaming tcgen05.ld", "S+dP+dQ + commits + 3 warps streaming STS.128", "S+dP+dQ + commits, random operands"};
+                         "S+dP+dQ + commits + 3 warps streaming tcgen05.ld", "S+dP+dQ + commits + 3 warps streaming STS.128", "S+dP+dQ + commits, random operands", "S+dP+dQ + commits + mbar wait + tcgen05 fence per group", "... + mbar wait only", "... + tcgen05 fence only", "... + mbarrier.test_wait spin"};
   printf("dq pattern mode %d (%s): %7.1f clk/block, %6.1f clk/MMA  %s\n", MODE, names[MODE], double(h[0]) / iters,
          double(h[0]) / (iters * per), cudaGetErrorString(e));
 }
@@ -189,5 +210,9 @@ int main() {
   run_dq<4>(d, 1000);
   run_dq<5>(d, 1000);
   run_dq<6>(d, 1000);
+  run_dq<7>(d, 1000);
+  run_dq<8>(d, 1000);
+  run_dq<9>(d, 1000);
+  run_dq<10>(d, 1000);
   return 0;
 }

@@ -58,8 +58,7 @@ struct DqCfg {
   static constexpr int kOffDO = kQBytes;
   static constexpr int kOffK = 2 * kQBytes;
   static constexpr int kOffV = kOffK + NS * kKVBytes;
-  static constexpr int kOffDS = kOffV + NS * kKVBytes;
-  static constexpr int kOffBar = kOffDS + 2 * kDSBytes;
+  static constexpr int kOffBar = kOffV + NS * kKVBytes;  // (dS lives in TMEM)
   static constexpr int kTmemCols = (2 * NB * BKV + DH) <= 256 ? 256 : 512;
   static_assert(2 * NB * BKV + DH <= 512 && NS >= NB, "dq kernel: TMEM / K-V ring too small");
   // a second co-resident CTA could not get TMEM (it would block in tcgen05.alloc while holding the
@@ -88,8 +87,13 @@ struct BwdParams {
 // pipeline alone), 2 = softmax warps do not wait for S (softmax alone), 4 = + clock64 trace of one
 // mid-grid CTA into g_attn_trace (tt_debug_attn_trace). TT_ATTN_DBG=3 -> trace, 5 -> skip + trace.
 __device__ long long g_attn_trace[6][256];
+// Two MMA-issuing warps: warp 1 issues S_j / dP_j, warp 10 issues dQ += dS_j K_j. An mbarrier wait in
+// an issuing thread costs ~180 clk while MMAs are in flight (tools/umma_probe.cu, mode 8), longer than
+// the tensor pipe takes for the 4-8 N=64 MMAs queued behind it; with one issuer per dependency chain
+// a wait on one chain never starves the pipe of the other chain's MMAs.
+constexpr int kThreadsDq = kThreads + 32;
 template <int DH, int NS, int POLY, int DBG = 0>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsDq, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                      BwdParams p) {
@@ -101,11 +105,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + NS;
-  uint64_t* s_full = kv_empty + NS;  // [NB] S_j and dP_j in TMEM
-  uint64_t* ds_full = s_full + C::NB;  // [2]  dS_j in smem
+  uint64_t* s_full = kv_empty + NS;    // [NB] S_j and dP_j in TMEM
+  uint64_t* ds_full = s_full + C::NB;  // [NB] softmax done with block j: S/dP_j read, dS_j in smem
   // kv_empty[j % NS] completes when dQ_j (the last reader of K_j and of dS_j) is done: it frees the
   // K/V stage for the producer AND the dS buffer for the softmax warps (one commit, two waiters)
-  uint64_t* dq_done = ds_full + 2;
+  uint64_t* dq_done = ds_full + C::NB;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dq_done + 1);
 
   const int warp = warp_id_sync();
@@ -129,8 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < C::NB; ++s) mbar_init(&s_full[s], 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::NB; ++s) {
+      mbar_init(&s_full[s], 1);
       mbar_init(&ds_full[s], kSmxWarps);
     }
     mbar_init(dq_done, 1);
@@ -166,46 +170,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);         // K-major tiles
-    const uint64_t dKmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // K_j read MN-major
+    // S_j = Q K_j^T ; dP_j = dO V_j^T into TMEM buffer j % NB, once the softmax is done with j - NB
+    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);  // K-major tiles
     const bool trace = (DBG & 4) && lane == 0 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
-    auto issue_s = [&](int j) {  // S_j = Q K_j^T ; dP_j = dO V_j^T
+    mbar_wait(q_full, 0);
+    for (int j = 0; j < nblk; ++j) {
       const int st = j % NS;
-      if (trace && j >= NB && j - NB < 256) g_attn_trace[4][j - NB] = clock64();
+      // buffer j % NB holds dS_{j-NB} (the A operand of dQ_{j-NB}) until that MMA completes
+      if (j >= NB) mbar_wait(&kv_empty[(j - NB) % NS], ((j - NB) / NS) & 1);
+      if (trace && j < 256) g_attn_trace[4][j] = clock64();
       mbar_wait(&kv_full[st], (j / NS) & 1);
-      if (trace && j >= NB && j - NB < 256) g_attn_trace[5][j - NB] = clock64();
       tc_fence_after();
       if (lane == 0) {
         const uint32_t k_off = C::kOffK + st * C::kKVBytes, v_off = C::kOffV + st * C::kKVBytes;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
           const uint32_t ao = (k / 4) * (128 * 128) + (k % 4) * 32, bo = (k / 4) * (BKV * 128) + (k % 4) * 32;
-          umma_bf16_ss(t_S + (j % NB) * BKV, sdesc_add(d16, ao), sdesc_add(sdesc_add(d16, k_off), bo), C::kIdescS, k > 0);
-          umma_bf16_ss(t_dP + (j % NB) * BKV, sdesc_add(d16, C::kOffDO + ao), sdesc_add(sdesc_add(d16, v_off), bo), C::kIdescS,
+          umma_bf16_ss(t_S + (j % NB) * BKV, sdesc_add(d16, ao), sdesc_add(sdesc_add(d16, k_off), bo), C::kIdescS,
                        k > 0);
+          umma_bf16_ss(t_dP + (j % NB) * BKV, sdesc_add(d16, C::kOffDO + ao), sdesc_add(sdesc_add(d16, v_off), bo),
+                       C::kIdescS, k > 0);
         }
         umma_commit(&s_full[j % NB]);
       }
       __syncwarp();
-    };
-    mbar_wait(q_full, 0);
-    for (int j = 0; j < NB && j < nblk; ++j) issue_s(j);
+      if (trace && j < 256) g_attn_trace[5][j] = clock64();
+    }
+  } else if (warp == 10) {
+    // dQ += dS_j K_j (B = K_j read MN-major: N = dh, K = keys), in block order
+    const uint64_t dKmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);
+    const bool trace = (DBG & 4) && lane == 0 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&ds_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&ds_full[j % NB], (j / NB) & 1);
       if (trace && j < 256) g_attn_trace[0][j] = clock64();
       tc_fence_after();
-      if (lane == 0) {  // dQ += dS_j K_j   (B = K_j read MN-major: N = dh, K = keys)
+      if (lane == 0) {
         const int st = j % NS;
-        const uint32_t ds_off = C::kOffDS + (j & 1) * C::kDSBytes, k_off = C::kOffK + st * C::kKVBytes;
+        const uint32_t k_off = C::kOffK + st * C::kKVBytes;
+        // A = dS_j straight from TMEM (bf16 pairs in the S_j buffer, per half of the keys)
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          umma_bf16_ss(t_dQ, sdesc_add(sdesc_add(d16, ds_off), k * 32), sdesc_add(sdesc_add(dKmn, k_off), k * 2048), C::kIdescQ,
+          umma_bf16_ts(t_dQ, t_S + (j % NB) * BKV + packed_col<BKV / 2>(k), sdesc_add(sdesc_add(dKmn, k_off), k * 2048), C::kIdescQ,
                        (j > 0 || k > 0));
         umma_commit(&kv_empty[st]);
         if (j == nblk - 1) umma_commit(dq_done);
       }
       __syncwarp();
-      if (j + NB < nblk) issue_s(j + NB);
       if (trace && j < 256) g_attn_trace[1][j] = clock64();
     }
   } else {
@@ -227,11 +237,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (trace && j < 256) g_attn_trace[2][j] = clock64();
       tc_fence_after();
       if ((DBG & 1)) {
-        if (j >= 2) mbar_wait(&kv_empty[(j - 2) % NS], ((j - 2) / NS) & 1);
-        fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_full[j & 1]);
+        if (lane == 0) mbar_arrive(&ds_full[j % NB]);
         continue;
       }
       float s[HC], dp[HC];
@@ -263,12 +271,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 ds = __fmul2_rn(pe, __fadd2_rn(make_float2(dp[i], dp[i + 1]), nD2));
         w[i / 2] = pack_bf16x2(ds.x, ds.y);
       }
-      if (j >= 2) mbar_wait(&kv_empty[(j - 2) % NS], ((j - 2) / NS) & 1);  // dQ_{j-2} done: dS buffer free
-      st_halfrow_sw128(smem + C::kOffDS + (j & 1) * C::kDSBytes, rloc, half, w);
-      fence_proxy_async_smem();
+      // dS_j (bf16 pairs) into the first HC/2 columns of this half's OWN S_j columns (the other half
+      // may still be reading its S columns): the A operand of dQ_j
+      tmem_st16(t_S + (j % NB) * BKV + half * HC + lane_off, w);
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&ds_full[j & 1]);
+      if (lane == 0) mbar_arrive(&ds_full[j % NB]);
       if (trace && j < 256) g_attn_trace[3][j] = clock64();
     }
     mbar_wait(dq_done, 0);
@@ -303,9 +312,7 @@ struct DkvCfg {
   static constexpr int kOffV = kKVBytes;
   static constexpr int kOffQ = 2 * kKVBytes;
   static constexpr int kOffDO = kOffQ + NS * kQBytes;
-  static constexpr int kOffP = kOffDO + NS * kQBytes;   // [2]
-  static constexpr int kOffDS = kOffP + 2 * kPBytes;    // [2]
-  static constexpr int kOffStat = kOffDS + 2 * kPBytes; // [2][2][BQ] floats: lse2, D
+  static constexpr int kOffStat = kOffDO + NS * kQBytes;  // [2][2][BQ] floats: lse2, D (P^T, dS^T in TMEM)
   static constexpr int kOffBar = kOffStat + 2 * 2 * BQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kTmemCols = 512;
@@ -314,8 +321,10 @@ struct DkvCfg {
   static constexpr uint32_t kIdescKV = make_idesc_bf16(128, DH, false, true);
 };
 
+// Like the dq kernel: two MMA-issuing warps (warp 1: S^T_i / dP^T_i; warp 10: dV / dK), and P^T_i /
+// dS^T_i go back into TMEM (bf16 pairs over the S^T_i / dP^T_i buffers) as the A operands of dV / dK.
 template <int DH, int NS, int POLY>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreadsDq, 1)
     fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        BwdParams p) {
@@ -328,9 +337,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_full = bars + 1;
   uint64_t* q_empty = q_full + NS;
   uint64_t* s_full = q_empty + NS;    // [NB]
-  uint64_t* p_full = s_full + C::NB;  // [2]
-  // q_empty[i % NS] completes when dV/dK_i are done: frees the Q/dO stage AND the P/dS buffers
-  uint64_t* acc_done = p_full + 2;
+  uint64_t* p_full = s_full + C::NB;  // [NB] softmax done with block i (P^T / dS^T in TMEM)
+  // q_empty[i % NS] completes when dV/dK_i are done: frees the Q/dO stage AND the TMEM buffers of i
+  uint64_t* acc_done = p_full + C::NB;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
   float* stat = reinterpret_cast<float*>(smem + C::kOffStat);
 
@@ -355,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
-    for (int s = 0; s < C::NB; ++s) mbar_init(&s_full[s], 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::NB; ++s) {
+      mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSmxWarps);
     }
     mbar_init(acc_done, 1);
@@ -392,10 +401,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);        // K-major tiles
-    const uint64_t dmn = make_sdesc_sw128(smem_u32(smem), BQ * 128, 1024);  // Q_i / dO_i read MN-major
-    auto issue_s = [&](int i) {  // S^T_i = K Q_i^T ; dP^T_i = V dO_i^T   (M = 128 keys, N = 64 queries)
+    // S^T_i = K Q_i^T ; dP^T_i = V dO_i^T   (M = 128 keys, N = 64 queries) into TMEM buffer i % NB,
+    // once dV/dK_{i-NB} (whose A operands P^T / dS^T live in that buffer) are done
+    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);  // K-major tiles
+    mbar_wait(kv_full, 0);
+    for (int i = 0; i < nq; ++i) {
       const int st = i % NS;
+      if (i >= NB) mbar_wait(&q_empty[(i - NB) % NS], ((i - NB) / NS) & 1);
       mbar_wait(&q_full[st], (i / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
@@ -403,35 +415,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
           const uint32_t ao = (k / 4) * (128 * 128) + (k % 4) * 32, bo = (k / 4) * (BQ * 128) + (k % 4) * 32;
-          umma_bf16_ss(t_S + (i % NB) * BQ, sdesc_add(d16, ao), sdesc_add(sdesc_add(d16, q_off), bo), C::kIdescS, k > 0);
-          umma_bf16_ss(t_dP + (i % NB) * BQ, sdesc_add(d16, C::kOffV + ao), sdesc_add(sdesc_add(d16, do_off), bo), C::kIdescS,
+          umma_bf16_ss(t_S + (i % NB) * BQ, sdesc_add(d16, ao), sdesc_add(sdesc_add(d16, q_off), bo), C::kIdescS,
                        k > 0);
+          umma_bf16_ss(t_dP + (i % NB) * BQ, sdesc_add(d16, C::kOffV + ao), sdesc_add(sdesc_add(d16, do_off), bo),
+                       C::kIdescS, k > 0);
         }
         umma_commit(&s_full[i % NB]);
       }
       __syncwarp();
-    };
-    mbar_wait(kv_full, 0);
-    for (int i = 0; i < NB && i < nq; ++i) issue_s(i);
+    }
+  } else if (warp == 10) {
+    // dV += P^T dO_i ; dK += dS^T Q_i   (A from TMEM; B read MN-major: N = dh, K = queries)
+    const uint64_t dmn = make_sdesc_sw128(smem_u32(smem), BQ * 128, 1024);  // Q_i / dO_i read MN-major
     for (int i = 0; i < nq; ++i) {
-      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+      mbar_wait(&p_full[i % NB], (i / NB) & 1);
       tc_fence_after();
-      if (lane == 0) {  // dV += P^T dO_i ; dK += dS^T Q_i   (B read MN-major: N = dh, K = queries)
+      if (lane == 0) {
         const int st = i % NS;
-        const uint32_t p_off = C::kOffP + (i & 1) * C::kPBytes, ds_off = C::kOffDS + (i & 1) * C::kPBytes;
         const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
 #pragma unroll
         for (int k = 0; k < BQ / 16; ++k) {
-          umma_bf16_ss(t_dV, sdesc_add(sdesc_add(d16, p_off), k * 32), sdesc_add(sdesc_add(dmn, do_off), k * 2048), C::kIdescKV,
+          umma_bf16_ts(t_dV, t_S + (i % NB) * BQ + packed_col<BQ / 2>(k), sdesc_add(sdesc_add(dmn, do_off), k * 2048), C::kIdescKV,
                        (i > 0 || k > 0));
-          umma_bf16_ss(t_dK, sdesc_add(sdesc_add(d16, ds_off), k * 32), sdesc_add(sdesc_add(dmn, q_off), k * 2048), C::kIdescKV,
+          umma_bf16_ts(t_dK, t_dP + (i % NB) * BQ + packed_col<BQ / 2>(k), sdesc_add(sdesc_add(dmn, q_off), k * 2048), C::kIdescKV,
                        (i > 0 || k > 0));
         }
-        umma_commit(&q_empty[st]);
+        umma_commit(&q_empty[st]);  // frees the Q/dO stage and the TMEM buffers of block i
         if (i == nq - 1) umma_commit(acc_done);
       }
       __syncwarp();
-      if (i + NB < nq) issue_s(i + NB);
     }
   } else {
     const int quad = warp & 3;
@@ -508,13 +520,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         wd[c / 2] = pack_bf16x2(da.x, da.y);
         wd[c / 2 + 1] = pack_bf16x2(db.x, db.y);
       }
-      if (i >= 2) mbar_wait(&q_empty[(i - 2) % NS], ((i - 2) / NS) & 1);  // dV/dK_{i-2} done: P/dS free
-      st_halfrow_sw128(smem + C::kOffP + (i & 1) * C::kPBytes, krow, half, wp);
-      st_halfrow_sw128(smem + C::kOffDS + (i & 1) * C::kPBytes, krow, half, wd);
-      fence_proxy_async_smem();
+      // P^T_i / dS^T_i (bf16 pairs) into this half's OWN columns of the S^T_i / dP^T_i buffers
+      tmem_st16(t_S + (i % NB) * BQ + half * HC + lane_off, wp);
+      tmem_st16(t_dP + (i % NB) * BQ + half * HC + lane_off, wd);
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[i & 1]);
+      if (lane == 0) mbar_arrive(&p_full[i % NB]);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
@@ -550,7 +562,7 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
   // read Q_i/dO_i), so the refill of the stage NS blocks ahead only starts then. The ring must cover
   // that plus the L2/HBM TMA latency (~1-2 us under load), i.e. several block periods.
   constexpr int NSQ = DH == 64 ? 8 : 4;  // dq kernel K/V stages (smem: 192 KB / 224 KB)
-  constexpr int NSK = DH == 64 ? 7 : 2;  // dkdv kernel Q/dO stages (smem-limited at dh 128)
+  constexpr int NSK = DH == 64 ? 8 : 4;  // dkdv kernel Q/dO stages
   using CQ = DqCfg<DH, NSQ>;
   using CK = DkvCfg<DH, NSK>;
   const int d = a.H * DH;
@@ -575,9 +587,9 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
                           : (dbg == 2 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 2>
                                       : (dbg == 3 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 4> : fa_bwd_dq_kernel<DH, NSQ, POLY, 5>));
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CQ::kSmem);
-      kfn<<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
+      kfn<<<dim3(n_dq, a.H), kThreadsDq, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
     } else {
-      fa_bwd_dq_kernel<DH, NSQ, POLY><<<dim3(n_dq, a.H), kThreads, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
+      fa_bwd_dq_kernel<DH, NSQ, POLY><<<dim3(n_dq, a.H), kThreadsDq, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
     }
   }
   if (n_kv > 0) {
@@ -592,7 +604,7 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     (void)once;
     p.blocks = kv_items;
     p.blocks2 = kv_items2;
-    fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreads, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreadsDq, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
   }
 }
 

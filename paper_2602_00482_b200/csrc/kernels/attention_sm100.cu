@@ -27,7 +27,8 @@ namespace ttb {
 
 namespace {
 
-constexpr int kFwdThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax (2 per TMEM quadrant)
+// warp 0 TMA, warp 1 S-MMA issuer, warps 2..9 softmax (2 per TMEM quadrant), warp 10 PV-MMA issuer
+constexpr int kFwdThreads = 352;
 constexpr int kSmxWarps = 8;
 constexpr int kBQ = 128;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -40,14 +41,12 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("ba
 
 template <int DH, int BKV, int NS>
 struct FwdCfg {
-  static constexpr int NB = 3;  // S (TMEM) and P (smem) buffers: the MMA warp runs NB-1 blocks ahead
+  static constexpr int NB = 3;  // S / P TMEM buffers: the S issuer runs NB-1 blocks ahead of the softmax
   static constexpr int kQBytes = kBQ * DH * 2;
   static constexpr int kKVBytes = BKV * DH * 2;           // one K (or V) tile
-  static constexpr int kPBytes = kBQ * BKV * 2;           // one P tile
   static constexpr int kOffK = kQBytes;
   static constexpr int kOffV = kOffK + NS * kKVBytes;
-  static constexpr int kOffP = kOffV + NS * kKVBytes;
-  static constexpr int kOffX = kOffP + NB * kPBytes;   // [2 bufs][2 halves][128 rows] f32: row-max exchange
+  static constexpr int kOffX = kOffV + NS * kKVBytes;  // [2 bufs][2 halves][128 rows] f32: row-max exchange
   static constexpr int kOffBar = kOffX + 2 * 2 * kBQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kOCol = (NB * BKV + DH - 1) / DH * DH;
@@ -153,12 +152,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer
-    // descriptors = one base (smem start) + byte offsets: keeps the single-thread issue path short
-    const uint64_t dK16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);         // K-major tiles
-    const uint64_t dVmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // V read MN-major
-    auto issue_s = [&](int j) {
+    // ------------------------------------------------------------------ S issuer
+    // S_j = Q K_j^T into TMEM buffer j % NB once PV_{j-NB} (which read P_{j-NB} from it) is done.
+    // Two issuing warps (S and PV): an mbarrier wait in an issuing thread costs ~180 clk with MMAs in
+    // flight (tools/umma_probe.cu), so each dependency chain gets its own issuer.
+    const uint64_t dK16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);  // K-major tiles
+    mbar_wait(q_full, 0);
+    for (int j = 0; j < nblk; ++j) {
       const int st = j % NS;
+      if (j >= NB) mbar_wait(&pv_done[(j - NB) % NB], ((j - NB) / NB) & 1);
       mbar_wait(&k_full[st], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
@@ -173,28 +175,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         umma_commit(&k_empty[st]);
       }
       __syncwarp();
-    };
-    mbar_wait(q_full, 0);
-    for (int j = 0; j < NB && j < nblk; ++j) issue_s(j);
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------------ PV issuer
+    // O += P_j V_j with A = P_j from TMEM: keys [h*BKV/2, +BKV/2) as bf16 pairs at columns h*BKV/2 + ...
+    const uint64_t dVmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // V read MN-major
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&p_full[j % NB], (j / NB) & 1);
       mbar_wait(&v_full[j % NS], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
         const int st = j % NS;
-        const uint32_t p_off = C::kOffP + (j % NB) * C::kPBytes;
         const uint32_t v_off = C::kOffV + st * C::kKVBytes;
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {
-          const uint64_t da = sdesc_add(sdesc_add(dK16, p_off), (k / 4) * (kBQ * 128) + (k % 4) * 32);
-          const uint64_t db = sdesc_add(sdesc_add(dVmn, v_off), k * 2048);
-          umma_bf16_ss(tmem_O, da, db, C::kIdescO, (j > 0 || k > 0) ? 1u : 0u);
-        }
+        for (int k = 0; k < BKV / 16; ++k)
+          umma_bf16_ts(tmem_O, tmem_S + (j % NB) * BKV + packed_col<BKV / 2>(k), sdesc_add(sdesc_add(dVmn, v_off), k * 2048),
+                       C::kIdescO,
+                       (j > 0 || k > 0) ? 1u : 0u);
         umma_commit(&v_empty[st]);
         umma_commit(&pv_done[j % NB]);
       }
       __syncwarp();
-      if (j + NB < nblk) issue_s(j + NB);
     }
   } else {
     // ------------------------------------------------------------------ softmax
@@ -253,25 +254,23 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float mb = m_used == -INFINITY ? 0.f : m_used;
       float2 rs2 = make_float2(0.f, 0.f);
       const float2 c22 = make_float2(c2, c2), nmb2 = make_float2(-mb, -mb);
-      // this half's columns start at key half*HC: panel (half*HC)/64, 16B chunk ((half*HC)%64)/8 of
-      // buffer j%NB; the buffer is free since S_j (issued after PV_{j-NB}) has completed
-      uint8_t* pbuf = smem + C::kOffP + (j % NB) * C::kPBytes + ((half * HC) / 64) * (kBQ * 128);
-      const int chunk0 = ((half * HC) % 64) / 8;
+      // P_j (bf16 pairs) into the first HC/2 columns of this half's OWN S_j columns [half*HC, +HC)
+      // (the other half may still be reading its S columns): the A operand of PV_j
+      uint32_t w[HC / 2];
 #pragma unroll
       for (int cch = 0; cch < HC / 8; ++cch) {
-        uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           // paired FP32 (FFMA2 / FADD2): x = s*c - m ; p = 2^x ; row sum += p
           const float2 x = __ffma2_rn(make_float2(s[cch * 8 + 2 * e], s[cch * 8 + 2 * e + 1]), c22, nmb2);
           const float2 pe = e < POLY ? ex2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
           rs2 = __fadd2_rn(rs2, pe);
-          w[e] = pack_bf16x2(pe.x, pe.y);
+          w[cch * 4 + e] = pack_bf16x2(pe.x, pe.y);
         }
-        // 128B swizzle: 16B chunk index XOR (row % 8)
-        uint4* dst = reinterpret_cast<uint4*>(pbuf + rloc * 128 + (((chunk0 + cch) ^ (rloc & 7)) * 16));
-        *dst = make_uint4(w[0], w[1], w[2], w[3]);
       }
+#pragma unroll
+      for (int c = 0; c < HC / 2; c += 16)
+        tmem_st16(tmem_S + (j % NB) * BKV + half * HC + c + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&w[c]));
       const float rs = rs2.x + rs2.y;
       l += rs;
       if (j > 0 && __any_sync(0xffffffff, resc)) {
@@ -287,9 +286,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
           tmem_st16(tmem_O + c + lane_off, r);
         }
-        tmem_st_wait();
       }
-      fence_proxy_async_smem();  // P stores (generic proxy) -> visible to tcgen05.mma (async proxy)
+      tmem_st_wait();  // P (and any O rescale) in TMEM before the PV issuer is released
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j % NB]);

@@ -172,6 +172,14 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, bool a_mn_m
          | ((static_cast<uint32_t>(M) >> 4) << 24);  // m_dim
 }
 
+// TMEM column of the bf16 A-operand k-step k (16 elements = 8 packed columns) when two softmax
+// warps each own HALF columns of a fp32 buffer and pack their bf16 results into the start of their own
+// half: elements [h*HALF, (h+1)*HALF) sit at columns h*HALF + (e - h*HALF)/2.
+template <int HALF>
+__device__ __forceinline__ uint32_t packed_col(int k) {
+  return static_cast<uint32_t>((k * 16 / HALF) * HALF + (k * 16 % HALF) / 2);
+}
+
 // ---------------------------------------------------------------- exp2
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;

@@ -27,7 +27,9 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 constexpr int kQBlock = 64;
-constexpr int kQChunk = 1024;  // query rows per backward work item
+constexpr int kQChunk = 1024;  // query rows per backward work item (mma.sync kernels)
+constexpr int kQChunkPrefix = 4096;  // tcgen05 dK/dV items over prefix rows (span members)
+constexpr int kQChunkOwn = 2048;     // tcgen05 dK/dV items over a member's own rows (causal)
 
 void ck(cudaError_t e, const char* what) { check_cuda(e, what); }
 
@@ -357,17 +359,24 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
                                      int32_t(q), int32_t(std::min<int64_t>(q + kQChunk, end))});
         b.kvit2.insert(b.kvit2.end(), {int32_t(so), 1});
       }
-    for (int64_t kv = 0; kv < b.S; kv += kBwdBlockKV)
-      for (int64_t q = so; q < end; q += kQChunk) {
-        b.kvit128.insert(b.kvit128.end(), {int32_t(kv), int32_t(std::min<int64_t>(kBwdBlockKV, b.S - kv)), int32_t(q),
-                                           int32_t(std::min<int64_t>(q + kQChunk, end))});
-        b.kvit128_2.insert(b.kvit128_2.end(), {int32_t(so), 0});
-      }
     for (int64_t kt = 0; kt < b.seg_len[i]; kt += kBwdBlockKV)
-      for (int64_t q = so + kt; q < end; q += kQChunk) {
+      for (int64_t q = so + kt; q < end; q += kQChunkOwn) {
         b.kvit128.insert(b.kvit128.end(), {int32_t(b.S + so + kt), int32_t(std::min<int64_t>(kBwdBlockKV, b.seg_len[i] - kt)),
-                                           int32_t(q), int32_t(std::min<int64_t>(q + kQChunk, end))});
+                                           int32_t(q), int32_t(std::min<int64_t>(q + kQChunkOwn, end))});
         b.kvit128_2.insert(b.kvit128_2.end(), {int32_t(so), 1});
+      }
+  }
+  // tcgen05 dK/dV items of the shared prefix rows: every query of every member attends them fully, so
+  // one item spans members (fewer items: less per-item fixed cost and fewer red.add passes over the
+  // same prefix dK/dV rows)
+  {
+    int64_t n_rows = 0;
+    for (size_t i = 0; i < b.seg_off.size(); ++i) n_rows = std::max<int64_t>(n_rows, b.seg_off[i] + b.seg_len[i]);
+    for (int64_t kv = 0; kv < b.S; kv += kBwdBlockKV)
+      for (int64_t q = 0; q < n_rows; q += kQChunkPrefix) {
+        b.kvit128.insert(b.kvit128.end(), {int32_t(kv), int32_t(std::min<int64_t>(kBwdBlockKV, b.S - kv)), int32_t(q),
+                                           int32_t(std::min<int64_t>(q + kQChunkPrefix, n_rows))});
+        b.kvit128_2.insert(b.kvit128_2.end(), {0, 0});
       }
   }
   b.o_tok = put(b.tokens.data(), b.tokens.size() * 4);

@@ -110,6 +110,34 @@ int tt_greedy_least_loaded(const int32_t* tokens, const uint64_t* offsets, uint6
                            int32_t cost_mode, int32_t* group_of_seq, uint64_t* group_costs, uint64_t* max_cost,
                            uint64_t* duplicated);
 
+/* ------------------------------------------------------------------ corpus */
+/* A rollout corpus: JSON lines {"seq_id": str, "tokens": [int], "weights": [float]} (weights
+ * optional: 0 on the first "prompt_len" positions when given, else 1). */
+typedef struct tt_corpus tt_corpus;
+/* CorpusSpec; lengths uniform in [lo, hi]. */
+typedef struct tt_corpus_spec {
+  uint64_t num_prompts;
+  uint64_t group_size;
+  uint64_t prompt_len_lo, prompt_len_hi;
+  uint64_t response_len_lo, response_len_hi;
+  double branch_prob;
+  uint64_t vocab_size;
+  uint64_t seed;
+} tt_corpus_spec;
+int tt_corpus_load_jsonl(const char* path, tt_corpus** out);
+/* gen-corpus: deterministic per seed. */
+int tt_corpus_generate(const tt_corpus_spec* spec, tt_corpus** out);
+/* CSR view in, string ids optional (NULL -> "0", "1", ...). */
+int tt_corpus_from_csr(const int32_t* tokens, const uint64_t* offsets, const double* weights, uint64_t n_seqs,
+                       const char* const* seq_ids, tt_corpus** out);
+int tt_corpus_save_jsonl(const tt_corpus* corpus, const char* path);
+int tt_corpus_size(const tt_corpus* corpus, uint64_t* n_seqs, uint64_t* n_tokens);
+/* offsets[n_seqs + 1], tokens[n_tokens], weights[n_tokens] (any may be NULL). */
+int tt_corpus_export(const tt_corpus* corpus, int32_t* tokens, uint64_t* offsets, double* weights);
+/* seq_id of sequence i into buf (NUL-terminated, truncated to buf_len); *needed = strlen + 1. */
+int tt_corpus_seq_id(const tt_corpus* corpus, uint64_t i, char* buf, uint64_t buf_len, uint64_t* needed);
+int tt_corpus_destroy(tt_corpus* corpus);
+
 /* ------------------------------------------------------------------ engine */
 typedef struct tt_engine tt_engine;
 

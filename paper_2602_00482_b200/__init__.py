@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -27,6 +27,7 @@ from . import _native
 __all__ = [
     "ModelConfig", "TokenSequence", "SchedulerConfig", "TrainStepResult", "PrefixTree", "Engine",
     "build_prefix_tree", "lexicographic_sort", "partition_contiguous", "greedy_least_loaded", "POLICIES",
+    "CorpusSpec", "gen_corpus", "load_corpus_jsonl", "save_corpus_jsonl",
 ]
 
 POLICIES = {"as_built": 0, "lexicographic": 1, "subtree_tokens_desc": 2, "subtree_tokens_asc": 3}
@@ -216,6 +217,80 @@ def partition_contiguous(seqs: Sequence[TokenSequence], K: int):
 def greedy_least_loaded(seqs: Sequence[TokenSequence], K: int, cost_model: str = "raw_tokens"):
     """SPEC.md:393-401."""
     return _plan(_native.lib().tt_greedy_least_loaded, seqs, K, 1 if cost_model == "raw_tokens" else 0)
+
+
+# ------------------------------------------------------------------ corpus (SPEC.md:192, 484-501)
+@dataclass
+class CorpusSpec:
+    """[TYPE] CorpusSpec; lengths uniform in [lo, hi]."""
+
+    num_prompts: int = 1
+    group_size: int = 1
+    prompt_len: Tuple[int, int] = (1, 1)
+    response_len: Tuple[int, int] = (1, 1)
+    branch_prob: float = 1.0
+    vocab_size: int = 2
+    seed: int = 0
+
+
+def _corpus_to_seqs(h) -> List[TokenSequence]:
+    L = _native.lib()
+    n, nt = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(L.tt_corpus_size(h, ctypes.byref(n), ctypes.byref(nt)))
+    tok = np.zeros(nt.value, dtype=np.int32)
+    off = np.zeros(n.value + 1, dtype=np.uint64)
+    w = np.zeros(nt.value, dtype=np.float64)
+    _check(L.tt_corpus_export(h, _ptr(tok, ctypes.c_int32), _ptr(off, ctypes.c_uint64), _ptr(w, ctypes.c_double)))
+    out = []
+    buf = ctypes.create_string_buffer(256)
+    need = ctypes.c_uint64()
+    for i in range(n.value):
+        _check(L.tt_corpus_seq_id(h, i, buf, len(buf), ctypes.byref(need)))
+        if need.value > len(buf):
+            buf = ctypes.create_string_buffer(int(need.value))
+            _check(L.tt_corpus_seq_id(h, i, buf, len(buf), ctypes.byref(need)))
+        sid = buf.value.decode()
+        a, b = int(off[i]), int(off[i + 1])
+        # integer ids stay integers (the dense oracle sums in seq_id order, SPEC.md:330); any other
+        # string id maps to its line index and is kept as .name
+        ts = TokenSequence(int(sid) if sid.lstrip("-").isdigit() else i, tok[a:b].copy(), w[a:b].copy())
+        ts.name = sid
+        out.append(ts)
+    return out
+
+
+def _with_corpus(fn):
+    h = ctypes.c_void_p()
+    _check(fn(ctypes.byref(h)))
+    try:
+        return _corpus_to_seqs(h)
+    finally:
+        _native.lib().tt_corpus_destroy(h)
+
+
+def load_corpus_jsonl(path: str) -> List[TokenSequence]:
+    """Corpus JSONL reader: {"seq_id", "tokens", "weights"} per line."""
+    return _with_corpus(lambda out: _native.lib().tt_corpus_load_jsonl(str(path).encode(), out))
+
+
+def gen_corpus(spec: CorpusSpec) -> List[TokenSequence]:
+    """[OP] gen-corpus, deterministic per seed."""
+    c = _native.CorpusSpecC(spec.num_prompts, spec.group_size, spec.prompt_len[0], spec.prompt_len[1],
+                            spec.response_len[0], spec.response_len[1], spec.branch_prob, spec.vocab_size, spec.seed)
+    return _with_corpus(lambda out: _native.lib().tt_corpus_generate(ctypes.byref(c), out))
+
+
+def save_corpus_jsonl(seqs: Sequence[TokenSequence], path: str) -> None:
+    """Corpus JSONL writer (exact double round trip of the weights)."""
+    tok, off, w = _csr(seqs)
+    ids = (ctypes.c_char_p * max(1, len(seqs)))(*[str(getattr(s, "name", s.seq_id)).encode() for s in seqs])
+    h = ctypes.c_void_p()
+    _check(_native.lib().tt_corpus_from_csr(_ptr(tok, ctypes.c_int32), _ptr(off, ctypes.c_uint64),
+                                            _ptr(w, ctypes.c_double), len(seqs), ids, ctypes.byref(h)))
+    try:
+        _check(_native.lib().tt_corpus_save_jsonl(h, str(path).encode()))
+    finally:
+        _native.lib().tt_corpus_destroy(h)
 
 
 class StepPlan:

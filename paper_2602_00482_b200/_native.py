@@ -31,7 +31,21 @@ class StepResultC(c.Structure):
         "num_launches", "peak_hbm_bytes", "h2d_bytes", "d2h_bytes")]
 
 
+class CorpusSpecC(c.Structure):
+    _fields_ = [("num_prompts", u64), ("group_size", u64), ("prompt_len_lo", u64), ("prompt_len_hi", u64),
+                ("response_len_lo", u64), ("response_len_hi", u64), ("branch_prob", f64), ("vocab_size", u64),
+                ("seed", u64)]
+
+
 EXPORTS = {
+    "tt_corpus_load_jsonl": [c.c_char_p, P(vp)],
+    "tt_corpus_generate": [P(CorpusSpecC), P(vp)],
+    "tt_corpus_from_csr": [P(i32), P(u64), P(f64), u64, P(c.c_char_p), P(vp)],
+    "tt_corpus_save_jsonl": [vp, c.c_char_p],
+    "tt_corpus_size": [vp, P(u64), P(u64)],
+    "tt_corpus_export": [vp, P(i32), P(u64), P(f64)],
+    "tt_corpus_seq_id": [vp, u64, c.c_char_p, u64, P(u64)],
+    "tt_corpus_destroy": [vp],
     "tt_tree_build": [P(i32), P(u64), P(f64), u64, P(vp)],
     "tt_tree_destroy": [vp],
     "tt_tree_order_children": [vp, i32],

@@ -1,11 +1,13 @@
 // extern "C" entry points declared in include/treetrain_b200.h. Each maps onto one reference
 // operation (cited per function in the header) and converts exceptions into status codes.
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "capi_internal.h"
+#include "corpus_io.hpp"
 #include "engine.hpp"
 #include "prefix_tree.hpp"
 #include "ttpm.hpp"
@@ -135,6 +137,115 @@ int tt_greedy_least_loaded(const int32_t* tokens, const uint64_t* offsets, uint6
     fill_plan(ttb::greedy_least_loaded(views(tokens, offsets, nullptr, n_seqs), K, cost_mode), n_seqs, group_of_seq,
               group_costs, max_cost, duplicated);
   });
+}
+
+// ------------------------------------------------------------------ corpus
+struct tt_corpus {
+  std::vector<ttb::CorpusSeq> seqs;
+};
+
+int tt_corpus_load_jsonl(const char* path, tt_corpus** out) {
+  return ttb::guarded([&] {
+    need(path, "path");
+    need(out, "out");
+    auto c = std::make_unique<tt_corpus>();
+    c->seqs = ttb::load_corpus_jsonl(path);
+    *out = c.release();
+  });
+}
+
+int tt_corpus_generate(const tt_corpus_spec* spec, tt_corpus** out) {
+  return ttb::guarded([&] {
+    need(spec, "spec");
+    need(out, "out");
+    ttb::CorpusSpec sp;
+    sp.num_prompts = spec->num_prompts;
+    sp.group_size = spec->group_size;
+    sp.prompt_len_lo = spec->prompt_len_lo;
+    sp.prompt_len_hi = spec->prompt_len_hi;
+    sp.response_len_lo = spec->response_len_lo;
+    sp.response_len_hi = spec->response_len_hi;
+    sp.branch_prob = spec->branch_prob;
+    sp.vocab_size = spec->vocab_size;
+    sp.seed = spec->seed;
+    auto c = std::make_unique<tt_corpus>();
+    c->seqs = ttb::gen_corpus(sp);
+    *out = c.release();
+  });
+}
+
+int tt_corpus_from_csr(const int32_t* tokens, const uint64_t* offsets, const double* weights, uint64_t n_seqs,
+                       const char* const* seq_ids, tt_corpus** out) {
+  return ttb::guarded([&] {
+    need(out, "out");
+    if (n_seqs > 0) {
+      need(tokens, "tokens");
+      need(offsets, "offsets");
+    }
+    auto c = std::make_unique<tt_corpus>();
+    c->seqs.resize(n_seqs);
+    for (uint64_t i = 0; i < n_seqs; ++i) {
+      auto& q = c->seqs[i];
+      if (offsets[i + 1] < offsets[i]) throw std::invalid_argument("tt_corpus_from_csr: offsets not ascending");
+      q.seq_id = seq_ids && seq_ids[i] ? std::string(seq_ids[i]) : std::to_string(i);
+      q.tokens.assign(tokens + offsets[i], tokens + offsets[i + 1]);
+      if (weights) q.weights.assign(weights + offsets[i], weights + offsets[i + 1]);
+      else q.weights.assign(q.tokens.size(), 1.0);
+    }
+    *out = c.release();
+  });
+}
+
+int tt_corpus_save_jsonl(const tt_corpus* corpus, const char* path) {
+  return ttb::guarded([&] {
+    need(corpus, "corpus");
+    need(path, "path");
+    ttb::save_corpus_jsonl(path, corpus->seqs);
+  });
+}
+
+int tt_corpus_size(const tt_corpus* corpus, uint64_t* n_seqs, uint64_t* n_tokens) {
+  return ttb::guarded([&] {
+    need(corpus, "corpus");
+    uint64_t t = 0;
+    for (const auto& q : corpus->seqs) t += q.tokens.size();
+    if (n_seqs) *n_seqs = corpus->seqs.size();
+    if (n_tokens) *n_tokens = t;
+  });
+}
+
+int tt_corpus_export(const tt_corpus* corpus, int32_t* tokens, uint64_t* offsets, double* weights) {
+  return ttb::guarded([&] {
+    need(corpus, "corpus");
+    uint64_t o = 0;
+    for (size_t i = 0; i < corpus->seqs.size(); ++i) {
+      const auto& q = corpus->seqs[i];
+      if (offsets) offsets[i] = o;
+      if (tokens) std::memcpy(tokens + o, q.tokens.data(), q.tokens.size() * sizeof(int32_t));
+      if (weights) std::memcpy(weights + o, q.weights.data(), q.weights.size() * sizeof(double));
+      o += q.tokens.size();
+    }
+    if (offsets) offsets[corpus->seqs.size()] = o;
+  });
+}
+
+int tt_corpus_seq_id(const tt_corpus* corpus, uint64_t i, char* buf, uint64_t buf_len, uint64_t* needed) {
+  return ttb::guarded([&] {
+    need(corpus, "corpus");
+    if (i >= corpus->seqs.size()) throw std::invalid_argument("tt_corpus_seq_id: index out of range");
+    const std::string& id = corpus->seqs[i].seq_id;
+    if (needed) *needed = id.size() + 1;
+    if (buf && buf_len > 0) {
+      const size_t n = std::min<size_t>(id.size(), buf_len - 1);
+      std::memcpy(buf, id.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+
+int tt_corpus_destroy(tt_corpus* corpus) {
+  delete corpus;
+  return TT_OK;
 }
 
 // ------------------------------------------------------------------ engine

@@ -48,7 +48,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
                cudaStream_t stream);
 int gemm_choose_splits(int M, int N, int K);
 int gemm_pick_bn(int N, bool b_mn_major);
-int gemm_pick_bn2(int N);
+int gemm_pick_bn2(int M, int N);
 // 2-CTA (cta_group::2) tiles for M >= 256 (default on); 0 forces the single-CTA kernel.
 void gemm_set_2cta(int on);
 void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -655,10 +656,28 @@ bool gemm_use_2cta(int M) {
 }
 
 // 2-CTA tile width: 256 unless its padding waste outweighs the halved per-CTA B traffic
-int gemm_pick_bn2(int N) {
-  const double c256 = static_cast<double>((N + 255) / 256) * 256;
-  const double c128 = static_cast<double>((N + 127) / 128) * 128 * 1.08;
-  return c256 <= c128 ? 256 : 128;
+// 2-CTA tile width from a wave model: time ~ waves x per-tile cost, with a 128-wide pair tile ~25%
+// less efficient per column than a 256-wide one (twice the A re-reads per FLOP, shorter MMAs).
+// Measured (profiles/r1/gemm_shapes_bn2.log): N = 896 at M = 32768 runs 17-22% faster with 256-wide
+// tiles despite 12.5% padding; M = 4864 prefers 128 (76 vs 133 tiles on 74 CTA pairs).
+int gemm_pick_bn2(int M, int N) {
+  static const int force = [] {  // TT_GEMM_BN2: force 128 / 256 (tile-shape experiments only)
+    const char* e = std::getenv("TT_GEMM_BN2");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force == 128 || force == 256) return force;
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long pairs = std::max(1, g_num_sms / 2);
+  const long m_tiles = (M + 255) / 256;
+  auto cost = [&](int bn, double f) {
+    const long tiles = m_tiles * ((N + bn - 1) / bn);
+    return static_cast<double>((tiles + pairs - 1) / pairs) * bn * f;
+  };
+  return cost(256, 1.0) <= cost(128, 1.25) ? 256 : 128;
 }
 
 int gemm_pick_bn(int N, bool b_mn_major) {
@@ -690,7 +709,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
   return launch<BN_, CG_, true, false>(A, B, M, N, K, epi, splits, stream);
   if (gemm_use_2cta(M)) {
     // CTA pairs: 256-row tiles; BN 128 or 256 (each CTA stages a 64-aligned half of B)
-    if (gemm_pick_bn2(N) == 256) {
+    if (gemm_pick_bn2(M, N) == 256) {
       TTB_DISPATCH(256, 2)
     } else {
       TTB_DISPATCH(128, 2)
@@ -714,7 +733,7 @@ int gemm_choose_splits(int M, int N, int K) {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const bool two = gemm_use_2cta(M);
-  const int bn = two ? gemm_pick_bn2(N) : gemm_pick_bn(N, true);
+  const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
   const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);  // per-CTA tiles (a pair counts as 2)
   const int kb = (K + BK - 1) / BK;
   if (tiles >= g_num_sms || kb < 8) return 1;

@@ -374,6 +374,16 @@ def run_b200(args):
     nodes = tree_nodes_of(seqs)
     fl_step = step_flops((V, d, H, L, F), nodes)
     prof_total_ms = sum(v["ms"] for v in prof.values())
+    # ncu-measured DRAM traffic of the dominant GEMM launch (the LM-head logits GEMM), committed under
+    # profiles/ (the live run cannot be profiled without perturbing the timing)
+    traffic, traffic_note = None, None
+    tpath = os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")
+    if os.path.exists(tpath) and args.config == "c2":
+        tj = json.load(open(tpath))
+        kname, kv = next((k, v) for k, v in tj["kernels"].items() if k.startswith("gemm LM-head"))
+        traffic = kv["dram_bytes"]
+        traffic_note = (f"{kname}: {kv['dram_bytes'] / 1e9:.3f} GB DRAM per launch vs "
+                        f"{kv['algorithmic_bytes'] / 1e9:.3f} GB algorithmic (profiles/r1/ncu_traffic.json)")
     line = {
         "metric": METRIC, "value": value, "unit": "rollout tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -388,7 +398,7 @@ def run_b200(args):
                 "includes": "host tree build + schedule/metadata upload (pinned) + execute + loss read"},
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": sust, "unit": "TFLOP/s",
-                     "frac": gemm_tflops / sust if sust else None, "traffic": None,
+                     "frac": gemm_tflops / sust if sust else None, "traffic": traffic, "traffic_note": traffic_note,
                      "kernel": "tcgen05 GEMM (all projection/MLP/LM-head GEMMs of the step)",
                      "peak_source": f"MEASURED_PEAKS.json bf16_tflops_sustained ({src})",
                      "gemm_share_of_step": gm["ms"] / prof_total_ms if prof_total_ms else None},

@@ -46,12 +46,13 @@ struct FwdCfg {
   static constexpr int kKVBytes = BKV * DH * 2;           // one K (or V) tile
   static constexpr int kOffK = kQBytes;
   static constexpr int kOffV = kOffK + NS * kKVBytes;
-  static constexpr int kOffX = kOffV + NS * kKVBytes;  // [2 bufs][2 halves][128 rows] f32: row-max exchange
-  static constexpr int kOffBar = kOffX + 2 * 2 * kBQ * 4;
+  static constexpr int kOffX = kOffV + NS * kKVBytes;  // end-of-row combine: per-half running max and sum
+  static constexpr int kOffBar = kOffX + 4 * kBQ * 4;  // [m0, m1, l0, l1] x 128 rows
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kOCol = (NB * BKV + DH - 1) / DH * DH;
-  static constexpr int kTmemCols = (kOCol + DH) <= 256 ? 256 : 512;
-  static_assert(kOCol + DH <= 512 && NS >= NB, "fwd kernel: TMEM / K-V ring too small");
+  // two O accumulators (one per softmax half, each on its own running max): kOCol, kOCol + DH
+  static constexpr int kTmemCols = (kOCol + 2 * DH) <= 256 ? 256 : 512;
+  static_assert(kOCol + 2 * DH <= 512 && NS >= NB, "fwd kernel: TMEM / K-V ring too small");
   static constexpr uint32_t kIdescS = make_idesc_bf16(128, BKV, false, false);
   static constexpr uint32_t kIdescO = make_idesc_bf16(128, DH, false, true);
 };
@@ -178,7 +179,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else if (warp == 10) {
     // ------------------------------------------------------------------ PV issuer
-    // O += P_j V_j with A = P_j from TMEM: keys [h*BKV/2, +BKV/2) as bf16 pairs at columns h*BKV/2 + ...
+    // O_h += P_j[:, keys of half h] V_j[keys of half h]: each softmax half runs its own max / sum, so its
+    // keys accumulate into their own O (combined once at the end). A = P_j from TMEM (bf16 pairs at
+    // columns h*BKV/2 + ...)
     const uint64_t dVmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);  // V read MN-major
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&p_full[j % NB], (j / NB) & 1);
@@ -188,10 +191,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int st = j % NS;
         const uint32_t v_off = C::kOffV + st * C::kKVBytes;
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k)
-          umma_bf16_ts(tmem_O, tmem_S + (j % NB) * BKV + packed_col<BKV / 2>(k), sdesc_add(sdesc_add(dVmn, v_off), k * 2048),
-                       C::kIdescO,
-                       (j > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < BKV / 16; ++k) {
+          const int hk = k / (BKV / 32), kl = k % (BKV / 32);  // half of the keys, k-step within it
+          umma_bf16_ts(tmem_O + hk * DH, tmem_S + (j % NB) * BKV + packed_col<BKV / 2>(k),
+                       sdesc_add(sdesc_add(dVmn, v_off), k * 2048), C::kIdescO, (j > 0 || kl > 0) ? 1u : 0u);
+        }
         umma_commit(&v_empty[st]);
         umma_commit(&pv_done[j % NB]);
       }
@@ -199,9 +203,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else {
     // ------------------------------------------------------------------ softmax
-    // One query row per TMEM lane; the two warps on a lane quadrant split the BKV columns (half).
-    // The row max is exchanged through smem (double-buffered, 64-thread named barrier per
-    // quadrant); row sums stay partial per half until the end.
+    // One query row per TMEM lane; the two warps on a lane quadrant split the BKV columns (half) and
+    // each keeps its own running max / sum and its own O accumulator (no per-block max exchange);
+    // the halves are combined once at the end.
     const int quad = warp & 3;
     const int half = (warp - 2) / 4;
     const int rloc = quad * 32 + lane;  // row within the tile == TMEM lane
@@ -239,10 +243,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
       for (int i = 3; i + 1 < HC; i += 2) mx = fmax3f(mx, s[i], s[i + 1]);
       if ((HC - 3) % 2) mx = fmaxf(mx, s[HC - 1]);
-      float* xb = xch + (j & 1) * (2 * kBQ);
-      xb[half * kBQ + rloc] = mx;
-      named_bar_sync(bar_id, 64);
-      mx = fmaxf(mx, xb[(1 - half) * kBQ + rloc]);
       const float m_new = fmaxf(m_used, mx * c2);
       const bool resc = m_new > m_used + kRescaleThreshold;
       float corr = 1.f;
@@ -274,17 +274,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       const float rs = rs2.x + rs2.y;
       l += rs;
       if (j > 0 && __any_sync(0xffffffff, resc)) {
-        // O (from PV_{j-1}) must be final before it is rescaled; each warp rescales its half of dh
+        // O_half (from PV_{j-1}) must be final before this warp rescales it
         mbar_wait(&pv_done[(j - 1) % NB], ((j - 1) / NB) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
+        for (int c = 0; c < DH; c += 16) {
           uint32_t r[16];
-          tmem_ld16(tmem_O + c + lane_off, r);
+          tmem_ld16(tmem_O + half * DH + c + lane_off, r);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
-          tmem_st16(tmem_O + c + lane_off, r);
+          tmem_st16(tmem_O + half * DH + c + lane_off, r);
         }
       }
       tmem_st_wait();  // P (and any O rescale) in TMEM before the PV issuer is released
@@ -293,37 +293,48 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (lane == 0) mbar_arrive(&p_full[j % NB]);
     }
     // combine the two partial row sums
-    float* lb = xch + (nblk & 1) * (2 * kBQ);
-    lb[half * kBQ + rloc] = l;
+    // combine the halves: m = max(m0, m1); l = sum_h l_h 2^(m_h - m); O = sum_h O_h 2^(m_h - m) / l
+    float* lb = xch;
+    lb[half * kBQ + rloc] = m_used;
+    lb[(2 + half) * kBQ + rloc] = l;
     named_bar_sync(bar_id, 64);
-    l += lb[(1 - half) * kBQ + rloc];
-    const float m = m_used;
+    const float m_o = lb[(1 - half) * kBQ + rloc], l_o = lb[(3 - half) * kBQ + rloc];
+    const float m0 = half == 0 ? m_used : m_o, m1 = half == 0 ? m_o : m_used;
+    const float l0 = half == 0 ? l : l_o, l1 = half == 0 ? l_o : l;
+    const float m = fmaxf(m0, m1);
+    const float f0 = m0 == -INFINITY ? 0.f : ex2_approx(m0 - m), f1 = m1 == -INFINITY ? 0.f : ex2_approx(m1 - m);
+    const float lt = l0 * f0 + l1 * f1;
     mbar_wait(&pv_done[(nblk - 1) % NB], ((nblk - 1) / NB) & 1);
     tc_fence_after();
-    const float inv_l = 1.f / l;
+    const float inv_l = 1.f / lt;
+    const float g0 = f0 * inv_l, g1 = f1 * inv_l;
     // tcgen05.ld is .sync.aligned: every lane executes it (convergently); only valid rows store.
     const bool row_ok = row < q_end;
     __nv_bfloat16* orow = p.o + static_cast<long>(row) * p.ldo + h * DH;
 #pragma unroll
     for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
-      uint32_t r[16];
+      uint32_t r[16], r1[16];
       tmem_ld16(tmem_O + c + lane_off, r);
+      tmem_ld16(tmem_O + DH + c + lane_off, r1);
       tmem_ld_wait();
       if (row_ok) {
+        float o[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i] = __uint_as_float(r[i]) * g0 + __uint_as_float(r1[i]) * g1;
         uint4 w0, w1;
-        w0.x = pack_bf16x2(__uint_as_float(r[0]) * inv_l, __uint_as_float(r[1]) * inv_l);
-        w0.y = pack_bf16x2(__uint_as_float(r[2]) * inv_l, __uint_as_float(r[3]) * inv_l);
-        w0.z = pack_bf16x2(__uint_as_float(r[4]) * inv_l, __uint_as_float(r[5]) * inv_l);
-        w0.w = pack_bf16x2(__uint_as_float(r[6]) * inv_l, __uint_as_float(r[7]) * inv_l);
-        w1.x = pack_bf16x2(__uint_as_float(r[8]) * inv_l, __uint_as_float(r[9]) * inv_l);
-        w1.y = pack_bf16x2(__uint_as_float(r[10]) * inv_l, __uint_as_float(r[11]) * inv_l);
-        w1.z = pack_bf16x2(__uint_as_float(r[12]) * inv_l, __uint_as_float(r[13]) * inv_l);
-        w1.w = pack_bf16x2(__uint_as_float(r[14]) * inv_l, __uint_as_float(r[15]) * inv_l);
+        w0.x = pack_bf16x2(o[0], o[1]);
+        w0.y = pack_bf16x2(o[2], o[3]);
+        w0.z = pack_bf16x2(o[4], o[5]);
+        w0.w = pack_bf16x2(o[6], o[7]);
+        w1.x = pack_bf16x2(o[8], o[9]);
+        w1.y = pack_bf16x2(o[10], o[11]);
+        w1.z = pack_bf16x2(o[12], o[13]);
+        w1.w = pack_bf16x2(o[14], o[15]);
         *reinterpret_cast<uint4*>(orow + c) = w0;
         *reinterpret_cast<uint4*>(orow + c + 8) = w1;
       }
     }
-    if (half == 0 && row_ok) p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(l)) * 0.6931471805599453f;
+    if (half == 0 && row_ok) p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(lt)) * 0.6931471805599453f;
 
   }
   tc_fence_before();

@@ -169,6 +169,9 @@ void Engine::set_option(const std::string& key, int64_t value) {
   } else if (key == "attn_bwd_impl") {
     if (value != 0 && value != 1) throw std::invalid_argument("attn_bwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
     attn_bwd_impl_ = static_cast<int>(value);
+  } else if (key == "root_batch_tokens") {
+    if (value < 0) throw std::invalid_argument("root_batch_tokens must be >= 0");
+    root_batch_tokens_ = value;
   } else if (key == "ce_stats") {
     // 1: LM-head GEMM epilogue emits per-32-column softmax statistics, CE reads logits once
     // (default); 0: CE does both passes over the logits row itself
@@ -349,19 +352,19 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
     }
     for (int64_t kv = 0; kv < b.S; kv += 64)  // prefix rows: every query of the member attends
       for (int64_t q = so; q < end; q += kQChunk) {
-        b.kvit.insert(b.kvit.end(), {int32_t(kv), int32_t(std::min<int64_t>(64, b.S - kv)), int32_t(q),
+        b.kvit.insert(b.kvit.end(), {int32_t(b.pbase + kv), int32_t(std::min<int64_t>(64, b.S - kv)), int32_t(q),
                                      int32_t(std::min<int64_t>(q + kQChunk, end))});
         b.kvit2.insert(b.kvit2.end(), {int32_t(so), 0});
       }
     for (int64_t kt = 0; kt < b.seg_len[i]; kt += 64)  // own rows: queries at or after the key
       for (int64_t q = so + kt; q < end; q += kQChunk) {
-        b.kvit.insert(b.kvit.end(), {int32_t(b.S + so + kt), int32_t(std::min<int64_t>(64, b.seg_len[i] - kt)),
+        b.kvit.insert(b.kvit.end(), {int32_t(b.row0() + so + kt), int32_t(std::min<int64_t>(64, b.seg_len[i] - kt)),
                                      int32_t(q), int32_t(std::min<int64_t>(q + kQChunk, end))});
         b.kvit2.insert(b.kvit2.end(), {int32_t(so), 1});
       }
     for (int64_t kt = 0; kt < b.seg_len[i]; kt += kBwdBlockKV)
       for (int64_t q = so + kt; q < end; q += kQChunkOwn) {
-        b.kvit128.insert(b.kvit128.end(), {int32_t(b.S + so + kt), int32_t(std::min<int64_t>(kBwdBlockKV, b.seg_len[i] - kt)),
+        b.kvit128.insert(b.kvit128.end(), {int32_t(b.row0() + so + kt), int32_t(std::min<int64_t>(kBwdBlockKV, b.seg_len[i] - kt)),
                                            int32_t(q), int32_t(std::min<int64_t>(q + kQChunkOwn, end))});
         b.kvit128_2.insert(b.kvit128_2.end(), {int32_t(so), 1});
       }
@@ -374,7 +377,7 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
     for (size_t i = 0; i < b.seg_off.size(); ++i) n_rows = std::max<int64_t>(n_rows, b.seg_off[i] + b.seg_len[i]);
     for (int64_t kv = 0; kv < b.S; kv += kBwdBlockKV)
       for (int64_t q = 0; q < n_rows; q += kQChunkPrefix) {
-        b.kvit128.insert(b.kvit128.end(), {int32_t(kv), int32_t(std::min<int64_t>(kBwdBlockKV, b.S - kv)), int32_t(q),
+        b.kvit128.insert(b.kvit128.end(), {int32_t(b.pbase + kv), int32_t(std::min<int64_t>(kBwdBlockKV, b.S - kv)), int32_t(q),
                                            int32_t(std::min<int64_t>(q + kQChunkPrefix, n_rows))});
         b.kvit128_2.insert(b.kvit128_2.end(), {0, 0});
       }
@@ -518,8 +521,8 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       e.mode = EPI_STORE_BF16;
       e.split_w = d;
       e.out[0] = q;
-      e.out[1] = K + b.S * d_;
-      e.out[2] = Vv + b.S * d_;
+      e.out[1] = K + b.row0() * d_;
+      e.out[2] = Vv + b.row0() * d_;
       e.ldo[0] = e.ldo[1] = e.ldo[2] = d;
       gemm(op(n1, d, false), op(wqkv_[l], 3 * d, true), n, 3 * d, d, e, 1);
     }
@@ -537,6 +540,8 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       a.H = static_cast<int>(H_);
       a.dh = static_cast<int>(dh_);
       a.S = static_cast<int>(b.S);
+      a.pbase = static_cast<int>(b.pbase);
+      a.r0 = static_cast<int>(b.row0());
       a.scale = scale;
       if (attn_fwd_impl_ == 1) {
         a.qblocks = meta<int4>(b.o_qblk128);
@@ -786,6 +791,8 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       a.H = static_cast<int>(H_);
       a.dh = static_cast<int>(dh_);
       a.S = static_cast<int>(b.S);
+      a.pbase = static_cast<int>(b.pbase);
+      a.r0 = static_cast<int>(b.row0());
       a.items = meta<int4>(b.o_kvit);
       a.items2 = meta<int2>(b.o_kvit2);
       a.nitems = static_cast<int>(b.kvit.size() / 4);
@@ -807,7 +814,7 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
     }
     // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
     tag("k_pack_dqkv");
-    run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.S * d_, dV + b.S * d_, dqkv, n, d, stream_); });
+    run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
     {  // dW_{q,k,v} += normed1^T [dq | dk | dv]  (model.hpp:610-612)
       EpiParams e;
       e.mode = EPI_ADD_F32;
@@ -909,7 +916,8 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
   };
   std::string& trace = plan->trace;
   const uint64_t budget = (sc.batch_token_budget == 0 && sc.sibling_batch)
-                              ? auto_batch_budget(tree.nodes[0].max_path_below)
+                              ? auto_batch_budget(tree.nodes[0].max_path_below +
+                                                  static_cast<uint64_t>(std::max<int64_t>(root_batch_tokens_, 0)))
                               : sc.batch_token_budget;
   // chunk [a, b) of node u (S = the node's start): a chained sub-segment (chunked backward,
   // SPEC.md:234-251); the loss pairs of rows in [a, b) move with it
@@ -946,25 +954,71 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
   auto short_leaf = [&](int32_t c) {
     return tree.nodes[c].children.empty() && (chunk == 0 || tree.nodes[c].tokens.size() <= chunk);
   };
+  // one or more batches of consecutive short-leaf children of `parent` (sibling batching), pushed and
+  // popped in turn; prefix rows [pbase, pbase + S), own rows from R0 (< 0: right after the prefix)
+  auto leaf_runs = [&](const std::vector<int32_t>& ch, size_t i, size_t i_end, int64_t S, int64_t pbase,
+                       int64_t R0) {
+    while (i < i_end) {
+      std::vector<int32_t> run_nodes = {ch[i]};
+      uint64_t tok = tree.nodes[ch[i]].tokens.size();
+      size_t j = i + 1;
+      while (j < i_end && (budget == 0 || tok + tree.nodes[ch[j]].tokens.size() <= budget)) {
+        tok += tree.nodes[ch[j]].tokens.size();
+        run_nodes.push_back(ch[j++]);
+      }
+      const int bi = make_batch(run_nodes, S);
+      batches[bi].leaf_batch = true;
+      batches[bi].pbase = pbase;
+      batches[bi].R0 = R0;
+      ops.push_back({bi, OP_FWD, 0});
+      ops.push_back({bi, OP_BWD, 0});
+      for (int32_t m : run_nodes) trace += "PUSH " + std::to_string(pid[m]) + "\nPOP " + std::to_string(pid[m]) + "\n";
+      i = j;
+    }
+  };
+  // a forest root that can join a multi-root batch: unchunked, with children that are all short leaves
+  auto root_groupable = [&](int32_t c) {
+    const auto& nd = tree.nodes[c];
+    if (nd.children.empty() || (chunk != 0 && nd.tokens.size() > chunk)) return false;
+    for (int32_t g : nd.children)
+      if (!short_leaf(g)) return false;
+    return true;
+  };
   std::function<void(int32_t, int64_t)> visit = [&](int32_t u, int64_t S) {
     const auto& ch = tree.nodes[u].children;
     size_t i = 0;
     while (i < ch.size()) {
       const int32_t c = ch[i];
       const int64_t len = static_cast<int64_t>(tree.nodes[c].tokens.size());
-      if (sc.sibling_batch && short_leaf(c)) {
-        std::vector<int32_t> run_nodes = {c};
-        uint64_t tok = tree.nodes[c].tokens.size();
+      if (u == 0 && S == 0 && sc.sibling_batch && root_batch_tokens_ > 0 && root_groupable(c)) {
+        // multi-root batch: the prompts of several trees share one push (larger GEMM M, fewer
+        // launches); each root's leaf batches then see only that root's rows as their prefix
+        std::vector<int32_t> roots = {c};
+        int64_t tok = len;
         size_t j = i + 1;
-        while (j < ch.size() && short_leaf(ch[j]) && (budget == 0 || tok + tree.nodes[ch[j]].tokens.size() <= budget)) {
-          tok += tree.nodes[ch[j]].tokens.size();
-          run_nodes.push_back(ch[j++]);
+        while (j < ch.size() && root_groupable(ch[j]) &&
+               tok + static_cast<int64_t>(tree.nodes[ch[j]].tokens.size()) <= root_batch_tokens_) {
+          tok += static_cast<int64_t>(tree.nodes[ch[j]].tokens.size());
+          roots.push_back(ch[j++]);
         }
-        const int bi = make_batch(run_nodes, S);
-        batches[bi].leaf_batch = true;
+        const int bi = make_batch(roots, 0);
+        const int64_t n_roots = batches[bi].n;
         ops.push_back({bi, OP_FWD, 0});
+        int64_t off = 0;
+        for (int32_t r : roots) {
+          const int64_t rl = static_cast<int64_t>(tree.nodes[r].tokens.size());
+          const auto& rch = tree.nodes[r].children;
+          trace += "PUSH " + std::to_string(pid[r]) + "\n";
+          leaf_runs(rch, 0, rch.size(), rl, off, n_roots);
+          trace += "POP " + std::to_string(pid[r]) + "\n";
+          off += rl;
+        }
         ops.push_back({bi, OP_BWD, 0});
-        for (int32_t m : run_nodes) trace += "PUSH " + std::to_string(pid[m]) + "\nPOP " + std::to_string(pid[m]) + "\n";
+        i = j;
+      } else if (sc.sibling_batch && short_leaf(c)) {
+        size_t j = i + 1;
+        while (j < ch.size() && short_leaf(ch[j])) ++j;
+        leaf_runs(ch, i, j, S, 0, -1);
         i = j;
       } else if (chunk == 0 || static_cast<uint64_t>(len) <= chunk) {
         const int bi = make_batch({c}, S);
@@ -1004,11 +1058,11 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
     Batch& b = batches[op.b];
     const size_t sz = align_up(layout(b.n).total);
     if (op.code != OP_BWD) {
-      plan->rows = std::max<int64_t>(plan->rows, b.S + b.n);
+      plan->rows = std::max<int64_t>(plan->rows, b.row0() + b.n);
       plan->max_n = std::max<int64_t>(plan->max_n, b.n);
       plan->max_loss = std::max<int64_t>(plan->max_loss, static_cast<int64_t>(b.loss_rows.size()));
       // live KV (ledger semantics): childless leaves skip KV storage with leaf_kv_skip
-      const uint64_t kv = static_cast<uint64_t>(b.S) + ((sc.leaf_kv_skip && b.leaf_batch) ? 0 : b.n);
+      const uint64_t kv = static_cast<uint64_t>(b.row0()) + ((sc.leaf_kv_skip && b.leaf_batch) ? 0 : b.n);
       peak_kv = std::max(peak_kv, kv);
     }
     switch (op.code) {

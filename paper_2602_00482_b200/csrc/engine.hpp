@@ -44,6 +44,10 @@ struct DevBuf {
 // the prefix rows [0, S). Members are laid out contiguously on rows [S, S+n).
 struct Batch {
   int64_t S = 0, n = 0;
+  // stack rows: the prefix occupies [pbase, pbase + S), the batch's own rows start at row0() (= S
+  // unless set: members of a multi-root batch keep their children's prefix at their own rows)
+  int64_t pbase = 0, R0 = -1;
+  int64_t row0() const { return R0 < 0 ? S : R0; }
   std::vector<int32_t> nodes;
   std::vector<int64_t> seg_off, seg_len;
   // host-built metadata (uploaded once per step)
@@ -221,6 +225,9 @@ class Engine {
   int attn_fwd_impl_ = 1;
   int attn_bwd_impl_ = 1;
   bool ce_stats_ = true;
+  // multi-root batching: consecutive forest roots whose children are all short leaves are pushed as
+  // ONE batch of up to this many tokens (0 = off); each root's leaves attend to its own rows
+  int64_t root_batch_tokens_ = 4096;
   KStats kstats_;
   struct Pending {
     KClass cls;

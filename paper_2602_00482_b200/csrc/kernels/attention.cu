@@ -94,12 +94,12 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(AttnFwdArgs a) {
 
   auto kv_block = [&](int b, long& row0, int& valid, int& kt0) {
     if (b < n_pre) {
-      row0 = static_cast<long>(b) * kBK;
+      row0 = static_cast<long>(a.pbase) + static_cast<long>(b) * kBK;
       valid = min(kBK, S - b * kBK);
       kt0 = -1;
     } else {
       const int ob = b - n_pre;
-      row0 = static_cast<long>(S) + seg_off + ob * kBK;
+      row0 = static_cast<long>(a.r0 < 0 ? S : a.r0) + seg_off + ob * kBK;
       valid = min(kBK, own_rows - ob * kBK);
       kt0 = ob * kBK;
     }
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(AttnBwdArgs a) {
   const int kv_valid = it.y, q_lo = it.z, q_hi = it.w;
   const int seg_off = it2.x;
   const bool own = it2.y != 0;
-  const int kt_base = own ? static_cast<int>(kv0 - a.S - seg_off) : 0;  // local key index of row 0
+  const int kt_base = own ? static_cast<int>(kv0 - (a.r0 < 0 ? a.S : a.r0) - seg_off) : 0;  // local key of row 0
   const int h = blockIdx.y;
   const long col0 = static_cast<long>(h) * DH;
   const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;

@@ -16,6 +16,8 @@ struct AttnFwdArgs {
   long ldo = 0;
   float* lse = nullptr;  // [H x n], natural log
   int n = 0, H = 0, dh = 0, S = 0;
+  // stack rows: the prefix is rows [pbase, pbase + S), the batch's own rows start at r0 (< 0: r0 = S)
+  int pbase = 0, r0 = -1;
   const int4* qblocks = nullptr;
   int nqb = 0;
   float scale = 1.0f;
@@ -43,6 +45,7 @@ struct AttnBwdArgs {
   const int4* items = nullptr;
   const int2* items2 = nullptr;
   int nitems = 0;
+  int pbase = 0, r0 = -1;  // as in AttnFwdArgs (the dK/dV items carry absolute rows already)
   float scale = 1.0f;
 };
 

@@ -78,6 +78,7 @@ struct BwdParams {
   float* dv;
   long lddkv;
   int n, S, H;
+  int pbase, r0;        // prefix rows [pbase, pbase + S); own rows from r0
   const int4* blocks;   // dq: {q_start, q_end, seg_off, 0}; dkdv: {kv_row0, kv_rows, q_lo, q_hi}
   const int2* blocks2;  // dkdv: {seg_off, is_own}
   float scale, scale_log2;
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
   const int n_pre = (S + BKV - 1) / BKV;
   const int own_rows = q_end - seg_off;
   const int nblk = n_pre + (own_rows + BKV - 1) / BKV;
-  auto kv_row0 = [&](int j) { return j < n_pre ? j * BKV : S + seg_off + (j - n_pre) * BKV; };
+  auto kv_row0 = [&](int j) { return j < n_pre ? p.pbase + j * BKV : p.r0 + seg_off + (j - n_pre) * BKV; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_q);
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
   const int kv0 = it.x, kv_rows = it.y, q_lo = it.z, q_hi = it.w;
   const int seg_off = it2.x;
   const bool own = it2.y != 0;
-  const int kt_base = own ? kv0 - p.S - seg_off : 0;
+  const int kt_base = own ? kv0 - p.r0 - seg_off : 0;
   const int h = blockIdx.y;
   const int nq = (q_hi - q_lo + BQ - 1) / BQ;
 
@@ -566,7 +567,8 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
   using CQ = DqCfg<DH, NSQ>;
   using CK = DkvCfg<DH, NSK>;
   const int d = a.H * DH;
-  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, dq_blocks, nullptr, a.scale,
+  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0,
+              dq_blocks, nullptr, a.scale,
               a.scale * kLog2e};
   if (n_dq > 0) {
     CUtensorMap tq, tdo, tk, tv;
@@ -618,9 +620,20 @@ int attn_debug_trace(long long* host, int n) {
 void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                     const int2* kv_items2, int n_kv, cudaStream_t stream) {
   attn_bwd_pre(a, stream);
-  // exponentials stay on MUFU here (measured: the FMA-pipe polynomial only pays in the forward)
-  if (a.dh == 64) return launch_bwd<64, 0>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
-  if (a.dh == 128) return launch_bwd<128, 0>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
+  // TT_ATTN_BWD_POLY: exponential pairs (of 4) on the FMA pipe (timing experiments)
+  static const int bpoly = [] {
+    const char* e = std::getenv("TT_ATTN_BWD_POLY");
+    return e ? std::atoi(e) : 0;
+  }();
+#define TT_BWD(P)                                                                                          \
+  if (a.dh == 64) return launch_bwd<64, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream); \
+  if (a.dh == 128) return launch_bwd<128, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
+  switch (bpoly) {
+    case 1: TT_BWD(1) break;
+    case 2: TT_BWD(2) break;
+    default: TT_BWD(0) break;
+  }
+#undef TT_BWD
   throw std::invalid_argument("attention: head_dim must be 64 or 128");
 }
 

@@ -62,6 +62,7 @@ struct FwdParams {
   long ldo;
   float* lse;
   int n, S, H;
+  int pbase, r0;  // prefix rows [pbase, pbase + S); own rows from r0
   const int4* qblocks;
   float scale_log2;
 };
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int own_rows = q_end - seg_off;
   const int n_own = (own_rows + BKV - 1) / BKV;
   const int nblk = n_pre + n_own;
-  auto kv_row0 = [&](int j) { return j < n_pre ? j * BKV : S + seg_off + (j - n_pre) * BKV; };
+  auto kv_row0 = [&](int j) { return j < n_pre ? p.pbase + j * BKV : p.r0 + seg_off + (j - n_pre) * BKV; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_q);
@@ -354,7 +355,7 @@ void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
                                            C::kSmem),
                       true);
   (void)once;
-  FwdParams p{a.o, a.ldo, a.lse, a.n, a.S, a.H, a.qblocks, a.scale * kLog2e};
+  FwdParams p{a.o, a.ldo, a.lse, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, a.qblocks, a.scale * kLog2e};
   dim3 grid(a.nqb, a.H);
   fa_fwd_kernel<DH, BKV, NS, POLY><<<grid, kFwdThreads, C::kSmem, stream>>>(tq, tk, tv, p);
 }

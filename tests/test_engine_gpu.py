@@ -304,3 +304,21 @@ def test_c4_shape_7b_tree_equals_flat():
     # BASELINE configs[3] model (7B shape) on one rollout group
     seqs = O.grouped_corpus(1, 4, 512, 768, 152064, 23)
     _shape_property((152064, 3584, 28, 28, 18944, 1300), seqs)
+
+
+@pytest.mark.parametrize("root_tokens", [0, 300, 4096])
+@pytest.mark.parametrize("fwd_impl,bwd_impl", [(1, 1), (0, 0)])
+def test_multi_root_batching_vs_oracle(root_tokens, fwd_impl, bwd_impl):
+    # several prompt trees (forest roots whose children are all leaves) pushed as one multi-root
+    # batch; each root's leaves attend to that root's rows only (prefix row base != 0). 0 = off.
+    cfg, flat, eng = make(SMALL, 31)
+    eng.set_option("root_batch_tokens", root_tokens)
+    eng.set_option("attn_fwd_impl", fwd_impl)
+    eng.set_option("attn_bwd_impl", bwd_impl)
+    seqs = O.grouped_corpus(5, 3, 90, 70, cfg.vocab_size, 32, weight_jitter=True)
+    r, _ = tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
+    tree = tt.build_prefix_tree([tt.TokenSequence(s.seq_id, s.tokens, s.weights) for s in seqs])
+    plan = eng.plan(tree, tt.SchedulerConfig())
+    assert plan.trace() == tree.dfs_trace()  # the logical DFS trace is unchanged by batching
+    if root_tokens >= 5 * 90:
+        assert r.num_batches < 5 * 2  # prompts share pushes

@@ -46,11 +46,15 @@ struct Cfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BNC * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (160 * 1024) / kStageBytes > 8 ? 8 : (160 * 1024) / kStageBytes;
+  // epilogue staging slots per warp: 2 (a store drains while the next chunk is staged), 1 for the
+  // single-CTA 256-wide tile, whose 48 KB operand stages would otherwise drop to 3
+  static constexpr int kSlots = (CG == 1 && BN == 256) ? 1 : 2;
+  static constexpr int kStageBudget = 227 * 1024 - kEpiWarps * kSlots * 4096 - 2048;
+  static constexpr int kStages = kStageBudget / kStageBytes > 8 ? 8 : kStageBudget / kStageBytes;
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;  // two accumulator slots (power of 2)
   static constexpr int kOffBar = kStages * kStageBytes;
-  static constexpr int kOffStage = kOffBar + 1024;  // epilogue staging: kEpiWarps x 2 slots x 4 KB
-  static constexpr int kSmem = kOffStage + kEpiWarps * 2 * 4096 + 1024 /*align*/;
+  static constexpr int kOffStage = kOffBar + 1024;  // epilogue staging: kEpiWarps x kSlots x 4 KB
+  static constexpr int kSmem = kOffStage + kEpiWarps * kSlots * 4096 + 1024 /*align*/;
   static_assert(kSmem <= 227 * 1024, "GEMM smem budget");
   static_assert(BNC % 64 == 0 || CG == 1, "2-CTA MN-major B needs 64-column halves");
 };
@@ -179,7 +183,8 @@ __device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* 
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -449,7 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int CW = BN / 2;
     constexpr int NCH = CW / 32;
     const int ew = warp - 2;
-    uint8_t* stg = smem + C::kOffStage + ew * 8192;
+    uint8_t* stg = smem + C::kOffStage + ew * (C::kSlots * 4096);
     uint64_t* wld = ld_bar + 2 * ew;
     const int mode = epi.mode;
     const bool need_ld = mode == EPI_RESID_F32 || mode == EPI_DSILU;
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int ch = 0; ch < NCH; ++ch) {
         const int n0 = n_base + ch * 32;
         const bool active = n0 < N;  // warp-uniform
-        const int slot = gc & 1;
+        const int slot = C::kSlots == 2 ? static_cast<int>(gc & 1) : 0;
         uint8_t* buf = stg + slot * 4096;
         int blk = 0, xc = n0;
         if (epi.split_w > 0) {
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           xc = n0 - blk * epi.split_w;
         }
         if (active) {
-          if (lane == 0) bulk_wait_read1();  // the store issued from this slot two chunks ago has read it
+          if (lane == 0) bulk_wait_read<C::kSlots - 1>();  // the store that last used this slot has read it
           __syncwarp();
           if (need_ld && lane == 0) {
             mbar_arrive_expect_tx(&wld[slot], ld_bytes);
@@ -648,11 +653,24 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
 int g_gemm_2cta = 1;
 void gemm_set_2cta(int on) { g_gemm_2cta = on; }
 
-// CTA pairs (256-row tiles) unless padding M to 256 wastes more than ~5% (e.g. M = 896)
-bool gemm_use_2cta(int M) {
+// CTA pairs (256-row tiles) unless padding M to 256 wastes more than ~5% (e.g. M = 896); up to 15%
+// when the GEMM has many waves of pair tiles anyway (e.g. the LM-head dW: 896 x 151936), where the
+// pair's halved operand traffic outweighs the padding (profiles/r1: 0.556 -> 0.513 ms).
+bool gemm_use_2cta(int M, int N) {
   if (!g_gemm_2cta || M < 256) return false;
-  const int padded = (M + 255) / 256 * 256;
-  return (padded - M) * 20 <= M;
+  static const int waste_pct = [] {  // TT_GEMM_2CTA_WASTE: allowed M padding in % (experiments)
+    const char* e = std::getenv("TT_GEMM_2CTA_WASTE");
+    return e ? std::atoi(e) : 5;
+  }();
+  const long padded = (M + 255) / 256 * 256;
+  if ((padded - M) * 100 <= static_cast<long>(M) * waste_pct) return true;
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long pair_tiles = (padded / 256) * ((N + 255) / 256);
+  return (padded - M) * 100 <= static_cast<long>(M) * 15 && pair_tiles >= 4L * (g_num_sms / 2);
 }
 
 // 2-CTA tile width: 256 unless its padding waste outweighs the halved per-CTA B traffic
@@ -707,7 +725,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
   if (!amn && !bmn) return launch<BN_, CG_, false, false>(A, B, M, N, K, epi, splits, stream); \
   if (amn && bmn) return launch<BN_, CG_, true, true>(A, B, M, N, K, epi, splits, stream);     \
   return launch<BN_, CG_, true, false>(A, B, M, N, K, epi, splits, stream);
-  if (gemm_use_2cta(M)) {
+  if (gemm_use_2cta(M, N)) {
     // CTA pairs: 256-row tiles; BN 128 or 256 (each CTA stages a 64-aligned half of B)
     if (gemm_pick_bn2(M, N) == 256) {
       TTB_DISPATCH(256, 2)
@@ -732,7 +750,7 @@ int gemm_choose_splits(int M, int N, int K) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const bool two = gemm_use_2cta(M);
+  const bool two = gemm_use_2cta(M, N);
   const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
   const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);  // per-CTA tiles (a pair counts as 2)
   const int kb = (K + BK - 1) / BK;

@@ -752,12 +752,31 @@ int gemm_choose_splits(int M, int N, int K) {
   }
   const bool two = gemm_use_2cta(M, N);
   const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
-  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);  // per-CTA tiles (a pair counts as 2)
+  // Time model: waves of (tile, K/s) items at ~9 TFLOP/s per SM, plus the fp32 reduce-add of every
+  // split's partial output through L2 (~2.5 TB/s). Split only when the tiles alone leave units idle
+  // (e.g. 49 tiles on 148 SMs: 3 splits = one wave, 4 splits = 1.3 waves); never for outputs whose
+  // reduce traffic dominates (the LM-head dW: 896 x 151936 fp32).
+  const long units = two ? g_num_sms / 2 : g_num_sms;
+  const long tiles = (two ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM) * static_cast<long>((N + bn - 1) / bn);
   const int kb = (K + BK - 1) / BK;
-  if (tiles >= g_num_sms || kb < 8) return 1;
-  int s = (g_num_sms + tiles - 1) / tiles;
-  if (s > kb / 4) s = kb / 4;
-  return s < 1 ? 1 : s;
+  if (kb < 8 || tiles >= units) return 1;
+  const double unit_rate = (two ? 2.0 : 1.0) * 9e12;
+  const double tile_flops = 2.0 * (two ? 2 * BM : BM) * bn * static_cast<double>(K);
+  auto cost = [&](int sp) {
+    const double waves = static_cast<double>((tiles * sp + units - 1) / units);
+    const double red = sp > 1 ? sp * static_cast<double>(M) * N * 4.0 / 2.5e12 : 0.0;
+    return waves * tile_flops / sp / unit_rate + red;
+  };
+  int best_s = 1;
+  double best = cost(1);
+  for (int sp = 2; sp <= 16 && sp <= kb / 4; ++sp) {
+    const double c = cost(sp);
+    if (c < best * 0.98) {  // a split must buy a clear win
+      best = c;
+      best_s = sp;
+    }
+  }
+  return best_s;
 }
 
 }  // namespace ttb

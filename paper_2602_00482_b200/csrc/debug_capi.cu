@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "capi_internal.h"
@@ -95,9 +96,18 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
       }
     };
     const int d = H * dh;
+    // TT_ATTN_NSEG (timing experiments): the n queries form nseg equal sibling segments over the shared
+    // prefix, with the engine's work-item chunking (tcgen05 path) — the c2 leaf-batch shape
+    static const int nseg = [] {
+      const char* e = std::getenv("TT_ATTN_NSEG");
+      return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    const int seg = (n + nseg - 1) / nseg;
     std::vector<int> q64, q128, it, it2;
     for (int qs = 0; qs < n; qs += 64) q64.insert(q64.end(), {qs, std::min(qs + 64, n), 0, 0});
-    for (int qs = 0; qs < n; qs += 128) q128.insert(q128.end(), {qs, std::min(qs + 128, n), 0, 0});
+    for (int so = 0; so < n; so += seg)
+      for (int qs = so; qs < std::min(n, so + seg); qs += 128)
+        q128.insert(q128.end(), {qs, std::min({qs + 128, so + seg, n}), so, 0});
     for (int kv = 0; kv < S; kv += 64) {
       it.insert(it.end(), {kv, std::min(64, S - kv), 0, n});
       it2.insert(it2.end(), {0, 0});
@@ -164,13 +174,19 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
       a.scale = scale;
       if (impl == 1) {
         std::vector<int> k128, k128b;
-        for (int kv = 0; kv < S; kv += 128) {
-          k128.insert(k128.end(), {kv, std::min(128, S - kv), 0, n});
-          k128b.insert(k128b.end(), {0, 0});
-        }
-        for (int kt = 0; kt < n; kt += 128) {
-          k128.insert(k128.end(), {S + kt, std::min(128, n - kt), kt, n});
-          k128b.insert(k128b.end(), {0, 1});
+        const int chunk_pre = nseg > 1 ? 4096 : n, chunk_own = nseg > 1 ? 2048 : n;  // engine.cpp kQChunk*
+        for (int kv = 0; kv < S; kv += 128)
+          for (int q0 = 0; q0 < n; q0 += chunk_pre) {
+            k128.insert(k128.end(), {kv, std::min(128, S - kv), q0, std::min(n, q0 + chunk_pre)});
+            k128b.insert(k128b.end(), {0, 0});
+          }
+        for (int so = 0; so < n; so += seg) {
+          const int end = std::min(n, so + seg);
+          for (int kt = 0; kt < end - so; kt += 128)
+            for (int q0 = so + kt; q0 < end; q0 += chunk_own) {
+              k128.insert(k128.end(), {S + so + kt, std::min(128, end - so - kt), q0, std::min(end, q0 + chunk_own)});
+              k128b.insert(k128b.end(), {so, 1});
+            }
         }
         void *dk128 = up(k128), *dk128b = up(k128b);
         timed([&] {

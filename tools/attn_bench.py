@@ -43,7 +43,9 @@ def main():
                                  dh, rows, iters, ctypes.byref(ms)) == 0, lib.tt_last_error()
         return ms.value
 
-    ctx = n * S + n * (n + 1) / 2
+    nseg = int(os.environ.get("TT_ATTN_NSEG", "1"))  # sibling segments sharing the prefix (c2: 16)
+    seg = (n + nseg - 1) // nseg
+    ctx = n * S + sum(m * (m + 1) / 2 for m in [min(seg, n - i) for i in range(0, n, seg)])
     for name, fn, impl, fl in (("fwd", fwd, impl_f, 4.0 * d * ctx), ("bwd", bwd, impl_b, 8.0 * d * ctx)):
         t = fn(impl, iters=10)
         print(f"attn {name} impl={impl} n={n} S={S} H={H} dh={dh}: {t:.3f} ms/launch, "

@@ -53,5 +53,7 @@ int gemm_pick_bn2(int M, int N);
 void gemm_set_2cta(int on);
 void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
+void make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
+                      uint32_t box_inner, uint32_t box_outer);
 
 }  // namespace ttb

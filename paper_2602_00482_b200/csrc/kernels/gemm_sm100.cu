@@ -202,16 +202,30 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
   switch (epi.mode) {
     case EPI_STORE_F32_STATS:
       if (row < M) {
-        // per-row (max, sum exp) of this 32-column group (columns >= N excluded)
-        float mx = -INFINITY;
+        // per-row (max, sum exp) of this 32-column group (columns >= N excluded): 3-input max, then
+        // 2^(v log2e - mx log2e) as one FFMA + MUFU per element, paired adds
+        constexpr float kL2e = 1.4426950408889634f;
+        float mx;
+        if (n0 + 32 <= N) {
+          mx = fmax3f(v[0], v[1], v[2]);
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (n0 + i < N) mx = fmaxf(mx, v[i]);
-        float sum = 0.f;
+          for (int i = 3; i < 31; i += 2) mx = fmax3f(mx, v[i], v[i + 1]);
+          mx = fmaxf(mx, v[31]);
+        } else {
+          mx = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (n0 + i < N) sum += __expf(v[i] - mx);
-        reinterpret_cast<float2*>(epi.out2)[static_cast<long>(row) * epi.ldo2 + n0 / 32] = make_float2(mx, sum);
+          for (int i = 0; i < 32; ++i)
+            if (n0 + i < N) mx = fmaxf(mx, v[i]);
+        }
+        const float nm = -mx * kL2e;
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float e0 = n0 + i < N ? ex2_approx(fmaf(v[i], kL2e, nm)) : 0.f;
+          const float e1 = n0 + i + 1 < N ? ex2_approx(fmaf(v[i + 1], kL2e, nm)) : 0.f;
+          acc = __fadd2_rn(acc, make_float2(e0, e1));
+        }
+        reinterpret_cast<float2*>(epi.out2)[static_cast<long>(row) * epi.ldo2 + n0 / 32] = make_float2(mx, acc.x + acc.y);
       }
       [[fallthrough]];
     case EPI_STORE_F32:

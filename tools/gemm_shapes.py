@@ -10,7 +10,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_00482_b200 import _native  # noqa: E402
 
-EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU, EPI_RESID = range(6)
+EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU, EPI_RESID, EPI_STATS = range(7)
 n, d, F, V = 32768, 896, 4864, 151936
 SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
     ("fwd qkv", n, 3 * d, d, 0, 1, EPI_STORE_BF16),
@@ -18,6 +18,7 @@ SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
     ("fwd mlp_in", n, F, d, 0, 1, EPI_SILU),
     ("fwd mlp_out", n, d, F, 0, 1, EPI_RESID),
     ("fwd head", 2048, V, d, 0, 1, EPI_STORE_F32),
+    ("fwd head stats", 2304, V, d, 0, 1, EPI_STATS),
     ("dX mlp_out", n, F, d, 0, 0, EPI_DSILU),
     ("dX mlp_in", n, d, F, 0, 0, EPI_STORE_F32),
     ("dX o", n, d, d, 0, 0, EPI_STORE_BF16),
@@ -53,7 +54,7 @@ def main():
         o16 = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
         act = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
         aux = torch.zeros(M, N, device="cuda", dtype=torch.float32 if epi == EPI_RESID else torch.bfloat16)
-        outp = o32 if epi in (EPI_STORE_F32, EPI_ADD_F32, EPI_RESID) else o16
+        outp = o32 if epi in (EPI_STORE_F32, EPI_ADD_F32, EPI_RESID, EPI_STATS) else o16
         lda = a.stride(0)
         ldb = b.stride(0)
         splits = lib.tt_debug_gemm_splits(M, N, K) if epi == EPI_ADD_F32 else 1

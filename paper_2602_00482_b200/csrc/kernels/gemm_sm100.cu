@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t ld_bytes = epi_f32_out(mode) ? 4096u : 2048u;
     uint32_t gc = 0;        // chunks staged by this warp: slot = gc & 1
     uint32_t ld_phase = 0;  // per-slot parity of the operand-load barriers
+    bool ld_ahead = false;  // the current chunk's operand load was issued during the previous chunk
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cid; t < num_tiles; t += ncl) {
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           blk = n0 / epi.split_w;
           xc = n0 - blk * epi.split_w;
         }
-        if (active) {
+        if (active && !ld_ahead) {
           if (lane == 0) bulk_wait_read<C::kSlots - 1>();  // the store that last used this slot has read it
           __syncwarp();
           if (need_ld && lane == 0) {
@@ -506,6 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(&tm_x, &wld[slot], buf, n0, row0);
           }
         }
+        ld_ahead = false;
         tmem_ld_wait_regs(rr[ch & 1]);
         if (ch + 1 < NCH) {
           tmem_ld32(t_row + (ch + 1) * 32, rr[(ch + 1) & 1]);
@@ -533,6 +535,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_commit();
           }
           ++gc;
+          // operand epilogues (residual / SiLU input): start the next chunk's TMA load now, into the
+          // other slot once its previous store has been read, so it overlaps this chunk's tail
+          if (C::kSlots == 2 && need_ld && ch + 1 < NCH && n0 + 32 < N) {
+            const int ns = static_cast<int>(gc & 1);
+            if (lane == 0) {
+              bulk_wait_read<1>();
+              mbar_arrive_expect_tx(&wld[ns], ld_bytes);
+              tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 32, row0);
+            }
+            __syncwarp();
+            ld_ahead = true;
+          }
         }
       }
       if (++acc == 2) {

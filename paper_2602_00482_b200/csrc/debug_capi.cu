@@ -189,30 +189,12 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
             }
         }
         void *dk128 = up(k128), *dk128b = up(k128b);
-        // the tcgen05 backward TMA-loads LSE/D tiles: per-head pitch must be a multiple of 4
-        const long ldl = (n + 3) / 4 * 4;
-        float *lse_p = lse, *D_p = D;
-        if (ldl != n) {
-          ttb::check_cuda(cudaMalloc(&lse_p, H * ldl * 4), "cudaMalloc");
-          ttb::check_cuda(cudaMalloc(&D_p, H * ldl * 4), "cudaMalloc");
-          ttb::check_cuda(cudaMemcpy2D(lse_p, ldl * 4, lse, static_cast<size_t>(n) * 4, static_cast<size_t>(n) * 4, H,
-                                       cudaMemcpyDeviceToDevice), "memcpy2d");
-          a.lse = lse_p;
-          a.D = D_p;
-        }
-        a.ld_lse = ldl;
         timed([&] {
           ttb::attn_bwd_sm100(a, rows_cap, static_cast<const int4*>(d128), static_cast<int>(q128.size() / 4),
                               static_cast<const int4*>(dk128), static_cast<const int2*>(dk128b),
                               static_cast<int>(k128.size() / 4), nullptr);
         });
         ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_attn sync");
-        if (ldl != n) {
-          ttb::check_cuda(cudaMemcpy2D(D, static_cast<size_t>(n) * 4, D_p, ldl * 4, static_cast<size_t>(n) * 4, H,
-                                       cudaMemcpyDeviceToDevice), "memcpy2d");
-          cudaFree(lse_p);
-          cudaFree(D_p);
-        }
         cudaFree(dk128);
         cudaFree(dk128b);
       } else {

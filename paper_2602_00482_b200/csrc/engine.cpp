@@ -264,7 +264,7 @@ ActLayout Engine::layout(int64_t n) const {
   a.n1 = take(n * d_ * 2);
   a.q = take(n * d_ * 2);
   a.attn = take(n * d_ * 2);
-  a.lse = take(H_ * ((n + 3) / 4 * 4) * 4);  // per-head pitch rounded to 4 (TMA-loadable tiles)
+  a.lse = take(H_ * n * 4);
   a.xmid = take(n * d_ * 4);
   a.inv2 = take(n * 4);
   a.n2 = take(n * d_ * 2);
@@ -306,7 +306,7 @@ void Engine::ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, in
     sc_gn_.ensure(n * d_ * 4);
     sc_gh_.ensure(n * F_ * 2);
     sc_dO_.ensure(n * d_ * 2);
-    sc_D_.ensure(H_ * ((n + 3) / 4 * 4) * 4);
+    sc_D_.ensure(H_ * n * 4);
     sc_dq_.ensure(n * d_ * 4);
     sc_dqkv_.ensure(n * 3 * d_ * 2);
   }
@@ -536,7 +536,6 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       a.o = attn;
       a.ldo = d;
       a.lse = lse;
-      a.ld_lse = (n + 3) / 4 * 4;
       a.n = n;
       a.H = static_cast<int>(H_);
       a.dh = static_cast<int>(dh_);
@@ -783,7 +782,6 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       a.ldkv = d;
       a.lse = lse;
       a.D = sc_D_.as<float>();
-      a.ld_lse = (n + 3) / 4 * 4;
       a.dq = dq;
       a.lddq = d;
       a.dk = dK;

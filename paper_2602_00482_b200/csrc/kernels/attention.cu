@@ -236,9 +236,8 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(AttnFwdArgs a) {
   }
   if (c4 == 0) {
     const float ln2 = 0.6931471805599453f;
-    const long ldl = a.ld_lse > 0 ? a.ld_lse : a.n;
-    if (r0 < q_end) a.lse[static_cast<long>(h) * ldl + r0] = (m_r[0] + log2f(l_r[0])) * ln2;
-    if (r1 < q_end) a.lse[static_cast<long>(h) * ldl + r1] = (m_r[1] + log2f(l_r[1])) * ln2;
+    if (r0 < q_end) a.lse[static_cast<long>(h) * a.n + r0] = (m_r[0] + log2f(l_r[0])) * ln2;
+    if (r1 < q_end) a.lse[static_cast<long>(h) * a.n + r1] = (m_r[1] + log2f(l_r[1])) * ln2;
   }
 }
 
@@ -289,9 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(AttnBwdArgs a) {
     cp_async_commit();
     for (int i = threadIdx.x; i < 64; i += kThreads) {
       const bool ok = i < qn;
-      const long ldl = a.ld_lse > 0 ? a.ld_lse : a.n;
-      lse_s[i] = ok ? a.lse[static_cast<long>(h) * ldl + q0 + i] * kLog2e : INFINITY;
-      D_s[i] = ok ? a.D[static_cast<long>(h) * ldl + q0 + i] : 0.f;
+      lse_s[i] = ok ? a.lse[static_cast<long>(h) * a.n + q0 + i] * kLog2e : INFINITY;
+      D_s[i] = ok ? a.D[static_cast<long>(h) * a.n + q0 + i] : 0.f;
     }
     cp_async_wait_all();
     __syncthreads();
@@ -422,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(AttnBwdArgs a) {
 
 // D[h][r] = sum_c dO[r, h*dh+c] * O[r, h*dh+c]
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
-                                    long ld, float* __restrict__ D, long ldd, int n, int H, int dh) {
+                                    long ld, float* __restrict__ D, int n, int H, int dh) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (w >= n * H) return;
@@ -437,7 +435,7 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dO, const 
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
-  if (lane == 0) D[static_cast<long>(h) * ldd + r] = s;
+  if (lane == 0) D[static_cast<long>(h) * n + r] = s;
 }
 
 template <int DH>
@@ -473,9 +471,7 @@ void attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
 
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream) {
   const int warps = a.n * a.H;
-  if (warps > 0)
-    attn_bwd_pre_kernel<<<(warps * 32 + 255) / 256, 256, 0, stream>>>(a.dO, a.o, a.ldq, a.D,
-                                                                       a.ld_lse > 0 ? a.ld_lse : a.n, a.n, a.H, a.dh);
+  if (warps > 0) attn_bwd_pre_kernel<<<(warps * 32 + 255) / 256, 256, 0, stream>>>(a.dO, a.o, a.ldq, a.D, a.n, a.H, a.dh);
 }
 
 void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {

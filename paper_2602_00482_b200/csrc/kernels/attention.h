@@ -14,9 +14,7 @@ struct AttnFwdArgs {
   long ldkv = 0;
   __nv_bfloat16* o = nullptr;  // [n x ldo]
   long ldo = 0;
-  float* lse = nullptr;  // [H x ld_lse], natural log
-  long ld_lse = 0;       // row pitch of lse (and D) per head; 0 = n. A multiple of 4 lets the tcgen05
-                         // backward fetch LSE/D tiles with TMA
+  float* lse = nullptr;  // [H x n], natural log
   int n = 0, H = 0, dh = 0, S = 0;
   // stack rows: the prefix is rows [pbase, pbase + S), the batch's own rows start at r0 (< 0: r0 = S)
   int pbase = 0, r0 = -1;
@@ -36,9 +34,8 @@ struct AttnBwdArgs {
   const __nv_bfloat16* k = nullptr;
   const __nv_bfloat16* v = nullptr;
   long ldkv = 0;
-  const float* lse = nullptr;  // [H x ld_lse]
-  float* D = nullptr;          // [H x ld_lse] scratch: rowsum(dO * O)
-  long ld_lse = 0;             // 0 = n
+  const float* lse = nullptr;  // [H x n]
+  float* D = nullptr;          // [H x n] scratch: rowsum(dO * O)
   float* dq = nullptr;         // [n x lddq] fp32, accumulated
   long lddq = 0;
   float* dk = nullptr;  // fp32 dK/dV stack rows (absolute), accumulated

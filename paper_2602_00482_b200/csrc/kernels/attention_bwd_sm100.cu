@@ -70,9 +70,8 @@ struct DqCfg {
 };
 
 struct BwdParams {
-  const float* lse;  // [H x ld_lse]
-  const float* D;    // [H x ld_lse]
-  long ld_lse;
+  const float* lse;  // [H x n]
+  const float* D;    // [H x n]
   float* dq;         // [n x lddq]
   long lddq;
   float* dk;  // stack rows (this layer), fp32
@@ -229,8 +228,8 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
     const bool row_ok = row < q_end;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     // invalid rows: lse2 = +inf -> P = 0 (their dQ rows are never stored)
-    const float lse2 = row_ok ? p.lse[static_cast<long>(h) * p.ld_lse + row] * kLog2e : INFINITY;
-    const float Dr = row_ok ? p.D[static_cast<long>(h) * p.ld_lse + row] : 0.f;
+    const float lse2 = row_ok ? p.lse[static_cast<long>(h) * p.n + row] * kLog2e : INFINITY;
+    const float Dr = row_ok ? p.D[static_cast<long>(h) * p.n + row] : 0.f;
     const float c2 = p.scale_log2;
     constexpr int HC = BKV / 2;
     const bool trace = (DBG & 4) && threadIdx.x == 64 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
@@ -314,10 +313,8 @@ struct DkvCfg {
   static constexpr int kOffV = kKVBytes;
   static constexpr int kOffQ = 2 * kKVBytes;
   static constexpr int kOffDO = kOffQ + NS * kQBytes;
-  // per Q/dO stage: the LSE and D of its 64 queries (TMA-loaded with the stage); P^T, dS^T in TMEM
-  static constexpr int kStatBytes = 2 * BQ * 4;
-  static constexpr int kOffStat = kOffDO + NS * kQBytes;
-  static constexpr int kOffBar = kOffStat + NS * kStatBytes;
+  static constexpr int kOffStat = kOffDO + NS * kQBytes;  // [2][2][BQ] floats: lse2, D (P^T, dS^T in TMEM)
+  static constexpr int kOffBar = kOffStat + 2 * 2 * BQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kTmemCols = 512;
   static_assert(2 * NB * BQ + 2 * DH <= 512 && NS >= NB, "dkdv kernel: TMEM / Q ring too small");
@@ -331,7 +328,6 @@ template <int DH, int NS, int POLY>
 __global__ void __launch_bounds__(kThreadsDq, 1)
     fa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                       const __grid_constant__ CUtensorMap tm_lse, const __grid_constant__ CUtensorMap tm_D,
                        BwdParams p) {
   using C = DkvCfg<DH, NS>;
   constexpr int BQ = C::BQ;
@@ -396,12 +392,8 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
       for (int i = 0; i < nq; ++i) {
         const int st = i % NS;
         mbar_wait(&q_empty[st], ((i / NS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[st], 2 * C::kQBytes + C::kStatBytes);
+        mbar_arrive_expect_tx(&q_full[st], 2 * C::kQBytes);
         const int q0 = q_lo + i * BQ;
-        // the stage's LSE / D tiles (queries past the batch end arrive as zeros; the softmax masks
-        // queries >= q_hi)
-        tma_load_2d(&tm_lse, &q_full[st], smem + C::kOffStat + st * C::kStatBytes, q0, h);
-        tma_load_2d(&tm_D, &q_full[st], smem + C::kOffStat + st * C::kStatBytes + BQ * 4, q0, h);
 #pragma unroll
         for (int pn = 0; pn < DH / 64; ++pn) {
           tma_load_2d(&tm_q, &q_full[st], smem + C::kOffQ + st * C::kQBytes + pn * (BQ * 128), h * DH + pn * 64, q0);
@@ -461,13 +453,30 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
     const bool key_ok = krow < kv_rows;
     const int kt = kt_base + krow;      // own: local key index
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int tid = threadIdx.x - 64;   // 0..255
     constexpr int HC = BQ / 2;
+    // LSE/D of query block i are loaded one block ahead into registers (tid < BQ) and published to
+    // the stat buffer of that block at the start of its iteration (hides the global-load latency)
+    float nl = INFINITY, nd = 0.f;
+    auto fetch = [&](int i) {
+      const int q = q_lo + i * BQ + tid;
+      const bool ok = tid < BQ && i < nq && q < q_hi;
+      // raw values only: the log2e scaling happens at the smem store one iteration later, so no
+      // instruction consumes the global load until its latency is hidden
+      nl = ok ? p.lse[static_cast<long>(h) * p.n + q] : INFINITY;
+      nd = ok ? p.D[static_cast<long>(h) * p.n + q] : 0.f;
+    };
+    fetch(0);
     for (int i = 0; i < nq; ++i) {
       const int q0 = q_lo + i * BQ;
-      // LSE / D of block i: TMA-loaded with its Q/dO stage (complete: S^T_i was computed from it),
-      // valid until dV/dK_i free the stage
-      const float* st_lse = stat + (i % NS) * (C::kStatBytes / 4);
-      const float* st_D = st_lse + BQ;
+      float* st_lse = stat + (i & 1) * 2 * BQ;
+      float* st_D = st_lse + BQ;
+      if (tid < BQ) {
+        st_lse[tid] = nl * kLog2e;
+        st_D[tid] = nd;
+      }
+      named_bar_sync(1, 32 * kSmxWarps);
+      fetch(i + 1);
       mbar_wait(&s_full[i % NB], (i / NB) & 1);
       tc_fence_after();
       float s[HC], dp[HC];
@@ -496,12 +505,9 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
       const float* lz_base = st_lse + half * HC;
       const float* dz_base = st_D + half * HC;
       uint32_t wp[HC / 2], wd[HC / 2];
-      const int qv = q_hi - (q0 + half * HC);  // valid query columns of this half: [0, qv)
 #pragma unroll
       for (int c = 0; c < HC; c += 4) {
-        float4 lz = *reinterpret_cast<const float4*>(lz_base + c);
-        lz = make_float4(c < qv ? lz.x * kLog2e : INFINITY, c + 1 < qv ? lz.y * kLog2e : INFINITY,
-                         c + 2 < qv ? lz.z * kLog2e : INFINITY, c + 3 < qv ? lz.w * kLog2e : INFINITY);
+        const float4 lz = *reinterpret_cast<const float4*>(lz_base + c);
         const float4 dz = *reinterpret_cast<const float4*>(dz_base + c);
         const float2 c22 = make_float2(c2, c2);
         const float2 xa = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, make_float2(-lz.x, -lz.y));
@@ -561,7 +567,7 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
   using CQ = DqCfg<DH, NSQ>;
   using CK = DkvCfg<DH, NSK>;
   const int d = a.H * DH;
-  BwdParams p{a.lse, a.D, a.ld_lse > 0 ? a.ld_lse : a.n, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0,
+  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0,
               dq_blocks, nullptr, a.scale,
               a.scale * kLog2e};
   if (n_dq > 0) {
@@ -594,18 +600,13 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, CK::BQ);
     make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, 128);
     make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, 128);
-    const long ldl = a.ld_lse > 0 ? a.ld_lse : a.n;
-    if (ldl % 4 != 0) throw std::invalid_argument("attn_bwd_sm100: ld_lse must be a multiple of 4 (TMA pitch)");
-    CUtensorMap tl, tD;
-    make_tmap_f32_2d(&tl, a.lse, a.n, a.H, ldl, CK::BQ, 1);
-    make_tmap_f32_2d(&tD, a.D, a.n, a.H, ldl, CK::BQ, 1);
     static bool once = (cudaFuncSetAttribute(fa_bwd_dkdv_kernel<DH, NSK, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              CK::kSmem),
                         true);
     (void)once;
     p.blocks = kv_items;
     p.blocks2 = kv_items2;
-    fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreadsDq, CK::kSmem, stream>>>(tq, tdo, tk, tv, tl, tD, p);
+    fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreadsDq, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
   }
 }
 

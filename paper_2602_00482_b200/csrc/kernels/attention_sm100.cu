@@ -61,7 +61,6 @@ struct FwdParams {
   __nv_bfloat16* o;
   long ldo;
   float* lse;
-  long ld_lse;
   int n, S, H;
   int pbase, r0;  // prefix rows [pbase, pbase + S); own rows from r0
   const int4* qblocks;
@@ -336,7 +335,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         *reinterpret_cast<uint4*>(orow + c + 8) = w1;
       }
     }
-    if (half == 0 && row_ok) p.lse[static_cast<long>(h) * p.ld_lse + row] = (m + log2f(lt)) * 0.6931471805599453f;
+    if (half == 0 && row_ok) p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(lt)) * 0.6931471805599453f;
 
   }
   tc_fence_before();
@@ -356,7 +355,7 @@ void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
                                            C::kSmem),
                       true);
   (void)once;
-  FwdParams p{a.o, a.ldo, a.lse, a.ld_lse > 0 ? a.ld_lse : a.n, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, a.qblocks, a.scale * kLog2e};
+  FwdParams p{a.o, a.ldo, a.lse, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, a.qblocks, a.scale * kLog2e};
   dim3 grid(a.nqb, a.H);
   fa_fwd_kernel<DH, BKV, NS, POLY><<<grid, kFwdThreads, C::kSmem, stream>>>(tq, tk, tv, p);
 }

@@ -221,7 +221,7 @@ def test_attention_forward(impl, n, S, H, dh):
 
 @pytest.mark.parametrize("impl", [0, 1])
 @pytest.mark.parametrize("n,S,H,dh", [(300, 200, 2, 64), (513, 129, 2, 128), (100, 0, 2, 64), (1200, 1024, 2, 64),
-                                      (64, 300, 1, 128)])
+                                      (64, 300, 1, 128), (40, 100, 2, 64), (33, 0, 2, 128)])
 def test_attention_backward(impl, n, S, H, dh):
     torch.manual_seed(7 + n)
     d = H * dh

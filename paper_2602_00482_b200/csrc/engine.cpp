@@ -7,6 +7,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -41,8 +42,14 @@ DevBuf::~DevBuf() {
   if (p) cudaFree(p);
 }
 
+namespace {
+std::atomic<uint64_t> g_alloc_gen{1};
+}
+uint64_t alloc_generation() { return g_alloc_gen.load(); }
+
 void DevBuf::ensure(size_t n) {
   if (n <= bytes) return;
+  g_alloc_gen.fetch_add(1);
   if (p) {
     cudaFree(p);
     p = nullptr;
@@ -172,6 +179,8 @@ void Engine::set_option(const std::string& key, int64_t value) {
   } else if (key == "root_batch_tokens") {
     if (value < 0) throw std::invalid_argument("root_batch_tokens must be >= 0");
     root_batch_tokens_ = value;
+  } else if (key == "cuda_graph") {
+    cuda_graph_ = value != 0;
   } else if (key == "ce_stats") {
     // 1: LM-head GEMM epilogue emits per-32-column softmax statistics, CE reads logits once
     // (default); 0: CE does both passes over the logits row itself
@@ -1120,8 +1129,59 @@ tt_step_result Engine::execute(StepPlan& plan) {
   if (!seg_stack_.empty()) throw std::runtime_error("tree_train_step: segment stack is not empty");
   ensure_capacity(plan.rows, plan.arena_peak, plan.max_n, plan.max_loss);
   cur_meta_ = plan.meta.as<char>();
-  ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
   const uint64_t launches0 = launches_;
+  // First execution eager (sets kernel attributes, proves the plan); from the second one on, the
+  // whole op list is one CUDA graph (re-captured if any device buffer was reallocated since).
+  const bool use_graph = cuda_graph_ && !profiling_ && plan.warmed;
+  if (use_graph && !(plan.graph && plan.graph_gen == alloc_generation())) {
+    if (plan.graph) {
+      cudaGraphExecDestroy(plan.graph);
+      plan.graph = nullptr;
+    }
+    cudaGraph_t g = nullptr;
+    ck(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "graph capture");
+    const uint64_t l0 = launches_;
+    try {
+      issue_ops(plan);
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    ck(cudaStreamEndCapture(stream_, &g), "graph capture end");
+    ck(cudaGraphInstantiate(&plan.graph, g, 0), "graph instantiate");
+    cudaGraphDestroy(g);
+    plan.graph_launches = launches_ - l0;
+    launches_ = l0;
+    plan.graph_gen = alloc_generation();
+  }
+  if (use_graph) {
+    ck(cudaGraphLaunch(plan.graph, stream_), "graph launch");
+    launches_ += plan.graph_launches;
+  } else {
+    issue_ops(plan);
+    plan.warmed = true;
+  }
+  ck(cudaGetLastError(), "tree_train_step launch");
+  ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
+  ck(cudaStreamSynchronize(stream_), "tree_train_step");
+  collect_profile();
+  tt_step_result res = plan.counters;
+  res.total_loss = *loss_host_;
+  res.num_launches = launches_ - launches0;
+  res.d2h_bytes = sizeof(double);
+  res.peak_hbm_bytes = wbuf_.bytes + gainbuf_.bytes + pe_.bytes + grads_.bytes + kst_.bytes + vst_.bytes +
+                       dkst_.bytes + dvst_.bytes + plan.arena_peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +
+                       sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes + sc_dq_.bytes + sc_dqkv_.bytes +
+                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + plan.meta.bytes;
+  arena_peak_ = std::max(arena_peak_, plan.arena_peak);
+  if (!std::isfinite(res.total_loss)) throw NonFiniteError("tree_train_step: non-finite loss");  // SPEC.md:228
+  return res;
+}
+
+// Enqueues one step of the plan on the engine stream (no host synchronisation: graph-capturable).
+void Engine::issue_ops(const StepPlan& plan) {
+  ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
   for (const auto& op : plan.ops) {
     const Batch& b = plan.batches[op.b];
     switch (op.code) {
@@ -1140,21 +1200,6 @@ tt_step_result Engine::execute(StepPlan& plan) {
         break;
     }
   }
-  ck(cudaGetLastError(), "tree_train_step launch");
-  ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
-  ck(cudaStreamSynchronize(stream_), "tree_train_step");
-  collect_profile();
-  tt_step_result res = plan.counters;
-  res.total_loss = *loss_host_;
-  res.num_launches = launches_ - launches0;
-  res.d2h_bytes = sizeof(double);
-  res.peak_hbm_bytes = wbuf_.bytes + gainbuf_.bytes + pe_.bytes + grads_.bytes + kst_.bytes + vst_.bytes +
-                       dkst_.bytes + dvst_.bytes + plan.arena_peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +
-                       sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes + sc_dq_.bytes + sc_dqkv_.bytes +
-                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + plan.meta.bytes;
-  arena_peak_ = std::max(arena_peak_, plan.arena_peak);
-  if (!std::isfinite(res.total_loss)) throw NonFiniteError("tree_train_step: non-finite loss");  // SPEC.md:228
-  return res;
 }
 
 tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config& sc) {

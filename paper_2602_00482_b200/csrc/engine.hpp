@@ -26,6 +26,9 @@ namespace ttb {
 
 using bf16 = __nv_bfloat16;
 
+// Bumped whenever any DevBuf (re)allocates: CUDA graphs captured before hold stale pointers.
+uint64_t alloc_generation();
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -88,6 +91,16 @@ struct StepPlan {
   size_t meta_bytes = 0;
   tt_step_result counters{};
   std::string trace;  // logical DFS trace of the executed schedule
+  // CUDA graph of the whole op list (captured on the second execute, replayed afterwards)
+  bool warmed = false;
+  cudaGraphExec_t graph = nullptr;
+  uint64_t graph_gen = 0, graph_launches = 0;
+  StepPlan() = default;
+  StepPlan(const StepPlan&) = delete;
+  StepPlan& operator=(const StepPlan&) = delete;
+  ~StepPlan() {
+    if (graph) cudaGraphExecDestroy(graph);
+  }
 };
 
 // Per-kernel-class device timing (profiling mode): CUDA events around every launch.
@@ -222,6 +235,8 @@ class Engine {
   const char* cur_meta_ = nullptr;
   std::string last_trace_;
   bool profiling_ = false;
+  bool cuda_graph_ = true;  // replay prepared plans as CUDA graphs (engine option "cuda_graph")
+  void issue_ops(const StepPlan& plan);
   int attn_fwd_impl_ = 1;
   int attn_bwd_impl_ = 1;
   bool ce_stats_ = true;

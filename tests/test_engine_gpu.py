@@ -322,3 +322,26 @@ def test_multi_root_batching_vs_oracle(root_tokens, fwd_impl, bwd_impl):
     assert plan.trace() == tree.dfs_trace()  # the logical DFS trace is unchanged by batching
     if root_tokens >= 5 * 90:
         assert r.num_batches < 5 * 2  # prompts share pushes
+
+
+def test_plan_cuda_graph_replay_matches_eager():
+    # a prepared plan is captured as one CUDA graph on its second execute and replayed afterwards;
+    # replays must give the eager step's loss and gradients (same kernels, same order)
+    cfg, flat, eng = make(SMALL, 41)
+    seqs = O.grouped_corpus(3, 4, 60, 50, cfg.vocab_size, 42, weight_jitter=True)
+    tree = tt.build_prefix_tree([tt.TokenSequence(s.seq_id, s.tokens, s.weights) for s in seqs])
+    plan = eng.plan(tree, tt.SchedulerConfig())
+    outs = []
+    for _ in range(4):  # eager, capture + launch, replay, replay
+        eng.zero_gradients()
+        r = plan.execute()
+        outs.append((r.total_loss, eng.gradients().copy(), r.num_launches))
+    # fp32 atomics (dK/dV stack, split-K reduce-add, gain gradients) make the summation order, hence
+    # the last bits, run-to-run dependent — eager runs differ from each other the same way
+    for loss, g, nl in outs[1:]:
+        assert abs(loss - outs[0][0]) <= 1e-9 * abs(outs[0][0]) and nl == outs[0][2]
+        assert rel(g, outs[0][1]) <= 1e-5
+    eng.set_option("cuda_graph", 0)
+    eng.zero_gradients()
+    r = plan.execute()
+    assert abs(r.total_loss - outs[0][0]) <= 1e-9 * abs(outs[0][0]) and rel(eng.gradients(), outs[0][1]) <= 1e-5

@@ -555,6 +555,277 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 
+// ================================================================= dK/dV kernel, 128 x 128 blocks
+// dh = 64 only. 128 keys x 128 queries per block: S^T / dP^T are N = 128 MMAs (full rate; the N = 64
+// ones run at 2/3), and each issuer wait now covers twice the MMA work. TMEM: S^T[2] (128 each),
+// ONE dP^T buffer (128), dK, dV (64 each) = 512 columns. P^T / dS^T (bf16 pairs) go over the S^T
+// buffer: half h of the query columns packs P^T into [64h, 64h+32) and dS^T into [64h+32, 64h+64);
+// the dP^T buffer is released as soon as the softmax has loaded it (dp_free), so dP^T_{i+1} is
+// computed while the softmax of block i finishes.
+template <int NS>
+struct Dkv128Cfg {
+  static constexpr int DH = 64, BKV = 128, BQ = 128;
+  static constexpr int kKVBytes = BKV * DH * 2;  // K (or V) block
+  static constexpr int kQBytes = BQ * DH * 2;    // Q_i (or dO_i) tile
+  static constexpr int kOffV = kKVBytes;
+  static constexpr int kOffQ = 2 * kKVBytes;
+  static constexpr int kOffDO = kOffQ + NS * kQBytes;
+  static constexpr int kOffStat = kOffDO + NS * kQBytes;  // [2][2][BQ] floats: lse2, D
+  static constexpr int kOffBar = kOffStat + 2 * 2 * BQ * 4;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+  static constexpr int kTmemCols = 512;
+  static_assert(kSmem <= 227 * 1024 && NS >= 2, "dkdv128: smem / ring");
+  static constexpr uint32_t kIdescS = make_idesc_bf16(128, BQ, false, false);
+  static constexpr uint32_t kIdescKV = make_idesc_bf16(128, DH, false, true);
+};
+
+template <int NS, int POLY>
+__global__ void __launch_bounds__(kThreadsDq, 1)
+    fa_bwd_dkdv128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                          BwdParams p) {
+  using C = Dkv128Cfg<NS>;
+  constexpr int DH = C::DH, BQ = C::BQ;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1024(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;
+  uint64_t* q_empty = q_full + NS;  // dV/dK_i done: frees the Q/dO stage and S^T buffer i % 2
+  uint64_t* s_full = q_empty + NS;  // [2]
+  uint64_t* p_full = s_full + 2;    // [2] softmax done with block i (P^T / dS^T in TMEM)
+  uint64_t* dp_full = p_full + 2;   // dP^T_i computed (single buffer)
+  uint64_t* dp_free = dp_full + 1;  // softmax has loaded dP^T_i
+  uint64_t* acc_done = dp_free + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
+  float* stat = reinterpret_cast<float*>(smem + C::kOffStat);
+
+  const int warp = warp_id_sync();
+  const int lane = threadIdx.x & 31;
+  const int4 it = p.blocks[blockIdx.x];
+  const int2 it2 = p.blocks2[blockIdx.x];
+  const int kv0 = it.x, kv_rows = it.y, q_lo = it.z, q_hi = it.w;
+  const int seg_off = it2.x;
+  const bool own = it2.y != 0;
+  const int kt_base = own ? kv0 - p.r0 - seg_off : 0;
+  const int h = blockIdx.y;
+  const int nq = (q_hi - q_lo + BQ - 1) / BQ;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_do);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_v);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], kSmxWarps);
+    }
+    mbar_init(dp_full, 1);
+    mbar_init(dp_free, kSmxWarps);
+    mbar_init(acc_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_S = tmem, t_dP = tmem + 256, t_dK = tmem + 384, t_dV = tmem + 448;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * C::kKVBytes);
+      tma_load_2d(&tm_k, kv_full, smem, h * DH, kv0);
+      tma_load_2d(&tm_v, kv_full, smem + C::kOffV, h * DH, kv0);
+      for (int i = 0; i < nq; ++i) {
+        const int st = i % NS;
+        mbar_wait(&q_empty[st], ((i / NS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[st], 2 * C::kQBytes);
+        const int q0 = q_lo + i * BQ;
+        tma_load_2d(&tm_q, &q_full[st], smem + C::kOffQ + st * C::kQBytes, h * DH, q0);
+        tma_load_2d(&tm_do, &q_full[st], smem + C::kOffDO + st * C::kQBytes, h * DH, q0);
+      }
+    }
+  } else if (warp == 1) {
+    // S^T_i = K Q_i^T into S buffer i % 2 (after dV/dK_{i-2}); dP^T_i = V dO_i^T into the single dP^T
+    // buffer (after the softmax loaded dP^T_{i-1})
+    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
+    mbar_wait(kv_full, 0);
+    for (int i = 0; i < nq; ++i) {
+      const int st = i % NS;
+      if (i >= 2) mbar_wait(&q_empty[(i - 2) % NS], ((i - 2) / NS) & 1);
+      mbar_wait(&q_full[st], (i / NS) & 1);
+      tc_fence_after();
+      const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k)
+          umma_bf16_ss(t_S + (i & 1) * 128, sdesc_add(d16, k * 32), sdesc_add(sdesc_add(d16, q_off), k * 32), C::kIdescS,
+                       k > 0);
+        umma_commit(&s_full[i & 1]);
+      }
+      __syncwarp();
+      if (i >= 1) mbar_wait(dp_free, (i - 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < DH / 16; ++k)
+          umma_bf16_ss(t_dP, sdesc_add(d16, C::kOffV + k * 32), sdesc_add(sdesc_add(d16, do_off), k * 32), C::kIdescS,
+                       k > 0);
+        umma_commit(dp_full);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 10) {
+    // dV += P^T dO_i ; dK += dS^T Q_i  (A from the S^T buffer: P^T at 64h + ..., dS^T at 64h + 32 + ...)
+    const uint64_t dmn = make_sdesc_sw128(smem_u32(smem), BQ * 128, 1024);
+    for (int i = 0; i < nq; ++i) {
+      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const int st = i % NS;
+        const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
+#pragma unroll
+        for (int k = 0; k < BQ / 16; ++k) {
+          const uint32_t col = (k / 4) * 64 + (k % 4) * 8;
+          umma_bf16_ts(t_dV, t_S + (i & 1) * 128 + col, sdesc_add(sdesc_add(dmn, do_off), k * 2048), C::kIdescKV,
+                       (i > 0 || k > 0));
+          umma_bf16_ts(t_dK, t_S + (i & 1) * 128 + col + 32, sdesc_add(sdesc_add(dmn, q_off), k * 2048), C::kIdescKV,
+                       (i > 0 || k > 0));
+        }
+        umma_commit(&q_empty[st]);
+        if (i == nq - 1) umma_commit(acc_done);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int quad = warp & 3;
+    const int half = (warp - 2) / 4;    // query columns [64*half, 64*half+64) of each 128-query block
+    const int krow = quad * 32 + lane;  // key row within the block == TMEM lane
+    const bool key_ok = krow < kv_rows;
+    const int kt = kt_base + krow;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const int tid = threadIdx.x - 64;  // 0..255
+    float nl = INFINITY, nd = 0.f;
+    auto fetch = [&](int i) {
+      const int q = q_lo + i * BQ + tid;
+      const bool ok = tid < BQ && i < nq && q < q_hi;
+      nl = ok ? p.lse[static_cast<long>(h) * p.n + q] : INFINITY;
+      nd = ok ? p.D[static_cast<long>(h) * p.n + q] : 0.f;
+    };
+    fetch(0);
+    const float c2 = p.scale_log2;
+    // P^T / dS^T of one 32-query sub-chunk sc (columns 64*half + 32*sc ...)
+    auto sub = [&](int i, int sc, const float (&s_in)[32], const float (&dp)[32], const float* st_lse,
+                   const float* st_D, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
+      const int q0 = q_lo + i * BQ;
+      const int cb = 64 * half + 32 * sc;  // block column of s_in[0]
+      float s[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) s[c] = s_in[c];
+      if (own) {
+        const int lo = kt - (q0 - seg_off) - cb;  // key kt sees query column c iff c >= lo
+        if (__any_sync(0xffffffff, lo > 0)) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) s[c] = c >= lo ? s[c] : -INFINITY;
+        }
+      }
+      const float* lz_base = st_lse + cb;
+      const float* dz_base = st_D + cb;
+#pragma unroll
+      for (int c = 0; c < 32; c += 4) {
+        const float4 lz = *reinterpret_cast<const float4*>(lz_base + c);
+        const float4 dz = *reinterpret_cast<const float4*>(dz_base + c);
+        const float2 c22 = make_float2(c2, c2);
+        const float2 xa = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, make_float2(-lz.x, -lz.y));
+        const float2 xb = __ffma2_rn(make_float2(s[c + 2], s[c + 3]), c22, make_float2(-lz.z, -lz.w));
+        const float2 pa = ((c / 2) & 3) < POLY ? ex2_poly2(xa) : make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
+        const float2 pb = ((c / 2 + 1) & 3) < POLY ? ex2_poly2(xb) : make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
+        const float2 da = __fmul2_rn(pa, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-dz.x, -dz.y)));
+        const float2 db = __fmul2_rn(pb, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-dz.z, -dz.w)));
+        wp[c / 2] = pack_bf16x2(pa.x, pa.y);
+        wp[c / 2 + 1] = pack_bf16x2(pb.x, pb.y);
+        wd[c / 2] = pack_bf16x2(da.x, da.y);
+        wd[c / 2 + 1] = pack_bf16x2(db.x, db.y);
+      }
+    };
+    auto ld32 = [&](uint32_t taddr, float (&v)[32]) {
+      uint32_t r[16], r2[16];
+      tmem_ld16(taddr + lane_off, r);
+      tmem_ld16(taddr + 16 + lane_off, r2);
+      tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        v[e] = __uint_as_float(r[e]);
+        v[16 + e] = __uint_as_float(r2[e]);
+      }
+    };
+    for (int i = 0; i < nq; ++i) {
+      float* st_lse = stat + (i & 1) * 2 * BQ;
+      float* st_D = st_lse + BQ;
+      if (tid < BQ) {
+        st_lse[tid] = nl * kLog2e;
+        st_D[tid] = nd;
+      }
+      named_bar_sync(1, 32 * kSmxWarps);
+      fetch(i + 1);
+      const uint32_t sb = t_S + (i & 1) * 128 + 64 * half;
+      const uint32_t pb = t_dP + 64 * half;
+      mbar_wait(&s_full[i & 1], (i >> 1) & 1);
+      tc_fence_after();
+      float s0[32], s1[32], dp[32];
+      ld32(sb, s0);
+      ld32(sb + 32, s1);  // loaded before dS^T of sub-chunk 0 overwrites these columns
+      mbar_wait(dp_full, i & 1);
+      tc_fence_after();
+      ld32(pb, dp);
+      uint32_t wp[16], wd[16];
+      sub(i, 0, s0, dp, st_lse, st_D, wp, wd);
+      ld32(pb + 32, dp);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dp_free);  // dP^T_i fully in registers: dP^T_{i+1} may overwrite it
+      tmem_st16(sb + lane_off, wp);         // P^T sub-chunk 0 -> [64h, 64h+16)
+      tmem_st16(sb + 32 + lane_off, wd);    // dS^T sub-chunk 0 -> [64h+32, 64h+48)
+      sub(i, 1, s1, dp, st_lse, st_D, wp, wd);
+      tmem_st16(sb + 16 + lane_off, wp);
+      tmem_st16(sb + 48 + lane_off, wd);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[i & 1]);
+    }
+    mbar_wait(acc_done, 0);
+    tc_fence_after();
+    float* dkr = p.dk + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+    float* dvr = p.dv + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+#pragma unroll
+    for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
+      uint32_t rk[16], rv[16];
+      tmem_ld16(t_dK + c + lane_off, rk);
+      tmem_ld16(t_dV + c + lane_off, rv);
+      tmem_ld_wait();
+      if (key_ok) {
+#pragma unroll
+        for (int e = 0; e < 16; e += 4) {
+          red_add_v4_f32(dkr + c + e, __uint_as_float(rk[e]) * p.scale, __uint_as_float(rk[e + 1]) * p.scale,
+                         __uint_as_float(rk[e + 2]) * p.scale, __uint_as_float(rk[e + 3]) * p.scale);
+          red_add_v4_f32(dvr + c + e, __uint_as_float(rv[e]), __uint_as_float(rv[e + 1]), __uint_as_float(rv[e + 2]),
+                         __uint_as_float(rv[e + 3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
+}
+
 template <int DH, int POLY>
 void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                 const int2* kv_items2, int n_kv, cudaStream_t stream) {
@@ -606,7 +877,23 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     (void)once;
     p.blocks = kv_items;
     p.blocks2 = kv_items2;
-    fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreadsDq, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    static const bool k128 = [] {  // TT_ATTN_DKDV128=0: the 64-query-block dK/dV kernel (A/B timing)
+      const char* e = std::getenv("TT_ATTN_DKDV128");
+      return !(e && std::atoi(e) == 0);
+    }();
+    if (DH == 64 && k128) {
+      using C8 = Dkv128Cfg<5>;
+      CUtensorMap tq8, tdo8;
+      make_tmap_bf16(&tq8, a.q, d, a.n, a.ldq, 64, C8::BQ);
+      make_tmap_bf16(&tdo8, a.dO, d, a.n, a.ldq, 64, C8::BQ);
+      static bool once8 = (cudaFuncSetAttribute(fa_bwd_dkdv128_kernel<5, POLY>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, C8::kSmem),
+                           true);
+      (void)once8;
+      fa_bwd_dkdv128_kernel<5, POLY><<<dim3(n_kv, a.H), kThreadsDq, C8::kSmem, stream>>>(tq8, tdo8, tk, tv, p);
+    } else {
+      fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreadsDq, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
+    }
   }
 }
 

@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -341,6 +343,7 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
   auto put = [&](const void* src, size_t bytes) {
     const size_t off = cursor;
     cursor = align_up(cursor + bytes);
+    if (host.capacity() < cursor) host.reserve(std::max(cursor, 2 * host.capacity()));
     if (host.size() < cursor) host.resize(cursor);
     if (bytes) std::memcpy(host.data() + off, src, bytes);
     return off;
@@ -879,7 +882,10 @@ uint64_t Engine::auto_batch_budget(uint64_t path_tokens) const {
   return tok < 2048 ? 2048 : static_cast<uint64_t>(tok);
 }
 
-std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched_config& sc) {
+std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched_config& sc, bool transient) {
+  static const bool timing = std::getenv("TT_PLAN_TIMING") != nullptr;  // host-phase timing (stderr)
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t_start = now();
   if (tree.nodes[0].max_path_below > cfg_.max_position)
     throw std::invalid_argument("tree_train_step: path exceeds max_position");
   auto plan = std::make_unique<StepPlan>();
@@ -1058,6 +1064,7 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
   };
   visit(0, 0);
 
+  const auto t_sched = now();
   // ---- memory plan: LIFO arena offsets, stack rows, scratch sizes, counters
   tt_step_result& res = plan->counters;
   size_t top = 0;
@@ -1118,17 +1125,26 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
   // ---- metadata for every batch, resident in HBM for the plan's lifetime
   std::vector<char> host;
   size_t cursor = 0;
+  const auto t_mem = now();
   for (auto& b : batches) build_meta(b, cursor, host);
-  plan->meta_bytes = upload_staged(host, plan->meta);
+  const auto t_meta = now();
+  DevBuf& mbuf = transient ? meta_ : plan->meta;
+  plan->meta_bytes = upload_staged(host, mbuf);
+  plan->meta_ptr = mbuf.as<char>();
   res.h2d_bytes = plan->meta_bytes;
   ck(cudaStreamSynchronize(stream_), "plan upload");
+  if (timing) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "prepare: schedule %.1f ms, memory plan %.1f ms, metadata %.1f ms, upload %.1f ms (%zu B)\n",
+                 ms(t_start, t_sched), ms(t_sched, t_mem), ms(t_mem, t_meta), ms(t_meta, now()), plan->meta_bytes);
+  }
   return plan;
 }
 
 tt_step_result Engine::execute(StepPlan& plan) {
   if (!seg_stack_.empty()) throw std::runtime_error("tree_train_step: segment stack is not empty");
   ensure_capacity(plan.rows, plan.arena_peak, plan.max_n, plan.max_loss);
-  cur_meta_ = plan.meta.as<char>();
+  cur_meta_ = plan.meta_ptr;
   const uint64_t launches0 = launches_;
   // First execution eager (sets kernel attributes, proves the plan); from the second one on, the
   // whole op list is one CUDA graph (re-captured if any device buffer was reallocated since).
@@ -1173,7 +1189,8 @@ tt_step_result Engine::execute(StepPlan& plan) {
   res.peak_hbm_bytes = wbuf_.bytes + gainbuf_.bytes + pe_.bytes + grads_.bytes + kst_.bytes + vst_.bytes +
                        dkst_.bytes + dvst_.bytes + plan.arena_peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +
                        sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes + sc_dq_.bytes + sc_dqkv_.bytes +
-                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + plan.meta.bytes;
+                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + plan.meta.bytes +
+                       meta_.bytes;
   arena_peak_ = std::max(arena_peak_, plan.arena_peak);
   if (!std::isfinite(res.total_loss)) throw NonFiniteError("tree_train_step: non-finite loss");
   return res;
@@ -1203,7 +1220,7 @@ void Engine::issue_ops(const StepPlan& plan) {
 }
 
 tt_step_result Engine::train_step(const PrefixTree& tree, const tt_sched_config& sc) {
-  auto plan = prepare(tree, sc);
+  auto plan = prepare(tree, sc, /*transient=*/true);
   last_trace_ = plan->trace;
   return execute(*plan);
 }

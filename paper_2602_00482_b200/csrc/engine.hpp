@@ -88,6 +88,7 @@ struct StepPlan {
   int64_t rows = 0, max_n = 0, max_loss = 0;
   size_t arena_peak = 0;
   DevBuf meta;
+  const char* meta_ptr = nullptr;  // device metadata (meta, or the engine's step buffer if transient)
   size_t meta_bytes = 0;
   tt_step_result counters{};
   std::string trace;  // logical DFS trace of the executed schedule
@@ -136,7 +137,9 @@ class Engine {
   uint64_t accum_count() const { return accum_count_; }
 
   tt_step_result train_step(const PrefixTree& tree, const tt_sched_config& sc);
-  std::unique_ptr<StepPlan> prepare(const PrefixTree& tree, const tt_sched_config& sc);
+  // transient = the plan is executed once right away (tree_train_step): its metadata goes into an
+  // engine-owned buffer reused across steps instead of a fresh allocation per plan
+  std::unique_ptr<StepPlan> prepare(const PrefixTree& tree, const tt_sched_config& sc, bool transient = false);
   tt_step_result execute(StepPlan& plan);
 
   void set_profiling(bool on) { profiling_ = on; }

@@ -90,6 +90,7 @@ EXPORTS = {
                             vp, c.c_long, c.c_int, vp, vp, c.c_int],
     "tt_debug_gemm_splits": [c.c_int, c.c_int, c.c_int],
     "tt_debug_gemm_set_2cta": [c.c_int],
+    "tt_debug_gemm_set_transpose": [c.c_int],
     "tt_debug_attn_trace": [vp, c.c_int],
     "tt_debug_rmsnorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, c.c_int, c.c_int],
 }

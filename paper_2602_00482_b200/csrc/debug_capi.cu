@@ -67,6 +67,7 @@ int tt_debug_rmsnorm_bwd(const float* gy, const float* x, const float* inv, cons
   });
 }
 void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
+void tt_debug_gemm_set_transpose(int mode) { ttb::gemm_set_transpose(mode); }
 
 // clock64 trace of the TT_ATTN_DBG=3 attention dq kernel (timing experiments only)
 int tt_debug_attn_trace(long long* out, int n) { return ttb::attn_debug_trace(out, n); }

@@ -489,7 +489,8 @@ void Engine::gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int 
   const double bytes = 2.0 * (double(M) * K + double(N) * K) + out_b * double(M) * N;
   if (profiling_) {
     pending_tag_ = std::to_string(M) + "x" + std::to_string(N) + "x" + std::to_string(K) + (A.mn_major ? " A:mn" : " A:k") +
-                   (B.mn_major ? " B:mn" : " B:k") + " epi" + std::to_string(e.mode) + " s" + std::to_string(splits);
+                   (B.mn_major ? " B:mn" : " B:k") + " epi" + std::to_string(e.mode) + " s" + std::to_string(splits) +
+                   (e.mode == EPI_ADD_F32 && e.split_w == 0 && gemm_prefer_transposed(M, N, K) ? " T" : "");
   }
   run(KC_GEMM, 2.0 * M * N * K, bytes, [&] { gemm_bf16(A, B, M, N, K, e, splits, stream_); });
 }

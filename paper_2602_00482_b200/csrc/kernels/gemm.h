@@ -25,6 +25,8 @@ enum EpiMode : int {
   EPI_STORE_F32_STATS = 6,  // out[0] (fp32) = alpha*acc, and out2 (float2, pitch ldo2) gets the per-row
                             // (max, sum exp(v - max)) of every 32-column group: the softmax statistics
                             // of LM-head logits, so the CE pass reads each logit row once
+  EPI_ADD_F32_T = 7,   // out[0] (fp32) [n * ldo + m] += alpha*acc: the transposed accumulate that
+                       // gemm_bf16 launches for EPI_ADD_F32 when C^T = B A^T tiles the SMs better
 };
 
 // Column blocks of width split_w go to out[n / split_w] (row pitch ldo[...]) so one GEMM can
@@ -47,6 +49,9 @@ struct EpiParams {
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
                cudaStream_t stream);
 int gemm_choose_splits(int M, int N, int K);
+// EPI_ADD_F32 GEMMs (dW accumulates) run as C^T = B A^T when the wave model prefers that shape
+bool gemm_prefer_transposed(int M, int N, int K);
+void gemm_set_transpose(int mode);  // 0 never, 1 modelled (default), 2 always
 int gemm_pick_bn(int N, bool b_mn_major);
 int gemm_pick_bn2(int M, int N);
 // 2-CTA (cta_group::2) tiles for M >= 256 (default on); 0 forces the single-CTA kernel.

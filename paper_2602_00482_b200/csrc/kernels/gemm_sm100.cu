@@ -189,7 +189,8 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ bool epi_f32_out(int mode) {
-  return mode == EPI_STORE_F32 || mode == EPI_STORE_F32_STATS || mode == EPI_ADD_F32 || mode == EPI_RESID_F32;
+  return mode == EPI_STORE_F32 || mode == EPI_STORE_F32_STATS || mode == EPI_ADD_F32 || mode == EPI_RESID_F32 ||
+         mode == EPI_ADD_F32_T;
 }
 
 // This thread's row (lane) of a 32-column chunk -> the warp's staging slot `buf`.
@@ -234,6 +235,11 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
       for (int u = 0; u < 8; ++u)
         *reinterpret_cast<float4*>(buf + sw128_off(lane, u)) =
             make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+      break;
+    case EPI_ADD_F32_T:  // staged transposed: 32 columns x 32 rows (128B swizzled), conflict-free
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        *reinterpret_cast<float*>(buf + sw128_off(c, lane >> 2) + (lane & 3) * 4) = v[c];
       break;
     case EPI_RESID_F32:  // out = resid + acc (model.hpp:427-428,447-448); resid chunk already in buf
 #pragma unroll
@@ -530,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             const CUtensorMap* tm = blk == 0 ? &tm_o0 : (blk == 1 ? &tm_o1 : &tm_o2);
             if (mode == EPI_ADD_F32) tma_reduce_add_2d(tm, buf, xc, row0);
+            else if (mode == EPI_ADD_F32_T) tma_reduce_add_2d(tm, buf, row0, n0);
             else tma_store_2d(tm, buf, xc, row0);
             if (mode == EPI_SILU) tma_store_2d(&tm_x, buf + 2048, n0, row0);
             bulk_commit();
@@ -662,7 +669,8 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   if (splits > 1) e.atomic = 1;
   // output tensor maps (and the epilogue operand map: silu output / dsilu input / residual input)
   const bool f32 = e.mode == EPI_STORE_F32 || e.mode == EPI_STORE_F32_STATS || e.mode == EPI_ADD_F32 ||
-                   e.mode == EPI_RESID_F32;
+                   e.mode == EPI_RESID_F32 || e.mode == EPI_ADD_F32_T;
+  if (e.mode == EPI_ADD_F32_T && e.split_w > 0) throw std::invalid_argument("gemm epilogue: transposed add takes no split_w");
   if (e.split_w > 0 && (e.split_w % 32 != 0 || e.mode == EPI_SILU || e.mode == EPI_DSILU || e.mode == EPI_RESID_F32))
     throw std::invalid_argument("gemm epilogue: split_w must be a multiple of 32 (store / add modes only)");
   CUtensorMap to[3], tx;
@@ -671,7 +679,9 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   const uint64_t width = e.split_w > 0 ? static_cast<uint64_t>(e.split_w) : static_cast<uint64_t>(N);
   const int nout = e.split_w > 0 ? (N + e.split_w - 1) / e.split_w : 1;
   if (nout > 3) throw std::invalid_argument("gemm epilogue: at most 3 column blocks");
-  for (int i = 0; i < nout; ++i) make_tmap_epi(&to[i], e.out[i], f32, width, M, e.ldo[i]);
+  if (e.mode == EPI_ADD_F32_T) make_tmap_epi(&to[0], e.out[0], true, M, N, e.ldo[0]);  // [N][M] output
+  else
+    for (int i = 0; i < nout; ++i) make_tmap_epi(&to[i], e.out[i], f32, width, M, e.ldo[i]);
   if (e.mode == EPI_SILU) make_tmap_epi(&tx, e.out2, false, N, M, e.ldo2);
   if (e.mode == EPI_DSILU) make_tmap_epi(&tx, e.aux, false, N, M, e.ld_aux);
   if (e.mode == EPI_RESID_F32) make_tmap_epi(&tx, e.resid, true, N, M, e.ld_resid);
@@ -760,7 +770,14 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
                cudaStream_t stream) {
   if (M <= 0 || N <= 0 || K <= 0) return;
   if (N % 16 != 0) throw std::invalid_argument("gemm_bf16: N must be a multiple of 16");
-  if (splits > 1 && epi.mode != EPI_ADD_F32) throw std::invalid_argument("gemm_bf16: split-K needs EPI_ADD_F32");
+  if (splits > 1 && epi.mode != EPI_ADD_F32 && epi.mode != EPI_ADD_F32_T)
+    throw std::invalid_argument("gemm_bf16: split-K needs EPI_ADD_F32");
+  if (epi.mode == EPI_ADD_F32 && epi.split_w == 0 && gemm_prefer_transposed(M, N, K)) {
+    // C += A B^T  <=>  C^T += B A^T with a transposed epilogue (operand views swap roles unchanged)
+    EpiParams et = epi;
+    et.mode = EPI_ADD_F32_T;
+    return gemm_bf16(B, A, N, M, K, et, gemm_choose_splits(N, M, K), stream);
+  }
   const bool amn = A.mn_major, bmn = B.mn_major;
 #define TTB_DISPATCH(BN_, CG_)                                                                      \
   if (!amn && bmn) return launch<BN_, CG_, false, true>(A, B, M, N, K, epi, splits, stream);  \
@@ -819,6 +836,43 @@ int gemm_choose_splits(int M, int N, int K) {
     }
   }
   return best_s;
+}
+
+// Wave model of one launch in SM-seconds: waves x (per-unit tile FLOPs / K-split) / unit rate, with the
+// narrower tiles' per-FLOP overhead (pick_bn / pick_bn2 weights) and the split reduce traffic.
+static double gemm_est_cost(int M, int N, int K) {
+  const bool two = gemm_use_2cta(M, N);
+  const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
+  const double f = two ? (bn == 256 ? 1.0 : 1.25) : (bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.10));
+  const long units = two ? g_num_sms / 2 : g_num_sms;
+  const long tiles = (two ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM) * static_cast<long>((N + bn - 1) / bn);
+  const int sp = gemm_choose_splits(M, N, K);
+  const double waves = static_cast<double>((tiles * sp + units - 1) / units);
+  const double tile_flops = 2.0 * (two ? 2 * BM : BM) * bn * static_cast<double>(K) / sp;
+  const double red = sp > 1 ? sp * static_cast<double>(M) * N * 4.0 / 2.5e12 : 0.0;
+  return waves * tile_flops * f / ((two ? 2.0 : 1.0) * 9e12) + red;
+}
+
+// Measured (profiles/r1): dW_out 4864 x 896 x 32768 ran at 763 TFLOP/s as 133 128-wide pair tiles
+// on 74 pairs (1.8 waves), its transpose 896 x 4864 at 1234 as 133 single-CTA 128 x 256 tiles in
+// one wave. Transpose only on a clear (>10%) modelled win; TT_GEMM_TRANSPOSE (or gemm_set_transpose):
+// 0 = never, 1 = modelled (default), 2 = always.
+static int g_gemm_transpose = [] {
+  const char* e = std::getenv("TT_GEMM_TRANSPOSE");
+  return e ? std::atoi(e) : 1;
+}();
+void gemm_set_transpose(int mode) { g_gemm_transpose = mode; }
+
+bool gemm_prefer_transposed(int M, int N, int K) {
+  const int mode = g_gemm_transpose;
+  if (mode == 0 || M % 16 != 0 || N % 16 != 0 || M == N) return false;
+  if (mode == 2) return true;  // force (tests)
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return gemm_est_cost(N, M, K) < 0.9 * gemm_est_cost(M, N, K);
 }
 
 }  // namespace ttb

@@ -81,6 +81,26 @@ def test_gemm_dw_mnmajor_mnmajor(T, Kw, Nw, splits):
     assert _rel(g, ref) < 1e-5
 
 
+@pytest.mark.parametrize("T,Kw,Nw,splits", [(2048, 4864, 896, 1), (512, 896, 4864, 1), (700, 256, 896, 2),
+                                            (333, 4864, 128, 1), (96, 1000, 48, 1)])
+@pytest.mark.parametrize("tmode", [2, 1], ids=["forced", "model"])
+def test_gemm_dw_transposed_epilogue(T, Kw, Nw, splits, tmode):
+    """dW += X^T dY computed as dW^T = dY^T X with the transposed reduce-add epilogue (EPI_ADD_F32_T)."""
+    torch.manual_seed(3)
+    x = torch.randn(T, Kw, device="cuda").bfloat16()
+    dy = torch.randn(T, Nw, device="cuda").bfloat16()
+    g = torch.randn(Kw, Nw + 16, device="cuda")  # padded pitch
+    g0 = g.clone()
+    _lib().tt_debug_gemm_set_transpose(tmode)
+    try:
+        _gemm(x, 1, dy, 1, Kw, Nw, T, EPI_ADD_F32, [g], Nw + 16, splits=splits)
+    finally:
+        _lib().tt_debug_gemm_set_transpose(1)
+    ref = g0[:, :Nw] + x.float().t() @ dy.float()
+    assert _rel(g[:, :Nw], ref) < 1e-5
+    assert torch.equal(g[:, Nw:], g0[:, Nw:])
+
+
 def test_gemm_split_columns_qkv():
     torch.manual_seed(3)
     M, d = 200, 256

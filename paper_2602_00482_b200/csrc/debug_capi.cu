@@ -189,6 +189,20 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
               k128b.insert(k128b.end(), {so, 1});
             }
         }
+        {  // longest first, as build_meta orders them
+          const size_t ni = k128.size() / 4;
+          std::vector<int> order(ni), a4(ni * 4), a2(ni * 2);
+          for (size_t i = 0; i < ni; ++i) order[i] = static_cast<int>(i);
+          std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+            return k128[4 * x + 3] - k128[4 * x + 2] > k128[4 * y + 3] - k128[4 * y + 2];
+          });
+          for (size_t i = 0; i < ni; ++i) {
+            for (int j = 0; j < 4; ++j) a4[4 * i + j] = k128[4 * order[i] + j];
+            for (int j = 0; j < 2; ++j) a2[2 * i + j] = k128b[2 * order[i] + j];
+          }
+          k128.swap(a4);
+          k128b.swap(a2);
+        }
         void *dk128 = up(k128), *dk128b = up(k128b);
         timed([&] {
           ttb::attn_bwd_sm100(a, rows_cap, static_cast<const int4*>(d128), static_cast<int>(q128.size() / 4),

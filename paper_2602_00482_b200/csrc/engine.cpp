@@ -394,6 +394,22 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
         b.kvit128_2.insert(b.kvit128_2.end(), {0, 0});
       }
   }
+  {
+    // longest first: the persistent dK/dV kernel deals items to CTAs in snake order (~LPT balance)
+    const size_t ni = b.kvit128.size() / 4;
+    std::vector<int32_t> order(ni);
+    for (size_t i = 0; i < ni; ++i) order[i] = static_cast<int32_t>(i);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+      return b.kvit128[4 * x + 3] - b.kvit128[4 * x + 2] > b.kvit128[4 * y + 3] - b.kvit128[4 * y + 2];
+    });
+    std::vector<int32_t> k4(ni * 4), k2(ni * 2);
+    for (size_t i = 0; i < ni; ++i) {
+      std::memcpy(&k4[4 * i], &b.kvit128[4 * order[i]], 16);
+      std::memcpy(&k2[2 * i], &b.kvit128_2[2 * order[i]], 8);
+    }
+    b.kvit128.swap(k4);
+    b.kvit128_2.swap(k2);
+  }
   b.o_tok = put(b.tokens.data(), b.tokens.size() * 4);
   b.o_pos = put(b.positions.data(), b.positions.size() * 4);
   b.o_qblk = put(b.qblk.data(), b.qblk.size() * 4);

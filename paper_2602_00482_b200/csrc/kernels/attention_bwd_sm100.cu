@@ -837,6 +837,12 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
   constexpr int NSK = DH == 64 ? 8 : 4;  // dkdv kernel Q/dO stages
   using CQ = DqCfg<DH, NSQ>;
   using CK = DkvCfg<DH, NSK>;
+  static const int part = [] {  // TT_ATTN_BWD_PART (timing experiments): 1 = dQ kernel only, 2 = dK/dV only
+    const char* e = std::getenv("TT_ATTN_BWD_PART");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (part == 2) n_dq = 0;
+  if (part == 1) n_kv = 0;
   const int d = a.H * DH;
   BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0,
               dq_blocks, nullptr, a.scale,

@@ -489,6 +489,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       const int row0 = m_blk * TM + static_cast<int>(rank) * BM + quad * 32;  // this warp's first row
       const int n_base = n_blk * BN + half * CW;
+      if (need_ld && !ld_ahead && n_base < N) {
+        // the tile's first epilogue operand chunk loads while its main loop still runs
+        const int slot = C::kSlots == 2 ? static_cast<int>(gc & 1) : 0;
+        if (lane == 0) {
+          bulk_wait_read<C::kSlots - 1>();
+          mbar_arrive_expect_tx(&wld[slot], ld_bytes);
+          tma_load_2d(&tm_x, &wld[slot], stg + slot * 4096, n_base, row0);
+        }
+        __syncwarp();
+        ld_ahead = true;
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + half * CW + (static_cast<uint32_t>(quad * 32) << 16);

@@ -16,6 +16,8 @@ GEMM_ONLY="fwd head" timeout 300 ncu --set full --clock-control none --import-so
   -o $O/${T}_gemm_head python tools/gemm_shapes.py > $O/${T}_ncu_gemm.log 2>&1
 GEMM_ONLY="fwd mlp_in" timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 2 -c 1 \
   -o $O/${T}_gemm_mlp_in python tools/gemm_shapes.py >> $O/${T}_ncu_gemm.log 2>&1
+GEMM_ONLY="dW mlp_out" timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 2 -c 1 \
+  -o $O/${T}_gemm_dw_mlp_out python tools/gemm_shapes.py >> $O/${T}_ncu_gemm.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:fa_fwd -s 2 -c 1 \
   -o $O/${T}_attn_fwd python tools/attn_bench.py 1 1 8192 1024 14 64 > $O/${T}_ncu_attn.log 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:fa_bwd -s 4 -c 2 \

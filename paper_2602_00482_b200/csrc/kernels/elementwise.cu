@@ -85,57 +85,65 @@ __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float* __restric
   }
 }
 
-// rmsnorm_backward (model.hpp:258-271), one warp per row, rows warp-strided over a ~2-wave grid:
+// rmsnorm_backward (model.hpp:258-271), WPR warps per row, row groups strided over a ~2-wave grid:
 //   gx = gres + gy*g*inv - x*(sum(gy*g*x)*inv^3/d);  ggain += sum_rows gy*x*inv
-// Each lane owns VPT float4 columns (c = (lane + 32 k) * 4); the row is held in registers when it
-// fits (KEEP), the gain-gradient partial stays in registers for all of the warp's rows, is reduced
-// across the block's warps in shared memory and lands with one red.global.add.v4 per column group.
-template <int VPT>
+// Each lane of a row group owns VPT float4 columns (c = (lr + 32 WPR k) * 4, lr = lane within the
+// group); the row is held in registers, the dot product is reduced across the group's warps through
+// shared memory (double-buffered, one barrier per row step), the gain-gradient partial stays in
+// registers for all of the group's rows, is reduced across the block in shared memory and lands with
+// one red.global.add.v4 per column group. WPR > 1 keeps VPT <= 8 for wide rows (d = 3584: one warp
+// per row needed 28 float4 per lane, 254 registers, 8 warps per SM and 1.6 TB/s).
+template <int VPT, int WPR>
 __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float* __restrict__ gy, const float* __restrict__ x,
                                                           const float* __restrict__ inv, const float* __restrict__ gain,
                                                           const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
                                                           float* __restrict__ ggain, int n, int d) {
-  constexpr bool KEEP = VPT <= 12;
+  constexpr int RPB = 8 / WPR;     // rows per block step
+  constexpr int STRIDE = 32 * WPR;  // float4 column stride between a lane's groups
   extern __shared__ float gsum[];  // [d]
+  __shared__ float red[2][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rloc = warp / WPR, lr = (warp % WPR) * 32 + lane;
   for (int c = threadIdx.x; c < d; c += 256) gsum[c] = 0.f;
-  float4 gacc[VPT];
-  float4 av[KEEP ? VPT : 1], bv[KEEP ? VPT : 1];
+  float4 gacc[VPT], av[VPT], bv[VPT];
 #pragma unroll
   for (int k = 0; k < VPT; ++k) gacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int nw = gridDim.x * 8;
-  for (int r = blockIdx.x * 8 + warp; r < n; r += nw) {
+  int step = 0;
+  for (int base = blockIdx.x * RPB; base < n; base += gridDim.x * RPB, ++step) {
+    const int r = base + rloc;
+    const bool valid = r < n;
     const long o = static_cast<long>(r) * d;
-    const float iv = inv[r];
+    const float iv = valid ? inv[r] : 0.f;
     float dot = 0.f;
+    if (valid) {
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int c = (lane + k * 32) * 4;
-      if (c < d) {
-        const float4 a = __ldcs(reinterpret_cast<const float4*>(gy + o + c));
-        const float4 b = *reinterpret_cast<const float4*>(x + o + c);
-        const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
-        dot += a.x * g.x * b.x + a.y * g.y * b.y + a.z * g.z * b.z + a.w * g.w * b.w;
-        if constexpr (KEEP) {
+      for (int k = 0; k < VPT; ++k) {
+        const int c = (lr + k * STRIDE) * 4;
+        if (c < d) {
+          const float4 a = __ldcs(reinterpret_cast<const float4*>(gy + o + c));
+          const float4 b = *reinterpret_cast<const float4*>(x + o + c);
+          const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
+          dot += a.x * g.x * b.x + a.y * g.y * b.y + a.z * g.z * b.z + a.w * g.w * b.w;
           av[k] = a;
           bv[k] = b;
         }
       }
     }
     dot = warp_sum(dot);
+    if constexpr (WPR > 1) {
+      if (lane == 0) red[step & 1][warp] = dot;
+      __syncthreads();
+      dot = 0.f;
+#pragma unroll
+      for (int j = 0; j < WPR; ++j) dot += red[step & 1][rloc * WPR + j];
+    }
+    if (!valid) continue;
     const float scale = dot * iv * iv * iv / static_cast<float>(d);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-      const int c = (lane + k * 32) * 4;
+      const int c = (lr + k * STRIDE) * 4;
       if (c < d) {
-        float4 a, b;
-        if constexpr (KEEP) {
-          a = av[k];
-          b = bv[k];
-        } else {
-          a = *reinterpret_cast<const float4*>(gy + o + c);
-          b = *reinterpret_cast<const float4*>(x + o + c);
-        }
+        const float4 a = av[k], b = bv[k];
         const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
         float4 res = gres ? *reinterpret_cast<const float4*>(gres + o + c) : make_float4(0.f, 0.f, 0.f, 0.f);
         res.x += a.x * g.x * iv - b.x * scale;
@@ -157,7 +165,7 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float* __restric
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int c = (lane + k * 32) * 4;
+    const int c = (lr + k * STRIDE) * 4;
     if (c < d) {
       atomicAdd(gsum + c, gacc[k].x);
       atomicAdd(gsum + c + 1, gacc[k].y);
@@ -169,11 +177,12 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float* __restric
   for (int c = threadIdx.x * 4; c < d; c += 1024) red_add_v4_f32(ggain + c, gsum[c], gsum[c + 1], gsum[c + 2], gsum[c + 3]);
 }
 
-template <int VPT>
+template <int VPT, int WPR>
 void launch_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres,
                         float* gx, __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
-  const int blocks = std::min((n + 7) / 8, 148 * 2);
-  rmsnorm_bwd_kernel<VPT><<<blocks, 256, d * sizeof(float), s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
+  constexpr int RPB = 8 / WPR;
+  const int blocks = std::min((n + RPB - 1) / RPB, 148 * 2);
+  rmsnorm_bwd_kernel<VPT, WPR><<<blocks, 256, d * sizeof(float), s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
 }
 
 // Weighted NLL over one vocab row with several (target, weight) pairs (weighted_nll,
@@ -383,14 +392,14 @@ void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16*
 void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
                    __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
   if (n <= 0) return;
-  const int vpt = (d + 127) / 128;  // float4 column groups per lane
-  if (vpt <= 2) launch_rmsnorm_bwd<2>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else if (vpt <= 4) launch_rmsnorm_bwd<4>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else if (vpt <= 7) launch_rmsnorm_bwd<7>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else if (vpt <= 12) launch_rmsnorm_bwd<12>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else if (vpt <= 16) launch_rmsnorm_bwd<16>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else if (vpt <= 28) launch_rmsnorm_bwd<28>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else launch_rmsnorm_bwd<64>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  const int vpt = (d + 127) / 128;  // float4 column groups per lane with one warp per row
+  if (vpt <= 2) launch_rmsnorm_bwd<2, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 4) launch_rmsnorm_bwd<4, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 7) launch_rmsnorm_bwd<7, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 14) launch_rmsnorm_bwd<7, 2>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 28) launch_rmsnorm_bwd<7, 4>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 64) launch_rmsnorm_bwd<8, 8>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else throw std::invalid_argument("rmsnorm backward: d_model > 8192");
 }
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
           __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {

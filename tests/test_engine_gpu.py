@@ -131,6 +131,21 @@ def test_tree_step_prefix_contained_and_deep():
         tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig(sibling_batch=sb))
 
 
+@pytest.mark.parametrize("tmode", [0, 2], ids=["dw_plain", "dw_transposed"])
+def test_tree_step_gemm_orientation_vs_oracle(tmode):
+    """Every dW / LM-head dX accumulate as C += A B^T (mode 0) or as C^T += B A^T (mode 2, the
+    transposed reduce-add epilogue) gives the oracle's loss and gradients."""
+    from paper_2602_00482_b200 import _native
+
+    cfg, flat, eng = make(C1, 11)
+    seqs = O.grouped_corpus(2, 4, 200, 120, cfg.vocab_size, 12, shared_response=6, weight_jitter=True)
+    _native.lib().tt_debug_gemm_set_transpose(tmode)
+    try:
+        tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
+    finally:
+        _native.lib().tt_debug_gemm_set_transpose(1)
+
+
 def test_tree_step_dh128():
     cfg, flat, eng = make(DH128, 5)
     seqs = O.grouped_corpus(2, 4, 130, 90, cfg.vocab_size, 6, shared_response=5)

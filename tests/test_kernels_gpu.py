@@ -169,7 +169,8 @@ def test_gemm_logits_with_softmax_stats(M, N):
     assert torch.allclose(lse, torch.logsumexp(out, -1), atol=1e-5)
 
 
-@pytest.mark.parametrize("n,d", [(1, 256), (37, 896), (4099, 896), (300, 1536), (129, 3584)])
+@pytest.mark.parametrize("n,d", [(1, 256), (37, 896), (4099, 896), (300, 1536), (129, 3584), (1001, 3584), (33, 2048),
+                                 (77, 4096), (5, 8192)])
 def test_rmsnorm_bwd_matches_torch(n, d):
     torch.manual_seed(7)
     lib = _lib()

@@ -827,6 +827,8 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       a.nitems = static_cast<int>(b.kvit.size() / 4);
       a.scale = scale;
       if (attn_bwd_impl_ == 1) {
+        a.dq16 = dqkv;  // dQ straight into the q block of the packed [dq | dk | dv] operand
+        a.lddq16 = 3 * d;
         tag("attn_bwd_sm100");
         run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
           attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_qblk128), static_cast<int>(b.qblk128.size() / 4),
@@ -842,8 +844,13 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       }
     }
     // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
-    tag("k_pack_dqkv");
-    run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
+    if (attn_bwd_impl_ == 1) {
+      tag("k_pack_dkv");
+      run(KC_ELEMWISE, 0, nd * 20, [&] { k_pack_dkv(dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
+    } else {
+      tag("k_pack_dqkv");
+      run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
+    }
     {  // dW_{q,k,v} += normed1^T [dq | dk | dv]  (model.hpp:610-612)
       EpiParams e;
       e.mode = EPI_ADD_F32;

@@ -38,6 +38,10 @@ struct AttnBwdArgs {
   float* D = nullptr;          // [H x n] scratch: rowsum(dO * O)
   float* dq = nullptr;         // [n x lddq] fp32, accumulated
   long lddq = 0;
+  // tcgen05 path: when set, dQ (scaled) goes straight to bf16 [n x lddq16] (the q block of the
+  // packed dqkv operand) instead of fp32 dq
+  __nv_bfloat16* dq16 = nullptr;
+  long lddq16 = 0;
   float* dk = nullptr;  // fp32 dK/dV stack rows (absolute), accumulated
   float* dv = nullptr;
   long lddkv = 0;

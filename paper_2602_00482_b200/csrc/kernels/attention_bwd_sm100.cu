@@ -74,6 +74,8 @@ struct BwdParams {
   const float* D;    // [H x n]
   float* dq;         // [n x lddq]
   long lddq;
+  __nv_bfloat16* dq16;  // if set: bf16 dQ [n x lddq16] instead of dq
+  long lddq16;
   float* dk;  // stack rows (this layer), fp32
   float* dv;
   long lddkv;
@@ -288,7 +290,15 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
       uint32_t r[16];
       tmem_ld16(t_dQ + c + lane_off, r);
       tmem_ld_wait();
-      if (row_ok) {
+      if (row_ok && p.dq16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          w[i] = pack_bf16x2(__uint_as_float(r[2 * i]) * p.scale, __uint_as_float(r[2 * i + 1]) * p.scale);
+        uint4* dst = reinterpret_cast<uint4*>(p.dq16 + static_cast<long>(row) * p.lddq16 + h * DH + c);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      } else if (row_ok) {
         float4* dst = reinterpret_cast<float4*>(p.dq + static_cast<long>(row) * p.lddq + h * DH + c);
 #pragma unroll
         for (int i = 0; i < 4; ++i)
@@ -844,7 +854,7 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
   if (part == 2) n_dq = 0;
   if (part == 1) n_kv = 0;
   const int d = a.H * DH;
-  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0,
+  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dq16, a.lddq16, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0,
               dq_blocks, nullptr, a.scale,
               a.scale * kLog2e};
   if (n_dq > 0) {

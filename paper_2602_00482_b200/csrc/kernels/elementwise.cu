@@ -333,6 +333,21 @@ __global__ void pack_dqkv_kernel(const float* __restrict__ dq, float* __restrict
   }
 }
 
+__global__ void pack_dkv_kernel(float* __restrict__ dk, float* __restrict__ dv, __nv_bfloat16* __restrict__ out,
+                                int d) {
+  const int r = blockIdx.x;
+  const long o = static_cast<long>(r) * d;
+  __nv_bfloat16* orow = out + static_cast<long>(r) * 3 * d;
+  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
+    const float4 b = *reinterpret_cast<float4*>(dk + o + c);
+    const float4 e = *reinterpret_cast<float4*>(dv + o + c);
+    *reinterpret_cast<uint2*>(orow + d + c) = make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+    *reinterpret_cast<uint2*>(orow + 2 * d + c) = make_uint2(pack_bf16x2(e.x, e.y), pack_bf16x2(e.z, e.w));
+    *reinterpret_cast<float4*>(dk + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    *reinterpret_cast<float4*>(dv + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // dE[tok[r]] += gx[r]   (model.hpp:627-630)
 __global__ void embed_grad_kernel(const float* __restrict__ gx, const int32_t* __restrict__ tok,
                                   float* __restrict__ gemb, int d) {
@@ -421,6 +436,9 @@ void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m,
 }
 void k_pack_dqkv(const float* dq, float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s) {
   if (n > 0) pack_dqkv_kernel<<<n, 128, 0, s>>>(dq, dk, dv, out, d);
+}
+void k_pack_dkv(float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s) {
+  if (n > 0) pack_dkv_kernel<<<n, 128, 0, s>>>(dk, dv, out, d);
 }
 void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s) {
   if (n > 0) embed_grad_kernel<<<n, 128, 0, s>>>(gx, tok, gemb, d);

@@ -22,6 +22,8 @@ void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloa
                         cudaStream_t s);
 void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m, int d, cudaStream_t s);
 void k_pack_dqkv(const float* dq, float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s);
+// the k/v blocks only (dq already written as bf16 by the attention backward): out row pitch 3d
+void k_pack_dkv(float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s);
 void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s);
 void k_f32_to_bf16_2d(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s);
 void k_init_normal(float* out, long n, uint64_t seed, float stdv, cudaStream_t s);

@@ -419,23 +419,29 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bwd_kernel(AttnBwdArgs a) {
 }
 
 // D[h][r] = sum_c dO[r, h*dh+c] * O[r, h*dh+c]
+// D[h][r] = rowsum(dO * O) over head h's dh columns: one thread per 8 columns (16-byte loads), a
+// group of dh/8 lanes per (row, head) reduces with shuffles.
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
                                     long ld, float* __restrict__ D, int n, int H, int dh) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) / 32;
-  const int lane = threadIdx.x & 31;
-  if (w >= n * H) return;
-  const int r = w / H, h = w % H;
-  const __nv_bfloat16* a = dO + static_cast<long>(r) * ld + h * dh;
-  const __nv_bfloat16* b = O + static_cast<long>(r) * ld + h * dh;
+  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int gpr = dh / 8;  // threads per (row, head): 8 or 16
+  const int cols8 = H * gpr;
+  const long r = t / cols8;
+  const int j = static_cast<int>(t - r * cols8);
   float s = 0.f;
-  for (int c = lane * 2; c < dh; c += 64) {
-    const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(a + c));
-    const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(b + c));
-    s += x.x * y.x + x.y * y.y;
-  }
+  if (r < n) {
+    const uint4 x = *reinterpret_cast<const uint4*>(dO + r * ld + j * 8);
+    const uint4 y = *reinterpret_cast<const uint4*>(O + r * ld + j * 8);
+    const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* ya = reinterpret_cast<const __nv_bfloat162*>(&y);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
-  if (lane == 0) D[static_cast<long>(h) * n + r] = s;
+    for (int i = 0; i < 4; ++i) {
+      const float2 p = __bfloat1622float2(xa[i]), q = __bfloat1622float2(ya[i]);
+      s += p.x * q.x + p.y * q.y;
+    }
+  }
+  for (int o = gpr / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  if (r < n && (j % gpr) == 0) D[static_cast<long>(j / gpr) * n + r] = s;
 }
 
 template <int DH>
@@ -470,8 +476,11 @@ void attn_fwd(const AttnFwdArgs& a, cudaStream_t stream) {
 }
 
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream) {
-  const int warps = a.n * a.H;
-  if (warps > 0) attn_bwd_pre_kernel<<<(warps * 32 + 255) / 256, 256, 0, stream>>>(a.dO, a.o, a.ldq, a.D, a.n, a.H, a.dh);
+  const long threads = static_cast<long>(a.n) * a.H * (a.dh / 8);
+  if (a.ldq % 8 != 0) throw std::invalid_argument("attention backward: dO/O pitch must be a multiple of 8");
+  if (threads > 0)
+    attn_bwd_pre_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(a.dO, a.o, a.ldq, a.D, a.n,
+                                                                                         a.H, a.dh);
 }
 
 void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream) {

@@ -306,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;          // [2]
-  uint64_t* ld_bar = tempty_bar + 2;  // [kEpiWarps][2]: TMA loads of epilogue operands into the slots
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ld_bar + 2 * kEpiWarps);
+  uint64_t* ld_bar = tempty_bar + 2;  // [kEpiWarps][4]: TMA loads of epilogue operands into the slots
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ld_bar + 4 * kEpiWarps);
 
   const int warp = warp_id_sync();
   const int lane = threadIdx.x & 31;
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], kEpiWarps * CG);  // leader: epilogue warps of both CTAs
     }
-    for (int s = 0; s < 2 * kEpiWarps; ++s) mbar_init(&ld_bar[s], 1);
+    for (int s = 0; s < 4 * kEpiWarps; ++s) mbar_init(&ld_bar[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, C::kTmemCols);
@@ -475,10 +475,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int NCH = CW / 32;
     const int ew = warp - 2;
     uint8_t* stg = smem + C::kOffStage + ew * (C::kSlots * 4096);
-    uint64_t* wld = ld_bar + 2 * ew;
+    uint64_t* wld = ld_bar + 4 * ew;
     const int mode = epi.mode;
     const bool need_ld = mode == EPI_RESID_F32 || mode == EPI_DSILU;
     const uint32_t ld_bytes = epi_f32_out(mode) ? 4096u : 2048u;
+    // SiLU' epilogue (bf16 operand in, bf16 out, in place): all NCH chunks' operands fit in the slots
+    const bool whole_tile_ld = mode == EPI_DSILU && NCH <= 4 && C::kSlots * 4096 >= NCH * 2048;
     uint32_t gc = 0;        // chunks staged by this warp: slot = gc & 1
     uint32_t ld_phase = 0;  // per-slot parity of the operand-load barriers
     bool ld_ahead = false;  // the current chunk's operand load was issued during the previous chunk
@@ -489,7 +491,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       const int row0 = m_blk * TM + static_cast<int>(rank) * BM + quad * 32;  // this warp's first row
       const int n_base = n_blk * BN + half * CW;
-      if (need_ld && !ld_ahead && n_base < N) {
+      if (whole_tile_ld) {
+        // every chunk's bf16 operand (2 KB) gets its own quarter slot: all loads issued before the
+        // accumulator wait, so their HBM latency hides behind the main loop
+        if (lane == 0) {
+          bulk_wait_read<0>();
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch)
+            if (n_base + ch * 32 < N) {
+              mbar_arrive_expect_tx(&wld[ch], 2048u);
+              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_base + ch * 32, row0);
+            }
+        }
+        __syncwarp();
+      } else if (need_ld && !ld_ahead && n_base < N) {
         // the tile's first epilogue operand chunk loads while its main loop still runs
         const int slot = C::kSlots == 2 ? static_cast<int>(gc & 1) : 0;
         if (lane == 0) {
@@ -509,14 +524,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int ch = 0; ch < NCH; ++ch) {
         const int n0 = n_base + ch * 32;
         const bool active = n0 < N;  // warp-uniform
-        const int slot = C::kSlots == 2 ? static_cast<int>(gc & 1) : 0;
-        uint8_t* buf = stg + slot * 4096;
+        const int slot = whole_tile_ld ? ch : (C::kSlots == 2 ? static_cast<int>(gc & 1) : 0);
+        uint8_t* buf = whole_tile_ld ? stg + ch * 2048 : stg + slot * 4096;
         int blk = 0, xc = n0;
         if (epi.split_w > 0) {
           blk = n0 / epi.split_w;
           xc = n0 - blk * epi.split_w;
         }
-        if (active && !ld_ahead) {
+        if (active && !ld_ahead && !whole_tile_ld) {
           if (lane == 0) bulk_wait_read<C::kSlots - 1>();  // the store that last used this slot has read it
           __syncwarp();
           if (need_ld && lane == 0) {
@@ -555,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++gc;
           // operand epilogues (residual / SiLU input): start the next chunk's TMA load now, into the
           // other slot once its previous store has been read, so it overlaps this chunk's tail
-          if (C::kSlots == 2 && need_ld && ch + 1 < NCH && n0 + 32 < N) {
+          if (C::kSlots == 2 && need_ld && !whole_tile_ld && ch + 1 < NCH && n0 + 32 < N) {
             const int ns = static_cast<int>(gc & 1);
             if (lane == 0) {
               bulk_wait_read<1>();

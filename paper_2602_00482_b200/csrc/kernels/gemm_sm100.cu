@@ -481,6 +481,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t ld_bytes = epi_f32_out(mode) ? 4096u : 2048u;
     // SiLU' epilogue (bf16 operand in, bf16 out, in place): all NCH chunks' operands fit in the slots
     const bool whole_tile_ld = mode == EPI_DSILU && NCH <= 4 && C::kSlots * 4096 >= NCH * 2048;
+    // residual epilogue (fp32 operand, 4 KB per chunk): two chunks loaded ahead, one per slot
+    const bool two_ahead = need_ld && !whole_tile_ld && C::kSlots == 2;
     uint32_t gc = 0;        // chunks staged by this warp: slot = gc & 1
     uint32_t ld_phase = 0;  // per-slot parity of the operand-load barriers
     bool ld_ahead = false;  // the current chunk's operand load was issued during the previous chunk
@@ -501,6 +503,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (n_base + ch * 32 < N) {
               mbar_arrive_expect_tx(&wld[ch], 2048u);
               tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_base + ch * 32, row0);
+            }
+        }
+        __syncwarp();
+      } else if (two_ahead) {
+        if (lane == 0) {
+          bulk_wait_read<0>();
+#pragma unroll
+          for (int k = 0; k < 2 && k < NCH; ++k)
+            if (n_base + k * 32 < N) {
+              const int sl = static_cast<int>((gc + k) & 1);
+              mbar_arrive_expect_tx(&wld[sl], ld_bytes);
+              tma_load_2d(&tm_x, &wld[sl], stg + sl * 4096, n_base + k * 32, row0);
             }
         }
         __syncwarp();
@@ -531,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           blk = n0 / epi.split_w;
           xc = n0 - blk * epi.split_w;
         }
-        if (active && !ld_ahead && !whole_tile_ld) {
+        if (active && !ld_ahead && !whole_tile_ld && !two_ahead) {
           if (lane == 0) bulk_wait_read<C::kSlots - 1>();  // the store that last used this slot has read it
           __syncwarp();
           if (need_ld && lane == 0) {
@@ -570,7 +584,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++gc;
           // operand epilogues (residual / SiLU input): start the next chunk's TMA load now, into the
           // other slot once its previous store has been read, so it overlaps this chunk's tail
-          if (C::kSlots == 2 && need_ld && !whole_tile_ld && ch + 1 < NCH && n0 + 32 < N) {
+          if (two_ahead) {
+            // this chunk's slot takes chunk ch + 2 once the store just issued has read it
+            if (ch + 2 < NCH && n0 + 64 < N) {
+              const int ns = static_cast<int>((gc + 1) & 1);  // == slot (gc was incremented)
+              if (lane == 0) {
+                bulk_wait_read<0>();
+                mbar_arrive_expect_tx(&wld[ns], ld_bytes);
+                tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 64, row0);
+              }
+              __syncwarp();
+            }
+          } else if (C::kSlots == 2 && need_ld && !whole_tile_ld && ch + 1 < NCH && n0 + 32 < N) {
             const int ns = static_cast<int>(gc & 1);
             if (lane == 0) {
               bulk_wait_read<1>();

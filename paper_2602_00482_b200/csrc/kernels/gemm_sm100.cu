@@ -51,12 +51,13 @@ struct Cfg {
   static constexpr int kSlots = (CG == 1 && BN == 256) ? 1 : 2;
   static constexpr int kStageBudget = 227 * 1024 - kEpiWarps * kSlots * 4096 - 2048;
   static constexpr int kStages = kStageBudget / kStageBytes > 8 ? 8 : kStageBudget / kStageBytes;
-  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;  // two accumulator slots (power of 2)
+  static constexpr int kAccStride = BN == 224 ? 256 : BN;  // TMEM columns between the accumulator slots
+  static constexpr int kTmemCols = 2 * kAccStride <= 256 ? 256 : 512;  // two slots (power of 2)
   static constexpr int kOffBar = kStages * kStageBytes;
   static constexpr int kOffStage = kOffBar + 1024;  // epilogue staging: kEpiWarps x kSlots x 4 KB
   static constexpr int kSmem = kOffStage + kEpiWarps * kSlots * 4096 + 1024 /*align*/;
   static_assert(kSmem <= 227 * 1024, "GEMM smem budget");
-  static_assert(BNC % 64 == 0 || CG == 1, "2-CTA MN-major B needs 64-column halves");
+  static_assert(BNC % 64 == 0 || CG == 1 || BN == 224, "2-CTA MN-major B needs 64-column halves");
 };
 
 // ---- CTA-pair (cluster of 2) helpers
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const __grid_constant__ CUtensorMap tm_o2, const __grid_constant__ CUtensorMap tm_x, int M, int N,
                 int K, int splits, EpiParams epi) {
   using C = Cfg<BN, CG>;
+  static_assert(!B_MN || CG == 1 || C::BNC % 64 == 0, "BN = 224 pairs need a K-major B (112-row halves)");
   constexpr int TM = BM * CG;  // tile rows (per CTA pair when CG = 2)
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
   const bool leader = rank == 0;
@@ -426,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * C::kAccStride;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
@@ -470,9 +472,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // chunk c+1 is in flight while chunk c is staged; the accumulator slot is handed back to the MMA
     // warp as soon as its last chunk is in registers; stores drain asynchronously (TMA).
     const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) / 4;       // which half of the BN columns this warp handles
-    constexpr int CW = BN / 2;
-    constexpr int NCH = CW / 32;
+    const int half = (warp - 2) / 4;       // which 32-column chunks of the tile this warp handles
+    constexpr int NCHT = BN / 32;          // chunks per tile; warp half h takes chunks h, h + 2, ...
+    constexpr int NCH = (NCHT + 1) / 2;    // chunk slots per warp (the last may be empty: BN = 224)
     const int ew = warp - 2;
     uint8_t* stg = smem + C::kOffStage + ew * (C::kSlots * 4096);
     uint64_t* wld = ld_bar + 4 * ew;
@@ -492,7 +494,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       const int row0 = m_blk * TM + static_cast<int>(rank) * BM + quad * 32;  // this warp's first row
-      const int n_base = n_blk * BN + half * CW;
+      const int n_base = n_blk * BN + half * 32;  // this warp's first chunk; chunk c at n_base + 64 c
+      auto chunk_ok = [&](int c) { return 2 * c + half < NCHT && n_base + 64 * c < N; };
       if (whole_tile_ld) {
         // every chunk's bf16 operand (2 KB) gets its own quarter slot: all loads issued before the
         // accumulator wait, so their HBM latency hides behind the main loop
@@ -500,9 +503,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_read<0>();
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch)
-            if (n_base + ch * 32 < N) {
+            if (chunk_ok(ch)) {
               mbar_arrive_expect_tx(&wld[ch], 2048u);
-              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_base + ch * 32, row0);
+              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_base + 64 * ch, row0);
             }
         }
         __syncwarp();
@@ -511,14 +514,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_wait_read<0>();
 #pragma unroll
           for (int k = 0; k < 2 && k < NCH; ++k)
-            if (n_base + k * 32 < N) {
+            if (chunk_ok(k)) {
               const int sl = static_cast<int>((gc + k) & 1);
               mbar_arrive_expect_tx(&wld[sl], ld_bytes);
-              tma_load_2d(&tm_x, &wld[sl], stg + sl * 4096, n_base + k * 32, row0);
+              tma_load_2d(&tm_x, &wld[sl], stg + sl * 4096, n_base + 64 * k, row0);
             }
         }
         __syncwarp();
-      } else if (need_ld && !ld_ahead && n_base < N) {
+      } else if (need_ld && !ld_ahead && chunk_ok(0)) {
         // the tile's first epilogue operand chunk loads while its main loop still runs
         const int slot = C::kSlots == 2 ? static_cast<int>(gc & 1) : 0;
         if (lane == 0) {
@@ -531,13 +534,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + acc * BN + half * CW + (static_cast<uint32_t>(quad * 32) << 16);
+      const uint32_t t_row = tmem_base + acc * C::kAccStride + half * 32 + (static_cast<uint32_t>(quad * 32) << 16);
       uint32_t rr[2][32];
       tmem_ld32(t_row, rr[0]);
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        const int n0 = n_base + ch * 32;
-        const bool active = n0 < N;  // warp-uniform
+        const int n0 = n_base + 64 * ch;
+        const bool active = chunk_ok(ch);  // warp-uniform
         const int slot = whole_tile_ld ? ch : (C::kSlots == 2 ? static_cast<int>(gc & 1) : 0);
         uint8_t* buf = whole_tile_ld ? stg + ch * 2048 : stg + slot * 4096;
         int blk = 0, xc = n0;
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ld_ahead = false;
         tmem_ld_wait_regs(rr[ch & 1]);
         if (ch + 1 < NCH) {
-          tmem_ld32(t_row + (ch + 1) * 32, rr[(ch + 1) & 1]);
+          tmem_ld32(t_row + (ch + 1) * 64, rr[(ch + 1) & 1]);
         } else {
           tc_fence_before();
           __syncwarp();
@@ -586,21 +589,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           // other slot once its previous store has been read, so it overlaps this chunk's tail
           if (two_ahead) {
             // this chunk's slot takes chunk ch + 2 once the store just issued has read it
-            if (ch + 2 < NCH && n0 + 64 < N) {
+            if (ch + 2 < NCH && chunk_ok(ch + 2)) {
               const int ns = static_cast<int>((gc + 1) & 1);  // == slot (gc was incremented)
               if (lane == 0) {
                 bulk_wait_read<0>();
                 mbar_arrive_expect_tx(&wld[ns], ld_bytes);
-                tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 64, row0);
+                tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 128, row0);
               }
               __syncwarp();
             }
-          } else if (C::kSlots == 2 && need_ld && !whole_tile_ld && ch + 1 < NCH && n0 + 32 < N) {
+          } else if (C::kSlots == 2 && need_ld && !whole_tile_ld && ch + 1 < NCH && chunk_ok(ch + 1)) {
             const int ns = static_cast<int>(gc & 1);
             if (lane == 0) {
               bulk_wait_read<1>();
               mbar_arrive_expect_tx(&wld[ns], ld_bytes);
-              tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 32, row0);
+              tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 64, row0);
             }
             __syncwarp();
             ld_ahead = true;
@@ -835,6 +838,16 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
   if (!amn && !bmn) return launch<BN_, CG_, false, false>(A, B, M, N, K, epi, splits, stream); \
   if (amn && bmn) return launch<BN_, CG_, true, true>(A, B, M, N, K, epi, splits, stream);     \
   return launch<BN_, CG_, true, false>(A, B, M, N, K, epi, splits, stream);
+  static const bool bn224 = [] {  // TT_GEMM_BN224=0 disables the 224-wide pair tiles (A/B timing)
+    const char* e = std::getenv("TT_GEMM_BN224");
+    return !(e && std::atoi(e) == 0);
+  }();
+  if (bn224 && !bmn && N % 256 != 0 && N % 224 == 0 && gemm_use_2cta(M, N)) {
+    // N = 896 (d of the 0.5B shape): 4 x 224 columns instead of 3.5 x 256 (12.5% padding); each CTA
+    // stages 112 rows of the K-major B
+    if (!amn) return launch<224, 2, false, false>(A, B, M, N, K, epi, splits, stream);
+    return launch<224, 2, true, false>(A, B, M, N, K, epi, splits, stream);
+  }
   if (gemm_use_2cta(M, N)) {
     // CTA pairs: 256-row tiles; BN 128 or 256 (each CTA stages a 64-aligned half of B)
     if (gemm_pick_bn2(M, N) == 256) {

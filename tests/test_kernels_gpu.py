@@ -57,7 +57,8 @@ def test_gemm_fwd_kmajor_mnmajor(M, N, K):
     assert _rel(out, ref) < 1e-5
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 128, 256), (77, 896, 4864), (513, 256, 896), (100, 2688, 256)])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 256), (77, 896, 4864), (513, 256, 896), (100, 2688, 256),
+                                   (512, 896, 256), (4096, 896, 2688), (300, 448, 512), (1000, 672, 896)])
 def test_gemm_dx_kmajor_kmajor(M, N, K):
     torch.manual_seed(1)
     dy = torch.randn(M, K, device="cuda").bfloat16()        # [tokens x N_w]
@@ -99,6 +100,18 @@ def test_gemm_dw_transposed_epilogue(T, Kw, Nw, splits, tmode):
     ref = g0[:, :Nw] + x.float().t() @ dy.float()
     assert _rel(g[:, :Nw], ref) < 1e-5
     assert torch.equal(g[:, Nw:], g0[:, Nw:])
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 896, 320), (776, 448, 64)])  # MN-major A: M * 2 bytes % 16 == 0
+def test_gemm_amn_bk_224_wide_pair_tiles(M, N, K):
+    """A MN-major, B K-major, N a multiple of 224 but not of 256: the 224-wide CTA-pair tiles."""
+    torch.manual_seed(4)
+    a = torch.randn(K, M, device="cuda").bfloat16()  # A(m, k) at a[k, m]
+    b = torch.randn(N, K, device="cuda").bfloat16()
+    out = torch.empty(M, N + 32, device="cuda", dtype=torch.float32)
+    _gemm(a, 1, b, 0, M, N, K, EPI_STORE_F32, [out], N + 32)
+    ref = a.float().t() @ b.float().t()
+    assert _rel(out[:, :N], ref) < 1e-5
 
 
 def test_gemm_split_columns_qkv():

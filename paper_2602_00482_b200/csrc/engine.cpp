@@ -210,6 +210,12 @@ void Engine::upload_params(const float* flat, uint64_t n) {
     ck(cudaStreamSynchronize(stream_), "params upload");
     src += rows * cols;
   };
+  auto put_t = [&](uint64_t rows, uint64_t cols, bf16* dst, long ldd) {  // transposed device copy
+    ck(cudaMemcpyAsync(tmp.p, src, rows * cols * sizeof(float), cudaMemcpyHostToDevice, stream_), "params upload");
+    k_f32_to_bf16_2d_t(tmp.as<float>(), cols, dst, ldd, rows, cols, stream_);
+    ck(cudaStreamSynchronize(stream_), "params upload");
+    src += rows * cols;
+  };
   auto put_gain = [&](float* dst) {
     ck(cudaMemcpyAsync(dst, src, d_ * sizeof(float), cudaMemcpyHostToDevice, stream_), "params upload");
     src += d_;
@@ -223,7 +229,7 @@ void Engine::upload_params(const float* flat, uint64_t n) {
     put(d_, d_, wo_[l], d_);
     put_gain(mlp_g_[l]);
     put(d_, F_, win_[l], F_);
-    put(F_, d_, wout_[l], d_);
+    put_t(F_, d_, wout_[l], F_);  // device layout W_out^T [d x F] (see forward_batch)
   }
   put_gain(final_g_);
   put(d_, V_, head_, V_);
@@ -243,7 +249,7 @@ void Engine::init_random(uint64_t seed) {
     fill(d_, 3 * d_, wqkv_[l], 3 * d_);
     fill(d_, d_, wo_[l], d_);
     fill(d_, F_, win_[l], F_);
-    fill(F_, d_, wout_[l], d_);
+    fill(d_, F_, wout_[l], F_);  // W_out^T [d x F]
   }
   fill(d_, V_, head_, V_);
   k_fill(gainbuf_.as<float>(), (2 * L_ + 1) * d_, 1.0f, stream_);
@@ -611,7 +617,9 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       e.ldo[0] = d;
       e.resid = xmid;
       e.ld_resid = d;
-      gemm(op(act, F, false), op(wout_[l], d, true), n, d, F, e, 1);
+      // W_out is kept transposed on the device ([d x F], K-major B): the N = d output then tiles with
+      // the 224-wide pair tiles at d = 896; the grad_hidden GEMM reads it MN-major instead
+      gemm(op(act, F, false), op(wout_[l], F, false), n, d, F, e, 1);
     }
   }
   tag("k_rmsnorm_fwd");
@@ -765,7 +773,7 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       e.ldo[0] = F;
       e.aux = h;
       e.ld_aux = F;
-      gemm(op(gxb, d, false), op(wout_[l], d, false), n, F, d, e, 1);
+      gemm(op(gxb, d, false), op(wout_[l], F, true), n, F, d, e, 1);
     }
     {  // dW_in += normed2^T grad_hidden  (model.hpp:533)
       EpiParams e;

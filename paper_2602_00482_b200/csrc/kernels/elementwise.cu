@@ -360,6 +360,17 @@ __global__ void embed_grad_kernel(const float* __restrict__ gx, const int32_t* _
   }
 }
 
+// dst[c * ldd + r] = bf16(src[r * lds + c]) (parameter upload into a transposed device layout)
+__global__ void f32_to_bf16_2d_t_kernel(const float* __restrict__ src, long lds, __nv_bfloat16* __restrict__ dst,
+                                        long ldd, int rows, int cols) {
+  const long total = static_cast<long>(rows) * cols;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long c = i / rows, r = i % rows;
+    dst[c * ldd + r] = __float2bfloat16_rn(src[r * lds + c]);
+  }
+}
+
 __global__ void f32_to_bf16_2d_kernel(const float* __restrict__ src, long lds, __nv_bfloat16* __restrict__ dst,
                                       long ldd, int rows, int cols) {
   const long total = static_cast<long>(rows) * cols;
@@ -442,6 +453,12 @@ void k_pack_dkv(float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStre
 }
 void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s) {
   if (n > 0) embed_grad_kernel<<<n, 128, 0, s>>>(gx, tok, gemb, d);
+}
+void k_f32_to_bf16_2d_t(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s) {
+  const long total = static_cast<long>(rows) * cols;
+  if (total > 0)
+    f32_to_bf16_2d_t_kernel<<<static_cast<int>(std::min<long>((total + 255) / 256, 148 * 32)), 256, 0, s>>>(src, lds, dst,
+                                                                                                          ldd, rows, cols);
 }
 void k_f32_to_bf16_2d(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s) {
   const long total = static_cast<long>(rows) * cols;

@@ -26,6 +26,8 @@ void k_pack_dqkv(const float* dq, float* dk, float* dv, __nv_bfloat16* out, int 
 void k_pack_dkv(float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s);
 void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s);
 void k_f32_to_bf16_2d(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s);
+// transposed: dst[c * ldd + r] = bf16(src[r * lds + c])
+void k_f32_to_bf16_2d_t(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s);
 void k_init_normal(float* out, long n, uint64_t seed, float stdv, cudaStream_t s);
 void k_fill(float* out, long n, float v, cudaStream_t s);
 

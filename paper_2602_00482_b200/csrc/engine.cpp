@@ -181,6 +181,9 @@ void Engine::set_option(const std::string& key, int64_t value) {
   } else if (key == "root_batch_tokens") {
     if (value < 0) throw std::invalid_argument("root_batch_tokens must be >= 0");
     root_batch_tokens_ = value;
+  } else if (key == "head_chunk_mb") {
+    if (value < 64) throw std::invalid_argument("head_chunk_mb must be >= 64");
+    head_chunk_bytes_ = value << 20;
   } else if (key == "cuda_graph") {
     cuda_graph_ = value != 0;
   } else if (key == "ce_stats") {
@@ -327,8 +330,8 @@ void Engine::ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, in
     sc_dq_.ensure(n * d_ * 4);
     sc_dqkv_.ensure(n * 3 * d_ * 2);
   }
-  // LM-head / CE chunk: ~2 GB of fp32 logits + bf16 dlogits at most
-  const int64_t cap = std::max<int64_t>(128, (int64_t(2) << 30) / (V_ * 6) / 128 * 128);
+  // LM-head / CE chunk: head_chunk_bytes_ of fp32 logits + bf16 dlogits at most
+  const int64_t cap = std::max<int64_t>(128, head_chunk_bytes_ / (V_ * 6) / 128 * 128);
   const int64_t chunk = std::min<int64_t>(cap, std::max<int64_t>(max_loss_rows, 1));
   if (chunk > head_chunk_) {
     head_chunk_ = chunk;
@@ -640,8 +643,11 @@ void Engine::head_backward(const Batch& b, const bf16* nf) {
   bf16* dlog = sc_dlog_.as<bf16>();
   bf16* nfl = sc_nfl_.as<bf16>();
   float* gnf = sc_gnf_.as<float>();
-  for (int64_t c0 = 0; c0 < m; c0 += head_chunk_) {
-    const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, m - c0));
+  // equal chunks (multiples of 128 rows) rather than full ones plus a short tail
+  const int64_t nch = (m + head_chunk_ - 1) / head_chunk_;
+  const int64_t per = nch <= 1 ? head_chunk_ : std::min<int64_t>(head_chunk_, ((m + nch - 1) / nch + 127) / 128 * 128);
+  for (int64_t c0 = 0; c0 < m; c0 += per) {
+    const int cm = static_cast<int>(std::min<int64_t>(per, m - c0));
     tag("k_gather_rows_bf16");
     run(KC_ELEMWISE, 0, 4.0 * cm * d, [&] { k_gather_rows_bf16(nf, meta<int32_t>(b.o_lrows) + c0, nfl, cm, d, stream_); });
     {
@@ -909,7 +915,7 @@ uint64_t Engine::auto_batch_budget(uint64_t path_tokens) const {
                              sc_gxb_.bytes + sc_gxf_.bytes + sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes +
                              sc_dq_.bytes + sc_dqkv_.bytes);
   const double per_tok = bytes_per_token();
-  const double avail = 0.85 * (double(free_b) + held) - 6e9 - double(path_tokens) * per_tok;
+  const double avail = 0.85 * (double(free_b) + held) - 4e9 - double(head_chunk_bytes_) - double(path_tokens) * per_tok;
   const double tok = avail / per_tok;
   return tok < 2048 ? 2048 : static_cast<uint64_t>(tok);
 }

@@ -246,6 +246,9 @@ class Engine {
   // multi-root batching: consecutive forest roots whose children are all short leaves are pushed as
   // ONE batch of up to this many tokens (0 = off); each root's leaves attend to its own rows
   int64_t root_batch_tokens_ = 4096;
+  // LM-head chunk scratch (fp32 logits + bf16 dlogits): larger chunks mean fewer fp32 read-modify-
+  // write passes of the V x d head gradient (one per chunk)
+  int64_t head_chunk_bytes_ = int64_t(6) << 30;
   KStats kstats_;
   struct Pending {
     KClass cls;

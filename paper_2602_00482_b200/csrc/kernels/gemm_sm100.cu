@@ -876,13 +876,14 @@ int gemm_choose_splits(int M, int N, int K) {
   const bool two = gemm_use_2cta(M, N);
   const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
   // Time model: waves of (tile, K/s) items at ~9 TFLOP/s per SM, plus the fp32 reduce-add of every
-  // split's partial output through L2 (~2.5 TB/s). Split only when the tiles alone leave units idle
-  // (e.g. 49 tiles on 148 SMs: 3 splits = one wave, 4 splits = 1.3 waves); never for outputs whose
+  // split's partial output through L2 (~2.5 TB/s). Splits pay when the tiles leave units idle: 49
+  // tiles on 148 SMs (3 splits = one wave), or 104 pair tiles on 74 pairs (2 waves, the second 40%
+  // full; 2 splits = 3 half-length waves: the LM-head dX at 6656 loss rows); never for outputs whose
   // reduce traffic dominates (the LM-head dW: 896 x 151936 fp32).
   const long units = two ? g_num_sms / 2 : g_num_sms;
   const long tiles = (two ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM) * static_cast<long>((N + bn - 1) / bn);
   const int kb = (K + BK - 1) / BK;
-  if (kb < 8 || tiles >= units) return 1;
+  if (kb < 8) return 1;
   const double unit_rate = (two ? 2.0 : 1.0) * 9e12;
   const double tile_flops = 2.0 * (two ? 2 * BM : BM) * bn * static_cast<double>(K);
   auto cost = [&](int sp) {

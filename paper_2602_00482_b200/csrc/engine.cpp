@@ -330,8 +330,19 @@ void Engine::ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, in
     sc_dq_.ensure(n * d_ * 4);
     sc_dqkv_.ensure(n * 3 * d_ * 2);
   }
-  // LM-head / CE chunk: head_chunk_bytes_ of fp32 logits + bf16 dlogits at most
-  const int64_t cap = std::max<int64_t>(128, head_chunk_bytes_ / (V_ * 6) / 128 * 128);
+  // LM-head / CE chunk: head_chunk_bytes_ of fp32 logits + bf16 dlogits at most, and no more than a
+  // third of the memory still free after the buffers above (at least 2 GB)
+  int64_t head_bytes = head_chunk_bytes_;
+  {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      const int64_t room = (static_cast<int64_t>(free_b) + static_cast<int64_t>(sc_logits_.bytes + sc_dlog_.bytes)) / 3;
+      head_bytes = std::min<int64_t>(head_bytes, std::max<int64_t>(room, int64_t(2) << 30));
+    } else {
+      (void)cudaGetLastError();
+    }
+  }
+  const int64_t cap = std::max<int64_t>(128, head_bytes / (V_ * 6) / 128 * 128);
   const int64_t chunk = std::min<int64_t>(cap, std::max<int64_t>(max_loss_rows, 1));
   if (chunk > head_chunk_) {
     head_chunk_ = chunk;
@@ -915,7 +926,9 @@ uint64_t Engine::auto_batch_budget(uint64_t path_tokens) const {
                              sc_gxb_.bytes + sc_gxf_.bytes + sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes +
                              sc_dq_.bytes + sc_dqkv_.bytes);
   const double per_tok = bytes_per_token();
-  const double avail = 0.85 * (double(free_b) + held) - 4e9 - double(head_chunk_bytes_) - double(path_tokens) * per_tok;
+  // 6 GB: a 2 GB LM-head chunk + slack; the head chunk grows past 2 GB only into memory left free
+  // after the plan's own buffers (ensure_buffers)
+  const double avail = 0.85 * (double(free_b) + held) - 6e9 - double(path_tokens) * per_tok;
   const double tok = avail / per_tok;
   return tok < 2048 ? 2048 : static_cast<uint64_t>(tok);
 }

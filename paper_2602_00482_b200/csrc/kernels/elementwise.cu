@@ -277,17 +277,25 @@ __global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restri
       for (int u = 0; u < U; ++u) {
         const long c = c0 + u * kStep;
         if (c >= V) break;
-        float g[4] = {wsum * __expf(v[u].x - lse), wsum * __expf(v[u].y - lse), wsum * __expf(v[u].z - lse),
-                      wsum * __expf(v[u].w - lse)};
-        for (int p = p0; p < p1; ++p) {
-          const long t = tgt[p];
-          if (t >= c && t < c + 4) g[t - c] -= static_cast<float>(w[p]);
-        }
         uint2 o;
-        o.x = pack_bf16x2(g[0], g[1]);
-        o.y = pack_bf16x2(g[2], g[3]);
+        o.x = pack_bf16x2(wsum * __expf(v[u].x - lse), wsum * __expf(v[u].y - lse));
+        o.y = pack_bf16x2(wsum * __expf(v[u].z - lse), wsum * __expf(v[u].w - lse));
         *reinterpret_cast<uint2*>(dr + c) = o;
       }
+    }
+    // target columns: - sum_j w_j onehot(t_j), rewritten after the streaming pass (one thread per
+    // distinct target; the block barrier orders it after the pass's store of that column)
+    __syncthreads();
+    for (int p = p0 + static_cast<int>(threadIdx.x); p < p1; p += kCeThreads) {
+      const long t = tgt[p];
+      bool first = true;
+      float wt = 0.f;
+      for (int q = p0; q < p1; ++q)
+        if (tgt[q] == t) {
+          first = first && q >= p;
+          wt += static_cast<float>(w[q]);
+        }
+      if (first) dr[t] = __float2bfloat16_rn(wsum * __expf(lr[t] - lse) - wt);
     }
     if (threadIdx.x == 0) {
       double acc = 0.0;

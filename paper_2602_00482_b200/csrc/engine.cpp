@@ -184,6 +184,7 @@ void Engine::set_option(const std::string& key, int64_t value) {
   } else if (key == "head_chunk_mb") {
     if (value < 64) throw std::invalid_argument("head_chunk_mb must be >= 64");
     head_chunk_bytes_ = value << 20;
+    head_cap_rows_ = 0;
   } else if (key == "cuda_graph") {
     cuda_graph_ = value != 0;
   } else if (key == "ce_stats") {
@@ -332,17 +333,18 @@ void Engine::ensure_capacity(int64_t rows, size_t arena_bytes, int64_t max_n, in
   }
   // LM-head / CE chunk: head_chunk_bytes_ of fp32 logits + bf16 dlogits at most, and no more than a
   // third of the memory still free after the buffers above (at least 2 GB)
-  int64_t head_bytes = head_chunk_bytes_;
-  {
-    size_t free_b = 0, total_b = 0;
+  if (head_cap_rows_ == 0 && std::max<int64_t>(max_loss_rows, 1) > head_chunk_) {
+    int64_t head_bytes = head_chunk_bytes_;
+    size_t free_b = 0, total_b = 0;  // the query is slow: once, not per plan
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
       const int64_t room = (static_cast<int64_t>(free_b) + static_cast<int64_t>(sc_logits_.bytes + sc_dlog_.bytes)) / 3;
       head_bytes = std::min<int64_t>(head_bytes, std::max<int64_t>(room, int64_t(2) << 30));
     } else {
       (void)cudaGetLastError();
     }
+    head_cap_rows_ = std::max<int64_t>(128, head_bytes / (V_ * 6) / 128 * 128);
   }
-  const int64_t cap = std::max<int64_t>(128, head_bytes / (V_ * 6) / 128 * 128);
+  const int64_t cap = head_cap_rows_ > 0 ? head_cap_rows_ : std::max<int64_t>(128, head_chunk_bytes_ / (V_ * 6) / 128 * 128);
   const int64_t chunk = std::min<int64_t>(cap, std::max<int64_t>(max_loss_rows, 1));
   if (chunk > head_chunk_) {
     head_chunk_ = chunk;

@@ -249,6 +249,7 @@ class Engine {
   // LM-head chunk scratch (fp32 logits + bf16 dlogits): larger chunks mean fewer fp32 read-modify-
   // write passes of the V x d head gradient (one per chunk)
   int64_t head_chunk_bytes_ = int64_t(6) << 30;
+  int64_t head_cap_rows_ = 0;  // chunk row cap, fixed at the first plan that needs it (0 = not yet)
   KStats kstats_;
   struct Pending {
     KClass cls;

@@ -184,8 +184,14 @@ int tt_plan_destroy(tt_step_plan* plan);
  * Arrays have TT_NUM_KCLASS entries: accumulated ms, algorithmic FLOPs, algorithmic bytes, launches. */
 #define TT_NUM_KCLASS 5
 int tt_engine_set_profiling(tt_engine* eng, int32_t on);
-/* Implementation switches for cross-checks and ablations: "attn_fwd_impl" 0 = mma.sync (sm80-style
- * baseline), 1 = tcgen05/TMEM/TMA (default). */
+/* Implementation switches for cross-checks and ablations:
+ *   "attn_fwd_impl" / "attn_bwd_impl"  0 = mma.sync (sm80-style baseline), 1 = tcgen05/TMEM/TMA (default)
+ *   "gemm_2cta"          0 = single-CTA GEMM tiles only, 1 = CTA pairs (cta_group::2) where they fit (default)
+ *   "root_batch_tokens"  token cap of a multi-root prompt push (default 4096; 0 = one root per push)
+ *   "cuda_graph"         0 = eager launches, 1 = capture a prepared plan's op list on its 2nd execute (default)
+ *   "ce_stats"           1 = LM-head GEMM emits per-row softmax statistics for CE (default), 0 = CE two-pass
+ *   "head_chunk_mb"      LM-head / CE scratch budget per loss-row chunk (default 6144; capped by free HBM)
+ * Unknown keys and out-of-range values return TT_ERR_INVALID_ARGUMENT. */
 int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value);
 int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset);
 /* Per-GEMM-shape breakdown of the profiled launches (text, one shape per line, slowest first). */

@@ -146,6 +146,14 @@ def test_tree_step_gemm_orientation_vs_oracle(tmode):
         _native.lib().tt_debug_gemm_set_transpose(1)
 
 
+def test_tree_step_d448_224_wide_gemm_tiles_vs_oracle():
+    """d = 448 (7 heads of 64): every d-wide dX GEMM with >= 256 rows runs the 224-wide CTA-pair
+    tiles (N % 256 != 0, K-major B); the step must still match the oracle."""
+    cfg, flat, eng = make((512, 448, 7, 2, 1024, 1024), 13)
+    seqs = O.grouped_corpus(2, 4, 256, 128, cfg.vocab_size, 14, shared_response=4, weight_jitter=True)
+    tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
+
+
 def test_tree_step_dh128():
     cfg, flat, eng = make(DH128, 5)
     seqs = O.grouped_corpus(2, 4, 130, 90, cfg.vocab_size, 6, shared_response=5)

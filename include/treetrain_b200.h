@@ -159,8 +159,34 @@ int tt_params_load_ttpm(tt_engine* eng, const char* path);
 /* GradientStore (model.hpp:76-81): fp32 flat buffer in for_each_tensor order. */
 int tt_grads_zero(tt_engine* eng); /* zero_gradients, model.hpp:110-117 */
 int tt_grads_download_f32(tt_engine* eng, float* out, uint64_t n);
+/* GradientStore<double> (model.hpp:76-81): the fp32 device gradients widened to double. */
+int tt_grads_download_f64(tt_engine* eng, double* out, uint64_t n);
 int tt_grads_device_ptr(tt_engine* eng, float** dptr, uint64_t* n);
 int tt_grads_accum_count(tt_engine* eng, uint64_t* count);
+
+/* weighted_nll (model.hpp:643-677) on the device: logits [n x V] fp32 (host or device pointer),
+ * loss = sum_p w_p (lse - logit[target_p]) in fp64, grad_logits_out [n x V] fp32 (host or device,
+ * may be NULL) = per row (sum_p w_p) softmax - sum_p w_p onehot(target_p). row_off[n + 1] makes
+ * rows multi-target (the tree's node-boundary rows); NULL = one (target, weight) per
+ * row, exactly the reference signature. Pairs of weight 0 contribute nothing (model.hpp:658).
+ * Errors as the reference: target out of range / non-finite weight -> TT_ERR_INVALID_ARGUMENT. */
+int tt_weighted_nll(tt_engine* eng, const float* logits, uint64_t n, const uint64_t* row_off, const int32_t* targets,
+                    const double* weights, double* loss_out, float* grad_logits_out);
+
+/* ------------------------------------------------------------------ multi-GPU
+ * One process per GPU (or one process driving all GPUs with tt_nccl_comm_init_all), one NCCL
+ * communicator per engine, ONE in-place sum all-reduce of the fp32 GradientStore per step — the
+ * reduction the reference does across workers in worker order. Communicators are
+ * ncclComm_t values passed as void*; libnccl.so.2 is bound at run time (the copy already loaded in
+ * the process if any). */
+#define TT_NCCL_UNIQUE_ID_BYTES 128
+int tt_nccl_unique_id(uint8_t* id_out /* TT_NCCL_UNIQUE_ID_BYTES */);
+int tt_nccl_comm_init_rank(const uint8_t* id, int32_t nranks, int32_t rank, int32_t device, void** comm_out);
+int tt_nccl_comm_init_all(int32_t ndev, const int32_t* devices, void** comms_out);
+int tt_nccl_comm_destroy(void* comm);
+/* In-place ncclAllReduce(sum, fp32) of the engine's GradientStore on the engine stream; returns
+ * after it completed. */
+int tt_grads_allreduce(tt_engine* eng, void* nccl_comm);
 
 /* tree_train_step: one DFS push/visit/pop pass over `tree`, gradients added
  * into the engine's GradientStore, loss in result->total_loss. */
@@ -184,13 +210,13 @@ int tt_plan_destroy(tt_step_plan* plan);
  * Arrays have TT_NUM_KCLASS entries: accumulated ms, algorithmic FLOPs, algorithmic bytes, launches. */
 #define TT_NUM_KCLASS 5
 int tt_engine_set_profiling(tt_engine* eng, int32_t on);
-/* Implementation switches for cross-checks and ablations:
- *   "attn_fwd_impl" / "attn_bwd_impl"  0 = mma.sync (sm80-style baseline), 1 = tcgen05/TMEM/TMA (default)
+/* Execution options (results are unchanged up to fp32 summation order; a prepared plan's CUDA graph
+ * is re-captured after any change):
  *   "gemm_2cta"          0 = single-CTA GEMM tiles only, 1 = CTA pairs (cta_group::2) where they fit (default)
  *   "root_batch_tokens"  token cap of a multi-root prompt push (default 4096; 0 = one root per push)
  *   "cuda_graph"         0 = eager launches, 1 = capture a prepared plan's op list on its 2nd execute (default)
  *   "ce_stats"           1 = LM-head GEMM emits per-row softmax statistics for CE (default), 0 = CE two-pass
- *   "head_chunk_mb"      LM-head / CE scratch budget per loss-row chunk (default 6144; capped by free HBM)
+ *   "head_chunk_mb"      LM-head / CE scratch budget per loss-row chunk (default 6144, >= 1; capped by free HBM)
  * Unknown keys and out-of-range values return TT_ERR_INVALID_ARGUMENT. */
 int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value);
 int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset);
@@ -199,13 +225,29 @@ int tt_engine_profile_gemm_text(tt_engine* eng, char* buf, uint64_t cap, uint64_
 
 /* ------------------------------------------------------------------ segment level (device KV stack)
  * forward_segment (model.hpp:328-463) continuing from the device stack (KVView of all pushed
- * segments, start_position = current stack length). logits_out: host [len x V] fp32 or NULL. */
+ * segments, start_position = current stack length). logits_out: [len x V] fp32, host or device
+ * pointer, or NULL. Equivalent to tt_segment_push_ex(..., want_kv = 1, want_activations = 1, ...). */
 int tt_segment_push(tt_engine* eng, const int32_t* tokens, uint64_t len, float* logits_out);
-/* backward_segment (model.hpp:474-633) of the top segment. grad_logits: host [len x V] fp32 or NULL
- * (= zero upstream). grad_new_kv is the dK/dV the popped segment's rows accumulated from segments
- * popped above it. grad_prefix (returned KVGrad, rows [0,S)) is added into the stack's dK/dV rows of
- * the ancestors; grad_prefix_out (host, layout [L][2][S][d] fp32, K then V) receives that
- * contribution when not NULL. */
+/* forward_segment's want_kv / want_activations (model.hpp:328-331, ForwardResult :232-237):
+ *   want_kv = 0           the segment's K/V rows are not kept for descendants: pushing on top of it
+ *                         fails with TT_ERR_INVALID_ARGUMENT (a childless node, leaf_kv_skip);
+ *   want_activations = 0  activations are dropped after the forward; its pop recomputes them from
+ *                         the stack before the backward (the chunked backward's recompute);
+ *   both 0                forward only (logits): nothing is pushed. */
+int tt_segment_push_ex(tt_engine* eng, const int32_t* tokens, uint64_t len, int32_t want_kv, int32_t want_activations,
+                       float* logits_out);
+/* weighted_nll of the TOP segment's logits, on the device (the VISIT of SPEC.md:225): pairs as in
+ * tt_weighted_nll over the segment's rows (row_off[len + 1] or NULL). *loss_out gets the loss now;
+ * the segment's pop then takes its upstream grad_logits from these pairs (fused LM-head GEMM + CE,
+ * no logits cross PCIe). */
+int tt_segment_loss(tt_engine* eng, const uint64_t* row_off, const int32_t* targets, const double* weights,
+                    double* loss_out);
+/* backward_segment (model.hpp:474-633) of the top segment. Upstream grad_logits: [len x V] fp32
+ * (host or device) or NULL (= zero, or the device pairs of tt_segment_loss; giving both is an
+ * error). grad_new_kv is the dK/dV the popped segment's rows accumulated from segments popped above
+ * it. grad_prefix (the returned KVGrad, rows [0,S)) is added into the ancestors' dK/dV stack rows
+ * (KVGrad::add_rows, model.hpp:193-206); grad_prefix_out (host or device, [L][2][S][d] fp32, K then
+ * V) additionally receives exactly this pop's contribution when not NULL. */
 int tt_segment_pop(tt_engine* eng, const float* grad_logits, float* grad_prefix_out);
 int tt_stack_reset(tt_engine* eng);
 int tt_stack_depth(tt_engine* eng, uint64_t* segments, uint64_t* tokens);

@@ -27,7 +27,7 @@ from . import _native
 __all__ = [
     "ModelConfig", "TokenSequence", "SchedulerConfig", "TrainStepResult", "PrefixTree", "Engine",
     "build_prefix_tree", "lexicographic_sort", "partition_contiguous", "greedy_least_loaded", "POLICIES",
-    "CorpusSpec", "gen_corpus", "load_corpus_jsonl", "save_corpus_jsonl",
+    "CorpusSpec", "gen_corpus", "load_corpus_jsonl", "save_corpus_jsonl", "NcclComm", "nccl_unique_id",
 ]
 
 POLICIES = {"as_built": 0, "lexicographic": 1, "subtree_tokens_desc": 2, "subtree_tokens_asc": 3}
@@ -322,6 +322,33 @@ class StepPlan:
             self._h = None
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0 creates it, every rank passes it to NcclComm)."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(_native.lib().tt_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class NcclComm:
+    """One NCCL communicator (ncclCommInitRank) for the engine on `device`."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int, device: int = 0):
+        if len(unique_id) != 128:
+            raise ValueError("NcclComm: unique id must be 128 bytes")
+        buf = (ctypes.c_uint8 * 128)(*unique_id)
+        h = ctypes.c_void_p()
+        _check(_native.lib().tt_nccl_comm_init_rank(buf, nranks, rank, device, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _native.lib().tt_nccl_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+
 class Engine:
     """One B200 engine (weights, GradientStore, KV/dKV stacks, activation arena, one stream)."""
 
@@ -362,10 +389,41 @@ class Engine:
     def zero_gradients(self) -> None:
         _check(_native.lib().tt_grads_zero(self._h))
 
-    def gradients(self) -> np.ndarray:
+    def gradients(self, dtype=np.float32) -> np.ndarray:
+        """GradientStore in for_each_tensor order (model.hpp:42-59, 76-81); float32 or float64."""
+        if np.dtype(dtype) == np.float64:
+            out = np.zeros(self.n_params, dtype=np.float64)
+            _check(_native.lib().tt_grads_download_f64(self._h, _ptr(out, ctypes.c_double), out.size))
+            return out
         out = np.zeros(self.n_params, dtype=np.float32)
         _check(_native.lib().tt_grads_download_f32(self._h, _ptr(out, ctypes.c_float), out.size))
         return out
+
+    def allreduce_gradients(self, comm: "NcclComm") -> None:
+        """One in-place NCCL sum all-reduce of the GradientStore."""
+        _check(_native.lib().tt_grads_allreduce(self._h, comm.handle))
+
+    def weighted_nll(self, logits: np.ndarray, targets: Sequence[int], weights: Sequence[float],
+                     row_off: Optional[Sequence[int]] = None, want_grad: bool = True):
+        """weighted_nll (model.hpp:643-677) on the device: returns (loss, grad_logits [n x V] fp32).
+        row_off (n + 1 offsets into targets/weights) makes rows multi-target."""
+        lg = np.ascontiguousarray(logits, dtype=np.float32)
+        if lg.ndim != 2 or lg.shape[1] != self.cfg.vocab_size:
+            raise ValueError("weighted_nll: logits must be [n x vocab_size]")
+        n = lg.shape[0]
+        tg = np.ascontiguousarray(targets, dtype=np.int32)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        ro = None if row_off is None else np.ascontiguousarray(row_off, dtype=np.uint64)
+        if ro is None and (tg.size != n or w.size != n):
+            raise ValueError("weighted_nll: one target and weight per loss position")
+        if ro is not None and (ro.size != n + 1 or int(ro[-1]) > min(tg.size, w.size)):
+            raise ValueError("weighted_nll: row_off must have n + 1 entries within targets / weights")
+        grad = np.zeros_like(lg) if want_grad else None
+        loss = ctypes.c_double()
+        _check(_native.lib().tt_weighted_nll(self._h, lg.ctypes.data, n, _ptr(ro, ctypes.c_uint64),
+                                             _ptr(tg, ctypes.c_int32), _ptr(w, ctypes.c_double), ctypes.byref(loss),
+                                             None if grad is None else grad.ctypes.data))
+        return loss.value, grad
 
     def grads_device_ptr(self) -> int:
         p, n = ctypes.c_void_p(), ctypes.c_uint64()
@@ -421,22 +479,50 @@ class Engine:
         return TrainStepResult._from(r)
 
     # ---- segment level (device KV stack)
-    def forward_segment(self, tokens: Sequence[int], want_logits: bool = True) -> Optional[np.ndarray]:
-        """PUSH: forward_segment continuing from the device stack; returns logits [len x V] (fp32)."""
+    def forward_segment(self, tokens: Sequence[int], want_logits: bool = True, want_kv: bool = True,
+                        want_activations: bool = True) -> Optional[np.ndarray]:
+        """PUSH: forward_segment (model.hpp:328-331) continuing from the device stack; returns logits
+        [len x V] (fp32) or None. want_kv / want_activations as the reference (tt_segment_push_ex)."""
         tok = np.ascontiguousarray(tokens, dtype=np.int32)
         out = np.zeros((tok.size, self.cfg.vocab_size), dtype=np.float32) if want_logits else None
-        _check(_native.lib().tt_segment_push(self._h, _ptr(tok, ctypes.c_int32), tok.size, _ptr(out, ctypes.c_float)))
-        self._lens.append(tok.size)
+        _check(_native.lib().tt_segment_push_ex(self._h, _ptr(tok, ctypes.c_int32), tok.size, int(want_kv),
+                                                int(want_activations), None if out is None else out.ctypes.data))
+        if want_kv or want_activations:
+            self._lens.append(tok.size)
         return out
+
+    def segment_loss(self, targets: Sequence[int], weights: Sequence[float],
+                     row_off: Optional[Sequence[int]] = None) -> float:
+        """VISIT: weighted_nll of the top segment on the device (tt_segment_loss); the pop then takes
+        its grad_logits from these pairs."""
+        if not self._lens:
+            raise ValueError("weighted_nll: empty stack")
+        n = self._lens[-1]
+        tg = np.ascontiguousarray(targets, dtype=np.int32)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        ro = None if row_off is None else np.ascontiguousarray(row_off, dtype=np.uint64)
+        if ro is None and (tg.size != n or w.size != n):
+            raise ValueError("weighted_nll: one target and weight per loss position")
+        if ro is not None and (ro.size != n + 1 or int(ro[-1]) > min(tg.size, w.size)):
+            raise ValueError("weighted_nll: row_off must have len + 1 entries within targets / weights")
+        loss = ctypes.c_double()
+        _check(_native.lib().tt_segment_loss(self._h, _ptr(ro, ctypes.c_uint64), _ptr(tg, ctypes.c_int32),
+                                             _ptr(w, ctypes.c_double), ctypes.byref(loss)))
+        return loss.value
 
     def backward_segment(self, grad_logits: Optional[np.ndarray] = None, want_grad_prefix: bool = True):
         """POP: backward_segment of the top segment; returns grad_prefix as (dK, dV) [L, S, d] or None."""
         if not self._lens:
             raise ValueError("backward_segment: empty stack")
         S_below = sum(self._lens[:-1])
-        gl = None if grad_logits is None else np.ascontiguousarray(grad_logits, dtype=np.float32)
+        gl = None
+        if grad_logits is not None:
+            gl = np.ascontiguousarray(grad_logits, dtype=np.float32)
+            if gl.shape != (self._lens[-1], self.cfg.vocab_size):  # model.hpp:488-490
+                raise ValueError("backward_segment: grad_logits shape mismatch")
         gp = np.zeros((self.cfg.n_layers, 2, S_below, self.cfg.d_model), dtype=np.float32) if want_grad_prefix else None
-        _check(_native.lib().tt_segment_pop(self._h, _ptr(gl, ctypes.c_float), _ptr(gp, ctypes.c_float)))
+        _check(_native.lib().tt_segment_pop(self._h, None if gl is None else gl.ctypes.data,
+                                            None if gp is None else gp.ctypes.data))
         self._lens.pop()
         if gp is None:
             return None

@@ -65,6 +65,13 @@ EXPORTS = {
     "tt_params_load_ttpm": [vp, c.c_char_p],
     "tt_grads_zero": [vp],
     "tt_grads_download_f32": [vp, P(c.c_float), u64],
+    "tt_grads_download_f64": [vp, P(f64), u64],
+    "tt_weighted_nll": [vp, vp, u64, P(u64), P(i32), P(f64), P(f64), vp],
+    "tt_nccl_unique_id": [P(c.c_uint8)],
+    "tt_nccl_comm_init_rank": [P(c.c_uint8), i32, i32, i32, P(vp)],
+    "tt_nccl_comm_init_all": [i32, P(i32), P(vp)],
+    "tt_nccl_comm_destroy": [vp],
+    "tt_grads_allreduce": [vp, vp],
     "tt_grads_device_ptr": [vp, P(vp), P(u64)],
     "tt_grads_accum_count": [vp, P(u64)],
     "tt_tree_train_step": [vp, vp, P(SchedConfigC), P(StepResultC)],
@@ -79,8 +86,10 @@ EXPORTS = {
                       c.c_long, c.c_int, P(c.c_float)],
     "tt_engine_profile": [vp, P(f64), P(f64), P(f64), P(u64), i32],
     "tt_engine_profile_gemm_text": [vp, c.c_char_p, u64, P(u64)],
-    "tt_segment_push": [vp, P(i32), u64, P(c.c_float)],
-    "tt_segment_pop": [vp, P(c.c_float), P(c.c_float)],
+    "tt_segment_push": [vp, P(i32), u64, vp],
+    "tt_segment_push_ex": [vp, P(i32), u64, i32, i32, vp],
+    "tt_segment_loss": [vp, P(u64), P(i32), P(f64), P(f64)],
+    "tt_segment_pop": [vp, vp, vp],
     "tt_stack_reset": [vp],
     "tt_stack_depth": [vp, P(u64), P(u64)],
     "tt_last_error": [],
@@ -91,7 +100,7 @@ EXPORTS = {
     "tt_debug_gemm_splits": [c.c_int, c.c_int, c.c_int],
     "tt_debug_gemm_set_2cta": [c.c_int],
     "tt_debug_gemm_set_transpose": [c.c_int],
-    "tt_debug_attn_trace": [vp, c.c_int],
+    "tt_debug_attn_set_segments": [c.c_int],
     "tt_debug_rmsnorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, c.c_int, c.c_int],
 }
 
@@ -99,8 +108,7 @@ EXPORTS = {
 def lib():
     global _lib
     if _lib is None:
-        # TT_LIB_PATH: an alternative build of the same library (A/B kernel timing in tools/ only)
-        path = os.environ.get("TT_LIB_PATH", LIB_PATH)
+        path = LIB_PATH
         if not os.path.exists(path):
             raise RuntimeError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
         L = ctypes.CDLL(path)

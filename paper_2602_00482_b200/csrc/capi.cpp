@@ -61,6 +61,14 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string("null ") + what);
 }
 
+// Every engine entry point first selects the engine's GPU: a process may hold engines on several
+// devices, and the caller's current device is not necessarily this engine's.
+ttb::Engine& use(tt_engine* eng) {
+  need(eng, "engine");
+  ttb::check_cuda(cudaSetDevice(eng->e->device()), "cudaSetDevice");
+  return *eng->e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -273,19 +281,22 @@ int tt_engine_create(const tt_model_config* cfg, int32_t device, tt_engine** out
 }
 
 int tt_engine_destroy(tt_engine* eng) {
-  return ttb::guarded([&] { delete eng; });
+  return ttb::guarded([&] {
+    if (eng) use(eng);
+    delete eng;
+  });
 }
 
 int tt_engine_stream(tt_engine* eng, void** stream) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     *stream = eng->e->stream();
   });
 }
 
 int tt_params_upload_f32(tt_engine* eng, const float* flat, uint64_t n) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(flat, "flat");
     eng->e->upload_params(flat, n);
   });
@@ -293,7 +304,7 @@ int tt_params_upload_f32(tt_engine* eng, const float* flat, uint64_t n) {
 
 int tt_params_upload_f64(tt_engine* eng, const double* flat, uint64_t n) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(flat, "flat");
     std::vector<float> f(flat, flat + n);
     eng->e->upload_params(f.data(), n);
@@ -302,14 +313,14 @@ int tt_params_upload_f64(tt_engine* eng, const double* flat, uint64_t n) {
 
 int tt_params_init_random(tt_engine* eng, uint64_t seed) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     eng->e->init_random(seed);
   });
 }
 
 int tt_params_load_ttpm(tt_engine* eng, const char* path) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(path, "path");
     ttb::TtpmFile f = ttb::read_ttpm(path);
     const tt_model_config& c = eng->e->config();
@@ -323,22 +334,46 @@ int tt_params_load_ttpm(tt_engine* eng, const char* path) {
 
 int tt_grads_zero(tt_engine* eng) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     eng->e->grads_zero();
   });
 }
 
 int tt_grads_download_f32(tt_engine* eng, float* out, uint64_t n) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(out, "out");
     eng->e->grads_download(out, n);
   });
 }
 
+int tt_grads_download_f64(tt_engine* eng, double* out, uint64_t n) {
+  return ttb::guarded([&] {
+    use(eng);
+    need(out, "out");
+    eng->e->grads_download_f64(out, n);
+  });
+}
+
+int tt_grads_allreduce(tt_engine* eng, void* nccl_comm) {
+  return ttb::guarded([&] {
+    use(eng);
+    eng->e->grads_allreduce(nccl_comm);
+  });
+}
+
+int tt_weighted_nll(tt_engine* eng, const float* logits, uint64_t n, const uint64_t* row_off, const int32_t* targets,
+                    const double* weights, double* loss_out, float* grad_logits_out) {
+  return ttb::guarded([&] {
+    use(eng);
+    const double l = eng->e->weighted_nll(logits, n, row_off, targets, weights, grad_logits_out);
+    if (loss_out) *loss_out = l;
+  });
+}
+
 int tt_grads_device_ptr(tt_engine* eng, float** dptr, uint64_t* n) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     *dptr = eng->e->grads_device();
     *n = eng->e->param_count();
   });
@@ -346,14 +381,14 @@ int tt_grads_device_ptr(tt_engine* eng, float** dptr, uint64_t* n) {
 
 int tt_grads_accum_count(tt_engine* eng, uint64_t* count) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     *count = eng->e->accum_count();
   });
 }
 
 int tt_tree_train_step(tt_engine* eng, const tt_tree* tree, const tt_sched_config* sched, tt_step_result* result) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(tree, "tree");
     need(sched, "sched");
     tt_step_result r = eng->e->train_step(tree->t, *sched);
@@ -364,7 +399,7 @@ int tt_tree_train_step(tt_engine* eng, const tt_tree* tree, const tt_sched_confi
 int tt_dense_train_step(tt_engine* eng, const int32_t* tokens, const uint64_t* offsets, const double* weights,
                         uint64_t n_seqs, tt_step_result* result) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     ttb::PrefixTree flat = ttb::build_flat_forest(views(tokens, offsets, weights, n_seqs));
     tt_sched_config sc{};
     sc.sibling_batch = 1;  // every sequence is its own root-level leaf: packed varlen batches
@@ -376,7 +411,7 @@ int tt_dense_train_step(tt_engine* eng, const int32_t* tokens, const uint64_t* o
 
 int tt_plan_create(tt_engine* eng, const tt_tree* tree, const tt_sched_config* sched, tt_step_plan** out) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(tree, "tree");
     need(sched, "sched");
     need(out, "out");
@@ -388,7 +423,7 @@ int tt_plan_create(tt_engine* eng, const tt_tree* tree, const tt_sched_config* s
 
 int tt_plan_execute(tt_engine* eng, tt_step_plan* plan, tt_step_result* result) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(plan, "plan");
     tt_step_result r = eng->e->execute(*plan->p);
     if (result) *result = r;
@@ -408,14 +443,14 @@ int tt_plan_destroy(tt_step_plan* plan) {
 
 int tt_engine_set_profiling(tt_engine* eng, int32_t on) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     eng->e->set_profiling(on != 0);
   });
 }
 
 int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(key, "key");
     eng->e->set_option(key, value);
   });
@@ -423,7 +458,7 @@ int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value) {
 
 int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, uint64_t* launches, int32_t reset) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     const ttb::KStats& k = eng->e->kstats();
     for (int i = 0; i < TT_NUM_KCLASS; ++i) {
       if (ms) ms[i] = k.ms[i];
@@ -437,36 +472,54 @@ int tt_engine_profile(tt_engine* eng, double* ms, double* flops, double* bytes, 
 
 int tt_engine_profile_gemm_text(tt_engine* eng, char* buf, uint64_t cap, uint64_t* len) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     copy_out(eng->e->gemm_profile_text(), buf, cap, len);
   });
 }
 
 int tt_segment_push(tt_engine* eng, const int32_t* tokens, uint64_t len, float* logits_out) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     need(tokens, "tokens");
-    eng->e->segment_push(tokens, len, logits_out);
+    eng->e->segment_push(tokens, len, true, true, logits_out);
+  });
+}
+
+int tt_segment_push_ex(tt_engine* eng, const int32_t* tokens, uint64_t len, int32_t want_kv, int32_t want_activations,
+                       float* logits_out) {
+  return ttb::guarded([&] {
+    use(eng);
+    need(tokens, "tokens");
+    eng->e->segment_push(tokens, len, want_kv != 0, want_activations != 0, logits_out);
+  });
+}
+
+int tt_segment_loss(tt_engine* eng, const uint64_t* row_off, const int32_t* targets, const double* weights,
+                    double* loss_out) {
+  return ttb::guarded([&] {
+    use(eng);
+    const double l = eng->e->segment_loss(row_off, targets, weights);
+    if (loss_out) *loss_out = l;
   });
 }
 
 int tt_segment_pop(tt_engine* eng, const float* grad_logits, float* grad_prefix_out) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     eng->e->segment_pop(grad_logits, grad_prefix_out);
   });
 }
 
 int tt_stack_reset(tt_engine* eng) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     eng->e->stack_reset();
   });
 }
 
 int tt_stack_depth(tt_engine* eng, uint64_t* segments, uint64_t* tokens) {
   return ttb::guarded([&] {
-    need(eng, "engine");
+    use(eng);
     if (segments) *segments = eng->e->stack_segments();
     if (tokens) *tokens = eng->e->stack_tokens();
   });

@@ -70,11 +70,14 @@ void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
 void tt_debug_gemm_set_transpose(int mode) { ttb::gemm_set_transpose(mode); }
 
 // clock64 trace of the TT_ATTN_DBG=3 attention dq kernel (timing experiments only)
-int tt_debug_attn_trace(long long* out, int n) { return ttb::attn_debug_trace(out, n); }
+static int g_attn_nseg = 1;
+// Timing tools: the n queries of tt_debug_attn form nseg equal sibling segments over the shared prefix
+// (the c2 leaf-batch shape), with the engine's work-item chunking.
+void tt_debug_attn_set_segments(int nseg) { g_attn_nseg = nseg < 1 ? 1 : nseg; }
 
 // Segment attention on one segment of n queries over stack rows [0, S) + own rows [S, S+n)
-// (k/v: [rows_cap x H*dh] bf16). dir 0: forward (impl 0 = mma.sync, 1 = tcgen05) -> o, lse.
-// dir 1: backward (impl 0 = mma.sync) from o, lse, dO -> dq (overwritten), dk/dv (added).
+// (k/v: [rows_cap x H*dh] bf16), tcgen05 kernels (impl must be 1). dir 0: forward -> o, lse.
+// dir 1: backward from o, lse, dO -> dq (fp32, overwritten), dk/dv (added).
 // iters > 0: additionally time `iters` back-to-back launches with CUDA events -> *ms_out (per launch).
 int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v, void* o, float* lse, const void* dO,
                   float* D, float* dq, float* dk, float* dv, int n, int S, int H, int dh, long rows_cap, int iters,
@@ -97,33 +100,20 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
       }
     };
     const int d = H * dh;
-    // TT_ATTN_NSEG (timing experiments): the n queries form nseg equal sibling segments over the shared
-    // prefix, with the engine's work-item chunking (tcgen05 path) — the c2 leaf-batch shape
-    static const int nseg = [] {
-      const char* e = std::getenv("TT_ATTN_NSEG");
-      return e ? std::max(1, std::atoi(e)) : 1;
-    }();
+    if (impl != 1) throw std::invalid_argument("tt_debug_attn: only the tcgen05 kernels (impl 1) exist");
+    const int nseg = g_attn_nseg;
     const int seg = (n + nseg - 1) / nseg;
-    std::vector<int> q64, q128, it, it2;
-    for (int qs = 0; qs < n; qs += 64) q64.insert(q64.end(), {qs, std::min(qs + 64, n), 0, 0});
+    std::vector<int> q128;
     for (int so = 0; so < n; so += seg)
       for (int qs = so; qs < std::min(n, so + seg); qs += 128)
         q128.insert(q128.end(), {qs, std::min({qs + 128, so + seg, n}), so, 0});
-    for (int kv = 0; kv < S; kv += 64) {
-      it.insert(it.end(), {kv, std::min(64, S - kv), 0, n});
-      it2.insert(it2.end(), {0, 0});
-    }
-    for (int kt = 0; kt < n; kt += 64) {
-      it.insert(it.end(), {S + kt, std::min(64, n - kt), kt, n});
-      it2.insert(it2.end(), {0, 1});
-    }
     auto up = [](const std::vector<int>& h) {
       void* p = nullptr;
       ttb::check_cuda(cudaMalloc(&p, std::max<size_t>(16, h.size() * 4)), "cudaMalloc");
       if (!h.empty()) ttb::check_cuda(cudaMemcpy(p, h.data(), h.size() * 4, cudaMemcpyHostToDevice), "memcpy");
       return p;
     };
-    void *d64 = up(q64), *d128 = up(q128), *dit = up(it), *dit2 = up(it2);
+    void* d128 = up(q128);
     const float scale = 1.0f / std::sqrt(static_cast<float>(dh));
     if (dir == 0) {
       ttb::AttnFwdArgs a;
@@ -140,15 +130,9 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
       a.dh = dh;
       a.S = S;
       a.scale = scale;
-      if (impl == 1) {
-        a.qblocks = static_cast<const int4*>(d128);
-        a.nqb = static_cast<int>(q128.size() / 4);
-        timed([&] { ttb::attn_fwd_sm100(a, rows_cap, nullptr); });
-      } else {
-        a.qblocks = static_cast<const int4*>(d64);
-        a.nqb = static_cast<int>(q64.size() / 4);
-        timed([&] { ttb::attn_fwd(a, nullptr); });
-      }
+      a.qblocks = static_cast<const int4*>(d128);
+      a.nqb = static_cast<int>(q128.size() / 4);
+      timed([&] { ttb::attn_fwd_sm100(a, rows_cap, nullptr); });
     } else {
       ttb::AttnBwdArgs a;
       a.q = static_cast<const __nv_bfloat16*>(q);
@@ -169,11 +153,8 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
       a.H = H;
       a.dh = dh;
       a.S = S;
-      a.items = static_cast<const int4*>(dit);
-      a.items2 = static_cast<const int2*>(dit2);
-      a.nitems = static_cast<int>(it.size() / 4);
       a.scale = scale;
-      if (impl == 1) {
+      {
         std::vector<int> k128, k128b;
         const int chunk_pre = nseg > 1 ? 4096 : n, chunk_own = nseg > 1 ? 2048 : n;  // engine.cpp kQChunk*
         for (int kv = 0; kv < S; kv += 128)
@@ -205,6 +186,7 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
         }
         void *dk128 = up(k128), *dk128b = up(k128b);
         timed([&] {
+          if (dh == 64) cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d * 4, nullptr);  // fused: dQ is added
           ttb::attn_bwd_sm100(a, rows_cap, static_cast<const int4*>(d128), static_cast<int>(q128.size() / 4),
                               static_cast<const int4*>(dk128), static_cast<const int2*>(dk128b),
                               static_cast<int>(k128.size() / 4), nullptr);
@@ -212,19 +194,11 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
         ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_attn sync");
         cudaFree(dk128);
         cudaFree(dk128b);
-      } else {
-        timed([&] {
-          cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d * 4, nullptr);
-          ttb::attn_bwd(a, nullptr);
-        });
       }
     }
     ttb::check_cuda(cudaGetLastError(), "tt_debug_attn launch");
     ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_attn sync");
-    cudaFree(d64);
     cudaFree(d128);
-    cudaFree(dit);
-    cudaFree(dit2);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   });

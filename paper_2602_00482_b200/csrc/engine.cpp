@@ -29,8 +29,6 @@ namespace {
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-constexpr int kQBlock = 64;
-constexpr int kQChunk = 1024;  // query rows per backward work item (mma.sync kernels)
 constexpr int kQChunkPrefix = 4096;  // tcgen05 dK/dV items over prefix rows (span members)
 constexpr int kQChunkOwn = 2048;     // tcgen05 dK/dV items over a member's own rows (causal)
 
@@ -170,19 +168,13 @@ Engine::~Engine() {
 }
 
 void Engine::set_option(const std::string& key, int64_t value) {
-  if (key == "attn_fwd_impl") {
-    if (value != 0 && value != 1) throw std::invalid_argument("attn_fwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
-    attn_fwd_impl_ = static_cast<int>(value);
-  } else if (key == "gemm_2cta") {
-    gemm_set_2cta(value != 0 ? 1 : 0);
-  } else if (key == "attn_bwd_impl") {
-    if (value != 0 && value != 1) throw std::invalid_argument("attn_bwd_impl must be 0 (mma.sync) or 1 (tcgen05)");
-    attn_bwd_impl_ = static_cast<int>(value);
+  if (key == "gemm_2cta") {
+    gemm_2cta_ = value != 0 ? 1 : 0;
   } else if (key == "root_batch_tokens") {
     if (value < 0) throw std::invalid_argument("root_batch_tokens must be >= 0");
     root_batch_tokens_ = value;
   } else if (key == "head_chunk_mb") {
-    if (value < 64) throw std::invalid_argument("head_chunk_mb must be >= 64");
+    if (value < 1) throw std::invalid_argument("head_chunk_mb must be >= 1");
     head_chunk_bytes_ = value << 20;
     head_cap_rows_ = 0;
   } else if (key == "cuda_graph") {
@@ -194,6 +186,7 @@ void Engine::set_option(const std::string& key, int64_t value) {
   } else {
     throw std::invalid_argument("unknown engine option: " + key);
   }
+  ++opt_epoch_;
 }
 
 // ----------------------------------------------------------------------------- parameters
@@ -267,8 +260,22 @@ void Engine::grads_zero() {
 
 void Engine::grads_download(float* out, uint64_t n) {
   if (n != n_params_) throw std::invalid_argument("grads download: wrong parameter count");
-  ck(cudaMemcpyAsync(out, grads_.p, n * sizeof(float), cudaMemcpyDeviceToHost, stream_), "grads download");
+  ck(cudaMemcpyAsync(out, grads_.p, n * sizeof(float), cudaMemcpyDefault, stream_), "grads download");
   ck(cudaStreamSynchronize(stream_), "grads download");
+}
+
+// GradientStore<double> (model.hpp:76-81): the fp32 device gradients widened on the host.
+void Engine::grads_download_f64(double* out, uint64_t n) {
+  if (n != n_params_) throw std::invalid_argument("grads download: wrong parameter count");
+  constexpr uint64_t kChunk = uint64_t(1) << 24;
+  std::vector<float> tmp(std::min<uint64_t>(n, kChunk));
+  for (uint64_t o = 0; o < n; o += kChunk) {
+    const uint64_t m = std::min<uint64_t>(kChunk, n - o);
+    ck(cudaMemcpyAsync(tmp.data(), grads_.as<float>() + o, m * sizeof(float), cudaMemcpyDeviceToHost, stream_),
+       "grads download");
+    ck(cudaStreamSynchronize(stream_), "grads download");
+    for (uint64_t i = 0; i < m; ++i) out[o + i] = tmp[i];
+  }
 }
 
 // ----------------------------------------------------------------------------- memory plan
@@ -370,32 +377,14 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
     if (bytes) std::memcpy(host.data() + off, src, bytes);
     return off;
   };
-  b.qblk.clear();
   b.qblk128.clear();
-  b.kvit.clear();
-  b.kvit2.clear();
   b.kvit128.clear();
   b.kvit128_2.clear();
   for (size_t i = 0; i < b.seg_off.size(); ++i) {
     const int64_t so = b.seg_off[i], end = so + b.seg_len[i];
-    for (int64_t q = so; q < end; q += kQBlock) {
-      b.qblk.insert(b.qblk.end(), {int32_t(q), int32_t(std::min<int64_t>(q + kQBlock, end)), int32_t(so), 0});
-    }
     for (int64_t q = so; q < end; q += kFwdBlockQ) {
       b.qblk128.insert(b.qblk128.end(), {int32_t(q), int32_t(std::min<int64_t>(q + kFwdBlockQ, end)), int32_t(so), 0});
     }
-    for (int64_t kv = 0; kv < b.S; kv += 64)  // prefix rows: every query of the member attends
-      for (int64_t q = so; q < end; q += kQChunk) {
-        b.kvit.insert(b.kvit.end(), {int32_t(b.pbase + kv), int32_t(std::min<int64_t>(64, b.S - kv)), int32_t(q),
-                                     int32_t(std::min<int64_t>(q + kQChunk, end))});
-        b.kvit2.insert(b.kvit2.end(), {int32_t(so), 0});
-      }
-    for (int64_t kt = 0; kt < b.seg_len[i]; kt += 64)  // own rows: queries at or after the key
-      for (int64_t q = so + kt; q < end; q += kQChunk) {
-        b.kvit.insert(b.kvit.end(), {int32_t(b.row0() + so + kt), int32_t(std::min<int64_t>(64, b.seg_len[i] - kt)),
-                                     int32_t(q), int32_t(std::min<int64_t>(q + kQChunk, end))});
-        b.kvit2.insert(b.kvit2.end(), {int32_t(so), 1});
-      }
     for (int64_t kt = 0; kt < b.seg_len[i]; kt += kBwdBlockKV)
       for (int64_t q = so + kt; q < end; q += kQChunkOwn) {
         b.kvit128.insert(b.kvit128.end(), {int32_t(b.row0() + so + kt), int32_t(std::min<int64_t>(kBwdBlockKV, b.seg_len[i] - kt)),
@@ -434,10 +423,7 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
   }
   b.o_tok = put(b.tokens.data(), b.tokens.size() * 4);
   b.o_pos = put(b.positions.data(), b.positions.size() * 4);
-  b.o_qblk = put(b.qblk.data(), b.qblk.size() * 4);
   b.o_qblk128 = put(b.qblk128.data(), b.qblk128.size() * 4);
-  b.o_kvit = put(b.kvit.data(), b.kvit.size() * 4);
-  b.o_kvit2 = put(b.kvit2.data(), b.kvit2.size() * 4);
   b.o_kvit128 = put(b.kvit128.data(), b.kvit128.size() * 4);
   b.o_kvit128_2 = put(b.kvit128_2.data(), b.kvit128_2.size() * 4);
   b.o_lrows = put(b.loss_rows.data(), b.loss_rows.size() * 4);
@@ -594,17 +580,10 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
       a.pbase = static_cast<int>(b.pbase);
       a.r0 = static_cast<int>(b.row0());
       a.scale = scale;
-      if (attn_fwd_impl_ == 1) {
-        a.qblocks = meta<int4>(b.o_qblk128);
-        a.nqb = static_cast<int>(b.qblk128.size() / 4);
-        tag("attn_fwd_sm100");
-        run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd_sm100(a, rows_cap_, stream_); });
-      } else {
-        a.qblocks = meta<int4>(b.o_qblk);
-        a.nqb = static_cast<int>(b.qblk.size() / 4);
-        tag("attn_fwd");
-        run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd(a, stream_); });
-      }
+      a.qblocks = meta<int4>(b.o_qblk128);
+      a.nqb = static_cast<int>(b.qblk128.size() / 4);
+      tag("attn_fwd_sm100");
+      run(KC_ATTN_FWD, 4.0 * d_ * b.attn_ctx, 0, [&] { attn_fwd_sm100(a, rows_cap_, stream_); });
     }
     {  // x_mid = x + attn W_o  (:410-411,427-428)
       EpiParams e;
@@ -648,7 +627,7 @@ void Engine::forward_batch(const Batch& b, size_t arena_off) {
 // ----------------------------------------------------------------------------- visit: LM head + weighted CE
 // For every loss row (compacted): logits = c W_head (fp32), CE -> loss (fp64) and dlogits (bf16),
 // dW_head += c^T dlogits, grad_c = dlogits W_head^T scattered back to the batch rows.
-void Engine::head_backward(const Batch& b, const bf16* nf) {
+void Engine::head_backward(const Batch& b, const bf16* nf, bool loss_only) {
   const int d = static_cast<int>(d_);
   const int V = static_cast<int>(V_);
   float* gxf = sc_gxf_.as<float>();
@@ -677,6 +656,7 @@ void Engine::head_backward(const Batch& b, const bf16* nf) {
       k_ce(sc_logits_.as<float>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt), meta<double>(b.o_pw),
            dlog, loss_.as<double>(), stream_, ce_stats_ ? sc_stats_.as<float2>() : nullptr, (V + 31) / 32);
     });
+    if (loss_only) continue;  // the VISIT of a segment-level caller: loss now, gradients at the pop
     {  // dW_head += c^T dlogits  (model.hpp:506)
       EpiParams e;
       e.mode = EPI_ADD_F32;
@@ -706,7 +686,7 @@ void Engine::head_backward_dense(const Batch& b, const bf16* nf, const float* ho
   for (int64_t c0 = 0; c0 < b.n; c0 += head_chunk_) {
     const int cm = static_cast<int>(std::min<int64_t>(head_chunk_, b.n - c0));
     ck(cudaMemcpyAsync(sc_logits_.p, host_grad_logits + c0 * V_, static_cast<size_t>(cm) * V_ * 4,
-                       cudaMemcpyHostToDevice, stream_),
+                       cudaMemcpyDefault, stream_),
        "grad_logits upload");
     tag("k_f32_to_bf16_2d");
     run(KC_ELEMWISE, 0, 6.0 * cm * V, [&] { k_f32_to_bf16_2d(sc_logits_.as<float>(), V, dlog, V, cm, V, stream_); });
@@ -728,7 +708,7 @@ void Engine::head_backward_dense(const Batch& b, const bf16* nf, const float* ho
 }
 
 // ----------------------------------------------------------------------------- pop (backward_segment)
-void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits) {
+void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits, float* grad_prefix) {
   const int n = static_cast<int>(b.n);
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
   const double nd = double(n) * d_;
@@ -843,40 +823,39 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       a.dk = dK;
       a.dv = dV;
       a.lddkv = d;
+      if (grad_prefix) {  // segment pop: this pop's prefix dK/dV into [L][2][S][d] (rows from pbase = 0)
+        a.dk_pre = grad_prefix + (2 * l) * b.S * d_;
+        a.dv_pre = grad_prefix + (2 * l + 1) * b.S * d_;
+      }
       a.n = n;
       a.H = static_cast<int>(H_);
       a.dh = static_cast<int>(dh_);
       a.S = static_cast<int>(b.S);
       a.pbase = static_cast<int>(b.pbase);
       a.r0 = static_cast<int>(b.row0());
-      a.items = meta<int4>(b.o_kvit);
-      a.items2 = meta<int2>(b.o_kvit2);
-      a.nitems = static_cast<int>(b.kvit.size() / 4);
       a.scale = scale;
-      if (attn_bwd_impl_ == 1) {
+      if (dh_ == 64) {
+        // fused kernel: dQ partials (one per key block) reduced into the fp32 accumulator
+        ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
+      } else {
         a.dq16 = dqkv;  // dQ straight into the q block of the packed [dq | dk | dv] operand
         a.lddq16 = 3 * d;
-        tag("attn_bwd_sm100");
-        run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
-          attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_qblk128), static_cast<int>(b.qblk128.size() / 4),
-                         meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2), static_cast<int>(b.kvit128.size() / 4),
-                         stream_);
-        });
-        launches_ += 2;  // D pre-pass + the dq and dkdv kernels
-      } else {
-        ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
-        tag("attn_bwd");
-        run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] { attn_bwd(a, stream_); });
-        ++launches_;  // the D = rowsum(dO*O) pre-pass inside attn_bwd
       }
+      tag("attn_bwd_sm100");
+      run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
+        attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_qblk128), static_cast<int>(b.qblk128.size() / 4),
+                       meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2), static_cast<int>(b.kvit128.size() / 4),
+                       stream_);
+      });
+      launches_ += dh_ == 64 ? 1 : 2;  // + the D pre-pass (and the dh = 128 dK/dV kernel)
     }
     // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
-    if (attn_bwd_impl_ == 1) {
-      tag("k_pack_dkv");
-      run(KC_ELEMWISE, 0, nd * 20, [&] { k_pack_dkv(dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
-    } else {
+    if (dh_ == 64) {
       tag("k_pack_dqkv");
       run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
+    } else {
+      tag("k_pack_dkv");
+      run(KC_ELEMWISE, 0, nd * 20, [&] { k_pack_dkv(dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
     }
     {  // dW_{q,k,v} += normed1^T [dq | dk | dv]  (model.hpp:610-612)
       EpiParams e;
@@ -941,7 +920,14 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
   const auto t_start = now();
   if (tree.nodes[0].max_path_below > cfg_.max_position)
     throw std::invalid_argument("tree_train_step: path exceeds max_position");
+  // every token is both an embedding row and (as the next token of its predecessor) a CE target:
+  // reject ids outside [0, V) before anything is uploaded (model.hpp:343,653)
+  for (const auto& nd : tree.nodes)
+    for (int32_t t : nd.tokens)
+      if (t < 0 || static_cast<uint64_t>(t) >= cfg_.vocab_size)
+        throw std::invalid_argument("tree_train_step: token id out of vocab range");
   auto plan = std::make_unique<StepPlan>();
+  plan->owner = this;
   auto& batches = plan->batches;
   auto& ops = plan->ops;
   const auto pre = preorder(tree);
@@ -1195,6 +1181,7 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
 }
 
 tt_step_result Engine::execute(StepPlan& plan) {
+  if (plan.owner != this) throw std::invalid_argument("plan_execute: the plan was prepared by another engine");
   if (!seg_stack_.empty()) throw std::runtime_error("tree_train_step: segment stack is not empty");
   ensure_capacity(plan.rows, plan.arena_peak, plan.max_n, plan.max_loss);
   cur_meta_ = plan.meta_ptr;
@@ -1202,7 +1189,7 @@ tt_step_result Engine::execute(StepPlan& plan) {
   // First execution eager (sets kernel attributes, proves the plan); from the second one on, the
   // whole op list is one CUDA graph (re-captured if any device buffer was reallocated since).
   const bool use_graph = cuda_graph_ && !profiling_ && plan.warmed;
-  if (use_graph && !(plan.graph && plan.graph_gen == alloc_generation())) {
+  if (use_graph && !(plan.graph && plan.graph_gen == alloc_generation() && plan.graph_opts == opt_epoch_)) {
     if (plan.graph) {
       cudaGraphExecDestroy(plan.graph);
       plan.graph = nullptr;
@@ -1223,6 +1210,7 @@ tt_step_result Engine::execute(StepPlan& plan) {
     plan.graph_launches = launches_ - l0;
     launches_ = l0;
     plan.graph_gen = alloc_generation();
+    plan.graph_opts = opt_epoch_;
   }
   if (use_graph) {
     ck(cudaGraphLaunch(plan.graph, stream_), "graph launch");
@@ -1251,6 +1239,7 @@ tt_step_result Engine::execute(StepPlan& plan) {
 
 // Enqueues one step of the plan on the engine stream (no host synchronisation: graph-capturable).
 void Engine::issue_ops(const StepPlan& plan) {
+  gemm_set_2cta(gemm_2cta_);
   ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
   for (const auto& op : plan.ops) {
     const Batch& b = plan.batches[op.b];
@@ -1289,8 +1278,14 @@ void Engine::stack_reset() {
   }
 }
 
-void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out) {
+// forward_segment (model.hpp:328-463) continuing from the device stack. want_kv = false: the
+// segment's K/V rows are not kept for descendants (no push on top of it); want_activations = false:
+// its activations are dropped right away (its pop recomputes them, the chunked backward's
+// recompute). Neither: forward only, the stack is unchanged.
+void Engine::segment_push(const int32_t* tokens, uint64_t len, bool want_kv, bool want_acts, float* logits_out) {
   if (len == 0) throw std::invalid_argument("forward_segment: empty token list");
+  if (!seg_stack_.empty() && seg_stack_.back().no_kv)
+    throw std::invalid_argument("forward_segment: the prefix segment was pushed with want_kv = false");
   const int64_t S = static_cast<int64_t>(stack_tokens());
   if (S + static_cast<int64_t>(len) > static_cast<int64_t>(cfg_.max_position))
     throw std::invalid_argument("forward_segment: position overflow beyond max_position");
@@ -1303,6 +1298,9 @@ void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out
   b.seg_off = {0};
   b.seg_len = {b.n};
   b.full_logits = true;
+  b.no_kv = !want_kv;
+  b.has_acts = want_acts;
+  b.leaf_batch = !want_kv;
   b.attn_ctx = double(b.n) * double(S) + 0.5 * double(b.n) * double(b.n + 1);
   for (uint64_t t = 0; t < len; ++t) {
     b.tokens.push_back(tokens[t]);
@@ -1317,13 +1315,13 @@ void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out
   b.arena_off = arena_top_;
   const size_t need = align_up(layout(b.n).total);
   if (arena_top_ + need > arena_.bytes) throw std::runtime_error("segment_push: activation arena exhausted");
-  arena_top_ += need;
   std::vector<Batch*> ptrs;
   for (auto& x : seg_stack_) ptrs.push_back(&x);
   ptrs.push_back(&b);
   upload_meta(ptrs);
+  gemm_set_2cta(gemm_2cta_);
   forward_batch(b, b.arena_off);
-  if (logits_out) {
+  if (logits_out) {  // host or device pointer (unified addressing)
     const ActLayout lay = layout(b.n);
     const bf16* nf = arena_.as<bf16>(b.arena_off + lay.nf);
     for (int64_t c0 = 0; c0 < b.n; c0 += head_chunk_) {
@@ -1334,46 +1332,155 @@ void Engine::segment_push(const int32_t* tokens, uint64_t len, float* logits_out
       e.ldo[0] = V_;
       gemm(op(nf + c0 * d_, d_, false), op(head_, V_, true), static_cast<int>(cm), static_cast<int>(V_),
            static_cast<int>(d_), e, 1);
-      ck(cudaMemcpyAsync(logits_out + c0 * V_, sc_logits_.p, cm * V_ * 4, cudaMemcpyDeviceToHost, stream_),
+      ck(cudaMemcpyAsync(logits_out + c0 * V_, sc_logits_.p, cm * V_ * 4, cudaMemcpyDefault, stream_),
          "logits download");
     }
   }
   ck(cudaGetLastError(), "segment_push");
   ck(cudaStreamSynchronize(stream_), "segment_push");
+  if (!want_kv && !want_acts) return;  // forward only
+  if (want_acts) arena_top_ += need;
   seg_stack_.push_back(std::move(b));
 }
 
+// weighted_nll (model.hpp:643-677) of the top segment on the device — the VISIT of SPEC.md:225.
+// row_off[n + 1] (NULL: one pair per row) indexes (targets, weights) pairs per segment row; pairs of
+// weight 0 contribute nothing. The pairs stay with the frame: its pop takes grad_logits from them
+// (fused LM-head GEMM + CE, no logits crossing PCIe).
+double Engine::segment_loss(const uint64_t* row_off, const int32_t* targets, const double* weights) {
+  if (seg_stack_.empty()) throw std::invalid_argument("weighted_nll: empty stack");
+  Batch& b = seg_stack_.back();
+  if (!b.has_acts) throw std::invalid_argument("weighted_nll: the segment was pushed with want_activations = false");
+  if (!targets || !weights) throw std::invalid_argument("weighted_nll: null targets / weights");
+  b.loss_rows.clear();
+  b.pair_off.clear();
+  b.pair_tgt.clear();
+  b.pair_w.clear();
+  for (int64_t r = 0; r < b.n; ++r) {
+    const uint64_t p0 = row_off ? row_off[r] : static_cast<uint64_t>(r);
+    const uint64_t p1 = row_off ? row_off[r + 1] : static_cast<uint64_t>(r + 1);
+    if (p1 < p0) throw std::invalid_argument("weighted_nll: row offsets must be non-decreasing");
+    bool row = false;
+    for (uint64_t p = p0; p < p1; ++p) {
+      if (targets[p] < 0 || static_cast<uint64_t>(targets[p]) >= cfg_.vocab_size)
+        throw std::invalid_argument("weighted_nll: target id out of vocab range");
+      if (!std::isfinite(weights[p])) throw std::invalid_argument("weighted_nll: non-finite weight");
+      if (weights[p] == 0.0) continue;
+      if (!row) {
+        b.loss_rows.push_back(static_cast<int32_t>(r));
+        b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
+        row = true;
+      }
+      b.pair_tgt.push_back(targets[p]);
+      b.pair_w.push_back(weights[p]);
+    }
+  }
+  b.pair_off.push_back(static_cast<int32_t>(b.pair_tgt.size()));
+  b.full_logits = false;
+  b.has_loss = true;
+  std::vector<Batch*> ptrs;
+  for (auto& x : seg_stack_) ptrs.push_back(&x);
+  upload_meta(ptrs);
+  gemm_set_2cta(gemm_2cta_);
+  ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
+  const ActLayout lay = layout(b.n);
+  head_backward(b, arena_.as<bf16>(b.arena_off + lay.nf), /*loss_only=*/true);
+  ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
+  ck(cudaStreamSynchronize(stream_), "weighted_nll");
+  if (!std::isfinite(*loss_host_)) throw NonFiniteError("weighted_nll: non-finite loss");
+  return *loss_host_;
+}
+
+// backward_segment (model.hpp:474-633) of the top segment. Upstream grad_logits: the caller's
+// [len x V] (host or device) or, after segment_loss, the device CE of the frame's pairs; grad_new_kv
+// is what the segments popped above it added into its dK/dV stack rows. The returned KVGrad
+// (grad_prefix, rows [0, S)) is added into the ancestors' rows; with grad_prefix_out (host or
+// device, [L][2][S][d] fp32) the attention backward writes it into a separate zeroed buffer that is
+// copied out and then added into the stack — the pop's own contribution, not a difference.
 void Engine::segment_pop(const float* grad_logits, float* grad_prefix_out) {
   if (seg_stack_.empty()) throw std::invalid_argument("backward_segment: empty stack");
   Batch& b = seg_stack_.back();
-  const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
-  std::vector<float> before;
+  if (b.has_loss && grad_logits)
+    throw std::invalid_argument("backward_segment: grad_logits given for a segment whose loss is on the device");
+  const bool want_gp = grad_prefix_out && b.S > 0;
   const size_t pre = static_cast<size_t>(b.S) * d_;
-  auto download = [&](float* dst) {
-    for (int64_t l = 0; l < L_; ++l) {
-      ck(cudaMemcpyAsync(dst + (2 * l) * pre, dkst_.as<float>() + l * kv_layer, pre * 4, cudaMemcpyDeviceToHost,
-                         stream_),
-         "dK download");
-      ck(cudaMemcpyAsync(dst + (2 * l + 1) * pre, dvst_.as<float>() + l * kv_layer, pre * 4, cudaMemcpyDeviceToHost,
-                         stream_),
-         "dV download");
-    }
-  };
-  if (grad_prefix_out && b.S > 0) {
-    before.resize(2 * L_ * pre);
-    download(before.data());
+  if (want_gp) {
+    sc_gpre_.ensure(2 * L_ * pre * sizeof(float));
+    ck(cudaMemsetAsync(sc_gpre_.p, 0, 2 * L_ * pre * sizeof(float), stream_), "memset");
   }
   std::vector<Batch*> ptrs;
   for (auto& x : seg_stack_) ptrs.push_back(&x);
   upload_meta(ptrs);
-  backward_batch(b, b.arena_off, grad_logits);
-  if (grad_prefix_out && b.S > 0) download(grad_prefix_out);
+  gemm_set_2cta(gemm_2cta_);
+  if (!b.has_acts) {  // recompute the activations from the stack (chunked backward)
+    if (b.arena_off + align_up(layout(b.n).total) > arena_.bytes)
+      throw std::runtime_error("segment_pop: activation arena exhausted");
+    forward_batch(b, b.arena_off);
+  }
+  backward_batch(b, b.arena_off, grad_logits, want_gp ? sc_gpre_.as<float>() : nullptr);
+  if (want_gp) {
+    ck(cudaMemcpyAsync(grad_prefix_out, sc_gpre_.p, 2 * L_ * pre * sizeof(float), cudaMemcpyDefault, stream_),
+       "grad_prefix download");
+    const size_t kv_layer = static_cast<size_t>(rows_cap_) * d_;
+    for (int64_t l = 0; l < L_; ++l) {  // KVGrad::add_rows into the ancestors' frames (model.hpp:193-206)
+      k_add_f32(dkst_.as<float>() + l * kv_layer, sc_gpre_.as<float>() + (2 * l) * pre, static_cast<long>(pre), stream_);
+      k_add_f32(dvst_.as<float>() + l * kv_layer, sc_gpre_.as<float>() + (2 * l + 1) * pre, static_cast<long>(pre),
+                stream_);
+    }
+  }
   ck(cudaGetLastError(), "segment_pop");
   ck(cudaStreamSynchronize(stream_), "segment_pop");
-  if (grad_prefix_out && b.S > 0)
-    for (size_t i = 0; i < before.size(); ++i) grad_prefix_out[i] -= before[i];
   arena_top_ = b.arena_off;
   seg_stack_.pop_back();
+}
+
+// weighted_nll (model.hpp:643-677) as a standalone device operation over caller logits.
+double Engine::weighted_nll(const float* logits, uint64_t n, const uint64_t* row_off, const int32_t* targets,
+                            const double* weights, float* grad_out) {
+  if (n == 0) return 0.0;
+  if (!logits || !targets || !weights) throw std::invalid_argument("weighted_nll: null logits / targets / weights");
+  std::vector<int32_t> off(n + 1), tgt;
+  std::vector<double> w;
+  for (uint64_t r = 0; r < n; ++r) {
+    const uint64_t p0 = row_off ? row_off[r] : r, p1 = row_off ? row_off[r + 1] : r + 1;
+    if (p1 < p0) throw std::invalid_argument("weighted_nll: row offsets must be non-decreasing");
+    off[r] = static_cast<int32_t>(tgt.size());
+    for (uint64_t p = p0; p < p1; ++p) {
+      if (targets[p] < 0 || static_cast<uint64_t>(targets[p]) >= cfg_.vocab_size)
+        throw std::invalid_argument("weighted_nll: target id out of vocab range");
+      if (!std::isfinite(weights[p])) throw std::invalid_argument("weighted_nll: non-finite weight");
+      if (weights[p] == 0.0) continue;
+      tgt.push_back(targets[p]);
+      w.push_back(weights[p]);
+    }
+  }
+  off[n] = static_cast<int32_t>(tgt.size());
+  DevBuf meta;
+  const size_t o_tgt = align_up(off.size() * 4), o_w = o_tgt + align_up(std::max<size_t>(tgt.size(), 1) * 4);
+  meta.ensure(o_w + std::max<size_t>(w.size(), 1) * 8);
+  ck(cudaMemcpyAsync(meta.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, stream_), "nll meta");
+  if (!tgt.empty()) {
+    ck(cudaMemcpyAsync(meta.as<char>(o_tgt), tgt.data(), tgt.size() * 4, cudaMemcpyHostToDevice, stream_), "nll meta");
+    ck(cudaMemcpyAsync(meta.as<char>(o_w), w.data(), w.size() * 8, cudaMemcpyHostToDevice, stream_), "nll meta");
+  }
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(static_cast<int64_t>(n), (int64_t(1) << 30) / (V_ * 8)));
+  DevBuf lg, gr;
+  lg.ensure(static_cast<size_t>(chunk) * V_ * 4);
+  gr.ensure(static_cast<size_t>(chunk) * V_ * 4);
+  ck(cudaMemsetAsync(loss_.p, 0, sizeof(double), stream_), "memset");
+  for (int64_t c0 = 0; c0 < static_cast<int64_t>(n); c0 += chunk) {
+    const int64_t cm = std::min<int64_t>(chunk, static_cast<int64_t>(n) - c0);
+    ck(cudaMemcpyAsync(lg.p, logits + c0 * V_, static_cast<size_t>(cm) * V_ * 4, cudaMemcpyDefault, stream_), "logits");
+    k_ce_f32(lg.as<float>(), static_cast<int>(cm), V_, meta.as<int32_t>() + c0, meta.as<int32_t>(o_tgt),
+             meta.as<double>(o_w), gr.as<float>(), loss_.as<double>(), stream_);
+    if (grad_out)
+      ck(cudaMemcpyAsync(grad_out + c0 * V_, gr.p, static_cast<size_t>(cm) * V_ * 4, cudaMemcpyDefault, stream_),
+         "grad_logits");
+  }
+  ck(cudaGetLastError(), "weighted_nll");
+  ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
+  ck(cudaStreamSynchronize(stream_), "weighted_nll");
+  return *loss_host_;
 }
 
 }  // namespace ttb

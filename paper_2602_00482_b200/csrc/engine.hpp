@@ -55,18 +55,19 @@ struct Batch {
   std::vector<int64_t> seg_off, seg_len;
   // host-built metadata (uploaded once per step)
   std::vector<int32_t> tokens, positions;
-  std::vector<int32_t> qblk;   // int4 per 64-row query block (mma.sync forward)
-  std::vector<int32_t> qblk128;  // int4 per 128-row query block (tcgen05 forward)
-  std::vector<int32_t> kvit;   // int4 per backward item
-  std::vector<int32_t> kvit2;  // int2 per backward item
-  std::vector<int32_t> kvit128, kvit128_2;  // 128-row stack blocks (tcgen05 dK/dV kernel)
+  std::vector<int32_t> qblk128;  // int4 per 128-row query block (forward; dh = 128 dQ kernel)
+  std::vector<int32_t> kvit128, kvit128_2;  // 128-row stack blocks {kv_row0, rows, q_lo, q_hi} / {seg_off, own}
   std::vector<int32_t> loss_rows, pair_off, pair_tgt;
   std::vector<double> pair_w;
   // device offsets (bytes) into the metadata buffer
-  size_t o_tok = 0, o_pos = 0, o_qblk = 0, o_qblk128 = 0, o_kvit = 0, o_kvit2 = 0, o_kvit128 = 0, o_kvit128_2 = 0, o_lrows = 0, o_poff = 0, o_ptgt = 0, o_pw = 0;
+  size_t o_tok = 0, o_pos = 0, o_qblk128 = 0, o_kvit128 = 0, o_kvit128_2 = 0, o_lrows = 0, o_poff = 0, o_ptgt = 0, o_pw = 0;
   size_t arena_off = 0;
   double attn_ctx = 0;       // sum over query rows of attended keys (S + t + 1): attention FLOP model
   bool full_logits = false;  // segment API: head over all rows with caller-provided grad_logits
+  // segment API frame state (forward_segment's want_kv / want_activations, model.hpp:328-331)
+  bool no_kv = false;        // pushed with want_kv = false: no segment may be pushed on top of it
+  bool has_acts = true;      // activations kept (false: the pop recomputes them from the stack)
+  bool has_loss = false;     // weighted_nll pairs set on the device (tt_segment_loss)
   bool leaf_batch = false;   // childless node(s): K/V not kept for descendants (leaf_kv_skip ledger)
   int accum_inc = 1;         // GradientStore::accum_count increment (nodes completed by this pop)
 };
@@ -95,7 +96,8 @@ struct StepPlan {
   // CUDA graph of the whole op list (captured on the second execute, replayed afterwards)
   bool warmed = false;
   cudaGraphExec_t graph = nullptr;
-  uint64_t graph_gen = 0, graph_launches = 0;
+  uint64_t graph_gen = 0, graph_launches = 0, graph_opts = 0;
+  const void* owner = nullptr;  // the Engine that prepared the plan (its buffers are baked in)
   StepPlan() = default;
   StepPlan(const StepPlan&) = delete;
   StepPlan& operator=(const StepPlan&) = delete;
@@ -126,6 +128,7 @@ class Engine {
   ~Engine();
 
   const tt_model_config& config() const { return cfg_; }
+  int device() const { return device_; }
   uint64_t param_count() const { return n_params_; }
   cudaStream_t stream() const { return stream_; }
 
@@ -133,6 +136,15 @@ class Engine {
   void init_random(uint64_t seed);
   void grads_zero();
   void grads_download(float* out, uint64_t n);
+  void grads_download_f64(double* out, uint64_t n);
+  // in-place sum all-reduce of the GradientStore over an NCCL communicator (ncclComm_t), on the
+  // engine stream (SPEC.md:278's worker-order reduction, replaced by one ncclAllReduce)
+  void grads_allreduce(void* nccl_comm);
+  // weighted_nll (model.hpp:643-677) on the device over caller logits [n x V] (host or device
+  // pointer); row_off (n + 1, NULL = one pair per row) indexes targets/weights; grad_out [n x V]
+  // fp32 (host or device, may be NULL). Returns the loss (fp64).
+  double weighted_nll(const float* logits, uint64_t n, const uint64_t* row_off, const int32_t* targets,
+                      const double* weights, float* grad_out);
   float* grads_device() const { return grads_.as<float>(); }
   uint64_t accum_count() const { return accum_count_; }
 
@@ -143,7 +155,6 @@ class Engine {
   tt_step_result execute(StepPlan& plan);
 
   void set_profiling(bool on) { profiling_ = on; }
-  // Implementation switches (ablation / cross-checks): attn_{fwd,bwd}_impl 0 = mma.sync, 1 = tcgen05.
   void set_option(const std::string& key, int64_t value);
   const KStats& kstats() const { return kstats_; }
   void reset_kstats() {
@@ -154,7 +165,8 @@ class Engine {
   const std::string& last_trace() const { return last_trace_; }
 
   // segment level (device stack)
-  void segment_push(const int32_t* tokens, uint64_t len, float* logits_out);
+  void segment_push(const int32_t* tokens, uint64_t len, bool want_kv, bool want_acts, float* logits_out);
+  double segment_loss(const uint64_t* row_off, const int32_t* targets, const double* weights);
   void segment_pop(const float* grad_logits, float* grad_prefix_out);
   void stack_reset();
   uint64_t stack_segments() const { return seg_stack_.size(); }
@@ -169,8 +181,8 @@ class Engine {
   void build_meta(Batch& b, size_t& cursor, std::vector<char>& host);
   void upload_meta(std::vector<Batch*>& batches);
   void forward_batch(const Batch& b, size_t arena_off);
-  void backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits);
-  void head_backward(const Batch& b, const bf16* nf);
+  void backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits, float* grad_prefix = nullptr);
+  void head_backward(const Batch& b, const bf16* nf, bool loss_only = false);
   void head_backward_dense(const Batch& b, const bf16* nf, const float* host_grad_logits);
   void gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& e, int splits);
   template <typename T>
@@ -229,6 +241,7 @@ class Engine {
   int64_t scratch_n_ = 0, head_chunk_ = 0;
   DevBuf sc_gx_, sc_gxb_, sc_gxf_, sc_gn_, sc_gh_, sc_dO_, sc_D_, sc_dq_, sc_dqkv_;
   DevBuf sc_nfl_, sc_logits_, sc_stats_, sc_dlog_, sc_gnf_;
+  DevBuf sc_gpre_;  // segment pop: this pop's grad_prefix by itself ([L][2][S][d] fp32)
   DevBuf meta_;
   DevBuf loss_;
   double* loss_host_ = nullptr;  // pinned
@@ -240,9 +253,9 @@ class Engine {
   bool profiling_ = false;
   bool cuda_graph_ = true;  // replay prepared plans as CUDA graphs (engine option "cuda_graph")
   void issue_ops(const StepPlan& plan);
-  int attn_fwd_impl_ = 1;
-  int attn_bwd_impl_ = 1;
   bool ce_stats_ = true;
+  int gemm_2cta_ = 1;
+  uint64_t opt_epoch_ = 1;  // bumped by set_option: a plan's CUDA graph is re-captured after a change
   // multi-root batching: consecutive forest roots whose children are all short leaves are pushed as
   // ONE batch of up to this many tokens (0 = off); each root's leaves attend to its own rows
   int64_t root_batch_tokens_ = 4096;

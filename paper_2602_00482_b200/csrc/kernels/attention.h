@@ -23,9 +23,7 @@ struct AttnFwdArgs {
   float scale = 1.0f;
 };
 
-// One backward work item per (stack KV block, query range):
-//   items[i]  = {kv_row0 (absolute stack row), kv_rows (<=64), q_lo, q_hi}
-//   items2[i] = {seg_off, is_own}
+// Backward arguments (the work lists are passed to attn_bwd_sm100 separately).
 struct AttnBwdArgs {
   const __nv_bfloat16* q = nullptr;
   const __nv_bfloat16* dO = nullptr;  // same pitch as q
@@ -45,35 +43,29 @@ struct AttnBwdArgs {
   float* dk = nullptr;  // fp32 dK/dV stack rows (absolute), accumulated
   float* dv = nullptr;
   long lddkv = 0;
+  // prefix-row (grad_prefix) destination, absolute rows with pitch lddkv; nullptr = dk / dv
+  float* dk_pre = nullptr;
+  float* dv_pre = nullptr;
   int n = 0, H = 0, dh = 0, S = 0;
-  const int4* items = nullptr;
-  const int2* items2 = nullptr;
-  int nitems = 0;
   int pbase = 0, r0 = -1;  // as in AttnFwdArgs (the dK/dV items carry absolute rows already)
   float scale = 1.0f;
 };
 
-void attn_fwd(const AttnFwdArgs& a, cudaStream_t stream);
-void attn_bwd(const AttnBwdArgs& a, cudaStream_t stream);
 
 // tcgen05/TMEM/TMA forward (attention_sm100.cu): qblocks hold 128-row query blocks; k/v are the
 // layer's stack base pointers with rows_cap rows.
 constexpr int kFwdBlockQ = 128;
 void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream);
 
-// Forward softmax exponentials taken on the FMA pipe per 4 element pairs (0..2; default 1). Tuning
-// knob: env TT_ATTN_POLY, read once.
-int attn_poly_pairs();
 
-// Copies the clock64 trace of the TT_ATTN_DBG=3 dq kernel (4 x 256: MMA ds_full wake, MMA issue
-// done, softmax s_full wake, softmax arrive). Returns the count copied or -1.
-int attn_debug_trace(long long* host, int n);
 
 // D = rowsum(dO * O) per (head, row) (the softmax-backward correction term).
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream);
 // tcgen05 backward (attention_bwd_sm100.cu): dq_blocks are 128-row query blocks (like the forward);
 // kv_items/kv_items2 are 128-row stack blocks {kv_row0, kv_rows, q_lo, q_hi} / {seg_off, is_own}.
-// dq is overwritten; dk/dv are accumulated (red.add) into the fp32 stack rows.
+// dk/dv are accumulated (red.add) into the fp32 stack rows (prefix rows into dk_pre/dv_pre when set).
+// dQ (scaled): dh = 64 ADDS into the fp32 accumulator dq [n x lddq] (zeroed by the caller); dh = 128
+// writes bf16 dq16 [n x lddq16].
 constexpr int kBwdBlockKV = 128;
 void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                     const int2* kv_items2, int n_kv, cudaStream_t stream);

@@ -3,16 +3,14 @@
 // Replaces the attention backward of backward_segment (model.hpp:546-604):
 //   P = softmax(scale Q K^T) (recomputed from the forward LSE), dP = dO V^T,
 //   dS = P * (dP - D) with D = rowsum(dO * O),  dQ = scale dS K,  dK = scale dS^T Q,  dV = P^T dO.
-// Two kernels, both tensor-core only (no atomics on the hot product):
-//   dq kernel   : CTA = (128-query block, head); loops over the block's KV blocks (BKV = 64).
-//                 S, dP double-buffered in TMEM; dS -> swizzled smem; dQ accumulated in TMEM and
-//                 written once (fp32) — the CTA owns its query rows.
-//   dkdv kernel : CTA = (128-key stack block, head, query range); loops over 64-query blocks.
-//                 S^T, dP^T double-buffered in TMEM; P^T, dS^T -> swizzled smem; dK, dV accumulated
-//                 in TMEM, added once into the fp32 dK/dV stack rows (red.add.v4: several query-range
-//                 items and several sibling segments contribute to the same prefix rows).
-// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM alloc + MMA issuer, warps 2..5 one
-// TMEM lane (= query row / key row) per thread.
+// dh = 64: ONE fused key-parallel kernel (fa_bwd_fused_kernel): P and dS once per (key block, query
+//   block) pair; dK/dV accumulate in TMEM and are added once into the fp32 dK/dV stack rows
+//   (red.add.v4: several query-range items and sibling segments contribute to the same prefix rows);
+//   dQ partials leave through cp.reduce.async.bulk into an fp32 accumulator.
+// dh = 128: a query-parallel dQ kernel (CTA owns its rows, dQ in TMEM, written once as bf16) and a
+//   key-parallel dK/dV kernel (red.add.v4 into the stack rows); TMEM has no room for a dQ accumulator
+//   next to 128-wide dK/dV. Both use two MMA-issuing warps and 8 softmax-gradient warps (2 per TMEM
+//   lane quadrant, each owning half of the columns).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -36,6 +34,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 // Writes 32 bf16 values (w[16] packed pairs) = chunks [4*half, 4*half+4) of a thread's 128B row.
 __device__ __forceinline__ void st_halfrow_sw128(uint8_t* panel, int row, int half, const uint32_t (&w)[16]) {
@@ -76,9 +77,11 @@ struct BwdParams {
   long lddq;
   __nv_bfloat16* dq16;  // if set: bf16 dQ [n x lddq16] instead of dq
   long lddq16;
-  float* dk;  // stack rows (this layer), fp32
+  float* dk;  // stack rows (this layer), fp32: the batch's own rows
   float* dv;
   long lddkv;
+  float* dk_pre;  // where the prefix rows' dK/dV go (absolute rows, same pitch): the stack, or a
+  float* dv_pre;  // separate buffer when the caller wants this pop's grad_prefix by itself
   int n, S, H;
   int pbase, r0;        // prefix rows [pbase, pbase + S); own rows from r0
   const int4* blocks;   // dq: {q_start, q_end, seg_off, 0}; dkdv: {kv_row0, kv_rows, q_lo, q_hi}
@@ -86,16 +89,12 @@ struct BwdParams {
   float scale, scale_log2;
 };
 
-// DBG (timing experiments only, TT_ATTN_DBG): 1 = softmax warps skip TMEM loads + math (MMA/TMA
-// pipeline alone), 2 = softmax warps do not wait for S (softmax alone), 4 = + clock64 trace of one
-// mid-grid CTA into g_attn_trace (tt_debug_attn_trace). TT_ATTN_DBG=3 -> trace, 5 -> skip + trace.
-__device__ long long g_attn_trace[6][256];
 // Two MMA-issuing warps: warp 1 issues S_j / dP_j, warp 10 issues dQ += dS_j K_j. An mbarrier wait in
 // an issuing thread costs ~180 clk while MMAs are in flight (tools/umma_probe.cu, mode 8), longer than
 // the tensor pipe takes for the 4-8 N=64 MMAs queued behind it; with one issuer per dependency chain
 // a wait on one chain never starves the pipe of the other chain's MMAs.
 constexpr int kThreadsDq = kThreads + 32;
-template <int DH, int NS, int POLY, int DBG = 0>
+template <int DH, int NS, int POLY>
 __global__ void __launch_bounds__(kThreadsDq, 1)
     fa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
                      const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
@@ -175,13 +174,11 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
   } else if (warp == 1) {
     // S_j = Q K_j^T ; dP_j = dO V_j^T into TMEM buffer j % NB, once the softmax is done with j - NB
     const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);  // K-major tiles
-    const bool trace = (DBG & 4) && lane == 0 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     mbar_wait(q_full, 0);
     for (int j = 0; j < nblk; ++j) {
       const int st = j % NS;
       // buffer j % NB holds dS_{j-NB} (the A operand of dQ_{j-NB}) until that MMA completes
       if (j >= NB) mbar_wait(&kv_empty[(j - NB) % NS], ((j - NB) / NS) & 1);
-      if (trace && j < 256) g_attn_trace[4][j] = clock64();
       mbar_wait(&kv_full[st], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
@@ -197,15 +194,12 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
         umma_commit(&s_full[j % NB]);
       }
       __syncwarp();
-      if (trace && j < 256) g_attn_trace[5][j] = clock64();
     }
   } else if (warp == 10) {
     // dQ += dS_j K_j (B = K_j read MN-major: N = dh, K = keys), in block order
     const uint64_t dKmn = make_sdesc_sw128(smem_u32(smem), BKV * 128, 1024);
-    const bool trace = (DBG & 4) && lane == 0 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&ds_full[j % NB], (j / NB) & 1);
-      if (trace && j < 256) g_attn_trace[0][j] = clock64();
       tc_fence_after();
       if (lane == 0) {
         const int st = j % NS;
@@ -219,7 +213,6 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
         if (j == nblk - 1) umma_commit(dq_done);
       }
       __syncwarp();
-      if (trace && j < 256) g_attn_trace[1][j] = clock64();
     }
   } else {
     const int quad = warp & 3;
@@ -234,17 +227,9 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
     const float Dr = row_ok ? p.D[static_cast<long>(h) * p.n + row] : 0.f;
     const float c2 = p.scale_log2;
     constexpr int HC = BKV / 2;
-    const bool trace = (DBG & 4) && threadIdx.x == 64 && blockIdx.x == gridDim.x / 2 && blockIdx.y == 0;
     for (int j = 0; j < nblk; ++j) {
-      if (DBG != 2) mbar_wait(&s_full[j % NB], (j / NB) & 1);
-      if (trace && j < 256) g_attn_trace[2][j] = clock64();
+      mbar_wait(&s_full[j % NB], (j / NB) & 1);
       tc_fence_after();
-      if ((DBG & 1)) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&ds_full[j % NB]);
-        continue;
-      }
       float s[HC], dp[HC];
 #pragma unroll
       for (int c = 0; c < HC; c += 16) {
@@ -281,7 +266,6 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&ds_full[j % NB]);
-      if (trace && j < 256) g_attn_trace[3][j] = clock64();
     }
     mbar_wait(dq_done, 0);
     tc_fence_after();
@@ -541,8 +525,8 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
-    float* dkr = p.dk + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
-    float* dvr = p.dv + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+    float* dkr = (own ? p.dk : p.dk_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+    float* dvr = (own ? p.dv : p.dv_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
 #pragma unroll
     for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
       uint32_t rk[16], rv[16];
@@ -565,48 +549,74 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 
-// ================================================================= dK/dV kernel, 128 x 128 blocks
-// dh = 64 only. 128 keys x 128 queries per block: S^T / dP^T are N = 128 MMAs (full rate; the N = 64
-// ones run at 2/3), and each issuer wait now covers twice the MMA work. TMEM: S^T[2] (128 each),
-// ONE dP^T buffer (128), dK, dV (64 each) = 512 columns. P^T / dS^T (bf16 pairs) go over the S^T
-// buffer: half h of the query columns packs P^T into [64h, 64h+32) and dS^T into [64h+32, 64h+64);
-// the dP^T buffer is released as soon as the softmax has loaded it (dp_free), so dP^T_{i+1} is
-// computed while the softmax of block i finishes.
+// ============================================================ fused dQ / dK / dV kernel, dh = 64
+// One kernel per (128-key stack block, head, query range) item; it loops over the range's 128-query
+// blocks i and computes P and dS ONCE per (key block, query block) pair:
+//   warp 1      S^T_i = K Q_i^T, dP^T_i = V dO_i^T                (SS, M = 128 keys, N = 128 queries)
+//   warps 8-15  P^T = 2^(S^T c - lse2),  dS^T = P^T (dP^T scale - D scale)  (the softmax-gradient
+//               stream): P^T back into TMEM as bf16 pairs over S^T_i columns [0, 64), dS^T into a
+//               swizzled 32 KB smem tile (two of them: block i + 1's softmax never waits for block i's
+//               dK / dQ MMAs)
+//   warp 2      dV += P^T_i dO_i (TS), dK += dS^T_i Q_i (SS, the tile read K-major),
+//               dQ_i = dS_i K (SS, the same tile read MN-major) into S^T_i columns [64, 128)
+//   warps 4-7   dQ_i: TMEM -> registers -> swizzled smem -> cp.reduce.async.bulk .add into the fp32
+//               dQ accumulator [n x d] (each query block receives one partial per key block)
+//   warp 0      TMA: K, V once; Q_i / dO_i through an NS-stage ring
+// The softmax scale is folded into dS, so dK and dQ need no epilogue scaling. The two separate
+// kernels this replaces (query-parallel dQ, key-parallel dK/dV) each recomputed P and dS.
+// TMEM (512 columns): S^T[2] (128 each; P^T / dQ_i reuse them), dP^T (128), dK (64), dV (64).
 template <int NS>
-struct Dkv128Cfg {
+struct FusedCfg {
   static constexpr int DH = 64, BKV = 128, BQ = 128;
-  static constexpr int kKVBytes = BKV * DH * 2;  // K (or V) block
-  static constexpr int kQBytes = BQ * DH * 2;    // Q_i (or dO_i) tile
+  static constexpr int kKVBytes = BKV * DH * 2;                // K (or V) block, loaded once
+  static constexpr int kQBytes = BQ * DH * 2;                  // Q_i (or dO_i) tile
   static constexpr int kOffV = kKVBytes;
   static constexpr int kOffQ = 2 * kKVBytes;
   static constexpr int kOffDO = kOffQ + NS * kQBytes;
-  static constexpr int kOffStat = kOffDO + NS * kQBytes;  // [2][2][BQ] floats: lse2, D
+  static constexpr int kDSBytes = 2 * BKV * 128;               // dS^T: 2 query panels x [128 keys][128 B]
+  static constexpr int kOffDS = kOffDO + NS * kQBytes;         // two dS^T tiles (blocks i, i + 1)
+  static constexpr int kOffDQ = kOffDS + 2 * kDSBytes;         // dQ staging: 4 warps x (32 x 32 fp32)
+  static constexpr int kOffStat = kOffDQ + 4 * 4096;           // [2][2][BQ] floats: lse2, -scale D
   static constexpr int kOffBar = kOffStat + 2 * 2 * BQ * 4;
   static constexpr int kSmem = kOffBar + 256 + 1024;
-  static constexpr int kTmemCols = 512;
-  static_assert(kSmem <= 227 * 1024 && NS >= 2, "dkdv128: smem / ring");
-  static constexpr uint32_t kIdescS = make_idesc_bf16(128, BQ, false, false);
-  static constexpr uint32_t kIdescKV = make_idesc_bf16(128, DH, false, true);
+  static_assert(kSmem <= 227 * 1024 && NS >= 2, "fused attention backward: smem / ring");
+  static constexpr uint32_t kIdescS = make_idesc_bf16(128, BQ, false, false);  // S^T, dP^T
+  static constexpr uint32_t kIdescKV = make_idesc_bf16(128, DH, false, true);  // dV (TS), dK (A K-major)
+  static constexpr uint32_t kIdescQ = make_idesc_bf16(128, DH, true, true);    // dQ (A = dS MN-major)
 };
+constexpr int kThreadsFused = 512;  // warps 0-2 control (3 idle), 4-7 dQ drain, 8-15 softmax
 
-template <int NS, int POLY>
-__global__ void __launch_bounds__(kThreadsDq, 1)
-    fa_bwd_dkdv128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                          BwdParams p) {
-  using C = Dkv128Cfg<NS>;
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, const void* smem_src, int32_t x, int32_t y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(smem_u32(smem_src)), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int NS>
+__global__ void __launch_bounds__(kThreadsFused, 1)
+    fa_bwd_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_do,
+                        const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                        const __grid_constant__ CUtensorMap tm_dq, BwdParams p) {
+  using C = FusedCfg<NS>;
   constexpr int DH = C::DH, BQ = C::BQ;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = align_smem_1024(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;
-  uint64_t* q_empty = q_full + NS;  // dV/dK_i done: frees the Q/dO stage and S^T buffer i % 2
-  uint64_t* s_full = q_empty + NS;  // [2]
-  uint64_t* p_full = s_full + 2;    // [2] softmax done with block i (P^T / dS^T in TMEM)
+  uint64_t* q_empty = q_full + NS;  // dV/dK/dQ_i issued and done: the Q/dO stage is free
+  uint64_t* s_full = q_empty + NS;  // [2] S^T_i in TMEM
+  uint64_t* p_full = s_full + 2;    // [2] softmax done with block i: P^T_i in TMEM, dS^T_i in smem
   uint64_t* dp_full = p_full + 2;   // dP^T_i computed (single buffer)
   uint64_t* dp_free = dp_full + 1;  // softmax has loaded dP^T_i
-  uint64_t* acc_done = dp_free + 1;
+  uint64_t* ds_free = dp_free + 1;  // [2] dK_i / dQ_i done: dS^T tile i % 2 may be rewritten
+  uint64_t* dq_full = ds_free + 2;  // [2] dQ_i in TMEM
+  uint64_t* dq_free = dq_full + 2;  // [2] dQ_i read out: S^T buffer i % 2 may take S^T_{i+2}
+  uint64_t* acc_done = dq_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
   float* stat = reinterpret_cast<float*>(smem + C::kOffStat);
 
@@ -626,6 +636,7 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
     tma_prefetch_desc(&tm_do);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_dq);
     mbar_init(kv_full, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&q_full[s], 1);
@@ -634,21 +645,25 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSmxWarps);
+      mbar_init(&dq_full[s], 1);
+      mbar_init(&dq_free[s], 4);
+      mbar_init(&ds_free[s], 1);
     }
     mbar_init(dp_full, 1);
     mbar_init(dp_free, kSmxWarps);
     mbar_init(acc_done, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_S = tmem, t_dP = tmem + 256, t_dK = tmem + 384, t_dV = tmem + 448;
+  const int wg = warp >> 2;
 
-  if (warp == 0) {
-    if (lane == 0) {
+  if (wg == 0) {
+    if (warp == 0 && lane == 0) {
       mbar_arrive_expect_tx(kv_full, 2 * C::kKVBytes);
       tma_load_2d(&tm_k, kv_full, smem, h * DH, kv0);
       tma_load_2d(&tm_v, kv_full, smem + C::kOffV, h * DH, kv0);
@@ -660,67 +675,116 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
         tma_load_2d(&tm_q, &q_full[st], smem + C::kOffQ + st * C::kQBytes, h * DH, q0);
         tma_load_2d(&tm_do, &q_full[st], smem + C::kOffDO + st * C::kQBytes, h * DH, q0);
       }
-    }
-  } else if (warp == 1) {
-    // S^T_i = K Q_i^T into S buffer i % 2 (after dV/dK_{i-2}); dP^T_i = V dO_i^T into the single dP^T
-    // buffer (after the softmax loaded dP^T_{i-1})
-    const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);
-    mbar_wait(kv_full, 0);
-    for (int i = 0; i < nq; ++i) {
-      const int st = i % NS;
-      if (i >= 2) mbar_wait(&q_empty[(i - 2) % NS], ((i - 2) / NS) & 1);
-      mbar_wait(&q_full[st], (i / NS) & 1);
-      tc_fence_after();
-      const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
-      if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < DH / 16; ++k)
-          umma_bf16_ss(t_S + (i & 1) * 128, sdesc_add(d16, k * 32), sdesc_add(sdesc_add(d16, q_off), k * 32), C::kIdescS,
-                       k > 0);
-        umma_commit(&s_full[i & 1]);
-      }
-      __syncwarp();
-      if (i >= 1) mbar_wait(dp_free, (i - 1) & 1);
-      tc_fence_after();
-      if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < DH / 16; ++k)
-          umma_bf16_ss(t_dP, sdesc_add(d16, C::kOffV + k * 32), sdesc_add(sdesc_add(d16, do_off), k * 32), C::kIdescS,
-                       k > 0);
-        umma_commit(dp_full);
-      }
-      __syncwarp();
-    }
-  } else if (warp == 10) {
-    // dV += P^T dO_i ; dK += dS^T Q_i  (A from the S^T buffer: P^T at 64h + ..., dS^T at 64h + 32 + ...)
-    const uint64_t dmn = make_sdesc_sw128(smem_u32(smem), BQ * 128, 1024);
-    for (int i = 0; i < nq; ++i) {
-      mbar_wait(&p_full[i & 1], (i >> 1) & 1);
-      tc_fence_after();
-      if (lane == 0) {
+    } else if (warp == 1) {
+      // S^T_i into buffer i % 2 once dQ_{i-2} has been read out of it; dP^T_i once the softmax has
+      // loaded dP^T_{i-1}
+      const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);  // K-major tiles
+      mbar_wait(kv_full, 0);
+      for (int i = 0; i < nq; ++i) {
         const int st = i % NS;
+        if (i >= 2) mbar_wait(&dq_free[i & 1], ((i - 2) >> 1) & 1);
+        mbar_wait(&q_full[st], (i / NS) & 1);
+        tc_fence_after();
         const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
+        if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < BQ / 16; ++k) {
-          const uint32_t col = (k / 4) * 64 + (k % 4) * 8;
-          umma_bf16_ts(t_dV, t_S + (i & 1) * 128 + col, sdesc_add(sdesc_add(dmn, do_off), k * 2048), C::kIdescKV,
-                       (i > 0 || k > 0));
-          umma_bf16_ts(t_dK, t_S + (i & 1) * 128 + col + 32, sdesc_add(sdesc_add(dmn, q_off), k * 2048), C::kIdescKV,
-                       (i > 0 || k > 0));
+          for (int k = 0; k < DH / 16; ++k)
+            umma_bf16_ss(t_S + (i & 1) * 128, sdesc_add(d16, k * 32), sdesc_add(d16, q_off + k * 32), C::kIdescS,
+                         k > 0);
+          umma_commit(&s_full[i & 1]);
         }
-        umma_commit(&q_empty[st]);
-        if (i == nq - 1) umma_commit(acc_done);
+        __syncwarp();
+        if (i >= 1) mbar_wait(dp_free, (i - 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+#pragma unroll
+          for (int k = 0; k < DH / 16; ++k)
+            umma_bf16_ss(t_dP, sdesc_add(d16, C::kOffV + k * 32), sdesc_add(d16, do_off + k * 32), C::kIdescS, k > 0);
+          umma_commit(dp_full);
+        }
+        __syncwarp();
+      }
+    } else if (warp == 2) {
+      // dV += P^T_i dO_i ; dK += dS^T_i Q_i ; dQ_i = dS_i K
+      const uint64_t dmn = make_sdesc_sw128(smem_u32(smem), BQ * 128, 1024);  // Q_i / dO_i / K as MN-major B
+      const uint64_t dsk = make_sdesc_sw128(smem_u32(smem + C::kOffDS), 16, 1024);           // dS^T, K-major A
+      const uint64_t dsm = make_sdesc_sw128(smem_u32(smem + C::kOffDS), C::BKV * 128, 1024);  // dS, MN-major A
+      for (int i = 0; i < nq; ++i) {
+        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const int st = i % NS;
+          const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
+#pragma unroll
+          const uint32_t ds_off = (i & 1) * C::kDSBytes;
+#pragma unroll
+          for (int k = 0; k < BQ / 16; ++k) {  // 16 queries per step
+            umma_bf16_ts(t_dV, t_S + (i & 1) * 128 + 8 * k, sdesc_add(dmn, do_off + k * 2048), C::kIdescKV,
+                         (i > 0 || k > 0));
+            umma_bf16_ss(t_dK, sdesc_add(dsk, ds_off + (k / 4) * 16384 + (k % 4) * 32), sdesc_add(dmn, q_off + k * 2048),
+                         C::kIdescKV, (i > 0 || k > 0));
+          }
+#pragma unroll
+          for (int k = 0; k < C::BKV / 16; ++k)  // 16 keys per step
+            umma_bf16_ss(t_S + (i & 1) * 128 + 64, sdesc_add(dsm, ds_off + k * 2048), sdesc_add(dmn, k * 2048), C::kIdescQ,
+                         k > 0);
+          umma_commit(&q_empty[st]);
+          umma_commit(&ds_free[i & 1]);
+          umma_commit(&dq_full[i & 1]);
+          if (i == nq - 1) umma_commit(acc_done);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (wg == 1) {
+    // dQ drain: warp w reads TMEM lanes (query rows) 32 (w % 4) .. +31 of dQ_i
+    const int qd = warp & 3;
+    const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
+    uint8_t* stage = smem + C::kOffDQ + qd * 4096;
+    for (int i = 0; i < nq; ++i) {
+      const int q0 = q_lo + i * BQ;
+      mbar_wait(&dq_full[i & 1], (i >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[64];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t t[16];
+        tmem_ld16(t_S + (i & 1) * 128 + 64 + 16 * c + lane_off, t);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) r[16 * c + e] = t[e];
+      }
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_free[i & 1]);
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        if (lane == 0) bulk_wait_read0();  // the previous reduce has read the staging buffer
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(stage + lane * 128 + ((c ^ (lane & 7)) * 16)) =
+              make_uint4(r[32 * cc + 4 * c], r[32 * cc + 4 * c + 1], r[32 * cc + 4 * c + 2], r[32 * cc + 4 * c + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(&tm_dq, stage, h * DH + 32 * cc, q0 + 32 * qd);
+          bulk_commit();
+        }
       }
       __syncwarp();
     }
+    if (lane == 0) bulk_wait_all();
+    __syncwarp();
   } else {
-    const int quad = warp & 3;
-    const int half = (warp - 2) / 4;    // query columns [64*half, 64*half+64) of each 128-query block
-    const int krow = quad * 32 + lane;  // key row within the block == TMEM lane
+    const int qd = warp & 3;
+    const int half = (warp - 8) >> 2;   // query columns [64 half, 64 half + 64) of each block
+    const int krow = qd * 32 + lane;    // key row within the block == TMEM lane
     const bool key_ok = krow < kv_rows;
-    const int kt = kt_base + krow;
-    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
-    const int tid = threadIdx.x - 64;  // 0..255
+    const int kt = kt_base + krow;      // own: local key index
+    const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
+    const int tid = threadIdx.x - 256;  // 0..255
+    uint8_t* ds_rows = smem + C::kOffDS + half * (C::BKV * 128) + krow * 128;
     float nl = INFINITY, nd = 0.f;
     auto fetch = [&](int i) {
       const int q = q_lo + i * BQ + tid;
@@ -729,91 +793,101 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
       nd = ok ? p.D[static_cast<long>(h) * p.n + q] : 0.f;
     };
     fetch(0);
-    const float c2 = p.scale_log2;
-    // P^T / dS^T of one 32-query sub-chunk sc (columns 64*half + 32*sc ...)
-    auto sub = [&](int i, int sc, const float (&s_in)[32], const float (&dp)[32], const float* st_lse,
-                   const float* st_D, uint32_t (&wp)[16], uint32_t (&wd)[16]) {
-      const int q0 = q_lo + i * BQ;
-      const int cb = 64 * half + 32 * sc;  // block column of s_in[0]
-      float s[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) s[c] = s_in[c];
-      if (own) {
-        const int lo = kt - (q0 - seg_off) - cb;  // key kt sees query column c iff c >= lo
-        if (__any_sync(0xffffffff, lo > 0)) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) s[c] = c >= lo ? s[c] : -INFINITY;
-        }
-      }
-      const float* lz_base = st_lse + cb;
-      const float* dz_base = st_D + cb;
-#pragma unroll
-      for (int c = 0; c < 32; c += 4) {
-        const float4 lz = *reinterpret_cast<const float4*>(lz_base + c);
-        const float4 dz = *reinterpret_cast<const float4*>(dz_base + c);
-        const float2 c22 = make_float2(c2, c2);
-        const float2 xa = __ffma2_rn(make_float2(s[c], s[c + 1]), c22, make_float2(-lz.x, -lz.y));
-        const float2 xb = __ffma2_rn(make_float2(s[c + 2], s[c + 3]), c22, make_float2(-lz.z, -lz.w));
-        const float2 pa = ((c / 2) & 3) < POLY ? ex2_poly2(xa) : make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
-        const float2 pb = ((c / 2 + 1) & 3) < POLY ? ex2_poly2(xb) : make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
-        const float2 da = __fmul2_rn(pa, __fadd2_rn(make_float2(dp[c], dp[c + 1]), make_float2(-dz.x, -dz.y)));
-        const float2 db = __fmul2_rn(pb, __fadd2_rn(make_float2(dp[c + 2], dp[c + 3]), make_float2(-dz.z, -dz.w)));
-        wp[c / 2] = pack_bf16x2(pa.x, pa.y);
-        wp[c / 2 + 1] = pack_bf16x2(pb.x, pb.y);
-        wd[c / 2] = pack_bf16x2(da.x, da.y);
-        wd[c / 2 + 1] = pack_bf16x2(db.x, db.y);
-      }
-    };
-    auto ld32 = [&](uint32_t taddr, float (&v)[32]) {
-      uint32_t r[16], r2[16];
-      tmem_ld16(taddr + lane_off, r);
-      tmem_ld16(taddr + 16 + lane_off, r2);
-      tmem_ld_wait();
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        v[e] = __uint_as_float(r[e]);
-        v[16 + e] = __uint_as_float(r2[e]);
-      }
-    };
+    const float c2 = p.scale_log2, sc = p.scale;
     for (int i = 0; i < nq; ++i) {
+      const int q0 = q_lo + i * BQ;
       float* st_lse = stat + (i & 1) * 2 * BQ;
-      float* st_D = st_lse + BQ;
+      float* st_nd = st_lse + BQ;
       if (tid < BQ) {
         st_lse[tid] = nl * kLog2e;
-        st_D[tid] = nd;
+        st_nd[tid] = -nd * sc;
       }
       named_bar_sync(1, 32 * kSmxWarps);
       fetch(i + 1);
-      const uint32_t sb = t_S + (i & 1) * 128 + 64 * half;
-      const uint32_t pb = t_dP + 64 * half;
+      // visibility: invalid keys see nothing; own rows: key kt sees query t iff kt <= t, i.e. block
+      // columns >= kt - (q0 - seg_off) (queries beyond q_hi have lse2 = +inf -> P = 0)
+      const int lo0 = key_ok ? (own ? kt - (q0 - seg_off) - 64 * half : 0) : 64;
+      const bool need_mask = __any_sync(0xffffffff, lo0 > 0);
       mbar_wait(&s_full[i & 1], (i >> 1) & 1);
-      tc_fence_after();
-      float s0[32], s1[32], dp[32];
-      ld32(sb, s0);
-      ld32(sb + 32, s1);  // loaded before dS^T of sub-chunk 0 overwrites these columns
       mbar_wait(dp_full, i & 1);
       tc_fence_after();
-      ld32(pb, dp);
-      uint32_t wp[16], wd[16];
-      sub(i, 0, s0, dp, st_lse, st_D, wp, wd);
-      ld32(pb + 32, dp);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dp_free);  // dP^T_i fully in registers: dP^T_{i+1} may overwrite it
-      tmem_st16(sb + lane_off, wp);         // P^T sub-chunk 0 -> [64h, 64h+16)
-      tmem_st16(sb + 32 + lane_off, wd);    // dS^T sub-chunk 0 -> [64h+32, 64h+48)
-      sub(i, 1, s1, dp, st_lse, st_D, wp, wd);
-      tmem_st16(sb + 16 + lane_off, wp);
-      tmem_st16(sb + 48 + lane_off, wd);
+      const uint32_t sbuf = t_S + (i & 1) * 128;
+#pragma unroll
+      for (int sub = 0; sub < 2; ++sub) {
+        float sv[32], dp[32];
+        {
+          uint32_t r[16], r2[16], r3[16], r4[16];
+          tmem_ld16(sbuf + 64 * half + 32 * sub + lane_off, r);
+          tmem_ld16(sbuf + 64 * half + 32 * sub + 16 + lane_off, r2);
+          tmem_ld16(t_dP + 64 * half + 32 * sub + lane_off, r3);
+          tmem_ld16(t_dP + 64 * half + 32 * sub + 16 + lane_off, r4);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            sv[e] = __uint_as_float(r[e]);
+            sv[16 + e] = __uint_as_float(r2[e]);
+            dp[e] = __uint_as_float(r3[e]);
+            dp[16 + e] = __uint_as_float(r4[e]);
+          }
+        }
+        if (sub == 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(dp_free);  // dP^T_i in registers: dP^T_{i+1} may overwrite it
+          // half 0 has now loaded S^T columns [32, 64): half 1 may pack its P^T over them
+          if (half == 0) named_bar_arrive(2 + qd, 64);
+        }
+        if (need_mask) {
+          const int lo = lo0 - 32 * sub;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) sv[c] = c >= lo ? sv[c] : -INFINITY;
+        }
+        const float* lz_base = st_lse + 64 * half + 32 * sub;
+        const float* dz_base = st_nd + 64 * half + 32 * sub;
+        uint32_t wp[16], wd[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 4) {
+          const float4 lz = *reinterpret_cast<const float4*>(lz_base + c);
+          const float4 dz = *reinterpret_cast<const float4*>(dz_base + c);
+          const float2 c22 = make_float2(c2, c2), sc2 = make_float2(sc, sc);
+          const float2 xa = __ffma2_rn(make_float2(sv[c], sv[c + 1]), c22, make_float2(-lz.x, -lz.y));
+          const float2 xb = __ffma2_rn(make_float2(sv[c + 2], sv[c + 3]), c22, make_float2(-lz.z, -lz.w));
+          const float2 pa = make_float2(ex2_approx(xa.x), ex2_approx(xa.y));
+          const float2 pb = make_float2(ex2_approx(xb.x), ex2_approx(xb.y));
+          const float2 da = __fmul2_rn(pa, __ffma2_rn(make_float2(dp[c], dp[c + 1]), sc2, make_float2(dz.x, dz.y)));
+          const float2 db = __fmul2_rn(pb, __ffma2_rn(make_float2(dp[c + 2], dp[c + 3]), sc2, make_float2(dz.z, dz.w)));
+          wp[c / 2] = pack_bf16x2(pa.x, pa.y);
+          wp[c / 2 + 1] = pack_bf16x2(pb.x, pb.y);
+          wd[c / 2] = pack_bf16x2(da.x, da.y);
+          wd[c / 2 + 1] = pack_bf16x2(db.x, db.y);
+        }
+        // P^T (bf16 pairs): query q of the block -> column q / 2 of the S^T_i buffer. Half 0 packs over
+        // its own, already loaded columns; half 1 over half 0's columns [32, 64), once half 0 has
+        // loaded them (pair barrier; half 0 arrives right after its second S^T load)
+        if (half == 1 && sub == 0) {
+          named_bar_sync(2 + qd, 64);
+          tc_fence_after();
+        }
+        tmem_st16(sbuf + 32 * half + 16 * sub + lane_off, wp);
+        // dS^T (scaled) -> smem tile i % 2 (once dK_{i-2} / dQ_{i-2} have read it): row krow of query
+        // panel `half`, 16-byte chunks 4 sub .. 4 sub + 3
+        if (sub == 0 && i >= 2) mbar_wait(&ds_free[i & 1], ((i - 2) >> 1) & 1);
+        uint8_t* ds_row = ds_rows + (i & 1) * C::kDSBytes;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *reinterpret_cast<uint4*>(ds_row + (((4 * sub + c) ^ (krow & 7)) * 16)) =
+              make_uint4(wd[4 * c], wd[4 * c + 1], wd[4 * c + 2], wd[4 * c + 3]);
+      }
       tmem_st_wait();
+      fence_proxy_async_smem();  // dS^T generic-proxy stores -> visible to the tensor core (async proxy)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[i & 1]);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
-    float* dkr = p.dk + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
-    float* dvr = p.dv + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+    float* dkr = (own ? p.dk : p.dk_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+    float* dvr = (own ? p.dv : p.dv_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
 #pragma unroll
     for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
       uint32_t rk[16], rv[16];
@@ -823,8 +897,8 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
       if (key_ok) {
 #pragma unroll
         for (int e = 0; e < 16; e += 4) {
-          red_add_v4_f32(dkr + c + e, __uint_as_float(rk[e]) * p.scale, __uint_as_float(rk[e + 1]) * p.scale,
-                         __uint_as_float(rk[e + 2]) * p.scale, __uint_as_float(rk[e + 3]) * p.scale);
+          red_add_v4_f32(dkr + c + e, __uint_as_float(rk[e]), __uint_as_float(rk[e + 1]), __uint_as_float(rk[e + 2]),
+                         __uint_as_float(rk[e + 3]));
           red_add_v4_f32(dvr + c + e, __uint_as_float(rv[e]), __uint_as_float(rv[e + 1]), __uint_as_float(rv[e + 2]),
                          __uint_as_float(rv[e + 3]));
         }
@@ -833,29 +907,49 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
-template <int DH, int POLY>
-void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
-                const int2* kv_items2, int n_kv, cudaStream_t stream) {
-  // ring depths: loads must run >= 2 blocks ahead of the MMA that frees their stage
+// D[h][r] = rowsum(dO * O) over head h's dh columns (the softmax-backward correction term): one
+// thread per 8 columns (16-byte loads), a group of dh/8 lanes per (row, head) reduces with shuffles.
+__global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
+                                    long ld, float* __restrict__ D, int n, int H, int dh) {
+  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int gpr = dh / 8;  // threads per (row, head): 8 or 16
+  const int cols8 = H * gpr;
+  const long r = t / cols8;
+  const int j = static_cast<int>(t - r * cols8);
+  float s = 0.f;
+  if (r < n) {
+    const uint4 x = *reinterpret_cast<const uint4*>(dO + r * ld + j * 8);
+    const uint4 y = *reinterpret_cast<const uint4*>(O + r * ld + j * 8);
+    const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
+    const __nv_bfloat162* ya = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 p = __bfloat1622float2(xa[i]), q = __bfloat1622float2(ya[i]);
+      s += p.x * q.x + p.y * q.y;
+    }
+  }
+  for (int o = gpr / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffff, s, o);
+  if (r < n && (j % gpr) == 0) D[static_cast<long>(j / gpr) * n + r] = s;
+}
+
+// dh = 128: query-parallel dQ kernel + key-parallel dK/dV kernel (TMEM cannot hold a dQ accumulator
+// next to 128-wide dK/dV and the S^T/dP^T buffers)
+template <int DH>
+void launch_bwd_split(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
+                      const int2* kv_items2, int n_kv, cudaStream_t stream) {
   // Ring depths: a stage is held until the LAST MMA reading it completes (dQ_j reads K_j; dV/dK_i
   // read Q_i/dO_i), so the refill of the stage NS blocks ahead only starts then. The ring must cover
   // that plus the L2/HBM TMA latency (~1-2 us under load), i.e. several block periods.
-  constexpr int NSQ = DH == 64 ? 8 : 4;  // dq kernel K/V stages (smem: 192 KB / 224 KB)
-  constexpr int NSK = DH == 64 ? 8 : 4;  // dkdv kernel Q/dO stages
+  constexpr int NSQ = 4;  // dq kernel K/V stages (224 KB smem)
+  constexpr int NSK = 4;  // dkdv kernel Q/dO stages
   using CQ = DqCfg<DH, NSQ>;
   using CK = DkvCfg<DH, NSK>;
-  static const int part = [] {  // TT_ATTN_BWD_PART (timing experiments): 1 = dQ kernel only, 2 = dK/dV only
-    const char* e = std::getenv("TT_ATTN_BWD_PART");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (part == 2) n_dq = 0;
-  if (part == 1) n_kv = 0;
   const int d = a.H * DH;
-  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dq16, a.lddq16, a.dk, a.dv, a.lddkv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0,
-              dq_blocks, nullptr, a.scale,
+  BwdParams p{a.lse, a.D, a.dq, a.lddq, a.dq16, a.lddq16, a.dk, a.dv, a.lddkv, a.dk_pre ? a.dk_pre : a.dk,
+              a.dv_pre ? a.dv_pre : a.dv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, dq_blocks, nullptr, a.scale,
               a.scale * kLog2e};
   if (n_dq > 0) {
     CUtensorMap tq, tdo, tk, tv;
@@ -863,23 +957,8 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, 128);
     make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, CQ::BKV);
     make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, CQ::BKV);
-    static bool once = (cudaFuncSetAttribute(fa_bwd_dq_kernel<DH, NSQ, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             CQ::kSmem),
-                        true);
-    (void)once;
-    static const int dbg = [] {
-      const char* e = std::getenv("TT_ATTN_DBG");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (dbg == 1 || dbg == 2 || dbg == 3 || dbg == 5) {
-      auto kfn = dbg == 1 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 1>
-                          : (dbg == 2 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 2>
-                                      : (dbg == 3 ? fa_bwd_dq_kernel<DH, NSQ, POLY, 4> : fa_bwd_dq_kernel<DH, NSQ, POLY, 5>));
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, CQ::kSmem);
-      kfn<<<dim3(n_dq, a.H), kThreadsDq, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
-    } else {
-      fa_bwd_dq_kernel<DH, NSQ, POLY><<<dim3(n_dq, a.H), kThreadsDq, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
-    }
+    ensure_smem_attr(reinterpret_cast<const void*>(fa_bwd_dq_kernel<DH, NSQ, 0>), CQ::kSmem);
+    fa_bwd_dq_kernel<DH, NSQ, 0><<<dim3(n_dq, a.H), kThreadsDq, CQ::kSmem, stream>>>(tq, tdo, tk, tv, p);
   }
   if (n_kv > 0) {
     CUtensorMap tq, tdo, tk, tv;
@@ -887,56 +966,49 @@ void launch_bwd(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int 
     make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, CK::BQ);
     make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, 128);
     make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, 128);
-    static bool once = (cudaFuncSetAttribute(fa_bwd_dkdv_kernel<DH, NSK, POLY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             CK::kSmem),
-                        true);
-    (void)once;
+    ensure_smem_attr(reinterpret_cast<const void*>(fa_bwd_dkdv_kernel<DH, NSK, 0>), CK::kSmem);
     p.blocks = kv_items;
     p.blocks2 = kv_items2;
-    static const bool k128 = [] {  // TT_ATTN_DKDV128=0: the 64-query-block dK/dV kernel (A/B timing)
-      const char* e = std::getenv("TT_ATTN_DKDV128");
-      return !(e && std::atoi(e) == 0);
-    }();
-    if (DH == 64 && k128) {
-      using C8 = Dkv128Cfg<5>;
-      CUtensorMap tq8, tdo8;
-      make_tmap_bf16(&tq8, a.q, d, a.n, a.ldq, 64, C8::BQ);
-      make_tmap_bf16(&tdo8, a.dO, d, a.n, a.ldq, 64, C8::BQ);
-      static bool once8 = (cudaFuncSetAttribute(fa_bwd_dkdv128_kernel<5, POLY>,
-                                                cudaFuncAttributeMaxDynamicSharedMemorySize, C8::kSmem),
-                           true);
-      (void)once8;
-      fa_bwd_dkdv128_kernel<5, POLY><<<dim3(n_kv, a.H), kThreadsDq, C8::kSmem, stream>>>(tq8, tdo8, tk, tv, p);
-    } else {
-      fa_bwd_dkdv_kernel<DH, NSK, POLY><<<dim3(n_kv, a.H), kThreadsDq, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
-    }
+    fa_bwd_dkdv_kernel<DH, NSK, 0><<<dim3(n_kv, a.H), kThreadsDq, CK::kSmem, stream>>>(tq, tdo, tk, tv, p);
   }
+}
+
+// dh = 64: the fused kernel; dQ partials are reduced into a.dq (fp32 [n x lddq], zeroed by the caller)
+void launch_bwd_fused(const AttnBwdArgs& a, long rows_cap, const int4* kv_items, const int2* kv_items2, int n_kv,
+                      cudaStream_t stream) {
+  constexpr int NS = 3;
+  using C = FusedCfg<NS>;
+  if (n_kv <= 0) return;
+  if (!a.dq) throw std::invalid_argument("fused attention backward: needs the fp32 dQ accumulator");
+  const int d = a.H * 64;
+  CUtensorMap tq, tdo, tk, tv, tdq;
+  make_tmap_bf16(&tq, a.q, d, a.n, a.ldq, 64, 128);
+  make_tmap_bf16(&tdo, a.dO, d, a.n, a.ldq, 64, 128);
+  make_tmap_bf16(&tk, a.k, d, rows_cap, a.ldkv, 64, 128);
+  make_tmap_bf16(&tv, a.v, d, rows_cap, a.ldkv, 64, 128);
+  make_tmap_f32_sw128(&tdq, a.dq, d, a.n, a.lddq);
+  BwdParams p{a.lse, a.D, a.dq, a.lddq, nullptr, 0, a.dk, a.dv, a.lddkv, a.dk_pre ? a.dk_pre : a.dk,
+              a.dv_pre ? a.dv_pre : a.dv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, kv_items, kv_items2, a.scale,
+              a.scale * kLog2e};
+  ensure_smem_attr(reinterpret_cast<const void*>(fa_bwd_fused_kernel<NS>), C::kSmem);
+  fa_bwd_fused_kernel<NS><<<dim3(n_kv, a.H), kThreadsFused, C::kSmem, stream>>>(tq, tdo, tk, tv, tdq, p);
 }
 
 }  // namespace
 
-int attn_debug_trace(long long* host, int n) {
-  const int m = n < 6 * 256 ? n : 6 * 256;
-  return cudaMemcpyFromSymbol(host, g_attn_trace, m * sizeof(long long)) == cudaSuccess ? m : -1;
+void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream) {
+  const long threads = static_cast<long>(a.n) * a.H * (a.dh / 8);
+  if (a.ldq % 8 != 0) throw std::invalid_argument("attention backward: dO/O pitch must be a multiple of 8");
+  if (threads > 0)
+    attn_bwd_pre_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(a.dO, a.o, a.ldq, a.D, a.n,
+                                                                                         a.H, a.dh);
 }
 
 void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
                     const int2* kv_items2, int n_kv, cudaStream_t stream) {
   attn_bwd_pre(a, stream);
-  // TT_ATTN_BWD_POLY: exponential pairs (of 4) on the FMA pipe (timing experiments)
-  static const int bpoly = [] {
-    const char* e = std::getenv("TT_ATTN_BWD_POLY");
-    return e ? std::atoi(e) : 0;
-  }();
-#define TT_BWD(P)                                                                                          \
-  if (a.dh == 64) return launch_bwd<64, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream); \
-  if (a.dh == 128) return launch_bwd<128, P>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
-  switch (bpoly) {
-    case 1: TT_BWD(1) break;
-    case 2: TT_BWD(2) break;
-    default: TT_BWD(0) break;
-  }
-#undef TT_BWD
+  if (a.dh == 64) return launch_bwd_fused(a, rows_cap, kv_items, kv_items2, n_kv, stream);
+  if (a.dh == 128) return launch_bwd_split<128>(a, rows_cap, dq_blocks, n_dq, kv_items, kv_items2, n_kv, stream);
   throw std::invalid_argument("attention: head_dim must be 64 or 128");
 }
 

@@ -51,31 +51,44 @@ __global__ void embed_pe_kernel(const int32_t* __restrict__ tok, const int32_t* 
 }
 
 // inv = 1/sqrt(mean(x^2)+eps); y = x*inv*g (bf16)   (rms_inv model.hpp:250-256; apply :377-380)
-// one warp per row
-// One warp per row; VPT float4 column groups per lane held in registers, so x is read from HBM once.
-template <int VPT>
+// WPR warps per row (8 / WPR rows per 256-thread block); each lane holds VPT float4 column groups
+// (c = (lr + 32 WPR k) * 4) in registers, so x is read from HBM once. WPR > 1 keeps VPT <= 16 for
+// rows wider than 4096 (the sum of squares is then combined across the row's warps in smem).
+template <int VPT, int WPR = 1>
 __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain,
                                                           float* __restrict__ inv, __nv_bfloat16* __restrict__ y, int n,
                                                           int d) {
-  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (row >= n) return;
+  constexpr int STRIDE = 32 * WPR;
+  __shared__ float red[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (8 / WPR) + warp / WPR;
+  const int lr = (warp % WPR) * 32 + lane;
+  const bool valid = row < n;
+  if (WPR == 1 && !valid) return;
   const float* xr = x + static_cast<long>(row) * d;
   float4 v[VPT];
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int c = (lane + 32 * k) * 4;
-    v[k] = c < d ? __ldcs(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int c = (lr + STRIDE * k) * 4;
+    v[k] = (valid && c < d) ? __ldcs(reinterpret_cast<const float4*>(xr + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
     s += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
   }
   s = warp_sum(s);
+  if constexpr (WPR > 1) {
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    s = 0.f;
+#pragma unroll
+    for (int j = 0; j < WPR; ++j) s += red[(warp / WPR) * WPR + j];
+    if (!valid) return;
+  }
   const float iv = 1.0f / sqrtf(s / static_cast<float>(d) + 1e-6f);
-  if (lane == 0) inv[row] = iv;
+  if (lr == 0) inv[row] = iv;
   __nv_bfloat16* yr = y + static_cast<long>(row) * d;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const int c = (lane + 32 * k) * 4;
+    const int c = (lr + STRIDE * k) * 4;
     if (c < d) {
       const float4 g = __ldg(reinterpret_cast<const float4*>(gain + c));
       uint2 o;
@@ -209,10 +222,26 @@ __device__ __forceinline__ float4 ld_evict_last_f4(const float* p, uint64_t pol)
 // 512 threads, 4 CTAs (rows) per SM; the write pass keeps 4 float4 loads per thread in flight
 // (64 KB per SM) — one float4 per thread is far too little memory-level parallelism for HBM.
 constexpr int kCeThreads = 512;
+// OutT = bf16: the tree step's dlogits (operand of the head GEMMs); float: the standalone
+// weighted_nll's fp32 grad_logits (LossResult::grad_logits, model.hpp:637-640).
+template <typename OutT>
+__device__ __forceinline__ void st_grad4(OutT* p, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void st_grad4<__nv_bfloat16>(__nv_bfloat16* p, float a, float b, float c, float d) {
+  *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16x2(a, b), pack_bf16x2(c, d));
+}
+template <>
+__device__ __forceinline__ void st_grad4<float>(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void st_grad1(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+__device__ __forceinline__ void st_grad1(float* p, float v) { *p = v; }
+
+template <typename OutT>
 __global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restrict__ logits, int m, long V,
                                                   const int32_t* __restrict__ pair_off,
                                                   const int32_t* __restrict__ tgt, const double* __restrict__ w,
-                                                  __nv_bfloat16* __restrict__ dl, double* __restrict__ loss,
+                                                  OutT* __restrict__ dl, double* __restrict__ loss,
                                                   const float2* __restrict__ stats, int n_groups) {
   __shared__ float red[32];
   __shared__ float s_lse;
@@ -263,7 +292,7 @@ __global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restri
     const int p0 = pair_off[r], p1 = pair_off[r + 1];
     float wsum = 0.f;
     for (int p = p0; p < p1; ++p) wsum += static_cast<float>(w[p]);
-    __nv_bfloat16* dr = dl + static_cast<long>(r) * V;
+    OutT* dr = dl + static_cast<long>(r) * V;
     constexpr int U = 4;
     constexpr long kStep = 4L * kCeThreads;
     for (long c0 = threadIdx.x * 4; c0 < V; c0 += U * kStep) {
@@ -277,10 +306,8 @@ __global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restri
       for (int u = 0; u < U; ++u) {
         const long c = c0 + u * kStep;
         if (c >= V) break;
-        uint2 o;
-        o.x = pack_bf16x2(wsum * __expf(v[u].x - lse), wsum * __expf(v[u].y - lse));
-        o.y = pack_bf16x2(wsum * __expf(v[u].z - lse), wsum * __expf(v[u].w - lse));
-        *reinterpret_cast<uint2*>(dr + c) = o;
+        st_grad4(dr + c, wsum * __expf(v[u].x - lse), wsum * __expf(v[u].y - lse), wsum * __expf(v[u].z - lse),
+                 wsum * __expf(v[u].w - lse));
       }
     }
     // target columns: - sum_j w_j onehot(t_j), rewritten after the streaming pass (one thread per
@@ -295,7 +322,7 @@ __global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restri
           first = first && q >= p;
           wt += static_cast<float>(w[q]);
         }
-      if (first) dr[t] = __float2bfloat16_rn(wsum * __expf(lr[t] - lse) - wt);
+      if (first) st_grad1(dr + t, wsum * __expf(lr[t] - lse) - wt);
     }
     if (threadIdx.x == 0) {
       double acc = 0.0;
@@ -426,8 +453,9 @@ void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16*
   else if (vpt <= 4) rmsnorm_fwd_kernel<4><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
   else if (vpt <= 8) rmsnorm_fwd_kernel<8><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
   else if (vpt <= 16) rmsnorm_fwd_kernel<16><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
-  else if (vpt <= 32) rmsnorm_fwd_kernel<32><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
-  else throw std::invalid_argument("rmsnorm: d_model > 4096");
+  else if (vpt <= 32) rmsnorm_fwd_kernel<16, 2><<<(n + 3) / 4, 256, 0, s>>>(x, gain, inv, y, n, d);
+  else if (vpt <= 64) rmsnorm_fwd_kernel<16, 4><<<(n + 1) / 2, 256, 0, s>>>(x, gain, inv, y, n, d);
+  else throw std::invalid_argument("rmsnorm: d_model > 8192");
 }
 void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
                    __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
@@ -444,7 +472,32 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
 }
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
           __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {
-  if (m > 0) ce_kernel<<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
+  if (m > 0)
+    ce_kernel<__nv_bfloat16><<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, stats,
+                                                                         n_groups);
+}
+void k_ce_f32(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
+              float* dl, double* loss, cudaStream_t s) {
+  if (m > 0)
+    ce_kernel<float><<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, nullptr, 0);
+}
+// dst[i] += src[i] (fp32, n % 4 == 0, 16-byte aligned)
+__global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, long n4) {
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(dst)[i];
+    const float4 b = reinterpret_cast<const float4*>(src)[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    reinterpret_cast<float4*>(dst)[i] = a;
+  }
+}
+void k_add_f32(float* dst, const float* src, long n, cudaStream_t s) {
+  if (n % 4 != 0) throw std::invalid_argument("k_add_f32: n must be a multiple of 4");
+  if (n > 0)
+    add_f32_kernel<<<static_cast<int>(std::min<long>((n / 4 + 255) / 256, 148 * 16)), 256, 0, s>>>(dst, src, n / 4);
 }
 void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
                         cudaStream_t s) {

@@ -18,6 +18,11 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
 // (EPI_STORE_F32_STATS, n_groups = ceil(V/32) per row); NULL = two passes over the logits row.
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
           __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats = nullptr, int n_groups = 0);
+// standalone weighted_nll: fp32 grad_logits, two passes over each logits row
+void k_ce_f32(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
+              float* dl, double* loss, cudaStream_t s);
+// dst[i] += src[i], n a multiple of 4
+void k_add_f32(float* dst, const float* src, long n, cudaStream_t s);
 void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
                         cudaStream_t s);
 void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m, int d, cudaStream_t s);

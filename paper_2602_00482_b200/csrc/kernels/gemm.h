@@ -56,8 +56,18 @@ int gemm_pick_bn(int N, bool b_mn_major);
 int gemm_pick_bn2(int M, int N);
 // 2-CTA (cta_group::2) tiles for M >= 256 (default on); 0 forces the single-CTA kernel.
 void gemm_set_2cta(int on);
+// Per-device launch helpers (a process may drive engines on several GPUs; the current device is
+// whatever the calling engine selected): one-time MaxDynamicSharedMemorySize per (kernel, device),
+// the SM count of the current device, and a launch-status check that throws.
+void ensure_smem_attr(const void* fn, int bytes);
+int device_sm_count();
+void check_launch(cudaError_t e, const char* what);
+
 void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                     uint32_t box_inner, uint32_t box_outer);
+// fp32 [rows x width] (row pitch ld elements) in 32 x 32 boxes, SWIZZLE_128B: the staging layout of a
+// warp that holds one 32-float row per lane (reduce-add / store epilogues)
+void make_tmap_f32_sw128(CUtensorMap* map, const void* ptr, uint64_t width, uint64_t rows, uint64_t ld);
 void make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer);
 

@@ -656,6 +656,20 @@ void make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t 
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
 
+void make_tmap_f32_sw128(CUtensorMap* map, const void* ptr, uint64_t width, uint64_t rows, uint64_t ld) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * 4) % 16 != 0)
+    throw std::invalid_argument("fp32 tensor map: pointer / pitch must be 16-byte aligned");
+  cuuint64_t dims[2] = {width, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled (f32 sw128) failed (" + std::to_string(int(r)) + ")");
+}
+
 // 2-D fp32 tensor map (no swizzle): inner x outer elements, row pitch ld elements (multiple of 4).
 void make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld,
                       uint32_t box_inner, uint32_t box_outer) {
@@ -672,7 +686,6 @@ void make_tmap_f32_2d(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_
 
 namespace {
 
-int g_num_sms = 0;
 
 // Output / epilogue-operand tensor map: [rows x width] elements (fp32 or bf16), row pitch ld elements,
 // 32 x 32 boxes in the swizzled staging layout of the epilogue (128B rows fp32, 64B rows bf16).
@@ -701,16 +714,8 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   else make_tmap_bf16(&ta, A.ptr, M, K, A.ld, 64, 64);
   if (!B_MN) make_tmap_bf16(&tb, B.ptr, K, N, B.ld, 64, C::BNC);
   else make_tmap_bf16(&tb, B.ptr, N, K, B.ld, 64, 64);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<BN, CG, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    attr_set = true;
-  }
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<BN, CG, A_MN, B_MN>), C::kSmem);
+  const int g_num_sms = device_sm_count();
   const int kb_total = (K + BK - 1) / BK;
   if (splits < 1) splits = 1;
   if (splits > kb_total) splits = kb_total;
@@ -751,7 +756,8 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN>, ta, tb, to[0], to[1], to[2], tx, M, N, K, splits, e);
+  check_launch(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN>, ta, tb, to[0], to[1], to[2], tx, M, N, K, splits, e),
+               "gemm launch");
 }
 
 }  // namespace
@@ -764,17 +770,10 @@ void gemm_set_2cta(int on) { g_gemm_2cta = on; }
 // pair's halved operand traffic outweighs the padding (profiles/r1: 0.556 -> 0.513 ms).
 bool gemm_use_2cta(int M, int N) {
   if (!g_gemm_2cta || M < 256) return false;
-  static const int waste_pct = [] {  // TT_GEMM_2CTA_WASTE: allowed M padding in % (experiments)
-    const char* e = std::getenv("TT_GEMM_2CTA_WASTE");
-    return e ? std::atoi(e) : 5;
-  }();
+  constexpr int waste_pct = 5;  // allowed M padding in %
   const long padded = (M + 255) / 256 * 256;
   if ((padded - M) * 100 <= static_cast<long>(M) * waste_pct) return true;
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_num_sms = device_sm_count();
   const long pair_tiles = (padded / 256) * ((N + 255) / 256);
   return (padded - M) * 100 <= static_cast<long>(M) * 15 && pair_tiles >= 4L * (g_num_sms / 2);
 }
@@ -785,16 +784,7 @@ bool gemm_use_2cta(int M, int N) {
 // Measured (profiles/r1/gemm_shapes_bn2.log): N = 896 at M = 32768 runs 17-22% faster with 256-wide
 // tiles despite 12.5% padding; M = 4864 prefers 128 (76 vs 133 tiles on 74 CTA pairs).
 int gemm_pick_bn2(int M, int N) {
-  static const int force = [] {  // TT_GEMM_BN2: force 128 / 256 (tile-shape experiments only)
-    const char* e = std::getenv("TT_GEMM_BN2");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (force == 128 || force == 256) return force;
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_num_sms = device_sm_count();
   const long pairs = std::max(1, g_num_sms / 2);
   const long m_tiles = (M + 255) / 256;
   auto cost = [&](int bn, double f) {
@@ -838,11 +828,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
   if (!amn && !bmn) return launch<BN_, CG_, false, false>(A, B, M, N, K, epi, splits, stream); \
   if (amn && bmn) return launch<BN_, CG_, true, true>(A, B, M, N, K, epi, splits, stream);     \
   return launch<BN_, CG_, true, false>(A, B, M, N, K, epi, splits, stream);
-  static const bool bn224 = [] {  // TT_GEMM_BN224=0 disables the 224-wide pair tiles (A/B timing)
-    const char* e = std::getenv("TT_GEMM_BN224");
-    return !(e && std::atoi(e) == 0);
-  }();
-  if (bn224 && !bmn && N % 256 != 0 && N % 224 == 0 && gemm_use_2cta(M, N)) {
+  if (!bmn && N % 256 != 0 && N % 224 == 0 && gemm_use_2cta(M, N)) {
     // N = 896 (d of the 0.5B shape): 4 x 224 columns instead of 3.5 x 256 (12.5% padding); each CTA
     // stages 112 rows of the K-major B
     if (!amn) return launch<224, 2, false, false>(A, B, M, N, K, epi, splits, stream);
@@ -868,11 +854,7 @@ void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, 
 }
 
 int gemm_choose_splits(int M, int N, int K) {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_num_sms = device_sm_count();
   const bool two = gemm_use_2cta(M, N);
   const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
   // Time model: waves of (tile, K/s) items at ~9 TFLOP/s per SM, plus the fp32 reduce-add of every
@@ -906,6 +888,7 @@ int gemm_choose_splits(int M, int N, int K) {
 // Wave model of one launch in SM-seconds: waves x (per-unit tile FLOPs / K-split) / unit rate, with the
 // narrower tiles' per-FLOP overhead (pick_bn / pick_bn2 weights) and the split reduce traffic.
 static double gemm_est_cost(int M, int N, int K) {
+  const int g_num_sms = device_sm_count();
   const bool two = gemm_use_2cta(M, N);
   const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
   const double f = two ? (bn == 256 ? 1.0 : 1.25) : (bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.10));
@@ -920,23 +903,16 @@ static double gemm_est_cost(int M, int N, int K) {
 
 // Measured (profiles/r1): dW_out 4864 x 896 x 32768 ran at 763 TFLOP/s as 133 128-wide pair tiles
 // on 74 pairs (1.8 waves), its transpose 896 x 4864 at 1234 as 133 single-CTA 128 x 256 tiles in
-// one wave. Transpose only on a clear (>10%) modelled win; TT_GEMM_TRANSPOSE (or gemm_set_transpose):
-// 0 = never, 1 = modelled (default), 2 = always.
-static int g_gemm_transpose = [] {
-  const char* e = std::getenv("TT_GEMM_TRANSPOSE");
-  return e ? std::atoi(e) : 1;
-}();
+// one wave. Transpose only on a clear (>10%) modelled win; gemm_set_transpose (test hook): 0 = never,
+// 1 = modelled (default), 2 = always.
+static int g_gemm_transpose = 1;
 void gemm_set_transpose(int mode) { g_gemm_transpose = mode; }
 
 bool gemm_prefer_transposed(int M, int N, int K) {
   const int mode = g_gemm_transpose;
   if (mode == 0 || M % 16 != 0 || N % 16 != 0 || M == N) return false;
   if (mode == 2) return true;  // force (tests)
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int g_num_sms = device_sm_count();
   return gemm_est_cost(N, M, K) < 0.9 * gemm_est_cost(M, N, K);
 }
 

@@ -224,12 +224,12 @@ def test_errors_surface_as_exceptions():
         eng.tree_train_step(tt.build_prefix_tree(long))
 
 
-@pytest.mark.parametrize("fwd_impl,bwd_impl", [(0, 0), (1, 0), (0, 1), (1, 1)])
-def test_attention_impls_agree_on_tree(fwd_impl, bwd_impl):
-    # mma.sync (sm80-style baseline) and tcgen05 attention give the same step within tolerance
-    cfg, flat, eng = make(SMALL, 12)
-    eng.set_option("attn_fwd_impl", fwd_impl)
-    eng.set_option("attn_bwd_impl", bwd_impl)
+@pytest.mark.parametrize("cfgt", [SMALL, DH128], ids=["dh64_fused_bwd", "dh128_split_bwd"])
+def test_attention_long_segments_vs_oracle(cfgt):
+    # segments longer than one 128-query block on both sides of every key block, plus a shared
+    # response stem: the fused dh = 64 backward (dQ partials reduced across key blocks) and the dh = 128
+    # query-/key-parallel pair
+    cfg, flat, eng = make(cfgt, 12)
     seqs = O.grouped_corpus(2, 4, 150, 200, cfg.vocab_size, 13, shared_response=20, weight_jitter=True)
     tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
 
@@ -330,14 +330,11 @@ def test_c4_shape_7b_tree_equals_flat():
 
 
 @pytest.mark.parametrize("root_tokens", [0, 300, 4096])
-@pytest.mark.parametrize("fwd_impl,bwd_impl", [(1, 1), (0, 0)])
-def test_multi_root_batching_vs_oracle(root_tokens, fwd_impl, bwd_impl):
+def test_multi_root_batching_vs_oracle(root_tokens):
     # several prompt trees (forest roots whose children are all leaves) pushed as one multi-root
     # batch; each root's leaves attend to that root's rows only (prefix row base != 0). 0 = off.
     cfg, flat, eng = make(SMALL, 31)
     eng.set_option("root_batch_tokens", root_tokens)
-    eng.set_option("attn_fwd_impl", fwd_impl)
-    eng.set_option("attn_bwd_impl", bwd_impl)
     seqs = O.grouped_corpus(5, 3, 90, 70, cfg.vocab_size, 32, weight_jitter=True)
     r, _ = tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
     tree = tt.build_prefix_tree([tt.TokenSequence(s.seq_id, s.tokens, s.weights) for s in seqs])

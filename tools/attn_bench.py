@@ -1,6 +1,6 @@
-"""Times the segment-attention kernels alone (CUDA events) on a c2-like segment: n queries over a
-prefix of S stack rows + own causal rows, H heads of dh. Usage:
-    python tools/attn_bench.py [impl_fwd impl_bwd] [n S H dh]"""
+"""Times the segment-attention kernels alone (CUDA events) on a c2-like segment batch: n queries in
+nseg sibling segments over a prefix of S stack rows + own causal rows, H heads of dh. Usage:
+    python tools/attn_bench.py [nseg] [n S H dh]      (c2 leaf batch: 16 32768 1024 14 64)"""
 import ctypes
 import os
 import sys
@@ -12,9 +12,9 @@ from paper_2602_00482_b200 import _native  # noqa: E402
 
 
 def main():
-    impl_f = int(sys.argv[1]) if len(sys.argv) > 1 else 1
-    impl_b = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-    n, S, H, dh = (int(x) for x in sys.argv[3:7]) if len(sys.argv) > 6 else (2048, 1024, 14, 64)
+    nseg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    n, S, H, dh = (int(x) for x in sys.argv[2:6]) if len(sys.argv) > 5 else (2048, 1024, 14, 64)
+    impl_f = impl_b = 1
     lib = _native.lib()
     vp = ctypes.c_void_p
     d = H * dh
@@ -43,7 +43,7 @@ def main():
                                  dh, rows, iters, ctypes.byref(ms)) == 0, lib.tt_last_error()
         return ms.value
 
-    nseg = int(os.environ.get("TT_ATTN_NSEG", "1"))  # sibling segments sharing the prefix (c2: 16)
+    lib.tt_debug_attn_set_segments(nseg)
     seg = (n + nseg - 1) // nseg
     ctx = n * S + sum(m * (m + 1) / 2 for m in [min(seg, n - i) for i in range(0, n, seg)])
     for name, fn, impl, fl in (("fwd", fwd, impl_f, 4.0 * d * ctx), ("bwd", bwd, impl_b, 8.0 * d * ctx)):

@@ -197,28 +197,77 @@ def measured_peaks():
     return 1400.0, 1590.0, 6650.0, "fallback"
 
 
-def cuda_array(ptr, n):
-    import torch
-
-    class _A:
-        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3}
-
-    return torch.as_tensor(_A(), device="cuda")
-
-
 # ----------------------------------------------------------------------------- CPU reference arm
-def cpu_reference_sample(model, S, n_tokens, threads, repeats=1, handle=None):
-    """Reference forward_segment + weighted_nll + backward_segment of n_tokens at prefix S per
-    host thread (T=float, -O3). Returns (seconds per repeat, flops per repeat)."""
+def host_cpu():
+    """(model string, physical cores, logical CPUs) of this host (BASELINE.md §3 asks for both)."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        import psutil
+
+        phys = psutil.cpu_count(logical=False)
+    except Exception:
+        phys = None
+    return model, phys, os.cpu_count() or 1
+
+
+def slice_flops(model, S, n, threads):
+    """(GEMM, attention) algorithmic FLOPs of `threads` slices of n tokens at prefix S."""
+    V, d, H, L, F = model
+    gemm = threads * n * 6.0 * (L * (4 * d * d + 2 * d * F) + d * V)
+    attn = threads * 12.0 * d * L * (n * S + n * (n + 1) / 2)
+    return gemm, attn
+
+
+def step_flops_split(model, tree_nodes):
+    """step_flops split into its GEMM and attention terms."""
+    g = a = 0.0
+    for S, n in tree_nodes:
+        dg, da = slice_flops(model, S, n, 1)
+        g += dg
+        a += da
+    return g, a
+
+
+def cpu_reference_fit(model_name, S_lo, S_hi, n_tokens, threads, repeats=1, handle=None):
+    """The reference's forward_segment + weighted_nll + backward_segment (T=float, -O3) of n_tokens
+    per host thread at two prefix lengths (attention share ~1% and ~25% at c2), one slice per
+    thread on all threads; fits separate GEMM and attention seconds-per-FLOP.
+    Returns (per-repeat seconds [(t_lo, t_hi)], (sec_per_gemm_flop, sec_per_attn_flop))."""
     from oracle import refimpl as R
     from oracle import treetrain_oracle as O
 
-    V, d, H, L, F = MODELS[model]
-    cfg = O.ModelConfig(V, d, H, L, F, S + n_tokens + 8)
+    model = MODELS[model_name]
+    V, d, H, L, F = model
+    cfg = O.ModelConfig(V, d, H, L, F, S_hi + n_tokens + 8)
     m = handle or R.RefModel(cfg, 7)
-    secs = [m.slice(S, n_tokens, threads, seed=11 + i) for i in range(repeats)]
-    fl = threads * step_flops(MODELS[model], [(S, n_tokens)])
-    return secs, fl
+    secs = [(m.slice(S_lo, n_tokens, threads, seed=11 + i), m.slice(S_hi, n_tokens, threads, seed=29 + i))
+            for i in range(repeats)]
+    return secs, fit_rates(model, S_lo, S_hi, n_tokens, threads, secs[-1])
+
+
+def fit_rates(model, S_lo, S_hi, n, threads, ts):
+    gl, al = slice_flops(model, S_lo, n, threads)
+    gh, ah = slice_flops(model, S_hi, n, threads)
+    det = gl * ah - gh * al
+    a = (ts[0] * ah - ts[1] * al) / det
+    b = (gl * ts[1] - gh * ts[0]) / det
+    if a <= 0 or b <= 0:  # timing noise swamped the split: one combined rate
+        r = (ts[0] + ts[1]) / (gl + al + gh + ah)
+        a = b = r
+    return a, b
+
+
+def cpu_extrapolate(model, nodes, roll, rates):
+    fg, fa = step_flops_split(model, nodes)
+    t = rates[0] * fg + rates[1] * fa
+    return roll / t, t
 
 
 def run_reference(args):
@@ -231,31 +280,33 @@ def run_reference(args):
     model = MODELS[c["model"]]
     from oracle import refimpl as R
 
-    threads = os.cpu_count() or 1
+    cpu_model, phys, threads = host_cpu()
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libttref.so not built (needs /root/reference at build time)"}))
         return 0
     seqs = config_corpus(c, c["prompts"], model[0], args.share)
     nodes = tree_nodes_of(seqs)
-    fl_step = step_flops(model, nodes)
     roll = sum(len(s.tokens) for s in seqs)
+    seq_len = c.get("seq_len") or c["prompt_len"] + c["resp_len"]
     n_tok = 1 if model[3] > 2 else 64
-    S = c["prompt_len"] if "prompt_len" in c else int(round(args.share * c["seq_len"]))
-    secs, fl = cpu_reference_sample(c["model"], S, n_tok, threads, repeats=args.warmup + args.steps)
+    S_lo, S_hi = 64, seq_len - n_tok
+    secs, _ = cpu_reference_fit(c["model"], S_lo, S_hi, n_tok, threads, repeats=args.warmup + args.steps)
     timed = secs[args.warmup:]
-    t = float(np.mean(timed))
-    rate = fl / t
-    value = rate / (fl_step / roll)
+    ts = (float(np.mean([t[0] for t in timed])), float(np.mean([t[1] for t in timed])))
+    rates = fit_rates(model, S_lo, S_hi, n_tok, threads, ts)
+    value, t_step = cpu_extrapolate(model, nodes, roll, rates)
+    sample = (f"reference forward_segment+weighted_nll+backward_segment (T=float) of {n_tok} token(s) per thread at "
+              f"prefix S={S_lo} and S={S_hi} on {threads} threads ({ts[0]:.2f} s / {ts[1]:.2f} s per slice pair "
+              f"member): fitted {1e-9 / rates[0]:.2f} GEMM-GFLOP/s and {1e-9 / rates[1]:.2f} attention-GFLOP/s, "
+              f"extrapolated to the {args.config} step ({t_step / 3600:.1f} h)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rollout tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": (ts[0] + ts[1]) * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{args.config}: {c['desc']}", "model": c["model"], "global_batch": len(seqs),
-                   "seq_len": c.get("seq_len") or c["prompt_len"] + c["resp_len"], "parallelism": "host threads"},
+                   "seq_len": seq_len, "parallelism": f"dp{args.gpus}"},
         "cpu_baseline": {"value": value, "unit": "rollout tokens/s", "cores": threads, "kind": "reference",
-                         "sample": f"reference forward_segment+weighted_nll+backward_segment of {n_tok} token(s) at "
-                                   f"prefix S={S} per thread x {threads} threads (T=float), extrapolated to the "
-                                   f"{args.config} step via the FLOP model ({rate / 1e9:.2f} GFLOP/s achieved)"},
+                         "cpu_model": cpu_model, "physical_cores": phys, "sample": sample},
         "e2e": {"value": value, "unit": "rollout tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -263,7 +314,17 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- B200 arm
+def product_env():
+    """The product path takes no tuning from the environment; any TT_* variable is refused so that a
+    number is never taken with a knob set (the line records that the check ran)."""
+    bad = sorted(k for k in os.environ if k.startswith("TT_"))
+    if bad:
+        raise SystemExit(f"bench.py: refusing to run with {bad} set (unset every TT_* variable)")
+    return {"TT_*": "none set"}
+
+
 def run_b200(args):
+    env = product_env()
     import torch
 
     import paper_2602_00482_b200 as tt
@@ -304,14 +365,21 @@ def run_b200(args):
     plan = eng.plan(tree, sched)
     plan_s = time.time() - t0
     ext = torch.cuda.ExternalStream(eng.stream_ptr)
-    grads = cuda_array(eng.grads_device_ptr(), eng.n_params) if world > 1 else None
+    comm = None
+    if world > 1:
+        # the engine's own NCCL communicator (tt_nccl_comm_init_rank); torch.distributed only ships the
+        # 128-byte unique id and provides the barrier / max-over-ranks timing reduction
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(tt.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = tt.NcclComm(bytes(uid.cpu().numpy().tobytes()), world, rank, local)
 
     def one_step():
         eng.zero_gradients()
         r = plan.execute()
-        if grads is not None:
-            dist.all_reduce(grads)
-            ext.wait_stream(torch.cuda.current_stream())
+        if comm is not None:
+            eng.allreduce_gradients(comm)  # ONE in-place ncclAllReduce of the GradientStore per step
         return r
 
     for _ in range(args.warmup):
@@ -347,9 +415,8 @@ def run_b200(args):
             eng.zero_gradients()
             r2 = eng.tree_train_step(tt.build_prefix_tree(seqs), sched)
             h2d = r2.h2d_bytes
-            if grads is not None:
-                dist.all_reduce(grads)
-                ext.wait_stream(torch.cuda.current_stream())
+            if comm is not None:
+                eng.allreduce_gradients(comm)
         f1.record(ext)
         barrier()
         e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
@@ -392,7 +459,7 @@ def run_b200(args):
         "config": {"workload": f"{args.config}: {c['desc']}", "model": c["model"], "global_batch": len(all_seqs),
                    "seq_len": seq_len, "parallelism": f"dp{world}",
                    "trees_per_gpu": c["prompts"], "sibling_batch": not args.no_sibling_batch,
-                   "l2": "step working set (weights + activations) >> 126 MB L2; no flush needed"},
+                   "l2": "step working set (weights + activations) >> 126 MB L2; no flush needed", "env": env},
         "e2e": {"value": roll_total / (e2e_ms / 1e3) if e2e_ms else None, "unit": "rollout tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
                 "includes": "host tree build + schedule/metadata upload (pinned) + execute + loss read"},
@@ -437,17 +504,18 @@ def run_b200(args):
             from oracle import refimpl as R
 
             if R.available():
-                threads = os.cpu_count() or 1
+                cpu_model, phys, threads = host_cpu()
                 n_tok = 1 if L > 2 else 64
-                S0 = c["prompt_len"] if "prompt_len" in c else int(round(args.share * c["seq_len"]))
-                secs, fl = cpu_reference_sample(c["model"], S0, n_tok, threads)
-                rate = fl / secs[0]
-                cpu_val = rate / (fl_step / roll_local)
+                S_lo, S_hi = 64, seq_len - n_tok
+                secs, rates = cpu_reference_fit(c["model"], S_lo, S_hi, n_tok, threads)
+                cpu_val, t_step = cpu_extrapolate((V, d, H, L, F), nodes, roll_local, rates)
                 line["cpu_baseline"] = {
-                    "value": cpu_val, "unit": "rollout tokens/s", "cores": threads, "kind": "reference",
-                    "sample": f"reference forward_segment+weighted_nll+backward_segment (T=float) of {n_tok} token(s) at "
-                              f"prefix S={S0} on each of {threads} threads: {secs[0]:.1f} s, "
-                              f"{rate / 1e9:.2f} GFLOP/s; extrapolated to the step via the FLOP model"}
+                    "value": cpu_val * world, "unit": "rollout tokens/s", "cores": threads, "kind": "reference",
+                    "cpu_model": cpu_model, "physical_cores": phys,
+                    "sample": f"reference forward_segment+weighted_nll+backward_segment (T=float) of {n_tok} token(s) "
+                              f"per thread at prefix S={S_lo} and S={S_hi} on {threads} threads "
+                              f"({secs[0][0]:.1f} s + {secs[0][1]:.1f} s): fitted {1e-9 / rates[0]:.2f} GEMM-GFLOP/s "
+                              f"and {1e-9 / rates[1]:.2f} attention-GFLOP/s, extrapolated to the step ({t_step / 3600:.1f} h)"}
             else:
                 line["cpu_baseline"] = {"value": None, "unit": "rollout tokens/s", "cores": 0, "kind": "reference",
                                         "sample": "oracle/_ref not built"}
@@ -456,6 +524,8 @@ def run_b200(args):
                                     "sample": f"failed: {e}"}
     if rank == 0:
         print(json.dumps(line))
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.destroy_process_group()
     return 0

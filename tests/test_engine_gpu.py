@@ -5,7 +5,15 @@ Tolerances (bf16 operands, fp32 accumulation / residual / dK-dV stack / gradient
   loss                 |rel| <= 5e-3
   logits               rel-Frobenius <= 1e-2
   gradients (per tensor of for_each_tensor order, model.hpp:42-59)
-                       rel-Frobenius <= 3e-2 and cosine >= 0.999
+                       rel-Frobenius <= 3e-2 and cosine >= 0.999; the attention query/key
+                       projections (w_q, w_k) rel-Frobenius <= 5e-2 and cosine >= 0.999
+The w_q / w_k gradients are contractions of dS = P*(dP - D), whose rows sum to zero (softmax shift
+invariance) while the bf16 activations feeding it (normed x, q, k, v, O, dO) carry a large common
+component (the sinusoidal PE dominates the random-init residual stream), so their relative error is
+amplified: at the c2 shape they measure 1.7e-2 median / 3.0e-2 max against 3.5e-3-5.4e-3 for every
+other tensor (tools/c2_grad_diag.py). The attention kernels themselves match an fp32
+emulation of their own bf16 operand rounding to three digits (tools/attn_precision.py), and
+tools/qk_grad_precision.py reproduces the amplification from activation rounding alone on the CPU.
 Tree structure and traversal are checked bit-exactly in tests/test_native_host.py.
 """
 import math
@@ -22,7 +30,7 @@ SMALL = (512, 128, 2, 2, 256, 1024)  # V, d, H, L, d_ff, max_position ; head_dim
 DH128 = (512, 256, 2, 2, 512, 1024)  # head_dim 128
 C1 = (1024, 256, 4, 2, 1024, 2048)   # BASELINE configs[0] model (V proposed in SURVEY §8(d))
 
-LOSS_TOL, LOGIT_TOL, GRAD_TOL, COS_TOL = 5e-3, 1e-2, 3e-2, 0.999
+LOSS_TOL, LOGIT_TOL, GRAD_TOL, QK_GRAD_TOL, COS_TOL = 5e-3, 1e-2, 3e-2, 5e-2, 0.999
 
 
 def make(cfgt, seed=0):
@@ -37,7 +45,11 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def check_grads(cfg, got, ref, tol=GRAD_TOL, cos_tol=COS_TOL):
+def check_grads(cfg, got, ref, tol=GRAD_TOL, cos_tol=COS_TOL, qk_tol=None):
+    """Per-tensor gradient check vs the oracle. qk_tol (default: QK_GRAD_TOL under the oracle
+    tolerance, else the same as tol) bounds w_q / w_k; engine-vs-engine checks stay uniform."""
+    if qk_tol is None:
+        qk_tol = QK_GRAD_TOL if tol == GRAD_TOL else tol
     o = 0
     worst = (0.0, "")
     scale = np.linalg.norm(ref)
@@ -52,7 +64,8 @@ def check_grads(cfg, got, ref, tol=GRAD_TOL, cos_tol=COS_TOL):
         e = rel(g, r)
         cs = float(g @ r / (np.linalg.norm(g) * rn))
         worst = max(worst, (e, name))
-        assert e <= tol and cs >= cos_tol, f"{name}: rel {e:.3e} cos {cs:.6f}"
+        lim = qk_tol if name.endswith((".w_q", ".w_k")) else tol
+        assert e <= lim and cs >= cos_tol, f"{name}: rel {e:.3e} cos {cs:.6f}"
     return worst
 
 

@@ -22,6 +22,26 @@
 #include "gemm.h"
 #include "sm100.cuh"
 
+// Pipeline trace (clock64 per event) of the fused dh=64 kernel: compiled only into the separate
+// debug library (make trace -> libtreetrain_b200_trace.so, -DTT_TRACE=1); the product build has none.
+#ifndef TT_TRACE
+#define TT_TRACE 0
+#endif
+#if TT_TRACE
+constexpr int kTrCtas = 96, kTrBlocks = 33, kTrEv = 10;  // block row kTrBlocks-1 holds CTA-level events
+__device__ long long g_tt_trace[kTrCtas][kTrBlocks][kTrEv];
+#define TT_TR(ev, i)                                                                            \
+  do {                                                                                          \
+    if (blockIdx.y == 0 && blockIdx.x < kTrCtas && (i) < kTrBlocks) g_tt_trace[blockIdx.x][(i)][(ev)] = clock64(); \
+  } while (0)
+constexpr int kTrBlocksLast = kTrBlocks - 1;
+#else
+constexpr int kTrBlocksLast = 0;
+#define TT_TR(ev, i) \
+  do {               \
+  } while (0)
+#endif
+
 namespace ttb {
 
 namespace {
@@ -470,6 +490,7 @@ __global__ void __launch_bounds__(kThreadsDq, 1)
         st_D[tid] = nd;
       }
       named_bar_sync(1, 32 * kSmxWarps);
+      if (warp == 8 && lane == 0) TT_TR(8, i);
       fetch(i + 1);
       mbar_wait(&s_full[i % NB], (i / NB) & 1);
       tc_fence_after();
@@ -661,6 +682,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_S = tmem, t_dP = tmem + 256, t_dK = tmem + 384, t_dV = tmem + 448;
   const int wg = warp >> 2;
+  if (threadIdx.x == 0) TT_TR(0, kTrBlocksLast);
 
   if (wg == 0) {
     if (warp == 0 && lane == 0) {
@@ -680,6 +702,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       // loaded dP^T_{i-1}
       const uint64_t d16 = make_sdesc_sw128(smem_u32(smem), 16, 1024);  // K-major tiles
       mbar_wait(kv_full, 0);
+      if (lane == 0) TT_TR(1, kTrBlocksLast);
       for (int i = 0; i < nq; ++i) {
         const int st = i % NS;
         if (i >= 2) mbar_wait(&dq_free[i & 1], ((i - 2) >> 1) & 1);
@@ -687,6 +710,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
         tc_fence_after();
         const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
         if (lane == 0) {
+          TT_TR(0, i);
 #pragma unroll
           for (int k = 0; k < DH / 16; ++k)
             umma_bf16_ss(t_S + (i & 1) * 128, sdesc_add(d16, k * 32), sdesc_add(d16, q_off + k * 32), C::kIdescS,
@@ -697,6 +721,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
         if (i >= 1) mbar_wait(dp_free, (i - 1) & 1);
         tc_fence_after();
         if (lane == 0) {
+          TT_TR(1, i);
 #pragma unroll
           for (int k = 0; k < DH / 16; ++k)
             umma_bf16_ss(t_dP, sdesc_add(d16, C::kOffV + k * 32), sdesc_add(d16, do_off + k * 32), C::kIdescS, k > 0);
@@ -713,24 +738,28 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
         mbar_wait(&p_full[i & 1], (i >> 1) & 1);
         tc_fence_after();
         if (lane == 0) {
+          TT_TR(5, i);
           const int st = i % NS;
           const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
-#pragma unroll
           const uint32_t ds_off = (i & 1) * C::kDSBytes;
+          // dV_i (reads P^T_i from S^T buffer i % 2), then dQ_i (into the same buffer): the dq_full
+          // commit covers both, so once dQ_i is drained the buffer is free for S^T_{i+2} — the
+          // loop-carried dependency of the pipeline; dK_i runs behind it, during the drain
 #pragma unroll
-          for (int k = 0; k < BQ / 16; ++k) {  // 16 queries per step
+          for (int k = 0; k < BQ / 16; ++k)  // 16 queries per step
             umma_bf16_ts(t_dV, t_S + (i & 1) * 128 + 8 * k, sdesc_add(dmn, do_off + k * 2048), C::kIdescKV,
                          (i > 0 || k > 0));
-            umma_bf16_ss(t_dK, sdesc_add(dsk, ds_off + (k / 4) * 16384 + (k % 4) * 32), sdesc_add(dmn, q_off + k * 2048),
-                         C::kIdescKV, (i > 0 || k > 0));
-          }
 #pragma unroll
           for (int k = 0; k < C::BKV / 16; ++k)  // 16 keys per step
             umma_bf16_ss(t_S + (i & 1) * 128 + 64, sdesc_add(dsm, ds_off + k * 2048), sdesc_add(dmn, k * 2048), C::kIdescQ,
                          k > 0);
+          umma_commit(&dq_full[i & 1]);
+#pragma unroll
+          for (int k = 0; k < BQ / 16; ++k)
+            umma_bf16_ss(t_dK, sdesc_add(dsk, ds_off + (k / 4) * 16384 + (k % 4) * 32), sdesc_add(dmn, q_off + k * 2048),
+                         C::kIdescKV, (i > 0 || k > 0));
           umma_commit(&q_empty[st]);
           umma_commit(&ds_free[i & 1]);
-          umma_commit(&dq_full[i & 1]);
           if (i == nq - 1) umma_commit(acc_done);
         }
         __syncwarp();
@@ -745,6 +774,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       const int q0 = q_lo + i * BQ;
       mbar_wait(&dq_full[i & 1], (i >> 1) & 1);
       tc_fence_after();
+      if (warp == 4 && lane == 0) TT_TR(6, i);
       uint32_t r[64];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -803,6 +833,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
         st_nd[tid] = -nd * sc;
       }
       named_bar_sync(1, 32 * kSmxWarps);
+      if (warp == 8 && lane == 0) TT_TR(8, i);
       fetch(i + 1);
       // visibility: invalid keys see nothing; own rows: key kt sees query t iff kt <= t, i.e. block
       // columns >= kt - (q0 - seg_off) (queries beyond q_hi have lse2 = +inf -> P = 0)
@@ -811,6 +842,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       mbar_wait(&s_full[i & 1], (i >> 1) & 1);
       mbar_wait(dp_full, i & 1);
       tc_fence_after();
+      if (warp == 8 && lane == 0) TT_TR(2, i);
       const uint32_t sbuf = t_S + (i & 1) * 128;
 #pragma unroll
       for (int sub = 0; sub < 2; ++sub) {
@@ -831,6 +863,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
           }
         }
         if (sub == 1) {
+          if (warp == 8 && lane == 0) TT_TR(3, i);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(dp_free);  // dP^T_i in registers: dP^T_{i+1} may overwrite it
@@ -883,9 +916,12 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[i & 1]);
+      if (lane == 0 && warp == 8) TT_TR(4, i);
+      if (lane == 0 && warp == 12) TT_TR(7, i);
     }
     mbar_wait(acc_done, 0);
     tc_fence_after();
+    if (warp == 8 && lane == 0) TT_TR(2, kTrBlocksLast);
     float* dkr = (own ? p.dk : p.dk_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
     float* dvr = (own ? p.dv : p.dv_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
 #pragma unroll
@@ -907,6 +943,17 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    TT_TR(3, kTrBlocksLast);
+#if TT_TRACE
+    if (blockIdx.y == 0 && blockIdx.x < kTrCtas) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_tt_trace[blockIdx.x][kTrBlocksLast][4] = smid;
+      g_tt_trace[blockIdx.x][kTrBlocksLast][5] = nq;
+    }
+#endif
+  }
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
@@ -995,6 +1042,18 @@ void launch_bwd_fused(const AttnBwdArgs& a, long rows_cap, const int4* kv_items,
 }
 
 }  // namespace
+
+#if TT_TRACE
+extern "C" int tt_debug_trace_read(long long* out, long n) {
+  const long cap = static_cast<long>(kTrCtas) * kTrBlocks * kTrEv;
+  if (n > cap) n = cap;
+  return cudaMemcpyFromSymbol(out, g_tt_trace, n * sizeof(long long)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int tt_debug_trace_clear() {
+  static long long zeros[kTrCtas][kTrBlocks][kTrEv];
+  return cudaMemcpyToSymbol(g_tt_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream) {
   const long threads = static_cast<long>(a.n) * a.H * (a.dh / 8);

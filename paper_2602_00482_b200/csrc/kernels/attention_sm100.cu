@@ -23,6 +23,39 @@
 #include "gemm.h"
 #include "sm100.cuh"
 
+#ifndef TT_TRACE
+#define TT_TRACE 0
+#endif
+#if TT_TRACE
+// pipeline trace of the forward (debug library only, -DTT_TRACE=1): [cta][block][event] clock64
+constexpr int kFTrCtas = 64, kFTrBlocks = 32, kFTrEv = 8;
+__device__ long long g_tt_ftrace[kFTrCtas][kFTrBlocks][kFTrEv];
+__device__ long long g_tt_fcta[kFTrCtas][4];  // start, all warps past setup, softmax done, end
+#define TT_FCTA(ev)                                                                      \
+  do {                                                                                   \
+    if (blockIdx.y == 0 && blockIdx.x < kFTrCtas) g_tt_fcta[blockIdx.x][(ev)] = clock64(); \
+  } while (0)
+extern "C" int tt_debug_fcta_read(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tt_fcta, sizeof(g_tt_fcta)) == cudaSuccess ? 0 : 1;
+}
+#define TT_FTR(ev, j)                                                                                      \
+  do {                                                                                                     \
+    if (blockIdx.y == 0 && blockIdx.x < kFTrCtas && (j) < kFTrBlocks) g_tt_ftrace[blockIdx.x][(j)][(ev)] = clock64(); \
+  } while (0)
+extern "C" int tt_debug_ftrace_read(long long* out, long n) {
+  const long cap = static_cast<long>(kFTrCtas) * kFTrBlocks * kFTrEv;
+  if (n > cap) n = cap;
+  return cudaMemcpyFromSymbol(out, g_tt_ftrace, n * sizeof(long long)) == cudaSuccess ? 0 : 1;
+}
+#else
+#define TT_FTR(ev, j) \
+  do {                \
+  } while (0)
+#define TT_FCTA(ev) \
+  do {              \
+  } while (0)
+#endif
+
 namespace ttb {
 
 namespace {
@@ -93,6 +126,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   const int warp = warp_id_sync();
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TT_FCTA(0);
   const int4 blk = p.qblocks[blockIdx.x];
   const int q_start = blk.x, q_end = blk.y, seg_off = blk.z;
   const int h = blockIdx.y;
@@ -126,6 +160,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TT_FCTA(1);
   constexpr int NB = C::NB;
   const uint32_t tmem_S = tmem;              // NB x BKV columns
   // O (N = DH) at a DH-aligned column (dh 128: 256, not 192)
@@ -166,6 +201,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_wait(&k_full[st], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
+        TT_FTR(0, j);
         const uint32_t k_off = C::kOffK + st * C::kKVBytes;
 #pragma unroll
         for (int k = 0; k < DH / 16; ++k) {
@@ -189,6 +225,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_wait(&v_full[j % NS], (j / NS) & 1);
       tc_fence_after();
       if (lane == 0) {
+        TT_FTR(1, j);
         const int st = j % NS;
         const uint32_t v_off = C::kOffV + st * C::kKVBytes;
 #pragma unroll
@@ -221,8 +258,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     float m_used = -INFINITY, l = 0.f;
     const float c2 = p.scale_log2;
     for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&s_full[j % NB], (j / NB) & 1);
+      mbar_wait_fast(&s_full[j % NB], (j / NB) & 1);
       tc_fence_after();
+      if (warp == 2 && lane == 0) TT_FTR(2, j);
       float s[HC];
 #pragma unroll
       for (int c = 0; c < HC; c += 16) {
@@ -232,6 +270,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int i = 0; i < 16; ++i) s[c + i] = __uint_as_float(r[i]);
       }
       tmem_ld_wait();
+      if (warp == 2 && lane == 0) TT_FTR(3, j);
       const bool pre = j < n_pre;
       // key index of this half's column 0 (prefix row / own local)
       const int base = (pre ? j * BKV : (j - n_pre) * BKV) + half * HC;
@@ -240,11 +279,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int i = 0; i < HC; ++i) s[i] = i < lim ? s[i] : -INFINITY;
       }
-      float mx = fmax3f(s[0], s[1], s[2]);
+      // row max as a 3-ary tree (depth 4 at HC = 64 instead of a 32-long dependent chain)
+      float mx;
+      {
+        constexpr int N1 = (HC + 2) / 3;
+        float t1[N1];
 #pragma unroll
-      for (int i = 3; i + 1 < HC; i += 2) mx = fmax3f(mx, s[i], s[i + 1]);
-      if ((HC - 3) % 2) mx = fmaxf(mx, s[HC - 1]);
+        for (int i = 0; i < N1; ++i)
+          t1[i] = fmax3f(s[3 * i], 3 * i + 1 < HC ? s[3 * i + 1] : s[3 * i], 3 * i + 2 < HC ? s[3 * i + 2] : s[3 * i]);
+        constexpr int N2 = (N1 + 2) / 3;
+        float t2[N2];
+#pragma unroll
+        for (int i = 0; i < N2; ++i)
+          t2[i] = fmax3f(t1[3 * i], 3 * i + 1 < N1 ? t1[3 * i + 1] : t1[3 * i], 3 * i + 2 < N1 ? t1[3 * i + 2] : t1[3 * i]);
+        mx = t2[0];
+#pragma unroll
+        for (int i = 1; i < N2; i += 2) mx = fmax3f(mx, t2[i], i + 1 < N2 ? t2[i + 1] : t2[i]);
+      }
       const float m_new = fmaxf(m_used, mx * c2);
+      if (warp == 2 && lane == 0) TT_FTR(4, j);
       const bool resc = m_new > m_used + kRescaleThreshold;
       float corr = 1.f;
       if (resc) {
@@ -269,6 +322,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w[cch * 4 + e] = pack_bf16x2(pe.x, pe.y);
         }
       }
+      if (warp == 2 && lane == 0) TT_FTR(5, j);
 #pragma unroll
       for (int c = 0; c < HC / 2; c += 16)
         tmem_st16(tmem_S + (j % NB) * BKV + half * HC + c + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&w[c]));
@@ -292,7 +346,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[j % NB]);
+      if (lane == 0 && warp == 2) TT_FTR(6, j);
+      if (lane == 0 && warp == 6) TT_FTR(7, j);
     }
+    if (warp == 2 && lane == 0) TT_FCTA(2);
     // combine the two partial row sums
     // combine the halves: m = max(m0, m1); l = sum_h l_h 2^(m_h - m); O = sum_h O_h 2^(m_h - m) / l
     float* lb = xch;
@@ -340,6 +397,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TT_FCTA(3);
   if (warp == 1) tmem_dealloc(tmem, C::kTmemCols);
 }
 

@@ -48,6 +48,21 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity
       : "memory");
   return ok;
 }
+// Non-blocking probe of the phase (mbarrier.test_wait): the fast path of a wait whose phase has most
+// likely completed already (try_wait costs ~200 clk even then).
+__device__ __forceinline__ uint32_t mbar_test_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t"
+      ".reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok;
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -55,6 +70,12 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 // Blocking wait on the phase with the given parity. A wait that does not complete within ~4 s is a
 // pipeline bug: report the barrier and trap (the launch fails loudly instead of hanging the GPU).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity);
+// The same with a non-blocking test first (consumers that usually find the phase complete).
+__device__ __forceinline__ void mbar_wait_fast(uint64_t* bar, uint32_t parity) {
+  if (mbar_test_wait(smem_u32(bar), parity)) return;
+  mbar_wait(bar, parity);
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;

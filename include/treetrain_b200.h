@@ -216,6 +216,8 @@ int tt_engine_set_profiling(tt_engine* eng, int32_t on);
  *   "root_batch_tokens"  token cap of a multi-root prompt push (default 4096; 0 = one root per push)
  *   "cuda_graph"         0 = eager launches, 1 = capture a prepared plan's op list on its 2nd execute (default)
  *   "ce_stats"           1 = LM-head GEMM emits per-row softmax statistics for CE (default), 0 = CE two-pass
+ *   "logits_bf16"        1 = LM-head logits stored bf16 relative to their 32-column group max (default; with
+ *                        ce_stats), 0 = fp32 logits (loss / gradients then differ by bf16 rounding only)
  *   "head_chunk_mb"      LM-head / CE scratch budget per loss-row chunk (default 6144, >= 1; capped by free HBM)
  * Unknown keys and out-of-range values return TT_ERR_INVALID_ARGUMENT. */
 int tt_engine_set_option(tt_engine* eng, const char* key, int64_t value);

@@ -183,6 +183,10 @@ void Engine::set_option(const std::string& key, int64_t value) {
     // 1: LM-head GEMM epilogue emits per-32-column softmax statistics, CE reads logits once
     // (default); 0: CE does both passes over the logits row itself
     ce_stats_ = value != 0;
+  } else if (key == "logits_bf16") {
+    // 1: LM-head logits as bf16 offsets from their 32-column group max (half the logits traffic;
+    // needs ce_stats); 0: fp32 logits
+    logits_bf16_ = value != 0;
   } else {
     throw std::invalid_argument("unknown engine option: " + key);
   }
@@ -508,6 +512,7 @@ std::string Engine::gemm_profile_text() const {
 void Engine::gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& e, int splits) {
   double out_b = 2.0;
   if (e.mode == EPI_STORE_F32 || e.mode == EPI_STORE_F32_STATS) out_b = 4.0;
+  if (e.mode == EPI_STORE_BF16_STATS) out_b = 2.0;
   if (e.mode == EPI_ADD_F32 || e.mode == EPI_RESID_F32) out_b = 8.0;
   if (e.mode == EPI_SILU || e.mode == EPI_DSILU) out_b = 4.0;
   const double bytes = 2.0 * (double(M) * K + double(N) * K) + out_b * double(M) * N;
@@ -642,9 +647,10 @@ void Engine::head_backward(const Batch& b, const bf16* nf, bool loss_only) {
     const int cm = static_cast<int>(std::min<int64_t>(per, m - c0));
     tag("k_gather_rows_bf16");
     run(KC_ELEMWISE, 0, 4.0 * cm * d, [&] { k_gather_rows_bf16(nf, meta<int32_t>(b.o_lrows) + c0, nfl, cm, d, stream_); });
+    const bool lbf = ce_stats_ && logits_bf16_;
     {
-      EpiParams e;  // logits = normed_final W_head (model.hpp:460-461), fp32, + per-row softmax stats
-      e.mode = ce_stats_ ? EPI_STORE_F32_STATS : EPI_STORE_F32;
+      EpiParams e;  // logits = normed_final W_head (model.hpp:460-461) + per-row softmax stats
+      e.mode = lbf ? EPI_STORE_BF16_STATS : (ce_stats_ ? EPI_STORE_F32_STATS : EPI_STORE_F32);
       e.out[0] = sc_logits_.p;
       e.ldo[0] = V;
       e.out2 = sc_stats_.p;
@@ -652,9 +658,13 @@ void Engine::head_backward(const Batch& b, const bf16* nf, bool loss_only) {
       gemm(op(nfl, d, false), op(head_, V, true), cm, V, d, e, 1);
     }
     tag("k_ce");
-    run(KC_CE, 0, 6.0 * cm * V, [&] {  // weighted_nll (model.hpp:643-677), multi-target rows
-      k_ce(sc_logits_.as<float>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt), meta<double>(b.o_pw),
-           dlog, loss_.as<double>(), stream_, ce_stats_ ? sc_stats_.as<float2>() : nullptr, (V + 31) / 32);
+    run(KC_CE, 0, (lbf ? 4.0 : 6.0) * cm * V, [&] {  // weighted_nll (model.hpp:643-677), multi-target rows
+      if (lbf)
+        k_ce_bf16(sc_logits_.as<bf16>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt),
+                  meta<double>(b.o_pw), dlog, loss_.as<double>(), stream_, sc_stats_.as<float2>(), (V + 31) / 32);
+      else
+        k_ce(sc_logits_.as<float>(), cm, V, meta<int32_t>(b.o_poff) + c0, meta<int32_t>(b.o_ptgt), meta<double>(b.o_pw),
+             dlog, loss_.as<double>(), stream_, ce_stats_ ? sc_stats_.as<float2>() : nullptr, (V + 31) / 32);
     });
     if (loss_only) continue;  // the VISIT of a segment-level caller: loss now, gradients at the pop
     {  // dW_head += c^T dlogits  (model.hpp:506)

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "elementwise.h"
+#include "gemm.h"
 #include "sm100.cuh"
 
 namespace ttb {
@@ -204,6 +205,144 @@ void launch_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const
   rmsnorm_bwd_kernel<VPT, WPR><<<blocks, 256, d * sizeof(float), s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
 }
 
+// rmsnorm_backward for rows of up to 1024 columns, fed by TMA: a persistent block per SM, one producer
+// warp streams each of its rows' gy / x / gres (3 x d fp32) into an NST-deep shared-memory ring with
+// cp.async.bulk (mbarrier complete_tx), eight consumer warps take the rows round-robin (warp w: the
+// block's rows k = w (mod 8)). The ring keeps ~16 rows (~170 KB) in flight per SM independently of the
+// consumers' reduce-then-store latency, which is what bounded the register version (one HBM round trip
+// for gy / x, a second for gres, 16 warps per SM: 4.1-4.5 TB/s). gain is held in registers; the
+// gain-gradient partials stay in registers for all of a warp's rows and leave through shared memory +
+// one red.global.add.v4 per column group.
+__device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem_dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+constexpr int kNormTmaThreads = 288;  // 8 consumer warps + 1 producer warp
+
+template <int VPT>
+__global__ void __launch_bounds__(kNormTmaThreads, 1)
+    rmsnorm_bwd_tma_kernel(const float* __restrict__ gy, const float* __restrict__ x, const float* __restrict__ inv,
+                           const float* __restrict__ gain, const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
+                           float* __restrict__ ggain, int n, int d, int nst) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int nb = gres ? 3 : 2;              // row buffers per stage
+  const int row_bytes = d * 4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + nst;
+  float* gsum = reinterpret_cast<float*>(empty + nst);  // [d]
+  uint8_t* ring = smem_raw + ((nst * 16 + d * 4 + 127) / 128) * 128;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nst; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_barrier_init();
+  }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) gsum[c] = 0.f;
+  __syncthreads();
+  const int rows_mine = n > static_cast<int>(blockIdx.x) ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int k = 0; k < rows_mine; ++k) {
+        const int st = k % nst;
+        const long r = blockIdx.x + static_cast<long>(k) * gridDim.x;
+        mbar_wait(&empty[st], ((k / nst) & 1) ^ 1);
+        uint8_t* b = ring + static_cast<long>(st) * nb * row_bytes;
+        mbar_arrive_expect_tx(&full[st], nb * row_bytes);
+        bulk_load_1d(b, gy + r * d, row_bytes, &full[st]);
+        bulk_load_1d(b + row_bytes, x + r * d, row_bytes, &full[st]);
+        if (gres) bulk_load_1d(b + 2 * row_bytes, gres + r * d, row_bytes, &full[st]);
+      }
+    }
+  } else {
+    float4 g[VPT], gacc[VPT];
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = (lane + 32 * k) * 4;
+      g[k] = c < d ? __ldg(reinterpret_cast<const float4*>(gain + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      gacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int k = warp; k < rows_mine; k += 8) {
+      const int st = k % nst;
+      const long r = blockIdx.x + static_cast<long>(k) * gridDim.x;
+      const float iv = inv[r];  // issued before the wait: its latency overlaps the ring
+      mbar_wait(&full[st], (k / nst) & 1);
+      const float* sgy = reinterpret_cast<const float*>(ring + static_cast<long>(st) * nb * row_bytes);
+      const float* sx = sgy + d;
+      const float* sres = sgy + 2 * d;
+      float4 av[VPT], bv[VPT];
+      float dot = 0.f;
+#pragma unroll
+      for (int q = 0; q < VPT; ++q) {
+        const int c = (lane + 32 * q) * 4;
+        if (c < d) {
+          av[q] = *reinterpret_cast<const float4*>(sgy + c);
+          bv[q] = *reinterpret_cast<const float4*>(sx + c);
+          dot += av[q].x * g[q].x * bv[q].x + av[q].y * g[q].y * bv[q].y + av[q].z * g[q].z * bv[q].z +
+                 av[q].w * g[q].w * bv[q].w;
+        }
+      }
+      dot = warp_sum(dot);
+      const float scale = dot * iv * iv * iv / static_cast<float>(d);
+      float* gxr = gx + r * d;
+      __nv_bfloat16* gxbr = gxb + r * d;
+#pragma unroll
+      for (int q = 0; q < VPT; ++q) {
+        const int c = (lane + 32 * q) * 4;
+        if (c < d) {
+          const float4 a = av[q], b = bv[q];
+          float4 res = gres ? *reinterpret_cast<const float4*>(sres + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          res.x += a.x * g[q].x * iv - b.x * scale;
+          res.y += a.y * g[q].y * iv - b.y * scale;
+          res.z += a.z * g[q].z * iv - b.z * scale;
+          res.w += a.w * g[q].w * iv - b.w * scale;
+          __stcs(reinterpret_cast<float4*>(gxr + c), res);
+          uint2 pb;
+          pb.x = pack_bf16x2(res.x, res.y);
+          pb.y = pack_bf16x2(res.z, res.w);
+          *reinterpret_cast<uint2*>(gxbr + c) = pb;
+          gacc[q].x += a.x * b.x * iv;
+          gacc[q].y += a.y * b.y * iv;
+          gacc[q].z += a.z * b.z * iv;
+          gacc[q].w += a.w * b.w * iv;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int c = (lane + 32 * q) * 4;
+      if (c < d) {
+        atomicAdd(gsum + c, gacc[q].x);
+        atomicAdd(gsum + c + 1, gacc[q].y);
+        atomicAdd(gsum + c + 2, gacc[q].z);
+        atomicAdd(gsum + c + 3, gacc[q].w);
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x * 4; c < d; c += 4 * blockDim.x)
+    red_add_v4_f32(ggain + c, gsum[c], gsum[c + 1], gsum[c + 2], gsum[c + 3]);
+}
+
+template <int VPT>
+void launch_rmsnorm_bwd_tma(const float* gy, const float* x, const float* inv, const float* gain, const float* gres,
+                            float* gx, __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
+  constexpr int kSmemMax = 227 * 1024;
+  const int stage_bytes = (gres ? 3 : 2) * d * 4;
+  const int head = ((16 * 32 + d * 4 + 127) / 128) * 128;  // barriers (<= 32 stages) + gsum
+  const int nst = std::min(32, (kSmemMax - head - 1024) / stage_bytes);
+  const int smem = ((nst * 16 + d * 4 + 127) / 128) * 128 + nst * stage_bytes;
+  ensure_smem_attr(reinterpret_cast<const void*>(rmsnorm_bwd_tma_kernel<VPT>), kSmemMax);
+  const int blocks = std::min(n, device_sm_count());
+  rmsnorm_bwd_tma_kernel<VPT><<<blocks, kNormTmaThreads, smem, s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, nst);
+}
+
 // Weighted NLL over one vocab row with several (target, weight) pairs (weighted_nll,
 // model.hpp:643-677, extended to multi-target rows):
 //   loss += sum_j w_j (lse - l[t_j])  (fp64);  dl = (sum_j w_j) softmax(l) - sum_j w_j onehot(t_j)  (bf16)
@@ -330,6 +469,101 @@ __global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restri
       atomicAdd(loss, acc);
     }
     __syncthreads();  // red / s_lse reuse by the next row
+  }
+}
+
+// weighted_nll over bf16 logits stored relative to their 32-column group max (the LM-head GEMM's
+// EPI_STORE_BF16_STATS epilogue): l = y + m_g. The row's lse comes from the per-group (m_g, s_g)
+// statistics alone; the streaming pass reads 2 B per logit (8 per 16-byte load, all in one group)
+// and writes the bf16 dlogits. Same multi-target semantics as ce_kernel.
+__global__ void __launch_bounds__(kCeThreads, 4)
+    ce_bf16_kernel(const __nv_bfloat16* __restrict__ y, int m, long V, const int32_t* __restrict__ pair_off,
+                   const int32_t* __restrict__ tgt, const double* __restrict__ w, __nv_bfloat16* __restrict__ dl,
+                   double* __restrict__ loss, const float2* __restrict__ stats, int n_groups) {
+  __shared__ float red[32];
+  __shared__ float s_lse;
+  constexpr float kL2e = 1.4426950408889634f;
+  const int wi = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int r = blockIdx.x; r < m; r += gridDim.x) {
+    const __nv_bfloat16* yr = y + static_cast<long>(r) * V;
+    const float2* sr = stats + static_cast<long>(r) * n_groups;
+    float mx = -INFINITY, s = 0.f;
+    for (int g = threadIdx.x; g < n_groups; g += kCeThreads) {
+      const float2 ms = sr[g];
+      if (ms.x > mx) {
+        s = s * __expf(mx - ms.x) + ms.y;
+        mx = ms.x;
+      } else {
+        s += ms.y * __expf(ms.x - mx);
+      }
+    }
+    float gm = warp_max(mx);
+    if (ln == 0) red[wi] = gm;
+    __syncthreads();
+    gm = warp_max(ln < kCeThreads / 32 ? red[ln] : -INFINITY);
+    __syncthreads();
+    s = (mx == -INFINITY) ? 0.f : s * __expf(mx - gm);
+    s = warp_sum(s);
+    if (ln == 0) red[wi] = s;
+    __syncthreads();
+    if (wi == 0) {
+      const float t = warp_sum(ln < kCeThreads / 32 ? red[ln] : 0.f);
+      if (ln == 0) s_lse = gm + logf(t);
+    }
+    __syncthreads();
+    const float lse = s_lse;
+    const int p0 = pair_off[r], p1 = pair_off[r + 1];
+    float wsum = 0.f;
+    for (int p = p0; p < p1; ++p) wsum += static_cast<float>(w[p]);
+    __nv_bfloat16* dr = dl + static_cast<long>(r) * V;
+    constexpr int U = 4;
+    constexpr long kStep = 8L * kCeThreads;
+    for (long c0 = threadIdx.x * 8; c0 < V; c0 += U * kStep) {
+      uint4 v[U];
+      float off[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long c = c0 + u * kStep;
+        v[u] = c < V ? __ldcs(reinterpret_cast<const uint4*>(yr + c)) : make_uint4(0, 0, 0, 0);
+        off[u] = c < V ? (sr[c >> 5].x - lse) * kL2e : 0.f;  // p = 2^((y + m_g - lse) log2e)
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long c = c0 + u * kStep;
+        if (c >= V) break;
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+        uint32_t o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          o[i] = pack_bf16x2(wsum * ex2_approx(fmaf(f.x, kL2e, off[u])), wsum * ex2_approx(fmaf(f.y, kL2e, off[u])));
+        }
+        __stcs(reinterpret_cast<uint4*>(dr + c), make_uint4(o[0], o[1], o[2], o[3]));
+      }
+    }
+    // target columns, after the streaming pass (the barrier orders it after that pass's store)
+    __syncthreads();
+    for (int p = p0 + static_cast<int>(threadIdx.x); p < p1; p += kCeThreads) {
+      const long t = tgt[p];
+      bool first = true;
+      float wt = 0.f;
+      for (int q = p0; q < p1; ++q)
+        if (tgt[q] == t) {
+          first = first && q >= p;
+          wt += static_cast<float>(w[q]);
+        }
+      if (first) st_grad1(dr + t, wsum * __expf(__bfloat162float(yr[t]) + sr[t >> 5].x - lse) - wt);
+    }
+    if (threadIdx.x == 0) {
+      double acc = 0.0;
+      for (int p = p0; p < p1; ++p) {
+        const long t = tgt[p];
+        const double lt = static_cast<double>(__bfloat162float(yr[t])) + static_cast<double>(sr[t >> 5].x);
+        acc += w[p] * (static_cast<double>(lse) - lt);
+      }
+      atomicAdd(loss, acc);
+    }
+    __syncthreads();
   }
 }
 
@@ -462,7 +696,11 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
   if (n <= 0) return;
   const int vpt = (d + 127) / 128;  // float4 column groups per lane with one warp per row
   // (two warps per row at d = 896 measured 3.6 vs 4.2 TB/s: one warp per row up to 7 float4 per lane)
-  if (vpt <= 2) launch_rmsnorm_bwd<2, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  // d <= 1024 with 16-byte rows: the TMA-fed persistent kernel; wider rows: several warps per row
+  if (d % 4 == 0 && vpt <= 2) launch_rmsnorm_bwd_tma<2>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (d % 4 == 0 && vpt <= 4) launch_rmsnorm_bwd_tma<4>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (d % 4 == 0 && vpt <= 8) launch_rmsnorm_bwd_tma<8>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 2) launch_rmsnorm_bwd<2, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else if (vpt <= 4) launch_rmsnorm_bwd<4, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else if (vpt <= 7) launch_rmsnorm_bwd<7, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else if (vpt <= 14) launch_rmsnorm_bwd<7, 2>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
@@ -475,6 +713,12 @@ void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int
   if (m > 0)
     ce_kernel<__nv_bfloat16><<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, stats,
                                                                          n_groups);
+}
+void k_ce_bf16(const __nv_bfloat16* y, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
+               __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {
+  if (V % 8 != 0) throw std::invalid_argument("k_ce_bf16: vocab_size must be a multiple of 8");
+  if (m > 0)
+    ce_bf16_kernel<<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(y, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
 }
 void k_ce_f32(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
               float* dl, double* loss, cudaStream_t s) {

@@ -19,6 +19,10 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
           __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats = nullptr, int n_groups = 0);
 // standalone weighted_nll: fp32 grad_logits, two passes over each logits row
+// weighted_nll from bf16 logits relative to their 32-column group max + the per-group (max, sum) stats
+// (the LM-head GEMM's EPI_STORE_BF16_STATS output); dlogits bf16.
+void k_ce_bf16(const __nv_bfloat16* y, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
+               __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups);
 void k_ce_f32(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
               float* dl, double* loss, cudaStream_t s);
 // dst[i] += src[i], n a multiple of 4

@@ -27,6 +27,9 @@ enum EpiMode : int {
                             // of LM-head logits, so the CE pass reads each logit row once
   EPI_ADD_F32_T = 7,   // out[0] (fp32) [n * ldo + m] += alpha*acc: the transposed accumulate that
                        // gemm_bf16 launches for EPI_ADD_F32 when C^T = B A^T tiles the SMs better
+  EPI_STORE_BF16_STATS = 8,  // as EPI_STORE_F32_STATS, but out[0] (bf16) = alpha*acc - (its 32-column
+                             // group's max): LM-head logits at 2 B each, exact to bf16 rounding of the
+                             // offset from the group max (the entries near the max keep the most bits)
 };
 
 // Column blocks of width split_w go to out[n / split_w] (row pitch ldo[...]) so one GEMM can

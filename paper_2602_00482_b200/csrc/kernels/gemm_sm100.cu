@@ -203,22 +203,23 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * alpha;
   switch (epi.mode) {
     case EPI_STORE_F32_STATS:
+    case EPI_STORE_BF16_STATS: {
+      // per-row (max, sum exp(v - max)) of this 32-column group (columns >= N excluded): 3-input max,
+      // then 2^(v log2e - mx log2e) as one FFMA + MUFU per element, paired adds
+      constexpr float kL2e = 1.4426950408889634f;
+      float mx;
+      if (n0 + 32 <= N) {
+        mx = fmax3f(v[0], v[1], v[2]);
+#pragma unroll
+        for (int i = 3; i < 31; i += 2) mx = fmax3f(mx, v[i], v[i + 1]);
+        mx = fmaxf(mx, v[31]);
+      } else {
+        mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (n0 + i < N) mx = fmaxf(mx, v[i]);
+      }
       if (row < M) {
-        // per-row (max, sum exp) of this 32-column group (columns >= N excluded): 3-input max, then
-        // 2^(v log2e - mx log2e) as one FFMA + MUFU per element, paired adds
-        constexpr float kL2e = 1.4426950408889634f;
-        float mx;
-        if (n0 + 32 <= N) {
-          mx = fmax3f(v[0], v[1], v[2]);
-#pragma unroll
-          for (int i = 3; i < 31; i += 2) mx = fmax3f(mx, v[i], v[i + 1]);
-          mx = fmaxf(mx, v[31]);
-        } else {
-          mx = -INFINITY;
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (n0 + i < N) mx = fmaxf(mx, v[i]);
-        }
         const float nm = -mx * kL2e;
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
@@ -229,6 +230,16 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
         }
         reinterpret_cast<float2*>(epi.out2)[static_cast<long>(row) * epi.ldo2 + n0 / 32] = make_float2(mx, acc.x + acc.y);
       }
+      if (epi.mode == EPI_STORE_BF16_STATS) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) =
+              make_uint4(pack_bf16x2(v[8 * u] - mx, v[8 * u + 1] - mx), pack_bf16x2(v[8 * u + 2] - mx, v[8 * u + 3] - mx),
+                         pack_bf16x2(v[8 * u + 4] - mx, v[8 * u + 5] - mx),
+                         pack_bf16x2(v[8 * u + 6] - mx, v[8 * u + 7] - mx));
+        break;
+      }
+    }
       [[fallthrough]];
     case EPI_STORE_F32:
     case EPI_ADD_F32:

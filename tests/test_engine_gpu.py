@@ -247,12 +247,14 @@ def test_attention_long_segments_vs_oracle(cfgt):
     tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
 
 
-@pytest.mark.parametrize("ce_stats", [0, 1])
-def test_lm_head_ce_variants_vs_oracle(ce_stats):
-    # weighted_nll (model.hpp:643-677): CE from the GEMM-epilogue softmax statistics (1) or from
-    # its own two passes over the logits row (0) — same step against the oracle
+@pytest.mark.parametrize("ce_stats,logits_bf16", [(0, 0), (1, 0), (1, 1)])
+def test_lm_head_ce_variants_vs_oracle(ce_stats, logits_bf16):
+    # weighted_nll (model.hpp:643-677): CE from the GEMM-epilogue softmax statistics (ce_stats 1) over
+    # fp32 logits or bf16 logits relative to the 32-column group max (logits_bf16 1, the default), or
+    # from its own two passes over fp32 logits (0) — same step against the oracle
     cfg, flat, eng = make(SMALL, 18)
     eng.set_option("ce_stats", ce_stats)
+    eng.set_option("logits_bf16", logits_bf16)
     seqs = O.grouped_corpus(2, 4, 150, 200, cfg.vocab_size, 19, shared_response=20, weight_jitter=True)
     tree_case(cfg, seqs, flat, eng, tt.SchedulerConfig())
 

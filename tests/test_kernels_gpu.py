@@ -182,9 +182,10 @@ def test_gemm_logits_with_softmax_stats(M, N):
     assert torch.allclose(lse, torch.logsumexp(out, -1), atol=1e-5)
 
 
-@pytest.mark.parametrize("n,d", [(1, 256), (37, 896), (4099, 896), (300, 1536), (129, 3584), (1001, 3584), (33, 2048),
-                                 (77, 4096), (5, 8192)])
-def test_rmsnorm_bwd_matches_torch(n, d):
+@pytest.mark.parametrize("n,d", [(1, 256), (37, 896), (4099, 896), (32768, 896), (150, 512), (300, 1536), (129, 3584),
+                                 (1001, 3584), (33, 2048), (77, 4096), (5, 8192), (2000, 1024)])
+@pytest.mark.parametrize("inplace", [False, True], ids=["gres", "inplace"])
+def test_rmsnorm_bwd_matches_torch(n, d, inplace):
     torch.manual_seed(7)
     lib = _lib()
     vp = ctypes.c_void_p
@@ -197,8 +198,11 @@ def test_rmsnorm_bwd_matches_torch(n, d):
     gxb = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
     gg = torch.randn(d, device="cuda")
     gg0 = gg.clone()
+    if inplace:  # the engine's call: the residual gradient is accumulated in place (gres == gx)
+        gx.copy_(gres)
     rc = lib.tt_debug_rmsnorm_bwd(vp(gy.data_ptr()), vp(x.data_ptr()), vp(inv.data_ptr()), vp(g.data_ptr()),
-                                  vp(gres.data_ptr()), vp(gx.data_ptr()), vp(gxb.data_ptr()), vp(gg.data_ptr()), n, d)
+                                  vp((gx if inplace else gres).data_ptr()), vp(gx.data_ptr()), vp(gxb.data_ptr()),
+                                  vp(gg.data_ptr()), n, d)
     assert rc == 0, lib.tt_last_error().decode()
     xr = x.clone().requires_grad_(True)
     gr = g.clone().requires_grad_(True)

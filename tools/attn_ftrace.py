@@ -1,7 +1,7 @@
 """Pipeline trace of the attention forward (debug library only: make -C paper_2602_00482_b200/csrc
 trace) on the c2 leaf-batch shape. Events per key block j (SM clocks, head 0, first CTAs):
-  S = S_j issued   PV = PV_j issued   w = softmax (w2) has S_j   ld = S_j in registers
-  mx = row max done   ex = exponentials done (before the P store)   ar = p_full arrive (w2)   ar6 = (w6, half 1)
+  S = S_j issued   PV = PV_j issued   pre = softmax (w2) about to wait for S_j   w = has S_j
+  ld = S_j in registers   mx = row max done   ex = exponentials done (before the P store)   ar = p_full arrive
 Usage: python tools/attn_ftrace.py [nseg n S H]"""
 import ctypes
 import os
@@ -12,7 +12,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CT, NB, NE = 64, 32, 8
-EV = ["S", "PV", "w", "ld", "mx", "ex", "ar", "ar6"]
+EV = ["S", "PV", "w", "ld", "mx", "ex", "ar", "pre"]
 
 
 def main():
@@ -39,7 +39,7 @@ def main():
     lib.tt_debug_ftrace_read(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), ctypes.c_long(buf.size))
     tr = buf.reshape(CT, NB, NE)
     print(f"forward {ms.value:.3f} ms per launch (nseg {nseg}, n {n}, S {S}, H {H})")
-    per, ld, mx, ex, st, wait = [], [], [], [], [], []
+    per, ld, mx, ex, st, wait, loop = [], [], [], [], [], [], []
     for c in range(CT):
         b = tr[c]
         nb = int((b[:, 6] != 0).sum())
@@ -49,7 +49,8 @@ def main():
                 print(f"CTA {c} j={j:2d} " + " ".join(f"{EV[e]}={b[j][e] - t0:7d}" for e in range(NE)))
         for j in range(1, nb):
             per.append(b[j][6] - b[j - 1][6])
-            wait.append(b[j][2] - b[j - 1][6])
+            wait.append(b[j][2] - b[j][7])
+            loop.append(b[j][7] - b[j - 1][6])
             ld.append(b[j][3] - b[j][2])
             mx.append(b[j][4] - b[j][3])
             ex.append(b[j][5] - b[j][4])
@@ -65,7 +66,7 @@ def main():
     nbk = (tr[:, :, 6] != 0).sum(1)
     print(f"CTA: total median {np.median(tot):.0f} clk for median {np.median(nbk):.0f} blocks; setup {np.median(setup):.0f}, "
           f"to first S {np.median(first):.0f}, blocks {np.median(body):.0f}, tail {np.median(tail):.0f}")
-    for name, v in (("period (ar_j - ar_j-1)", per), ("wait for S_j", wait), ("S load", ld), ("max", mx),
+    for name, v in (("period (ar_j - ar_j-1)", per), ("loop head (ar -> pre-wait)", loop), ("wait for S_j", wait), ("S load", ld), ("max", mx),
                     ("exp + pack", ex), ("P store + arrive", st)):
         print(f"{name:26s} median {np.median(v):7.0f}  p10 {np.percentile(v, 10):7.0f}  p90 {np.percentile(v, 90):7.0f}")
 

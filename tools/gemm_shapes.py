@@ -16,11 +16,13 @@ SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
     ("fwd qkv", n, 3 * d, d, 0, 1, EPI_STORE_BF16),
     ("fwd o", n, d, d, 0, 1, EPI_RESID),
     ("fwd mlp_in", n, F, d, 0, 1, EPI_SILU),
+    ("fwd mlp_in plain", n, F, d, 0, 1, EPI_STORE_BF16),  # same shape, one bf16 output, no SiLU
     ("fwd mlp_out", n, d, F, 0, 1, EPI_RESID),
     ("fwd head", 2048, V, d, 0, 1, EPI_STORE_F32),
     ("fwd head stats", 2304, V, d, 0, 1, EPI_STATS),
     ("fwd head stats c2", 6656, V, d, 0, 1, EPI_STATS),  # the c2 LM-head chunk (6 GB scratch budget)
     ("dX mlp_out", n, F, d, 0, 0, EPI_DSILU),
+    ("dX mlp_out plain", n, F, d, 0, 0, EPI_STORE_BF16),  # same shape without the SiLU' operand
     ("dX mlp_in", n, d, F, 0, 0, EPI_STORE_F32),
     ("dX o", n, d, d, 0, 0, EPI_STORE_BF16),
     ("dX qkv", n, d, 3 * d, 0, 0, EPI_STORE_F32),

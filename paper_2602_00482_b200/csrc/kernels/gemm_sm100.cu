@@ -274,6 +274,13 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
         float h[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(v[8 * u + i]));
+#if defined(TT_EXP_SILU_NOMUFU)  // experiment builds only (tools/gemm_epilogue_ab.sh)
+        *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) =
+            make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]), pack_bf16x2(h[6], h[7]));
+        *reinterpret_cast<uint4*>(buf + 2048 + sw64_off(lane, u)) =
+            make_uint4(pack_bf16x2(h[1], h[0]), pack_bf16x2(h[3], h[2]), pack_bf16x2(h[5], h[4]), pack_bf16x2(h[7], h[6]));
+        continue;
+#endif
         *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) =
             make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]),
                        pack_bf16x2(h[6], h[7]));
@@ -592,7 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (mode == EPI_ADD_F32) tma_reduce_add_2d(tm, buf, xc, row0);
             else if (mode == EPI_ADD_F32_T) tma_reduce_add_2d(tm, buf, row0, n0);
             else tma_store_2d(tm, buf, xc, row0);
+#if !defined(TT_EXP_SILU_ONESTORE)
             if (mode == EPI_SILU) tma_store_2d(&tm_x, buf + 2048, n0, row0);
+#endif
             bulk_commit();
           }
           ++gc;

@@ -36,6 +36,8 @@ SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
 
 
 def main():
+    if os.environ.get("GEMM_LIB"):  # experiment builds (tools/gemm_epilogue_ab.sh)
+        _native.LIB_PATH = os.path.abspath(os.environ["GEMM_LIB"])
     lib = _native.lib()
     lib.tt_debug_gemm_set_2cta(int(os.environ.get("GEMM_2CTA", "1")))
     only = os.environ.get("GEMM_ONLY")

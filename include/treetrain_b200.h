@@ -202,6 +202,13 @@ int tt_dense_train_step(tt_engine* eng, const int32_t* tokens, const uint64_t* o
 typedef struct tt_step_plan tt_step_plan;
 int tt_plan_create(tt_engine* eng, const tt_tree* tree, const tt_sched_config* sched, tt_step_plan** out);
 int tt_plan_execute(tt_engine* eng, tt_step_plan* plan, tt_step_result* result);
+/* Asynchronous execute: enqueue the step and return at once; tt_plan_wait blocks for it and fills the
+ * result (loss, counters; TT_ERR_NONFINITE as tt_plan_execute). One step in flight per engine. While
+ * it runs, the host may build and tt_plan_create the next step (plan metadata is copied on a separate
+ * stream without synchronising the engine), so a training loop overlaps host planning with the
+ * device step. tt_plan_execute == execute_async + wait. */
+int tt_plan_execute_async(tt_engine* eng, tt_step_plan* plan);
+int tt_plan_wait(tt_engine* eng, tt_step_plan* plan, tt_step_result* result);
 int tt_plan_trace(const tt_step_plan* plan, char* buf, uint64_t cap, uint64_t* len);
 int tt_plan_destroy(tt_step_plan* plan);
 

@@ -308,6 +308,17 @@ class StepPlan:
         _check(_native.lib().tt_plan_execute(self._eng._h, self._h, ctypes.byref(r)))
         return TrainStepResult._from(r)
 
+    def execute_async(self) -> "StepPlan":
+        """Enqueue the step and return at once (tt_plan_execute_async); wait() gives its result. The
+        next step's tree may be built and planned meanwhile."""
+        _check(_native.lib().tt_plan_execute_async(self._eng._h, self._h))
+        return self
+
+    def wait(self) -> TrainStepResult:
+        r = _native.StepResultC()
+        _check(_native.lib().tt_plan_wait(self._eng._h, self._h, ctypes.byref(r)))
+        return TrainStepResult._from(r)
+
     def trace(self) -> str:
         n = ctypes.c_uint64()
         _check(_native.lib().tt_plan_trace(self._h, None, 0, ctypes.byref(n)))

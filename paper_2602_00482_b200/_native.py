@@ -78,6 +78,8 @@ EXPORTS = {
     "tt_dense_train_step": [vp, P(i32), P(u64), P(f64), u64, P(StepResultC)],
     "tt_plan_create": [vp, vp, P(SchedConfigC), P(vp)],
     "tt_plan_execute": [vp, vp, P(StepResultC)],
+    "tt_plan_execute_async": [vp, vp],
+    "tt_plan_wait": [vp, vp, P(StepResultC)],
     "tt_plan_trace": [vp, c.c_char_p, u64, P(u64)],
     "tt_plan_destroy": [vp],
     "tt_engine_set_profiling": [vp, i32],

@@ -430,6 +430,23 @@ int tt_plan_execute(tt_engine* eng, tt_step_plan* plan, tt_step_result* result) 
   });
 }
 
+int tt_plan_execute_async(tt_engine* eng, tt_step_plan* plan) {
+  return ttb::guarded([&] {
+    use(eng);
+    need(plan, "plan");
+    eng->e->execute_async(*plan->p);
+  });
+}
+
+int tt_plan_wait(tt_engine* eng, tt_step_plan* plan, tt_step_result* result) {
+  return ttb::guarded([&] {
+    use(eng);
+    need(plan, "plan");
+    tt_step_result r = eng->e->wait(*plan->p);
+    if (result) *result = r;
+  });
+}
+
 int tt_plan_trace(const tt_step_plan* plan, char* buf, uint64_t cap, uint64_t* len) {
   return ttb::guarded([&] {
     need(plan, "plan");

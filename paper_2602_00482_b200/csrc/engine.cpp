@@ -81,6 +81,8 @@ Engine::Engine(const tt_model_config& cfg, int device) : cfg_(cfg), device_(devi
   if (d_ > 8192) throw std::invalid_argument("engine: d_model must be <= 8192");
   ck(cudaSetDevice(device_), "cudaSetDevice");
   ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  ck(cudaEventCreateWithFlags(&step_done_, cudaEventDisableTiming), "cudaEventCreate");
 
   // ---- weights (bf16), device layout
   const size_t n_w = V_ * d_ + L_ * (3 * d_ * d_ + d_ * d_ + 2 * d_ * F_) + d_ * V_;
@@ -165,6 +167,9 @@ Engine::~Engine() {
   if (loss_host_) cudaFreeHost(loss_host_);
   if (meta_host_) cudaFreeHost(meta_host_);
   cudaStreamDestroy(stream_);
+  cudaStreamSynchronize(copy_stream_);
+  cudaStreamDestroy(copy_stream_);
+  cudaEventDestroy(step_done_);
 }
 
 void Engine::set_option(const std::string& key, int64_t value) {
@@ -1177,11 +1182,25 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
   const auto t_mem = now();
   for (auto& b : batches) build_meta(b, cursor, host);
   const auto t_meta = now();
-  DevBuf& mbuf = transient ? meta_ : plan->meta;
-  plan->meta_bytes = upload_staged(host, mbuf);
-  plan->meta_ptr = mbuf.as<char>();
+  if (transient) {
+    plan->meta_bytes = upload_staged(host, meta_);
+    plan->meta_ptr = meta_.as<char>();
+    ck(cudaStreamSynchronize(stream_), "plan upload");
+  } else {
+    // the plan's own pinned staging + the copy stream: no synchronisation with a step in flight
+    plan->meta.ensure(std::max(host.size(), kAlign));
+    plan->meta_bytes = host.size();
+    plan->meta_ptr = plan->meta.as<char>();
+    if (!host.empty()) {
+      ck(cudaMallocHost(&plan->meta_host, host.size()), "cudaMallocHost plan meta");
+      std::memcpy(plan->meta_host, host.data(), host.size());
+      ck(cudaMemcpyAsync(plan->meta.p, plan->meta_host, host.size(), cudaMemcpyHostToDevice, copy_stream_),
+         "plan meta upload");
+    }
+    ck(cudaEventCreateWithFlags(&plan->uploaded, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(plan->uploaded, copy_stream_), "plan upload event");
+  }
   res.h2d_bytes = plan->meta_bytes;
-  ck(cudaStreamSynchronize(stream_), "plan upload");
   if (timing) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     std::fprintf(stderr, "prepare: schedule %.1f ms, memory plan %.1f ms, metadata %.1f ms, upload %.1f ms (%zu B)\n",
@@ -1191,11 +1210,31 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
 }
 
 tt_step_result Engine::execute(StepPlan& plan) {
+  execute_async(plan);
+  return wait(plan);
+}
+
+void Engine::execute_async(StepPlan& plan) {
   if (plan.owner != this) throw std::invalid_argument("plan_execute: the plan was prepared by another engine");
+  if (inflight_) throw std::runtime_error("plan_execute: another step is still in flight on this engine");
   if (!seg_stack_.empty()) throw std::runtime_error("tree_train_step: segment stack is not empty");
+  issue_step(plan);
+  ck(cudaEventRecord(step_done_, stream_), "step event");
+  inflight_ = &plan;
+}
+
+tt_step_result Engine::wait(StepPlan& plan) {
+  if (inflight_ != &plan) throw std::invalid_argument("plan_wait: this plan has no step in flight");
+  inflight_ = nullptr;
+  ck(cudaEventSynchronize(step_done_), "tree_train_step");
+  return finish_step(plan);
+}
+
+void Engine::issue_step(StepPlan& plan) {
   ensure_capacity(plan.rows, plan.arena_peak, plan.max_n, plan.max_loss);
+  if (plan.uploaded) ck(cudaStreamWaitEvent(stream_, plan.uploaded, 0), "plan upload wait");
   cur_meta_ = plan.meta_ptr;
-  const uint64_t launches0 = launches_;
+  step_launches0_ = launches_;
   // First execution eager (sets kernel attributes, proves the plan); from the second one on, the
   // whole op list is one CUDA graph (re-captured if any device buffer was reallocated since).
   const bool use_graph = cuda_graph_ && !profiling_ && plan.warmed;
@@ -1231,11 +1270,13 @@ tt_step_result Engine::execute(StepPlan& plan) {
   }
   ck(cudaGetLastError(), "tree_train_step launch");
   ck(cudaMemcpyAsync(loss_host_, loss_.p, sizeof(double), cudaMemcpyDeviceToHost, stream_), "loss download");
-  ck(cudaStreamSynchronize(stream_), "tree_train_step");
+}
+
+tt_step_result Engine::finish_step(StepPlan& plan) {
   collect_profile();
   tt_step_result res = plan.counters;
   res.total_loss = *loss_host_;
-  res.num_launches = launches_ - launches0;
+  res.num_launches = launches_ - step_launches0_;
   res.d2h_bytes = sizeof(double);
   res.peak_hbm_bytes = wbuf_.bytes + gainbuf_.bytes + pe_.bytes + grads_.bytes + kst_.bytes + vst_.bytes +
                        dkst_.bytes + dvst_.bytes + plan.arena_peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +

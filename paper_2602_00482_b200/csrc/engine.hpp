@@ -98,11 +98,21 @@ struct StepPlan {
   cudaGraphExec_t graph = nullptr;
   uint64_t graph_gen = 0, graph_launches = 0, graph_opts = 0;
   const void* owner = nullptr;  // the Engine that prepared the plan (its buffers are baked in)
+  // persistent plans: metadata staged in the plan's own pinned buffer and copied on the engine's copy
+  // stream (no host synchronisation, so a plan can be prepared while another step executes); the
+  // first execute orders itself after the copy through this event
+  void* meta_host = nullptr;
+  cudaEvent_t uploaded = nullptr;
   StepPlan() = default;
   StepPlan(const StepPlan&) = delete;
   StepPlan& operator=(const StepPlan&) = delete;
   ~StepPlan() {
     if (graph) cudaGraphExecDestroy(graph);
+    if (uploaded) {
+      cudaEventSynchronize(uploaded);
+      cudaEventDestroy(uploaded);
+    }
+    if (meta_host) cudaFreeHost(meta_host);
   }
 };
 
@@ -153,6 +163,11 @@ class Engine {
   // engine-owned buffer reused across steps instead of a fresh allocation per plan
   std::unique_ptr<StepPlan> prepare(const PrefixTree& tree, const tt_sched_config& sc, bool transient = false);
   tt_step_result execute(StepPlan& plan);
+  // Asynchronous form: enqueue the step and return; wait() blocks for it and returns the result.
+  // One step in flight per engine; prepare() of the next plan may run meanwhile (its metadata goes
+  // over the copy stream), which is how a training loop overlaps host planning with the device step.
+  void execute_async(StepPlan& plan);
+  tt_step_result wait(StepPlan& plan);
 
   void set_profiling(bool on) { profiling_ = on; }
   void set_option(const std::string& key, int64_t value);
@@ -212,12 +227,18 @@ class Engine {
   cudaEvent_t event();
   void collect_profile();
   size_t upload_staged(const std::vector<char>& host, DevBuf& dst);
+  void issue_step(StepPlan& plan);       // enqueue one step of a prepared plan (graph or eager)
+  tt_step_result finish_step(StepPlan& plan);  // wait for it; loss, counters, non-finite check
 
   tt_model_config cfg_;
   int device_ = 0;
   int64_t V_, d_, H_, L_, F_, dh_;
   uint64_t n_params_ = 0;
   cudaStream_t stream_ = nullptr;
+  cudaStream_t copy_stream_ = nullptr;  // metadata uploads of persistent plans
+  cudaEvent_t step_done_ = nullptr;     // end of the step in flight (execute_async / wait)
+  const StepPlan* inflight_ = nullptr;
+  uint64_t step_launches0_ = 0;
 
   // parameters (device layout) and gradients
   DevBuf wbuf_;  // all bf16 weights

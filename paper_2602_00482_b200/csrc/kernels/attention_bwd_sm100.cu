@@ -22,6 +22,13 @@
 #include "gemm.h"
 #include "sm100.cuh"
 
+// Resource experiments (tools/attn_bwd_ab.sh builds; the product and trace builds define none of
+// these): each drops one consumer of shared memory / the tensor pipe to find the binding resource.
+#ifndef TT_EXP_BWD
+#define TT_EXP_BWD 0  // 1 no dS^T smem stores, 2 no dQ drain stores/reduce, 3 no dK MMAs, 4 no dQ MMAs,
+                      // 5 no stats LDS
+#endif
+
 // Pipeline trace (clock64 per event) of the fused dh=64 kernel: compiled only into the separate
 // debug library (make trace -> libtreetrain_b200_trace.so, -DTT_TRACE=1); the product build has none.
 #ifndef TT_TRACE
@@ -636,9 +643,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   uint64_t* dp_free = dp_full + 1;  // softmax has loaded dP^T_i
   uint64_t* ds_free = dp_free + 1;  // [2] dK_i / dQ_i done: dS^T tile i % 2 may be rewritten
   uint64_t* dq_full = ds_free + 2;  // [2] dQ_i in TMEM
-  uint64_t* dq_free = dq_full + 2;  // [2] dQ_i read out of S^T buffer i % 2
-  uint64_t* p_used = dq_free + 2;   // [2] dV_i done: P^T_i in S^T buffer i % 2 consumed
-  uint64_t* acc_done = p_used + 2;
+  uint64_t* dq_free = dq_full + 2;  // [2] dQ_i read out: S^T buffer i % 2 may take S^T_{i+2}
+  uint64_t* acc_done = dq_free + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_done + 1);
   float* stat = reinterpret_cast<float*>(smem + C::kOffStat);
 
@@ -669,7 +675,6 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       mbar_init(&p_full[s], kSmxWarps);
       mbar_init(&dq_full[s], 1);
       mbar_init(&dq_free[s], 4);
-      mbar_init(&p_used[s], 1);
       mbar_init(&ds_free[s], 1);
     }
     mbar_init(dp_full, 1);
@@ -707,10 +712,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       if (lane == 0) TT_TR(1, kTrBlocksLast);
       for (int i = 0; i < nq; ++i) {
         const int st = i % NS;
-        if (i >= 2) {
-          mbar_wait(&dq_free[i & 1], ((i - 2) >> 1) & 1);
-          mbar_wait(&p_used[i & 1], ((i - 2) >> 1) & 1);
-        }
+        if (i >= 2) mbar_wait(&dq_free[i & 1], ((i - 2) >> 1) & 1);
         mbar_wait(&q_full[st], (i / NS) & 1);
         tc_fence_after();
         const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
@@ -747,24 +749,24 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
           const int st = i % NS;
           const uint32_t q_off = C::kOffQ + st * C::kQBytes, do_off = C::kOffDO + st * C::kQBytes;
           const uint32_t ds_off = (i & 1) * C::kDSBytes;
-          // S^T buffer i % 2 after the softmax: P^T (bf16 pairs) of queries 0-63 in columns [0, 32) and
-          // of queries 64-127 in [96, 128) (each softmax half packs into columns it has loaded itself),
-          // dQ_i into [32, 96). dQ_i first (its drain overlaps dV_i / dK_i), dV_i next: S^T_{i+2} needs
-          // both dQ_i drained and P^T_i consumed — the loop-carried dependency of the pipeline.
-#pragma unroll
-          for (int k = 0; k < C::BKV / 16; ++k)  // 16 keys per step
-            umma_bf16_ss(t_S + (i & 1) * 128 + 32, sdesc_add(dsm, ds_off + k * 2048), sdesc_add(dmn, k * 2048), C::kIdescQ,
-                         k > 0);
-          umma_commit(&dq_full[i & 1]);
+          // dV_i (reads P^T_i from S^T buffer i % 2), then dQ_i (into the same buffer): the dq_full
+          // commit covers both, so once dQ_i is drained the buffer is free for S^T_{i+2} — the
+          // loop-carried dependency of the pipeline; dK_i runs behind it, during the drain
 #pragma unroll
           for (int k = 0; k < BQ / 16; ++k)  // 16 queries per step
-            umma_bf16_ts(t_dV, t_S + (i & 1) * 128 + (k < 4 ? 8 * k : 96 + 8 * (k - 4)),
-                         sdesc_add(dmn, do_off + k * 2048), C::kIdescKV, (i > 0 || k > 0));
-          umma_commit(&p_used[i & 1]);
+            umma_bf16_ts(t_dV, t_S + (i & 1) * 128 + 8 * k, sdesc_add(dmn, do_off + k * 2048), C::kIdescKV,
+                         (i > 0 || k > 0));
+#pragma unroll
+          for (int k = 0; k < C::BKV / 16; ++k)  // 16 keys per step
+            if (TT_EXP_BWD != 4)
+              umma_bf16_ss(t_S + (i & 1) * 128 + 64, sdesc_add(dsm, ds_off + k * 2048), sdesc_add(dmn, k * 2048),
+                           C::kIdescQ, k > 0);
+          umma_commit(&dq_full[i & 1]);
 #pragma unroll
           for (int k = 0; k < BQ / 16; ++k)
-            umma_bf16_ss(t_dK, sdesc_add(dsk, ds_off + (k / 4) * 16384 + (k % 4) * 32), sdesc_add(dmn, q_off + k * 2048),
-                         C::kIdescKV, (i > 0 || k > 0));
+            if (TT_EXP_BWD != 3)
+              umma_bf16_ss(t_dK, sdesc_add(dsk, ds_off + (k / 4) * 16384 + (k % 4) * 32),
+                           sdesc_add(dmn, q_off + k * 2048), C::kIdescKV, (i > 0 || k > 0));
           umma_commit(&q_empty[st]);
           umma_commit(&ds_free[i & 1]);
           if (i == nq - 1) umma_commit(acc_done);
@@ -786,7 +788,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t t[16];
-        tmem_ld16(t_S + (i & 1) * 128 + 32 + 16 * c + lane_off, t);
+        tmem_ld16(t_S + (i & 1) * 128 + 64 + 16 * c + lane_off, t);
 #pragma unroll
         for (int e = 0; e < 16; ++e) r[16 * c + e] = t[e];
       }
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&dq_free[i & 1]);
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
+      for (int cc = 0; cc < (TT_EXP_BWD == 2 ? 0 : 2); ++cc) {
         if (lane == 0) bulk_wait_read0();  // the previous reduce has read the staging buffer
         __syncwarp();
 #pragma unroll
@@ -844,8 +846,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       fetch(i + 1);
       // visibility: invalid keys see nothing; own rows: key kt sees query t iff kt <= t, i.e. block
       // columns >= kt - (q0 - seg_off) (queries beyond q_hi have lse2 = +inf -> P = 0)
-      const int vis0 = own ? kt - (q0 - seg_off) : 0;  // first visible block column of this key
-      const bool need_mask = __any_sync(0xffffffff, !key_ok || vis0 - 64 * half > 0);
+      const int lo0 = key_ok ? (own ? kt - (q0 - seg_off) - 64 * half : 0) : 64;
+      const bool need_mask = __any_sync(0xffffffff, lo0 > 0);
       mbar_wait(&s_full[i & 1], (i >> 1) & 1);
       mbar_wait(dp_full, i & 1);
       tc_fence_after();
@@ -853,16 +855,13 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       const uint32_t sbuf = t_S + (i & 1) * 128;
 #pragma unroll
       for (int sub = 0; sub < 2; ++sub) {
-        // half 0 takes its columns [0, 32) then [32, 64); half 1 takes [96, 128) then [64, 96), so each
-        // packs its P^T into columns it has already loaded itself: [0, 32) and [96, 128)
-        const int col0 = 64 * half + 32 * (sub ^ half);
         float sv[32], dp[32];
         {
           uint32_t r[16], r2[16], r3[16], r4[16];
-          tmem_ld16(sbuf + col0 + lane_off, r);
-          tmem_ld16(sbuf + col0 + 16 + lane_off, r2);
-          tmem_ld16(t_dP + col0 + lane_off, r3);
-          tmem_ld16(t_dP + col0 + 16 + lane_off, r4);
+          tmem_ld16(sbuf + 64 * half + 32 * sub + lane_off, r);
+          tmem_ld16(sbuf + 64 * half + 32 * sub + 16 + lane_off, r2);
+          tmem_ld16(t_dP + 64 * half + 32 * sub + lane_off, r3);
+          tmem_ld16(t_dP + 64 * half + 32 * sub + 16 + lane_off, r4);
           tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -877,19 +876,21 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(dp_free);  // dP^T_i in registers: dP^T_{i+1} may overwrite it
+          // half 0 has now loaded S^T columns [32, 64): half 1 may pack its P^T over them
+          if (half == 0) named_bar_arrive(2 + qd, 64);
         }
         if (need_mask) {
-          const int lo = key_ok ? vis0 - col0 : 32;
+          const int lo = lo0 - 32 * sub;
 #pragma unroll
           for (int c = 0; c < 32; ++c) sv[c] = c >= lo ? sv[c] : -INFINITY;
         }
-        const float* lz_base = st_lse + col0;
-        const float* dz_base = st_nd + col0;
+        const float* lz_base = st_lse + 64 * half + 32 * sub;
+        const float* dz_base = st_nd + 64 * half + 32 * sub;
         uint32_t wp[16], wd[16];
 #pragma unroll
         for (int c = 0; c < 32; c += 4) {
-          const float4 lz = *reinterpret_cast<const float4*>(lz_base + c);
-          const float4 dz = *reinterpret_cast<const float4*>(dz_base + c);
+          const float4 lz = TT_EXP_BWD == 5 ? make_float4(nl, nl, nd, nd) : *reinterpret_cast<const float4*>(lz_base + c);
+          const float4 dz = TT_EXP_BWD == 5 ? make_float4(nd, nl, nd, nl) : *reinterpret_cast<const float4*>(dz_base + c);
           const float2 c22 = make_float2(c2, c2), sc2 = make_float2(sc, sc);
           const float2 xa = __ffma2_rn(make_float2(sv[c], sv[c + 1]), c22, make_float2(-lz.x, -lz.y));
           const float2 xb = __ffma2_rn(make_float2(sv[c + 2], sv[c + 3]), c22, make_float2(-lz.z, -lz.w));
@@ -902,18 +903,21 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
           wd[c / 2] = pack_bf16x2(da.x, da.y);
           wd[c / 2 + 1] = pack_bf16x2(db.x, db.y);
         }
-        // P^T (bf16 pairs): query q < 64 -> column q / 2, q >= 64 -> column 96 + (q - 64) / 2 of the
-        // S^T_i buffer, i.e. into the 16 columns [col0 / 2 ..) of half 0 / [96 + (col0 - 64) / 2 ..) of
-        // half 1, both inside the columns this warp loaded in its first sub-step (no cross-warp wait)
-        tmem_st16(sbuf + (half == 0 ? col0 / 2 : 96 + (col0 - 64) / 2) + lane_off, wp);
+        // P^T (bf16 pairs): query q of the block -> column q / 2 of the S^T_i buffer. Half 0 packs over
+        // its own, already loaded columns; half 1 over half 0's columns [32, 64), once half 0 has
+        // loaded them (pair barrier; half 0 arrives right after its second S^T load)
+        if (half == 1 && sub == 0) {
+          named_bar_sync(2 + qd, 64);
+          tc_fence_after();
+        }
+        tmem_st16(sbuf + 32 * half + 16 * sub + lane_off, wp);
         // dS^T (scaled) -> smem tile i % 2 (once dK_{i-2} / dQ_{i-2} have read it): row krow of query
-        // panel `half`, 16-byte chunks of this sub-step's 32 queries
+        // panel `half`, 16-byte chunks 4 sub .. 4 sub + 3
         if (sub == 0 && i >= 2) mbar_wait(&ds_free[i & 1], ((i - 2) >> 1) & 1);
         uint8_t* ds_row = ds_rows + (i & 1) * C::kDSBytes;
-        const int ch0 = 4 * (sub ^ half);
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          *reinterpret_cast<uint4*>(ds_row + (((ch0 + c) ^ (krow & 7)) * 16)) =
+        for (int c = 0; c < (TT_EXP_BWD == 1 ? 0 : 4); ++c)
+          *reinterpret_cast<uint4*>(ds_row + (((4 * sub + c) ^ (krow & 7)) * 16)) =
               make_uint4(wd[4 * c], wd[4 * c + 1], wd[4 * c + 2], wd[4 * c + 3]);
       }
       tmem_st_wait();

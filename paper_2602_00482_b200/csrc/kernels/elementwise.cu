@@ -208,7 +208,7 @@ void launch_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const
 // rmsnorm_backward for rows of up to 1024 columns, fed by TMA: a persistent block per SM, one producer
 // warp streams each of its rows' gy / x / gres (3 x d fp32) into an NST-deep shared-memory ring with
 // cp.async.bulk (mbarrier complete_tx), eight consumer warps take the rows round-robin (warp w: the
-// block's rows k = w (mod 8)). The ring keeps ~16 rows (~170 KB) in flight per SM independently of the
+// block's rows k = w (mod 8); NST is a multiple of 8, so stage k % NST belongs to warp k % 8). The ring keeps ~16 rows (~170 KB) in flight per SM independently of the
 // consumers' reduce-then-store latency, which is what bounded the register version (one HBM round trip
 // for gy / x, a second for gres, 16 warps per SM: 4.1-4.5 TB/s). gain is held in registers; the
 // gain-gradient partials stay in registers for all of a warp's rows and leave through shared memory +
@@ -336,7 +336,11 @@ void launch_rmsnorm_bwd_tma(const float* gy, const float* x, const float* inv, c
   constexpr int kSmemMax = 227 * 1024;
   const int stage_bytes = (gres ? 3 : 2) * d * 4;
   const int head = ((16 * 32 + d * 4 + 127) / 128) * 128;  // barriers (<= 32 stages) + gsum
-  const int nst = std::min(32, (kSmemMax - head - 1024) / stage_bytes);
+  // stage = k % nst and consumer warp = k % 8 for the block's k-th row: with nst a multiple of 8 every
+  // stage is only ever used by one warp, in order, so no warp can wait on a stage's next phase while
+  // its current one is still pending (a parity wait would then match the phase before)
+  const int nst = std::min(32, (kSmemMax - head - 1024) / stage_bytes) / 8 * 8;
+  if (nst < 8) throw std::invalid_argument("rmsnorm backward: row too wide for the TMA ring");
   const int smem = ((nst * 16 + d * 4 + 127) / 128) * 128 + nst * stage_bytes;
   ensure_smem_attr(reinterpret_cast<const void*>(rmsnorm_bwd_tma_kernel<VPT>), kSmemMax);
   const int blocks = std::min(n, device_sm_count());

@@ -380,3 +380,30 @@ def test_plan_cuda_graph_replay_matches_eager():
     eng.zero_gradients()
     r = plan.execute()
     assert abs(r.total_loss - outs[0][0]) <= 1e-9 * abs(outs[0][0]) and rel(eng.gradients(), outs[0][1]) <= 1e-5
+
+
+def test_plan_execute_async_overlapping_next_plan():
+    # tt_plan_execute_async + tt_plan_wait: while step k runs, the next tree is built and planned
+    # (its metadata goes over the copy stream); every step matches the synchronous execute, and a
+    # second async step cannot be enqueued while one is in flight
+    cfg, flat, eng = make(SMALL, 43)
+    corpora = [O.grouped_corpus(2, 4, 50 + 10 * k, 40, cfg.vocab_size, 44 + k, weight_jitter=True) for k in range(3)]
+    trees = lambda k: tt.build_prefix_tree([tt.TokenSequence(s.seq_id, s.tokens, s.weights) for s in corpora[k]])
+    ref = []
+    for k in range(3):
+        eng.zero_gradients()
+        r = eng.plan(trees(k), tt.SchedulerConfig()).execute()
+        ref.append((r.total_loss, eng.gradients().copy()))
+    plan = eng.plan(trees(0), tt.SchedulerConfig())
+    for k in range(3):
+        eng.zero_gradients()
+        plan.execute_async()
+        with pytest.raises(RuntimeError):
+            plan.execute_async()
+        nxt = eng.plan(trees(k + 1), tt.SchedulerConfig()) if k + 1 < 3 else None
+        r = plan.wait()
+        assert abs(r.total_loss - ref[k][0]) <= 1e-9 * abs(ref[k][0])
+        assert rel(eng.gradients(), ref[k][1]) <= 1e-5
+        plan = nxt
+    with pytest.raises(ValueError):  # nothing in flight
+        eng.plan(trees(0), tt.SchedulerConfig()).wait()

@@ -15,6 +15,8 @@ def main():
     nseg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
     n, S, H, dh = (int(x) for x in sys.argv[2:6]) if len(sys.argv) > 5 else (2048, 1024, 14, 64)
     impl_f = impl_b = 1
+    if os.environ.get("ATTN_LIB"):  # experiment builds (tools/attn_bwd_ab.sh)
+        _native.LIB_PATH = os.path.abspath(os.environ["ATTN_LIB"])
     lib = _native.lib()
     vp = ctypes.c_void_p
     d = H * dh

@@ -394,11 +394,16 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
     for (int64_t q = so; q < end; q += kFwdBlockQ) {
       b.qblk128.insert(b.qblk128.end(), {int32_t(q), int32_t(std::min<int64_t>(q + kFwdBlockQ, end)), int32_t(so), 0});
     }
+    // direct_kv (fused dh = 64 kernel): one item per own key block, so each own dK/dV row has a single
+    // writer that stores it as bf16 into the packed operand (flag 2); else ranges of kQChunkOwn
+    // queries accumulate into the fp32 stack rows (flag 1)
+    const bool direct = b.direct_kv && dh_ == 64;
+    const int64_t qchunk = direct ? std::max<int64_t>(b.seg_len[i], 1) : kQChunkOwn;
     for (int64_t kt = 0; kt < b.seg_len[i]; kt += kBwdBlockKV)
-      for (int64_t q = so + kt; q < end; q += kQChunkOwn) {
+      for (int64_t q = so + kt; q < end; q += qchunk) {
         b.kvit128.insert(b.kvit128.end(), {int32_t(b.row0() + so + kt), int32_t(std::min<int64_t>(kBwdBlockKV, b.seg_len[i] - kt)),
-                                           int32_t(q), int32_t(std::min<int64_t>(q + kQChunkOwn, end))});
-        b.kvit128_2.insert(b.kvit128_2.end(), {int32_t(so), 1});
+                                           int32_t(q), int32_t(std::min<int64_t>(q + qchunk, end))});
+        b.kvit128_2.insert(b.kvit128_2.end(), {int32_t(so), direct ? 2 : 1});
       }
   }
   // tcgen05 dK/dV items of the shared prefix rows: every query of every member attends them fully, so
@@ -849,6 +854,10 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       a.pbase = static_cast<int>(b.pbase);
       a.r0 = static_cast<int>(b.row0());
       a.scale = scale;
+      if (dh_ == 64 && b.direct_kv) {  // own rows' dK / dV straight into the packed operand (bf16)
+        a.dkv16 = dqkv + d;
+        a.lddkv16 = 3 * d;
+      }
       if (dh_ == 64) {
         // fused kernel: dQ partials (one per key block) reduced into the fp32 accumulator
         ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
@@ -865,7 +874,10 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       launches_ += dh_ == 64 ? 1 : 2;  // + the D pre-pass (and the dh = 128 dK/dV kernel)
     }
     // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
-    if (dh_ == 64) {
+    if (dh_ == 64 && b.direct_kv) {
+      tag("k_pack_dq");  // dK / dV are already in the operand; the stack rows were never written
+      run(KC_ELEMWISE, 0, nd * 6, [&] { k_pack_dqkv(dq, nullptr, nullptr, dqkv, n, d, stream_); });
+    } else if (dh_ == 64) {
       tag("k_pack_dqkv");
       run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
     } else {
@@ -1037,6 +1049,7 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
       }
       const int bi = make_batch(run_nodes, S);
       batches[bi].leaf_batch = true;
+      batches[bi].direct_kv = true;
       batches[bi].pbase = pbase;
       batches[bi].R0 = R0;
       ops.push_back({bi, OP_FWD, 0});
@@ -1092,6 +1105,7 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
       } else if (chunk == 0 || static_cast<uint64_t>(len) <= chunk) {
         const int bi = make_batch({c}, S);
         batches[bi].leaf_batch = tree.nodes[c].children.empty();
+        batches[bi].direct_kv = batches[bi].leaf_batch;
         ops.push_back({bi, OP_FWD, 0});
         trace += "PUSH " + std::to_string(pid[c]) + "\n";
         visit(c, S + len);

@@ -69,6 +69,9 @@ struct Batch {
   bool has_acts = true;      // activations kept (false: the pop recomputes them from the stack)
   bool has_loss = false;     // weighted_nll pairs set on the device (tt_segment_loss)
   bool leaf_batch = false;   // childless node(s): K/V not kept for descendants (leaf_kv_skip ledger)
+  // no contribution reaches the batch's own dK/dV rows before its pop (childless, not a chunk of a
+  // chunked node): the attention backward writes their bf16 dK/dV straight into the packed operand
+  bool direct_kv = false;
   int accum_inc = 1;         // GradientStore::accum_count increment (nodes completed by this pop)
 };
 

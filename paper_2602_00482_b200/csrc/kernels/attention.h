@@ -46,6 +46,10 @@ struct AttnBwdArgs {
   // prefix-row (grad_prefix) destination, absolute rows with pitch lddkv; nullptr = dk / dv
   float* dk_pre = nullptr;
   float* dv_pre = nullptr;
+  // dh = 64, items flagged 2 (own rows with a single writer): scaled dK as bf16 into dkv16 [batch row x
+  // lddkv16] at column h * dh, dV at column H * dh + h * dh (the dk / dv blocks of the packed operand)
+  __nv_bfloat16* dkv16 = nullptr;
+  long lddkv16 = 0;
   int n = 0, H = 0, dh = 0, S = 0;
   int pbase = 0, r0 = -1;  // as in AttnFwdArgs (the dK/dV items carry absolute rows already)
   float scale = 1.0f;

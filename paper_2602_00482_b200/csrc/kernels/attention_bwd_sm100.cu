@@ -112,8 +112,11 @@ struct BwdParams {
   int n, S, H;
   int pbase, r0;        // prefix rows [pbase, pbase + S); own rows from r0
   const int4* blocks;   // dq: {q_start, q_end, seg_off, 0}; dkdv: {kv_row0, kv_rows, q_lo, q_hi}
-  const int2* blocks2;  // dkdv: {seg_off, is_own}
+  const int2* blocks2;  // dkdv: {seg_off, is_own}: 0 prefix rows, 1 own rows (red.add), 2 own rows with
+                        // a single writer (fused kernel: bf16 store into kv16)
   float scale, scale_log2;
+  __nv_bfloat16* kv16;  // packed-operand dk block (dv block at + H * 64), batch-local rows, pitch ldkv16
+  long ldkv16;
 };
 
 // Two MMA-issuing warps: warp 1 issues S_j / dP_j, warp 10 issues dQ += dS_j K_j. An mbarrier wait in
@@ -933,13 +936,28 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
     if (warp == 8 && lane == 0) TT_TR(2, kTrBlocksLast);
     float* dkr = (own ? p.dk : p.dk_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
     float* dvr = (own ? p.dv : p.dv_pre) + static_cast<long>(kv0 + krow) * p.lddkv + h * DH;
+    const bool direct = it2.y == 2 && p.kv16 != nullptr;
+    __nv_bfloat16* k16 = direct ? p.kv16 + static_cast<long>(kv0 + krow - p.r0) * p.ldkv16 + h * DH : nullptr;
 #pragma unroll
     for (int c = half * (DH / 2); c < (half + 1) * (DH / 2); c += 16) {
       uint32_t rk[16], rv[16];
       tmem_ld16(t_dK + c + lane_off, rk);
       tmem_ld16(t_dV + c + lane_off, rv);
       tmem_ld_wait();
-      if (key_ok) {
+      if (key_ok && direct) {  // the row's only writer: bf16 straight into the packed operand
+        uint32_t wk[8], wv[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          wk[e] = pack_bf16x2(__uint_as_float(rk[2 * e]), __uint_as_float(rk[2 * e + 1]));  // scale is in dS
+          wv[e] = pack_bf16x2(__uint_as_float(rv[2 * e]), __uint_as_float(rv[2 * e + 1]));
+        }
+        uint4* pk = reinterpret_cast<uint4*>(k16 + c);
+        uint4* pv = reinterpret_cast<uint4*>(k16 + p.H * DH + c);
+        pk[0] = make_uint4(wk[0], wk[1], wk[2], wk[3]);
+        pk[1] = make_uint4(wk[4], wk[5], wk[6], wk[7]);
+        pv[0] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        pv[1] = make_uint4(wv[4], wv[5], wv[6], wv[7]);
+      } else if (key_ok) {
 #pragma unroll
         for (int e = 0; e < 16; e += 4) {
           red_add_v4_f32(dkr + c + e, __uint_as_float(rk[e]), __uint_as_float(rk[e + 1]), __uint_as_float(rk[e + 2]),
@@ -1045,7 +1063,7 @@ void launch_bwd_fused(const AttnBwdArgs& a, long rows_cap, const int4* kv_items,
   make_tmap_f32_sw128(&tdq, a.dq, d, a.n, a.lddq);
   BwdParams p{a.lse, a.D, a.dq, a.lddq, nullptr, 0, a.dk, a.dv, a.lddkv, a.dk_pre ? a.dk_pre : a.dk,
               a.dv_pre ? a.dv_pre : a.dv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, kv_items, kv_items2, a.scale,
-              a.scale * kLog2e};
+              a.scale * kLog2e, a.dkv16, a.lddkv16};
   ensure_smem_attr(reinterpret_cast<const void*>(fa_bwd_fused_kernel<NS>), C::kSmem);
   fa_bwd_fused_kernel<NS><<<dim3(n_kv, a.H), kThreadsFused, C::kSmem, stream>>>(tq, tdo, tk, tv, tdq, p);
 }

@@ -596,9 +596,10 @@ __global__ void pack_dqkv_kernel(const float* __restrict__ dq, float* __restrict
   __nv_bfloat16* orow = out + static_cast<long>(r) * 3 * d;
   for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
     const float4 a = *reinterpret_cast<const float4*>(dq + o + c);
+    *reinterpret_cast<uint2*>(orow + c) = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+    if (dk == nullptr) continue;  // dK / dV written into the operand by the attention backward
     const float4 b = *reinterpret_cast<float4*>(dk + o + c);
     const float4 e = *reinterpret_cast<float4*>(dv + o + c);
-    *reinterpret_cast<uint2*>(orow + c) = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
     *reinterpret_cast<uint2*>(orow + d + c) = make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
     *reinterpret_cast<uint2*>(orow + 2 * d + c) = make_uint2(pack_bf16x2(e.x, e.y), pack_bf16x2(e.z, e.w));
     *reinterpret_cast<float4*>(dk + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);

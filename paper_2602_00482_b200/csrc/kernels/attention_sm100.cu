@@ -437,13 +437,17 @@ void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
 
 }  // namespace
 
-// Forward with 128-query blocks (qblocks built with kFwdBlockQ rows). rows_cap = stack rows. A quarter
-// of the exponentials (one pair in four) run on the FMA pipe (ex2_poly2): +5-8% over MUFU only.
+// Forward with 128-query blocks (qblocks built with kFwdBlockQ rows). rows_cap = stack rows. dh 64: all
+// exponentials on the MUFU (c2 leaf batch: 0.416 ms vs 0.420 / 0.429 with one / two pairs in four on the
+// FMA pipe, tools/attn_fwd_poly_ab.sh; round 1, before the max tree, measured +5-8% for one in four).
 void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
   if (a.nqb == 0) return;
   // dh 64: two softmax warps per lane quadrant (four, with 32 columns each and two S buffers, measured
   // 0.433 vs 0.410 ms on the c2 leaf batch)
-  if (a.dh == 64) return launch_fwd<64, 128, 3, 1, 2>(a, rows_cap, stream);
+#ifndef TT_EXP_FWD_POLY
+#define TT_EXP_FWD_POLY 0  // experiment builds only (tools/attn_fwd_poly_ab.sh)
+#endif
+  if (a.dh == 64) return launch_fwd<64, 128, 3, TT_EXP_FWD_POLY, 2>(a, rows_cap, stream);
   if (a.dh == 128) return launch_fwd<128, 64, 3, 1, 2>(a, rows_cap, stream);
   throw std::invalid_argument("attention: head_dim must be 64 or 128");
 }

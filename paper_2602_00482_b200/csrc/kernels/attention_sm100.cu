@@ -26,6 +26,11 @@
 #ifndef TT_TRACE
 #define TT_TRACE 0
 #endif
+// Resource experiments (tools/attn_fwd_ab.sh builds only; timings, not results): 1 no exponentials
+// (p = x), 2 no P store to TMEM, 3 no PV MMAs, 4 no row max (base 0)
+#ifndef TT_EXP_FWD
+#define TT_EXP_FWD 0
+#endif
 #if TT_TRACE
 // pipeline trace of the forward (debug library only, -DTT_TRACE=1): [cta][block][event] clock64
 constexpr int kFTrCtas = 64, kFTrBlocks = 32, kFTrEv = 8;
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, BKV, NS, SPL>::kThreads, 1)
         for (int k = 0; k < BKV / 16; ++k) {
           constexpr int KPS = BKV / 16 / SPL;  // k-steps per softmax split
           const int hk = k / KPS, kl = k % KPS;  // split owning these keys, k-step within it
+          if (TT_EXP_FWD != 3)
           umma_bf16_ts(tmem_O + hk * DH, tmem_S + (j % NB) * BKV + packed_col<BKV / SPL>(k),
                        sdesc_add(sdesc_add(dVmn, v_off), k * 2048), C::kIdescO, (j > 0 || kl > 0) ? 1u : 0u);
         }
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, BKV, NS, SPL>::kThreads, 1)
 #pragma unroll
         for (int i = 1; i < N2; i += 2) mx = fmax3f(mx, t2[i], i + 1 < N2 ? t2[i + 1] : t2[i]);
       }
-      const float m_new = fmaxf(m_used, mx * c2);
+      const float m_new = TT_EXP_FWD == 4 ? 0.f : fmaxf(m_used, mx * c2);
       if (warp == 2 && lane == 0) TT_FTR(4, j);
       const bool resc = m_new > m_used + kRescaleThreshold;
       float corr = 1.f;
@@ -326,14 +332,14 @@ __global__ void __launch_bounds__(FwdCfg<DH, BKV, NS, SPL>::kThreads, 1)
         for (int e = 0; e < 4; ++e) {
           // paired FP32 (FFMA2 / FADD2): x = s*c - m ; p = 2^x ; row sum += p
           const float2 x = __ffma2_rn(make_float2(s[cch * 8 + 2 * e], s[cch * 8 + 2 * e + 1]), c22, nmb2);
-          const float2 pe = e < POLY ? ex2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          const float2 pe = TT_EXP_FWD == 1 ? x : (e < POLY ? ex2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y)));
           rs2 = __fadd2_rn(rs2, pe);
           w[cch * 4 + e] = pack_bf16x2(pe.x, pe.y);
         }
       }
       if (warp == 2 && lane == 0) TT_FTR(5, j);
 #pragma unroll
-      for (int c = 0; c < HC / 2; c += 16)
+      for (int c = 0; c < (TT_EXP_FWD == 2 ? 0 : HC / 2); c += 16)
         tmem_st16(tmem_S + (j % NB) * BKV + half * HC + c + lane_off, *reinterpret_cast<uint32_t(*)[16]>(&w[c]));
       const float rs = rs2.x + rs2.y;
       l += rs;
@@ -439,13 +445,13 @@ void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
 
 // Forward with 128-query blocks (qblocks built with kFwdBlockQ rows). rows_cap = stack rows. dh 64: all
 // exponentials on the MUFU (c2 leaf batch: 0.416 ms vs 0.420 / 0.429 with one / two pairs in four on the
-// FMA pipe, tools/attn_fwd_poly_ab.sh; round 1, before the max tree, measured +5-8% for one in four).
+// FMA pipe, tools/attn_fwd_ab.sh; round 1, before the max tree, measured +5-8% for one in four).
 void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
   if (a.nqb == 0) return;
   // dh 64: two softmax warps per lane quadrant (four, with 32 columns each and two S buffers, measured
   // 0.433 vs 0.410 ms on the c2 leaf batch)
 #ifndef TT_EXP_FWD_POLY
-#define TT_EXP_FWD_POLY 0  // experiment builds only (tools/attn_fwd_poly_ab.sh)
+#define TT_EXP_FWD_POLY 0  // experiment builds only (tools/attn_fwd_ab.sh)
 #endif
   if (a.dh == 64) return launch_fwd<64, 128, 3, TT_EXP_FWD_POLY, 2>(a, rows_cap, stream);
   if (a.dh == 128) return launch_fwd<128, 64, 3, 1, 2>(a, rows_cap, stream);

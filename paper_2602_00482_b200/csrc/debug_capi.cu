@@ -69,7 +69,6 @@ int tt_debug_rmsnorm_bwd(const float* gy, const float* x, const float* inv, cons
 void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
 void tt_debug_gemm_set_transpose(int mode) { ttb::gemm_set_transpose(mode); }
 
-// clock64 trace of the TT_ATTN_DBG=3 attention dq kernel (timing experiments only)
 static int g_attn_nseg = 1;
 // Timing tools: the n queries of tt_debug_attn form nseg equal sibling segments over the shared prefix
 // (the c2 leaf-batch shape), with the engine's work-item chunking.

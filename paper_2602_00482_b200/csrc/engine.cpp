@@ -188,6 +188,8 @@ void Engine::set_option(const std::string& key, int64_t value) {
     // 1: LM-head GEMM epilogue emits per-32-column softmax statistics, CE reads logits once
     // (default); 0: CE does both passes over the logits row itself
     ce_stats_ = value != 0;
+  } else if (key == "plan_timing") {
+    plan_timing_ = value != 0;
   } else if (key == "logits_bf16") {
     // 1: LM-head logits as bf16 offsets from their 32-column group max (half the logits traffic;
     // needs ce_stats); 0: fp32 logits
@@ -942,7 +944,7 @@ uint64_t Engine::auto_batch_budget(uint64_t path_tokens) const {
 }
 
 std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched_config& sc, bool transient) {
-  static const bool timing = std::getenv("TT_PLAN_TIMING") != nullptr;  // host-phase timing (stderr)
+  const bool timing = plan_timing_;  // option "plan_timing": host-phase timing of prepare() on stderr
   auto now = [] { return std::chrono::steady_clock::now(); };
   const auto t_start = now();
   if (tree.nodes[0].max_path_below > cfg_.max_position)

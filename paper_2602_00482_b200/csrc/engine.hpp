@@ -278,7 +278,8 @@ class Engine {
   bool cuda_graph_ = true;  // replay prepared plans as CUDA graphs (engine option "cuda_graph")
   void issue_ops(const StepPlan& plan);
   bool ce_stats_ = true;
-  bool logits_bf16_ = true;  // LM-head logits stored bf16 relative to the 32-column group max
+  bool logits_bf16_ = true;
+  bool plan_timing_ = false;  // LM-head logits stored bf16 relative to the 32-column group max
   int gemm_2cta_ = 1;
   uint64_t opt_epoch_ = 1;  // bumped by set_option: a plan's CUDA graph is re-captured after a change
   // multi-root batching: consecutive forest roots whose children are all short leaves are pushed as

@@ -1050,7 +1050,10 @@ void launch_bwd_split(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks
 // dh = 64: the fused kernel; dQ partials are reduced into a.dq (fp32 [n x lddq], zeroed by the caller)
 void launch_bwd_fused(const AttnBwdArgs& a, long rows_cap, const int4* kv_items, const int2* kv_items2, int n_kv,
                       cudaStream_t stream) {
-  constexpr int NS = 3;
+#ifndef TT_EXP_BWD_NS
+#define TT_EXP_BWD_NS 3  // Q / dO ring depth (experiment builds may change it)
+#endif
+  constexpr int NS = TT_EXP_BWD_NS;
   using C = FusedCfg<NS>;
   if (n_kv <= 0) return;
   if (!a.dq) throw std::invalid_argument("fused attention backward: needs the fp32 dQ accumulator");

@@ -550,7 +550,7 @@ def main():
     ap.add_argument("--no-flat", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-sibling-batch", action="store_true")
     ap.add_argument("--batch-budget", type=int, default=0)
     ap.add_argument("--prompts", type=int, default=0, help="override the config's prompts per GPU (quick profiling only)")

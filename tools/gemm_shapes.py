@@ -63,6 +63,8 @@ def main():
         lda = a.stride(0)
         ldb = b.stride(0)
         splits = lib.tt_debug_gemm_splits(M, N, K) if epi == EPI_ADD_F32 else 1
+        if os.environ.get("GEMM_SPLITS"):  # split-K sweep of the accumulate shapes
+            splits = int(os.environ["GEMM_SPLITS"]) if epi == EPI_ADD_F32 else 1
 
         def run():
             rc = lib.tt_debug_gemm_async(vp(a.data_ptr()), lda, amn, vp(b.data_ptr()), ldb, bmn, M, N, K, epi,

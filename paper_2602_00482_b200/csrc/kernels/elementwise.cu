@@ -205,14 +205,17 @@ void launch_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const
   rmsnorm_bwd_kernel<VPT, WPR><<<blocks, 256, d * sizeof(float), s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
 }
 
-// rmsnorm_backward for rows of up to 1024 columns, fed by TMA: a persistent block per SM, one producer
-// warp streams each of its rows' gy / x / gres (3 x d fp32) into an NST-deep shared-memory ring with
-// cp.async.bulk (mbarrier complete_tx), eight consumer warps take the rows round-robin (warp w: the
-// block's rows k = w (mod 8); NST is a multiple of 8, so stage k % NST belongs to warp k % 8). The ring keeps ~16 rows (~170 KB) in flight per SM independently of the
-// consumers' reduce-then-store latency, which is what bounded the register version (one HBM round trip
-// for gy / x, a second for gres, 16 warps per SM: 4.1-4.5 TB/s). gain is held in registers; the
-// gain-gradient partials stay in registers for all of a warp's rows and leave through shared memory +
-// one red.global.add.v4 per column group.
+// rmsnorm_backward fed by TMA (rows up to 4096 columns): a persistent block per SM, one producer warp
+// streams each of its rows' gy / x / gres (3 x d fp32) into an NST-deep shared-memory ring with
+// cp.async.bulk (mbarrier complete_tx), NCW consumer warps take the rows round-robin (warp w: the
+// block's rows k = w (mod NCW); NST is a multiple of NCW, so stage k % NST belongs to warp k % NCW and
+// is used in order — no warp can wait on a stage's next phase while its current one is pending). The
+// ring keeps ~170 KB of rows in flight per SM independently of the consumers' reduce-then-store
+// latency, which is what bounded the register version (one HBM round trip for gy / x, a second for
+// gres, 16 warps per SM: 4.1-4.5 TB/s). Each consumer reads its row from shared memory twice (dot
+// product, then outputs) instead of holding it in registers; the gain sits in registers (VPT <= 16) or
+// in shared memory (GS, wider rows); the gain-gradient partials stay in registers for all of a warp's
+// rows and leave through shared memory + one red.global.add.v4 per column group.
 __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(smem_dst)),
@@ -220,20 +223,21 @@ __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, ui
                : "memory");
 }
 
-constexpr int kNormTmaThreads = 288;  // 8 consumer warps + 1 producer warp
+constexpr int kNormTmaThreads = 288;  // up to 8 consumer warps + 1 producer warp (warp 8)
 
-template <int VPT>
+template <int VPT, bool GS>
 __global__ void __launch_bounds__(kNormTmaThreads, 1)
     rmsnorm_bwd_tma_kernel(const float* __restrict__ gy, const float* __restrict__ x, const float* __restrict__ inv,
                            const float* __restrict__ gain, const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
-                           float* __restrict__ ggain, int n, int d, int nst) {
+                           float* __restrict__ ggain, int n, int d, int nst, int ncw) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  const int nb = gres ? 3 : 2;              // row buffers per stage
+  const int nb = gres ? 3 : 2;  // row buffers per stage
   const int row_bytes = d * 4;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + nst;
   float* gsum = reinterpret_cast<float*>(empty + nst);  // [d]
-  uint8_t* ring = smem_raw + ((nst * 16 + d * 4 + 127) / 128) * 128;
+  float* gsm = gsum + d;                                 // [d] gain copy (GS)
+  uint8_t* ring = smem_raw + ((nst * 16 + 2 * d * 4 + 127) / 128) * 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int i = 0; i < nst; ++i) {
@@ -242,7 +246,10 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
     }
     fence_barrier_init();
   }
-  for (int c = threadIdx.x; c < d; c += blockDim.x) gsum[c] = 0.f;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    gsum[c] = 0.f;
+    if (GS) gsm[c] = gain[c];
+  }
   __syncthreads();
   const int rows_mine = n > static_cast<int>(blockIdx.x) ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (warp == 8) {
@@ -258,15 +265,19 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
         if (gres) bulk_load_1d(b + 2 * row_bytes, gres + r * d, row_bytes, &full[st]);
       }
     }
-  } else {
-    float4 g[VPT], gacc[VPT];
+  } else if (warp < ncw) {
+    float4 g[GS ? 1 : VPT], gacc[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int c = (lane + 32 * k) * 4;
-      g[k] = c < d ? __ldg(reinterpret_cast<const float4*>(gain + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if constexpr (!GS) g[k] = c < d ? __ldg(reinterpret_cast<const float4*>(gain + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
       gacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (int k = warp; k < rows_mine; k += 8) {
+    auto gain4 = [&](int q, int c) {
+      if constexpr (GS) return *reinterpret_cast<const float4*>(gsm + c);
+      else return g[q];
+    };
+    for (int k = warp; k < rows_mine; k += ncw) {
       const int st = k % nst;
       const long r = blockIdx.x + static_cast<long>(k) * gridDim.x;
       const float iv = inv[r];  // issued before the wait: its latency overlaps the ring
@@ -274,16 +285,15 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
       const float* sgy = reinterpret_cast<const float*>(ring + static_cast<long>(st) * nb * row_bytes);
       const float* sx = sgy + d;
       const float* sres = sgy + 2 * d;
-      float4 av[VPT], bv[VPT];
       float dot = 0.f;
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
         const int c = (lane + 32 * q) * 4;
         if (c < d) {
-          av[q] = *reinterpret_cast<const float4*>(sgy + c);
-          bv[q] = *reinterpret_cast<const float4*>(sx + c);
-          dot += av[q].x * g[q].x * bv[q].x + av[q].y * g[q].y * bv[q].y + av[q].z * g[q].z * bv[q].z +
-                 av[q].w * g[q].w * bv[q].w;
+          const float4 a = *reinterpret_cast<const float4*>(sgy + c);
+          const float4 b = *reinterpret_cast<const float4*>(sx + c);
+          const float4 gq = gain4(q, c);
+          dot += a.x * gq.x * b.x + a.y * gq.y * b.y + a.z * gq.z * b.z + a.w * gq.w * b.w;
         }
       }
       dot = warp_sum(dot);
@@ -294,12 +304,14 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
       for (int q = 0; q < VPT; ++q) {
         const int c = (lane + 32 * q) * 4;
         if (c < d) {
-          const float4 a = av[q], b = bv[q];
+          const float4 a = *reinterpret_cast<const float4*>(sgy + c);
+          const float4 b = *reinterpret_cast<const float4*>(sx + c);
+          const float4 gq = gain4(q, c);
           float4 res = gres ? *reinterpret_cast<const float4*>(sres + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          res.x += a.x * g[q].x * iv - b.x * scale;
-          res.y += a.y * g[q].y * iv - b.y * scale;
-          res.z += a.z * g[q].z * iv - b.z * scale;
-          res.w += a.w * g[q].w * iv - b.w * scale;
+          res.x += a.x * gq.x * iv - b.x * scale;
+          res.y += a.y * gq.y * iv - b.y * scale;
+          res.z += a.z * gq.z * iv - b.z * scale;
+          res.w += a.w * gq.w * iv - b.w * scale;
           __stcs(reinterpret_cast<float4*>(gxr + c), res);
           uint2 pb;
           pb.x = pack_bf16x2(res.x, res.y);
@@ -330,21 +342,22 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
     red_add_v4_f32(ggain + c, gsum[c], gsum[c + 1], gsum[c + 2], gsum[c + 3]);
 }
 
-template <int VPT>
+template <int VPT, bool GS>
 void launch_rmsnorm_bwd_tma(const float* gy, const float* x, const float* inv, const float* gain, const float* gres,
                             float* gx, __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
   constexpr int kSmemMax = 227 * 1024;
   const int stage_bytes = (gres ? 3 : 2) * d * 4;
-  const int head = ((16 * 32 + d * 4 + 127) / 128) * 128;  // barriers (<= 32 stages) + gsum
-  // stage = k % nst and consumer warp = k % 8 for the block's k-th row: with nst a multiple of 8 every
-  // stage is only ever used by one warp, in order, so no warp can wait on a stage's next phase while
-  // its current one is still pending (a parity wait would then match the phase before)
-  const int nst = std::min(32, (kSmemMax - head - 1024) / stage_bytes) / 8 * 8;
-  if (nst < 8) throw std::invalid_argument("rmsnorm backward: row too wide for the TMA ring");
-  const int smem = ((nst * 16 + d * 4 + 127) / 128) * 128 + nst * stage_bytes;
-  ensure_smem_attr(reinterpret_cast<const void*>(rmsnorm_bwd_tma_kernel<VPT>), kSmemMax);
+  const int head = ((16 * 32 + 2 * d * 4 + 127) / 128) * 128;  // barriers (<= 32 stages) + gsum + gain copy
+  const int fit = std::min(32, (kSmemMax - head - 1024) / stage_bytes);
+  // consumer warps: 8 when 8 stages fit, else 4 / 2 (stage k % nst must belong to warp k % ncw)
+  const int ncw = fit >= 8 ? 8 : (fit >= 4 ? 4 : 2);
+  const int nst = fit / ncw * ncw;
+  if (nst < 2) throw std::invalid_argument("rmsnorm backward: row too wide for the TMA ring");
+  const int smem = ((nst * 16 + 2 * d * 4 + 127) / 128) * 128 + nst * stage_bytes;
+  ensure_smem_attr(reinterpret_cast<const void*>(rmsnorm_bwd_tma_kernel<VPT, GS>), kSmemMax);
   const int blocks = std::min(n, device_sm_count());
-  rmsnorm_bwd_tma_kernel<VPT><<<blocks, kNormTmaThreads, smem, s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, nst);
+  rmsnorm_bwd_tma_kernel<VPT, GS><<<blocks, kNormTmaThreads, smem, s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d,
+                                                                        nst, ncw);
 }
 
 // Weighted NLL over one vocab row with several (target, weight) pairs (weighted_nll,
@@ -701,10 +714,12 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
   if (n <= 0) return;
   const int vpt = (d + 127) / 128;  // float4 column groups per lane with one warp per row
   // (two warps per row at d = 896 measured 3.6 vs 4.2 TB/s: one warp per row up to 7 float4 per lane)
-  // d <= 1024 with 16-byte rows: the TMA-fed persistent kernel; wider rows: several warps per row
-  if (d % 4 == 0 && vpt <= 2) launch_rmsnorm_bwd_tma<2>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else if (d % 4 == 0 && vpt <= 4) launch_rmsnorm_bwd_tma<4>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
-  else if (d % 4 == 0 && vpt <= 8) launch_rmsnorm_bwd_tma<8>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  // d <= 4096 with 16-byte rows: the TMA-fed persistent kernel; wider rows: several warps per row
+  if (d % 4 == 0 && vpt <= 2) launch_rmsnorm_bwd_tma<2, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (d % 4 == 0 && vpt <= 4) launch_rmsnorm_bwd_tma<4, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (d % 4 == 0 && vpt <= 8) launch_rmsnorm_bwd_tma<8, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (d % 4 == 0 && vpt <= 16) launch_rmsnorm_bwd_tma<16, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (d % 4 == 0 && vpt <= 32) launch_rmsnorm_bwd_tma<32, true>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else if (vpt <= 2) launch_rmsnorm_bwd<2, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else if (vpt <= 4) launch_rmsnorm_bwd<4, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else if (vpt <= 7) launch_rmsnorm_bwd<7, 1>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);

@@ -452,13 +452,13 @@ def run_b200(args):
     # ncu-measured DRAM traffic of the dominant GEMM launch (the LM-head logits GEMM), committed under
     # profiles/ (the live run cannot be profiled without perturbing the timing)
     traffic, traffic_note = None, None
-    tpath = os.path.join(ROOT, "profiles", "r1", "ncu_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r2", "ncu_traffic.json")
     if os.path.exists(tpath) and args.config == "c2":
         tj = json.load(open(tpath))
         kname, kv = next((k, v) for k, v in tj["kernels"].items() if k.startswith("gemm LM-head"))
         traffic = kv["dram_bytes"]
         traffic_note = (f"{kname}: {kv['dram_bytes'] / 1e9:.3f} GB DRAM per launch vs "
-                        f"{kv['algorithmic_bytes'] / 1e9:.3f} GB algorithmic (profiles/r1/ncu_traffic.json)")
+                        f"{kv['algorithmic_bytes'] / 1e9:.3f} GB algorithmic (profiles/r2/ncu_traffic.json)")
     line = {
         "metric": METRIC, "value": value, "unit": "rollout tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -29,7 +29,8 @@ int debug_gemm(bool sync, const void* a, long lda, int a_mn, const void* b, long
     e.out[2] = out2;
     e.ldo[0] = e.ldo[1] = e.ldo[2] = ldo;
     e.out2 = out_act;
-    e.ldo2 = mode == ttb::EPI_STORE_F32_STATS ? (N + 31) / 32 : ldo;  // stats: float2 per 32-column group
+    e.ldo2 = (mode == ttb::EPI_STORE_F32_STATS || mode == ttb::EPI_STORE_BF16_STATS) ? (N + 31) / 32
+                                                                                   : ldo;  // stats: float2 per 32-column group
     e.aux = static_cast<const __nv_bfloat16*>(aux);
     e.ld_aux = ldo;
     e.resid = static_cast<const float*>(aux);  // EPI_RESID_F32: aux is the fp32 residual input

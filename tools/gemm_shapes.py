@@ -11,6 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_00482_b200 import _native  # noqa: E402
 
 EPI_STORE_BF16, EPI_STORE_F32, EPI_ADD_F32, EPI_SILU, EPI_DSILU, EPI_RESID, EPI_STATS = range(7)
+EPI_BF16_STATS = 8
 n, d, F, V = 32768, 896, 4864, 151936
 SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
     ("fwd qkv", n, 3 * d, d, 0, 1, EPI_STORE_BF16),
@@ -21,6 +22,7 @@ SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
     ("fwd head", 2048, V, d, 0, 1, EPI_STORE_F32),
     ("fwd head stats", 2304, V, d, 0, 1, EPI_STATS),
     ("fwd head stats c2", 6656, V, d, 0, 1, EPI_STATS),  # the c2 LM-head chunk (6 GB scratch budget)
+    ("fwd head bf16 c2", 6656, V, d, 0, 1, EPI_BF16_STATS),  # the same with bf16 logits (the engine's default)
     ("dX mlp_out", n, F, d, 0, 0, EPI_DSILU),
     ("dX mlp_out plain", n, F, d, 0, 0, EPI_STORE_BF16),  # same shape without the SiLU' operand
     ("dX mlp_in", n, d, F, 0, 0, EPI_STORE_F32),

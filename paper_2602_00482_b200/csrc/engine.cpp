@@ -169,6 +169,11 @@ Engine::~Engine() {
   cudaStreamDestroy(stream_);
   cudaStreamSynchronize(copy_stream_);
   cudaStreamDestroy(copy_stream_);
+  for (int i = 0; i < 2; ++i) {
+    if (pin_ev_[i]) cudaEventDestroy(pin_ev_[i]);
+    if (pin_ring_[i]) cudaFreeHost(pin_ring_[i]);
+  }
+  for (auto& b : meta_pool_) cudaFree(b.first);
   cudaEventDestroy(step_done_);
 }
 
@@ -1203,15 +1208,39 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
     plan->meta_ptr = meta_.as<char>();
     ck(cudaStreamSynchronize(stream_), "plan upload");
   } else {
-    // the plan's own pinned staging + the copy stream: no synchronisation with a step in flight
-    plan->meta.ensure(std::max(host.size(), kAlign));
+    // pinned staging ring + the copy stream + a pooled device buffer: no synchronisation with a step
+    // in flight and no per-plan pinning / cudaMalloc
+    const size_t need = std::max(host.size(), kAlign);
+    size_t best = meta_pool_.size();
+    for (size_t i = 0; i < meta_pool_.size(); ++i)
+      if (meta_pool_[i].second >= need && (best == meta_pool_.size() || meta_pool_[i].second < meta_pool_[best].second))
+        best = i;
+    if (best < meta_pool_.size()) {
+      plan->meta_dev = meta_pool_[best].first;
+      plan->meta_dev_bytes = meta_pool_[best].second;
+      meta_pool_.erase(meta_pool_.begin() + static_cast<long>(best));
+    } else {
+      ck(cudaMalloc(&plan->meta_dev, need), "cudaMalloc plan meta");
+      plan->meta_dev_bytes = need;
+    }
+    plan->release_meta = [this](void* p, size_t n) { retire_meta(p, n); };
     plan->meta_bytes = host.size();
-    plan->meta_ptr = plan->meta.as<char>();
+    plan->meta_ptr = static_cast<const char*>(plan->meta_dev);
     if (!host.empty()) {
-      ck(cudaMallocHost(&plan->meta_host, host.size()), "cudaMallocHost plan meta");
-      std::memcpy(plan->meta_host, host.data(), host.size());
-      ck(cudaMemcpyAsync(plan->meta.p, plan->meta_host, host.size(), cudaMemcpyHostToDevice, copy_stream_),
+      const int slot = pin_next_;
+      pin_next_ ^= 1;
+      if (pin_ev_[slot]) ck(cudaEventSynchronize(pin_ev_[slot]), "staging slot");  // its last upload is done
+      if (host.size() > pin_cap_[slot]) {
+        if (pin_ring_[slot]) cudaFreeHost(pin_ring_[slot]);
+        pin_ring_[slot] = nullptr;
+        ck(cudaMallocHost(&pin_ring_[slot], host.size()), "cudaMallocHost plan meta");
+        pin_cap_[slot] = host.size();
+      }
+      std::memcpy(pin_ring_[slot], host.data(), host.size());
+      ck(cudaMemcpyAsync(plan->meta_dev, pin_ring_[slot], host.size(), cudaMemcpyHostToDevice, copy_stream_),
          "plan meta upload");
+      if (!pin_ev_[slot]) ck(cudaEventCreateWithFlags(&pin_ev_[slot], cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventRecord(pin_ev_[slot], copy_stream_), "staging event");
     }
     ck(cudaEventCreateWithFlags(&plan->uploaded, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventRecord(plan->uploaded, copy_stream_), "plan upload event");
@@ -1223,6 +1252,17 @@ std::unique_ptr<StepPlan> Engine::prepare(const PrefixTree& tree, const tt_sched
                  ms(t_start, t_sched), ms(t_sched, t_mem), ms(t_mem, t_meta), ms(t_meta, now()), plan->meta_bytes);
   }
   return plan;
+}
+
+// A destroyed plan's device metadata buffer: back to the pool (at most 4 kept), unless a step of that
+// plan may still be reading it.
+void Engine::retire_meta(void* p, size_t n) {
+  if (inflight_) cudaEventSynchronize(step_done_);
+  meta_pool_.emplace_back(p, n);
+  if (meta_pool_.size() > 4) {
+    cudaFree(meta_pool_.front().first);
+    meta_pool_.erase(meta_pool_.begin());
+  }
 }
 
 tt_step_result Engine::execute(StepPlan& plan) {
@@ -1297,7 +1337,7 @@ tt_step_result Engine::finish_step(StepPlan& plan) {
   res.peak_hbm_bytes = wbuf_.bytes + gainbuf_.bytes + pe_.bytes + grads_.bytes + kst_.bytes + vst_.bytes +
                        dkst_.bytes + dvst_.bytes + plan.arena_peak + sc_gx_.bytes + sc_gxb_.bytes + sc_gxf_.bytes +
                        sc_gn_.bytes + sc_gh_.bytes + sc_dO_.bytes + sc_D_.bytes + sc_dq_.bytes + sc_dqkv_.bytes +
-                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + plan.meta.bytes +
+                       sc_nfl_.bytes + sc_logits_.bytes + sc_dlog_.bytes + sc_gnf_.bytes + plan.meta_dev_bytes +
                        meta_.bytes;
   arena_peak_ = std::max(arena_peak_, plan.arena_peak);
   if (!std::isfinite(res.total_loss)) throw NonFiniteError("tree_train_step: non-finite loss");

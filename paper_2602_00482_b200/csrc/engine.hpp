@@ -14,6 +14,7 @@
 
 #include <cstdint>
 #include <map>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -91,8 +92,7 @@ struct StepPlan {
   std::vector<PlanOp> ops;  // DFS order
   int64_t rows = 0, max_n = 0, max_loss = 0;
   size_t arena_peak = 0;
-  DevBuf meta;
-  const char* meta_ptr = nullptr;  // device metadata (meta, or the engine's step buffer if transient)
+  const char* meta_ptr = nullptr;  // device metadata (meta_dev, or the engine's step buffer if transient)
   size_t meta_bytes = 0;
   tt_step_result counters{};
   std::string trace;  // logical DFS trace of the executed schedule
@@ -101,10 +101,13 @@ struct StepPlan {
   cudaGraphExec_t graph = nullptr;
   uint64_t graph_gen = 0, graph_launches = 0, graph_opts = 0;
   const void* owner = nullptr;  // the Engine that prepared the plan (its buffers are baked in)
-  // persistent plans: metadata staged in the plan's own pinned buffer and copied on the engine's copy
-  // stream (no host synchronisation, so a plan can be prepared while another step executes); the
-  // first execute orders itself after the copy through this event
-  void* meta_host = nullptr;
+  // persistent plans: metadata copied on the engine's copy stream from a pinned staging ring (no host
+  // synchronisation, so a plan can be prepared while another step executes) into a device buffer
+  // that returns to the engine's pool when the plan is destroyed (no cudaMalloc / cudaFree per step);
+  // the first execute orders itself after the copy through `uploaded`
+  void* meta_dev = nullptr;
+  size_t meta_dev_bytes = 0;
+  std::function<void(void*, size_t)> release_meta;
   cudaEvent_t uploaded = nullptr;
   StepPlan() = default;
   StepPlan(const StepPlan&) = delete;
@@ -115,7 +118,7 @@ struct StepPlan {
       cudaEventSynchronize(uploaded);
       cudaEventDestroy(uploaded);
     }
-    if (meta_host) cudaFreeHost(meta_host);
+    if (meta_dev && release_meta) release_meta(meta_dev, meta_dev_bytes);
   }
 };
 
@@ -171,6 +174,7 @@ class Engine {
   // over the copy stream), which is how a training loop overlaps host planning with the device step.
   void execute_async(StepPlan& plan);
   tt_step_result wait(StepPlan& plan);
+  void retire_meta(void* p, size_t n);
 
   void set_profiling(bool on) { profiling_ = on; }
   void set_option(const std::string& key, int64_t value);
@@ -239,6 +243,13 @@ class Engine {
   uint64_t n_params_ = 0;
   cudaStream_t stream_ = nullptr;
   cudaStream_t copy_stream_ = nullptr;  // metadata uploads of persistent plans
+  // pinned staging ring of the persistent plans' metadata (2 slots: the plan being prepared and the
+  // one executing) and the pool of retired plans' device metadata buffers
+  void* pin_ring_[2] = {nullptr, nullptr};
+  size_t pin_cap_[2] = {0, 0};
+  cudaEvent_t pin_ev_[2] = {nullptr, nullptr};
+  int pin_next_ = 0;
+  std::vector<std::pair<void*, size_t>> meta_pool_;
   cudaEvent_t step_done_ = nullptr;     // end of the step in flight (execute_async / wait)
   const StepPlan* inflight_ = nullptr;
   uint64_t step_launches0_ = 0;

@@ -401,10 +401,10 @@ void Engine::build_meta(Batch& b, size_t& cursor, std::vector<char>& host) {
     for (int64_t q = so; q < end; q += kFwdBlockQ) {
       b.qblk128.insert(b.qblk128.end(), {int32_t(q), int32_t(std::min<int64_t>(q + kFwdBlockQ, end)), int32_t(so), 0});
     }
-    // direct_kv (fused dh = 64 kernel): one item per own key block, so each own dK/dV row has a single
+    // direct_kv (fused kernels): one item per own key block, so each own dK/dV row has a single
     // writer that stores it as bf16 into the packed operand (flag 2); else ranges of kQChunkOwn
     // queries accumulate into the fp32 stack rows (flag 1)
-    const bool direct = b.direct_kv && dh_ == 64;
+    const bool direct = b.direct_kv;
     const int64_t qchunk = direct ? std::max<int64_t>(b.seg_len[i], 1) : kQChunkOwn;
     for (int64_t kt = 0; kt < b.seg_len[i]; kt += kBwdBlockKV)
       for (int64_t q = so + kt; q < end; q += qchunk) {
@@ -861,35 +861,27 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       a.pbase = static_cast<int>(b.pbase);
       a.r0 = static_cast<int>(b.row0());
       a.scale = scale;
-      if (dh_ == 64 && b.direct_kv) {  // own rows' dK / dV straight into the packed operand (bf16)
+      if (b.direct_kv) {  // own rows' dK / dV straight into the packed operand (bf16)
         a.dkv16 = dqkv + d;
         a.lddkv16 = 3 * d;
       }
-      if (dh_ == 64) {
-        // fused kernel: dQ partials (one per key block) reduced into the fp32 accumulator
-        ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
-      } else {
-        a.dq16 = dqkv;  // dQ straight into the q block of the packed [dq | dk | dv] operand
-        a.lddq16 = 3 * d;
-      }
+      // fused kernels (dh 64 and 128): dQ partials (one per key block) reduced into the fp32 accumulator
+      ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
       tag("attn_bwd_sm100");
       run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
         attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_qblk128), static_cast<int>(b.qblk128.size() / 4),
                        meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2), static_cast<int>(b.kvit128.size() / 4),
                        stream_);
       });
-      launches_ += dh_ == 64 ? 1 : 2;  // + the D pre-pass (and the dh = 128 dK/dV kernel)
+      launches_ += 1;  // + the D pre-pass
     }
     // pop: consume this batch's dK/dV rows (children + own contributions), zero them for reuse
-    if (dh_ == 64 && b.direct_kv) {
+    if (b.direct_kv) {
       tag("k_pack_dq");  // dK / dV are already in the operand; the stack rows were never written
       run(KC_ELEMWISE, 0, nd * 6, [&] { k_pack_dqkv(dq, nullptr, nullptr, dqkv, n, d, stream_); });
-    } else if (dh_ == 64) {
+    } else {
       tag("k_pack_dqkv");
       run(KC_ELEMWISE, 0, nd * 26, [&] { k_pack_dqkv(dq, dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
-    } else {
-      tag("k_pack_dkv");
-      run(KC_ELEMWISE, 0, nd * 20, [&] { k_pack_dkv(dK + b.row0() * d_, dV + b.row0() * d_, dqkv, n, d, stream_); });
     }
     {  // dW_{q,k,v} += normed1^T [dq | dk | dv]  (model.hpp:610-612)
       EpiParams e;

@@ -869,9 +869,8 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
       ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
       tag("attn_bwd_sm100");
       run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
-        attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_qblk128), static_cast<int>(b.qblk128.size() / 4),
-                       meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2), static_cast<int>(b.kvit128.size() / 4),
-                       stream_);
+        attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2),
+                       static_cast<int>(b.kvit128.size() / 4), stream_);
       });
       launches_ += 1;  // + the D pre-pass
     }

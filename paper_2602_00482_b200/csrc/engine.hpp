@@ -56,7 +56,7 @@ struct Batch {
   std::vector<int64_t> seg_off, seg_len;
   // host-built metadata (uploaded once per step)
   std::vector<int32_t> tokens, positions;
-  std::vector<int32_t> qblk128;  // int4 per 128-row query block (forward; dh = 128 dQ kernel)
+  std::vector<int32_t> qblk128;  // int4 per 128-row query block (forward)
   std::vector<int32_t> kvit128, kvit128_2;  // 128-row stack blocks {kv_row0, rows, q_lo, q_hi} / {seg_off, own}
   std::vector<int32_t> loss_rows, pair_off, pair_tgt;
   std::vector<double> pair_w;

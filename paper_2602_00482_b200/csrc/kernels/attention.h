@@ -34,19 +34,15 @@ struct AttnBwdArgs {
   long ldkv = 0;
   const float* lse = nullptr;  // [H x n]
   float* D = nullptr;          // [H x n] scratch: rowsum(dO * O)
-  float* dq = nullptr;         // [n x lddq] fp32, accumulated
+  float* dq = nullptr;         // [n x lddq] fp32, accumulated (zeroed by the caller)
   long lddq = 0;
-  // tcgen05 path: when set, dQ (scaled) goes straight to bf16 [n x lddq16] (the q block of the
-  // packed dqkv operand) instead of fp32 dq
-  __nv_bfloat16* dq16 = nullptr;
-  long lddq16 = 0;
   float* dk = nullptr;  // fp32 dK/dV stack rows (absolute), accumulated
   float* dv = nullptr;
   long lddkv = 0;
   // prefix-row (grad_prefix) destination, absolute rows with pitch lddkv; nullptr = dk / dv
   float* dk_pre = nullptr;
   float* dv_pre = nullptr;
-  // dh = 64, items flagged 2 (own rows with a single writer): scaled dK as bf16 into dkv16 [batch row x
+  // items flagged 2 (own rows with a single writer): scaled dK as bf16 into dkv16 [batch row x
   // lddkv16] at column h * dh, dV at column H * dh + h * dh (the dk / dv blocks of the packed operand)
   __nv_bfloat16* dkv16 = nullptr;
   long lddkv16 = 0;
@@ -65,13 +61,12 @@ void attn_fwd_sm100(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream);
 
 // D = rowsum(dO * O) per (head, row) (the softmax-backward correction term).
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream);
-// tcgen05 backward (attention_bwd_sm100.cu): dq_blocks are 128-row query blocks (like the forward);
-// kv_items/kv_items2 are 128-row stack blocks {kv_row0, kv_rows, q_lo, q_hi} / {seg_off, is_own}.
-// dk/dv are accumulated (red.add) into the fp32 stack rows (prefix rows into dk_pre/dv_pre when set).
-// dQ (scaled): dh = 64 ADDS into the fp32 accumulator dq [n x lddq] (zeroed by the caller); dh = 128
-// writes bf16 dq16 [n x lddq16].
+// tcgen05 backward (attention_bwd_sm100.cu, one fused kernel per head size): kv_items/kv_items2 are
+// 128-row stack blocks {kv_row0, kv_rows, q_lo, q_hi} / {seg_off, 0 prefix | 1 own | 2 own, single
+// writer}. dk/dv are accumulated (red.add) into the fp32 stack rows (prefix rows into dk_pre/dv_pre
+// when set; flag-2 rows as bf16 into dkv16). dQ (scaled) is ADDED into the fp32 accumulator dq.
 constexpr int kBwdBlockKV = 128;
-void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* dq_blocks, int n_dq, const int4* kv_items,
-                    const int2* kv_items2, int n_kv, cudaStream_t stream);
+void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* kv_items, const int2* kv_items2, int n_kv,
+                    cudaStream_t stream);
 
 }  // namespace ttb

@@ -24,10 +24,13 @@ timeout 300 $NCU -k regex:fa_fwd -s 2 -c 1 -o $O/${T}_attn_fwd python tools/attn
   > $O/${T}_ncu_attn.log 2>&1
 timeout 300 $NCU -k regex:fa_bwd -s 2 -c 1 -o $O/${T}_attn_bwd python tools/attn_bench.py 16 32768 1024 14 64 \
   >> $O/${T}_ncu_attn.log 2>&1
+# dh 128 (c3-like: 4 sibling segments of 2048 queries over a 2048-row prefix, 12 heads)
+timeout 300 $NCU -k regex:fa_bwd -s 2 -c 1 -o $O/${T}_attn_bwd128 python tools/attn_bench.py 4 8192 2048 12 128 \
+  >> $O/${T}_ncu_attn.log 2>&1
 fi
 if [ "$W" = all ] || [ "$W" = hbm ]; then
-for k in rmsnorm_bwd rmsnorm_fwd pack_dqkv pack_dkv embed_grad ce_kernel attn_bwd_pre; do
-  timeout 400 $NCU -k regex:$k -s 2 -c 2 -o $O/${T}_hbm_$k python bench.py --prompts 1 --steps 1 --warmup 1 \
+for k in rmsnorm_bwd rmsnorm_fwd pack_dqkv embed_grad ce_bf16_kernel attn_bwd_pre; do
+  timeout 400 $NCU -k regex:$k -s 40 -c 1 -o $O/${T}_hbm_$k python bench.py --prompts 1 --steps 1 --warmup 1 \
     --no-flat --no-cpu --no-e2e >> $O/${T}_ncu_hbm.log 2>&1
 done
 fi

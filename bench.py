@@ -157,35 +157,54 @@ def tree_nodes_of(seqs):
 
 
 class ClockSampler(threading.Thread):
+    """SM clock + clock-event reasons every 100 ms during the timed region (NVML). NVML is opened
+    before the thread starts and the first sample is taken at once, so short timed regions (c1 runs
+    in ~15 ms) still carry at least one sample; result() adds a closing sample."""
+
     def __init__(self, dev):
         super().__init__(daemon=True)
         self.dev, self.samples, self.reasons, self.stop_evt = dev, [], set(), threading.Event()
-        self.max_mhz = None
-
-    def run(self):
+        self.max_mhz, self.nv, self.h = None, None, None
         try:
             import pynvml as nv
 
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.dev)
-            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            names = {getattr(nv, k): k for k in dir(nv) if k.startswith("nvmlClocksEventReason") or k.startswith("nvmlClocksThrottleReason")}
+            self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            self.names = {getattr(nv, k): k for k in dir(nv)
+                          if k.startswith("nvmlClocksEventReason") or k.startswith("nvmlClocksThrottleReason")}
+        except Exception as e:  # pragma: no cover - reported, not fatal
+            self.reasons.add(f"sampler-error:{type(e).__name__}")
+
+    def sample(self):
+        nv, h = self.nv, self.h
+        self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        for bit, name in self.names.items():
+            if isinstance(bit, int) and bit and bit not in (0xFFFFFFFFFFFFFFFF,) and (r & bit) == bit and bit & (bit - 1) == 0:
+                self.reasons.add(name.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", ""))
+
+    def run(self):
+        if self.nv is None:
+            return
+        try:
             while not self.stop_evt.is_set():
-                self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                try:
-                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                except Exception:
-                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                for bit, name in names.items():
-                    if isinstance(bit, int) and bit and bit not in (0xFFFFFFFFFFFFFFFF,) and (r & bit) == bit and bit & (bit - 1) == 0:
-                        self.reasons.add(name.replace("nvmlClocksEventReason", "").replace("nvmlClocksThrottleReason", ""))
-                time.sleep(0.1)
+                self.sample()
+                self.stop_evt.wait(0.1)
         except Exception as e:  # pragma: no cover - reported, not fatal
             self.reasons.add(f"sampler-error:{type(e).__name__}")
 
     def result(self):
         self.stop_evt.set()
         self.join(timeout=2)
+        if self.nv is not None and len(self.samples) < 2:
+            try:
+                self.sample()
+            except Exception as e:  # pragma: no cover
+                self.reasons.add(f"sampler-error:{type(e).__name__}")
         med = statistics.median(self.samples) if self.samples else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 

@@ -123,16 +123,18 @@ __device__ __forceinline__ void tmem_dealloc_cg(uint32_t taddr, uint32_t ncols) 
   else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
 }
 
-__device__ __forceinline__ float fast_sigmoid(float u) {
-  // sigmoid(u) = 0.5 tanh(u/2) + 0.5: one MUFU op (tanh.approx, max rel err ~2^-11 < bf16 ulp)
-  float t;
-  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * u));
-  return fmaf(0.5f, t, 0.5f);
+// sigmoid(u) = 0.5 tanh(u/2) + 0.5 on a pair: one MUFU op per element (tanh.approx, max rel err ~2^-11
+// < bf16 ulp), the affine parts on FMUL2 / FFMA2
+__device__ __forceinline__ float2 fast_sigmoid2(float2 u) {
+  const float2 hu = __fmul2_rn(u, make_float2(0.5f, 0.5f));
+  float2 t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t.x) : "f"(hu.x));
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t.y) : "f"(hu.y));
+  return __ffma2_rn(t, make_float2(0.5f, 0.5f), make_float2(0.5f, 0.5f));
 }
-__device__ __forceinline__ float silu_f(float u) { return u * fast_sigmoid(u); }
-__device__ __forceinline__ float silu_grad_f(float u) {
-  const float s = fast_sigmoid(u);
-  return s * (1.0f + u * (1.0f - s));
+// bf16 pair (lo = element 0) -> two floats, exact
+__device__ __forceinline__ float2 unpack_bf16x2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
 // ---- epilogue helpers (one thread = one accumulator row; 32 columns per call)
@@ -200,7 +202,11 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
   const float alpha = epi.alpha;
   float v[32];
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * alpha;
+  for (int i = 0; i < 32; i += 2) {
+    const float2 a = __fmul2_rn(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), make_float2(alpha, alpha));
+    v[i] = a.x;
+    v[i + 1] = a.y;
+  }
   switch (epi.mode) {
     case EPI_STORE_F32_STATS:
     case EPI_STORE_BF16_STATS: {
@@ -268,45 +274,62 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
             make_uint4(pack_bf16x2(v[8 * u], v[8 * u + 1]), pack_bf16x2(v[8 * u + 2], v[8 * u + 3]),
                        pack_bf16x2(v[8 * u + 4], v[8 * u + 5]), pack_bf16x2(v[8 * u + 6], v[8 * u + 7]));
       break;
-    case EPI_SILU: {  // h (bf16) -> buf, silu(h) (bf16) -> buf + 2048 (model.hpp:443-444)
+    case EPI_SILU:  // h (bf16) -> buf, silu(h) (bf16) -> buf + 2048 (model.hpp:443-444)
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        float h[8];
+        // h rounded to bf16 once, silu of the rounded value; pairs on FMUL2 / FFMA2
+        uint32_t hw[4], sw[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) h[i] = __bfloat162float(__float2bfloat16_rn(v[8 * u + i]));
-#if defined(TT_EXP_SILU_NOMUFU)  // experiment builds only (tools/gemm_epilogue_ab.sh)
-        *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) =
-            make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]), pack_bf16x2(h[6], h[7]));
-        *reinterpret_cast<uint4*>(buf + 2048 + sw64_off(lane, u)) =
-            make_uint4(pack_bf16x2(h[1], h[0]), pack_bf16x2(h[3], h[2]), pack_bf16x2(h[5], h[4]), pack_bf16x2(h[7], h[6]));
-        continue;
-#endif
-        *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) =
-            make_uint4(pack_bf16x2(h[0], h[1]), pack_bf16x2(h[2], h[3]), pack_bf16x2(h[4], h[5]),
-                       pack_bf16x2(h[6], h[7]));
-        *reinterpret_cast<uint4*>(buf + 2048 + sw64_off(lane, u)) =
-            make_uint4(pack_bf16x2(silu_f(h[0]), silu_f(h[1])), pack_bf16x2(silu_f(h[2]), silu_f(h[3])),
-                       pack_bf16x2(silu_f(h[4]), silu_f(h[5])), pack_bf16x2(silu_f(h[6]), silu_f(h[7])));
+        for (int i = 0; i < 4; ++i) {
+          hw[i] = pack_bf16x2(v[8 * u + 2 * i], v[8 * u + 2 * i + 1]);
+          const float2 hh = unpack_bf16x2(hw[i]);
+          const float2 sv = __fmul2_rn(hh, fast_sigmoid2(hh));
+          sw[i] = pack_bf16x2(sv.x, sv.y);
+        }
+        *reinterpret_cast<uint4*>(buf + sw64_off(lane, u)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(buf + 2048 + sw64_off(lane, u)) = make_uint4(sw[0], sw[1], sw[2], sw[3]);
       }
       break;
-    }
     case EPI_DSILU:  // out = acc * silu'(h) (model.hpp:526-528); h chunk (bf16) already in buf
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         uint4* p = reinterpret_cast<uint4*>(buf + sw64_off(lane, u));
         const uint4 hw = *p;
-        const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hw);
-        float g[8];
+        // silu'(h) = s (1 + h (1 - s)), s = sigmoid(h), on pairs
+        const uint32_t hws[4] = {hw.x, hw.y, hw.z, hw.w};
+        uint32_t gw[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) g[i] = v[8 * u + i] * silu_grad_f(__bfloat162float(hb[i]));
-        *p = make_uint4(pack_bf16x2(g[0], g[1]), pack_bf16x2(g[2], g[3]), pack_bf16x2(g[4], g[5]),
-                        pack_bf16x2(g[6], g[7]));
+        for (int i = 0; i < 4; ++i) {
+          const float2 hh = unpack_bf16x2(hws[i]);
+          const float2 sg = fast_sigmoid2(hh);
+          const float2 oms = __ffma2_rn(sg, make_float2(-1.f, -1.f), make_float2(1.f, 1.f));
+          const float2 gr = __fmul2_rn(sg, __ffma2_rn(hh, oms, make_float2(1.f, 1.f)));
+          const float2 g = __fmul2_rn(make_float2(v[8 * u + 2 * i], v[8 * u + 2 * i + 1]), gr);
+          gw[i] = pack_bf16x2(g.x, g.y);
+        }
+        *p = make_uint4(gw[0], gw[1], gw[2], gw[3]);
       }
       break;
     default:
       break;
   }
 }
+
+#ifndef TT_TRACE
+#define TT_TRACE 0
+#endif
+#if TT_TRACE  // trace build only (make trace; tools/gemm_trace.py): per-warp, per-tile clock64 events
+constexpr int kGtCtas = 4, kGtTiles = 48, kGtEv = 8;
+__device__ long long g_gemm_trace[kGtCtas][kThreads / 32][kGtTiles][kGtEv];
+#define GT_TR(ev, ti)                                                                                       \
+  do {                                                                                                      \
+    if (blockIdx.x < kGtCtas && (ti) < kGtTiles) g_gemm_trace[blockIdx.x][warp][(ti)][(ev)] = clock64();    \
+  } while (0)
+#else
+#define GT_TR(ev, ti) \
+  do {                \
+  } while (0)
+#endif
 
 template <int BN, int CG, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -383,13 +406,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < num_tiles; t += ncl) {
+      int ti = 0;
+      for (int t = cid; t < num_tiles; t += ncl, ++ti) {
         int m_blk, n_blk, kb0, kb1;
         tile_coords(t, m_blk, n_blk, kb0, kb1);
         const int m0 = m_blk * TM + static_cast<int>(rank) * BM;         // this CTA's A rows
         const int n0 = n_blk * BN + static_cast<int>(rank) * C::BNC;     // this CTA's B half
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (kb == kb0) GT_TR(0, ti);
+          if (kb == kb1 - 1) GT_TR(1, ti);
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
           const int k0 = kb * BK;
@@ -441,11 +467,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < num_tiles; t += ncl) {
+    int ti = 0;
+    for (int t = cid; t < num_tiles; t += ncl, ++ti) {
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
+      if (lane == 0) GT_TR(0, ti);
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
+      if (lane == 0) GT_TR(1, ti);
       const uint32_t d_tmem = tmem_base + acc * C::kAccStride;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
@@ -475,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) {
         if constexpr (CG == 1) umma_commit(&tfull_bar[acc]);
         else umma_commit_2cta(&tfull_bar[acc]);
+        GT_TR(2, ti);
       }
       __syncwarp();
       if (++acc == 2) {
@@ -504,11 +534,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // residual epilogue (fp32 operand, 4 KB per chunk): two chunks loaded ahead, one per slot
     const bool two_ahead = need_ld && !whole_tile_ld && C::kSlots == 2;
     uint32_t gc = 0;        // chunks staged by this warp: slot = gc & 1
+    bool pf = false;        // SiLU' operand chunks 0 .. NCH-2 of this tile were prefetched by the last one
     uint32_t ld_phase = 0;  // per-slot parity of the operand-load barriers
     bool ld_ahead = false;  // the current chunk's operand load was issued during the previous chunk
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cid; t < num_tiles; t += ncl) {
+    int ti = 0;
+    for (int t = cid; t < num_tiles; t += ncl, ++ti) {
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       const int row0 = m_blk * TM + static_cast<int>(rank) * BM + quad * 32;  // this warp's first row
@@ -516,17 +548,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto chunk_ok = [&](int c) { return 2 * c + half < NCHT && n_base + 64 * c < N; };
       if (whole_tile_ld) {
         // every chunk's bf16 operand (2 KB) gets its own quarter slot: all loads issued before the
-        // accumulator wait, so their HBM latency hides behind the main loop
+        // accumulator wait (all but the last already at the end of the previous tile, see below)
         if (lane == 0) {
           bulk_wait_read<0>();
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch)
-            if (chunk_ok(ch)) {
+            if ((!pf || ch == NCH - 1) && chunk_ok(ch)) {
               mbar_arrive_expect_tx(&wld[ch], 2048u);
               tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_base + 64 * ch, row0);
             }
         }
         __syncwarp();
+        pf = false;
       } else if (two_ahead) {
         if (lane == 0) {
           bulk_wait_read<0>();
@@ -550,8 +583,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         ld_ahead = true;
       }
+      if (lane == 0) GT_TR(0, ti);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      if (lane == 0) GT_TR(1, ti);
       const uint32_t t_row = tmem_base + acc * C::kAccStride + half * 32 + (static_cast<uint32_t>(quad * 32) << 16);
       uint32_t rr[2][32];
       tmem_ld32(t_row, rr[0]);
@@ -566,15 +601,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           blk = n0 / epi.split_w;
           xc = n0 - blk * epi.split_w;
         }
-        if (active && !ld_ahead && !whole_tile_ld && !two_ahead) {
-          if (lane == 0) bulk_wait_read<C::kSlots - 1>();  // the store that last used this slot has read it
-          __syncwarp();
-          if (need_ld && lane == 0) {
-            mbar_arrive_expect_tx(&wld[slot], ld_bytes);
-            tma_load_2d(&tm_x, &wld[slot], buf, n0, row0);
-          }
-        }
-        ld_ahead = false;
+        // the chunk's accumulator columns first (the last chunk hands the slot back to the MMA warp),
+        // then the staging slot: a slow store drain does not hold the accumulator
         tmem_ld_wait_regs(rr[ch & 1]);
         if (ch + 1 < NCH) {
           tmem_ld32(t_row + (ch + 1) * 64, rr[(ch + 1) & 1]);
@@ -584,8 +612,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
             else mbar_arrive_remote(mapa_shared(smem_u32(&tempty_bar[acc]), 0));  // the leader's slot barrier
+            GT_TR(2, ti);
           }
         }
+        if (active && !ld_ahead && !whole_tile_ld && !two_ahead) {
+          if (lane == 0) bulk_wait_read<C::kSlots - 1>();  // the store that last used this slot has read it
+          __syncwarp();
+          if (need_ld && lane == 0) {
+            mbar_arrive_expect_tx(&wld[slot], ld_bytes);
+            tma_load_2d(&tm_x, &wld[slot], buf, n0, row0);
+          }
+        }
+        ld_ahead = false;
         if (active) {
           if (need_ld) {
             mbar_wait(&wld[slot], (ld_phase >> slot) & 1);
@@ -598,11 +636,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const CUtensorMap* tm = blk == 0 ? &tm_o0 : (blk == 1 ? &tm_o1 : &tm_o2);
             if (mode == EPI_ADD_F32) tma_reduce_add_2d(tm, buf, xc, row0);
             else if (mode == EPI_ADD_F32_T) tma_reduce_add_2d(tm, buf, row0, n0);
+#if defined(TT_EXP_SILU_NOSTORE)  // experiment builds only: the SiLU epilogue computes and stages, stores nothing
+            else if (mode != EPI_SILU) tma_store_2d(tm, buf, xc, row0);
+#else
             else tma_store_2d(tm, buf, xc, row0);
-#if !defined(TT_EXP_SILU_ONESTORE)
+#endif
+#if !defined(TT_EXP_SILU_ONESTORE) && !defined(TT_EXP_SILU_NOSTORE)
             if (mode == EPI_SILU) tma_store_2d(&tm_x, buf + 2048, n0, row0);
 #endif
             bulk_commit();
+            GT_TR(3, ti);  // the tile's last store issued (overwritten per chunk)
           }
           ++gc;
           // operand epilogues (residual / SiLU input): start the next chunk's TMA load now, into the
@@ -629,6 +672,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             ld_ahead = true;
           }
         }
+      }
+      if (whole_tile_ld && NCH >= 2 && t + ncl < num_tiles) {
+        // At K = 896 the main loop is short and this epilogue is the GEMM's critical path, so the next
+        // tile's SiLU' operand must not start loading only when that tile starts: chunks 0 .. NCH-2 load
+        // now, into quarter slots whose stores (all but this tile's last) have been read
+        int m2, n2, k0n, k1n;
+        tile_coords(t + ncl, m2, n2, k0n, k1n);
+        const int row0n = m2 * TM + static_cast<int>(rank) * BM + quad * 32;
+        const int n_basen = n2 * BN + half * 32;
+        if (lane == 0) {
+          if (chunk_ok(NCH - 1)) bulk_wait_read<1>();  // the last group is chunk NCH-1's store
+          else bulk_wait_read<0>();
+#pragma unroll
+          for (int ch = 0; ch < NCH - 1; ++ch)
+            if (2 * ch + half < NCHT && n_basen + 64 * ch < N) {
+              mbar_arrive_expect_tx(&wld[ch], 2048u);
+              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_basen + 64 * ch, row0n);
+            }
+        }
+        __syncwarp();
+        pf = true;
       }
       if (++acc == 2) {
         acc = 0;
@@ -829,6 +893,17 @@ int gemm_pick_bn(int N, bool b_mn_major) {
   }
   return best;
 }
+
+#if TT_TRACE
+extern "C" int tt_debug_gemm_trace_read(long long* out, long n) {
+  const long sz = static_cast<long>(sizeof(g_gemm_trace) / sizeof(long long));
+  return cudaMemcpyFromSymbol(out, g_gemm_trace, (n < sz ? n : sz) * sizeof(long long)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int tt_debug_gemm_trace_clear() {
+  static long long zero[sizeof(g_gemm_trace) / sizeof(long long)];
+  return cudaMemcpyToSymbol(g_gemm_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 void gemm_bf16(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
                cudaStream_t stream) {

@@ -37,6 +37,39 @@ SHAPES = [  # (label, M, N, K, a_mn, b_mn, epi)
 ]
 
 
+class _Sampler:
+    """SM clock (MHz) and board power (W) every 20 ms on a background thread (NVML)."""
+
+    def __init__(self):
+        import threading
+
+        import pynvml as nv
+
+        nv.nvmlInit()
+        self.nv, self.h = nv, nv.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        self.clk, self.pw, self.done = [], [], False
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        import time
+
+        while not self.done:
+            self.clk.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.pw.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1e3)
+            time.sleep(0.02)
+
+    def stop(self):
+        self.done = True
+        self.t.join()
+        k = len(self.clk) // 4  # drop the ramp-up quarter
+        c, w = sorted(self.clk[k:]) or [0], sorted(self.pw[k:]) or [0]
+        self.stats = dict(sm_mhz=c[len(c) // 2], power_w=w[len(w) // 2], samples=len(self.clk))
+
+    def summary(self):
+        return f"  sm {self.stats['sm_mhz']} MHz  {self.stats['power_w']:.0f} W"
+
+
 def main():
     if os.environ.get("GEMM_LIB"):  # experiment builds (tools/gemm_epilogue_ab.sh)
         _native.LIB_PATH = os.path.abspath(os.environ["GEMM_LIB"])
@@ -53,7 +86,7 @@ def main():
         shapes.append(("extra", M_, N_, K_, 0, 1, EPI_STORE_BF16))
         only = only or "extra"
     for label, M, N, K, amn, bmn, epi in shapes:
-        if only and label != only:
+        if only and label not in only.split(","):
             continue
         a = torch.randn(K, M, device="cuda").bfloat16() if amn else torch.randn(M, K, device="cuda").bfloat16()
         b = torch.randn(K, N, device="cuda").bfloat16() if bmn else torch.randn(N, K, device="cuda").bfloat16()
@@ -78,17 +111,25 @@ def main():
             run()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        it = 10
+        # GEMM_ITERS > 10: a sustained run (seconds) with the SM clock and board power sampled, so a
+        # variant's cost under the power cap shows up as clock, not only as time
+        it = int(os.environ.get("GEMM_ITERS", "10"))
+        smp = _Sampler() if it > 10 else None
         e0.record()
         for _ in range(it):
             run()
         e1.record()
         torch.cuda.synchronize()
+        if smp:
+            smp.stop()
         ms = e0.elapsed_time(e1) / it
         tf = 2.0 * M * N * K / (ms / 1e3) / 1e12
         out.append(dict(shape=label, M=M, N=N, K=K, ms=ms, tflops=tf, frac=tf / peaks["bf16_tflops"], splits=splits))
+        clk = smp.summary() if smp else ""
+        if smp:
+            out[-1].update(smp.stats)
         print(f"{label:12s} M={M:6d} N={N:6d} K={K:6d} splits={splits} {ms:8.3f} ms {tf:7.1f} TFLOP/s "
-              f"({100 * tf / peaks['bf16_tflops']:.0f}% of burst peak)", flush=True)
+              f"({100 * tf / peaks['bf16_tflops']:.0f}% of burst peak){clk}", flush=True)
         del a, b, o32, o16, act, aux
     json.dump(out, open(os.environ.get("GEMM_SHAPES_OUT", "gpurun_out/gemm_shapes.json"), "w"), indent=1)
 

@@ -8,11 +8,11 @@
 //   dX = dY W^T    (matrix.hpp:50-62 `matmul_transposed`)  : A K-major,  B K-major
 //   dW += X^T dY   (matrix.hpp:64-77 `accumulate_outer`)   : A MN-major, B MN-major
 //
-// Roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
-// warps 2..9 = epilogue (TMEM -> registers -> fused op -> global; two warps per TMEM lane quadrant
-// split the tile's columns). Smem ring of STAGES {A,B} tiles (128B swizzle); two TMEM accumulator
-// slots so the epilogue of tile i overlaps the main loop of tile i+1. Split-K partials reduce with
-// red.global.add.v4.f32.
+// Roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer, then 8 or 16 epilogue warps
+// (TMEM -> registers -> fused op -> smem -> TMA store; 2 or 4 warps per TMEM lane quadrant split the
+// tile's columns: 16 where the epilogue's per-element work is the critical path, see epi_warps).
+// Smem ring of STAGES {A,B} tiles (128B swizzle); two TMEM accumulator slots so the epilogue of tile
+// i overlaps the main loop of tile i+1. Split-K partials reduce through TMA reduce-add.
 //
 // CG = 2 (M >= 256): a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with
 // tcgen05.mma.cta_group::2 issued by the leader CTA: each CTA stages its own 128 rows of A and HALF
@@ -27,6 +27,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "gemm.h"
 #include "sm100.cuh"
@@ -37,25 +38,31 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quadrant)
-constexpr int kEpiWarps = 8;
+// warp 0 TMA, warp 1 MMA, then EPW = 8 or 16 epilogue warps: EPW / 4 per TMEM lane quadrant, each
+// taking every (EPW / 4)-th 32-column chunk of its quadrant's 32 rows. 16 (at most 96 registers per
+// thread) for the epilogues whose per-element work is the critical path at K = 896 (epi_warps), 8
+// (164 registers, two staging slots per warp) otherwise.
+constexpr int kMaxThreads = 64 + 32 * 16;
+constexpr int threads_of(int epw) { return 64 + 32 * epw; }
 
-template <int BN, int CG>
+template <int BN, int CG, int EPW>
 struct Cfg {
   static constexpr int BNC = BN / CG;  // B rows (K-major) / columns (MN-major) staged per CTA
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BNC * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  // epilogue staging slots per warp: 2 (a store drains while the next chunk is staged), 1 for the
-  // single-CTA 256-wide tile, whose 48 KB operand stages would otherwise drop to 3
-  static constexpr int kSlots = (CG == 1 && BN == 256) ? 1 : 2;
-  static constexpr int kStageBudget = 227 * 1024 - kEpiWarps * kSlots * 4096 - 2048;
+  // epilogue staging slots (4 KB) per warp: 2 with 8 warps (a store drains while the next chunk is
+  // staged), 1 with 16; 1 for the single-CTA 256-wide tile, whose 48 KB operand stages would
+  // otherwise drop to 3
+  static constexpr int kSlots = (EPW == 16 || (CG == 1 && BN == 256)) ? 1 : 2;
+  static constexpr int kStagingBytes = EPW * kSlots * 4096;
+  static constexpr int kStageBudget = 227 * 1024 - kStagingBytes - 2048;
   static constexpr int kStages = kStageBudget / kStageBytes > 8 ? 8 : kStageBudget / kStageBytes;
   static constexpr int kAccStride = BN == 224 ? 256 : BN;  // TMEM columns between the accumulator slots
   static constexpr int kTmemCols = 2 * kAccStride <= 256 ? 256 : 512;  // two slots (power of 2)
   static constexpr int kOffBar = kStages * kStageBytes;
-  static constexpr int kOffStage = kOffBar + 1024;  // epilogue staging: kEpiWarps x kSlots x 4 KB
-  static constexpr int kSmem = kOffStage + kEpiWarps * kSlots * 4096 + 1024 /*align*/;
+  static constexpr int kOffStage = kOffBar + 1024;  // epilogue staging
+  static constexpr int kSmem = kOffStage + kStagingBytes + 1024 /*align*/;
   static_assert(kSmem <= 227 * 1024, "GEMM smem budget");
   static_assert(BNC % 64 == 0 || CG == 1 || BN == 224, "2-CTA MN-major B needs 64-column halves");
 };
@@ -191,6 +198,13 @@ __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.w
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Epilogue warps per CTA: 16 for the epilogues whose per-element work is the GEMM's critical path at
+// K = 896 (SiLU' with its operand load, the LM-head logits with the softmax statistics), 8 otherwise
+// (profiles/r2/gemm_epilogue_ab.txt).
+inline int epi_warps(int mode, int bn, int cg) {
+  return (mode == EPI_DSILU || mode == EPI_STORE_BF16_STATS) && !(cg == 1 && bn == 256) ? 16 : 8;
+}
+
 __device__ __forceinline__ bool epi_f32_out(int mode) {
   return mode == EPI_STORE_F32 || mode == EPI_STORE_F32_STATS || mode == EPI_ADD_F32 || mode == EPI_RESID_F32 ||
          mode == EPI_ADD_F32_T;
@@ -320,24 +334,33 @@ __device__ __forceinline__ void epi_stage(const EpiParams& epi, const uint32_t (
 #endif
 #if TT_TRACE  // trace build only (make trace; tools/gemm_trace.py): per-warp, per-tile clock64 events
 constexpr int kGtCtas = 4, kGtTiles = 48, kGtEv = 8;
-__device__ long long g_gemm_trace[kGtCtas][kThreads / 32][kGtTiles][kGtEv];
+__device__ long long g_gemm_trace[kGtCtas][kMaxThreads / 32][kGtTiles][kGtEv];
 #define GT_TR(ev, ti)                                                                                       \
   do {                                                                                                      \
     if (blockIdx.x < kGtCtas && (ti) < kGtTiles) g_gemm_trace[blockIdx.x][warp][(ti)][(ev)] = clock64();    \
   } while (0)
+#define GT_ADD(ev, ti, v)                                                                                   \
+  do {                                                                                                      \
+    if (blockIdx.x < kGtCtas && (ti) < kGtTiles) g_gemm_trace[blockIdx.x][warp][(ti)][(ev)] += (v);         \
+  } while (0)
+#define GT_CLK() clock64()
 #else
 #define GT_TR(ev, ti) \
   do {                \
   } while (0)
+#define GT_ADD(ev, ti, v) \
+  do {                    \
+  } while (0)
+#define GT_CLK() 0LL
 #endif
 
-template <int BN, int CG, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int CG, bool A_MN, bool B_MN, int EPW>
+__global__ void __launch_bounds__(threads_of(EPW), 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                 const __grid_constant__ CUtensorMap tm_o0, const __grid_constant__ CUtensorMap tm_o1,
                 const __grid_constant__ CUtensorMap tm_o2, const __grid_constant__ CUtensorMap tm_x, int M, int N,
                 int K, int splits, EpiParams epi) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPW>;
   static_assert(!B_MN || CG == 1 || C::BNC % 64 == 0, "BN = 224 pairs need a K-major B (112-row halves)");
   constexpr int TM = BM * CG;  // tile rows (per CTA pair when CG = 2)
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -349,8 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;  // [2]
   uint64_t* tempty_bar = tfull_bar + 2;          // [2]
-  uint64_t* ld_bar = tempty_bar + 2;  // [kEpiWarps][4]: TMA loads of epilogue operands into the slots
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ld_bar + 4 * kEpiWarps);
+  uint64_t* ld_bar = tempty_bar + 2;  // [EPW][4]: TMA loads of epilogue operands into the slots
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ld_bar + 4 * EPW);
 
   const int warp = warp_id_sync();
   const int lane = threadIdx.x & 31;
@@ -370,9 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], kEpiWarps * CG);  // leader: epilogue warps of both CTAs
+      mbar_init(&tempty_bar[s], EPW * CG);  // leader: epilogue warps of both CTAs
     }
-    for (int s = 0; s < 4 * kEpiWarps; ++s) mbar_init(&ld_bar[s], 1);
+    for (int s = 0; s < 4 * EPW; ++s) mbar_init(&ld_bar[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_cg<CG>(tmem_slot, C::kTmemCols);
@@ -516,23 +539,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   mma_done:;
   } else {
     // ------------------------------------------------------------ epilogue
-    // Each warp drains 32 TMEM lanes (rows) x BN/2 columns in 32-column chunks. The TMEM load of
+    // Each warp drains 32 TMEM lanes (rows) x BN/kEG columns in 32-column chunks. The TMEM load of
     // chunk c+1 is in flight while chunk c is staged; the accumulator slot is handed back to the MMA
     // warp as soon as its last chunk is in registers; stores drain asynchronously (TMA).
+    constexpr int EG = EPW / 4;  // epilogue warps per TMEM lane quadrant
+    constexpr int SL = C::kSlots;  // staging slots per warp
     const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-    const int half = (warp - 2) / 4;       // which 32-column chunks of the tile this warp handles
-    constexpr int NCHT = BN / 32;          // chunks per tile; warp half h takes chunks h, h + 2, ...
-    constexpr int NCH = (NCHT + 1) / 2;    // chunk slots per warp (the last may be empty: BN = 224)
+    const int grp = (warp - 2) / 4;        // which 32-column chunks of the tile this warp handles
+    constexpr int NCHT = BN / 32;          // chunks per tile; warp group g takes chunks g, g + EG, ...
+    constexpr int NCH = (NCHT + EG - 1) / EG;  // chunk slots per warp (the last may be empty)
+    constexpr int CS = 32 * EG;           // columns between a warp's consecutive chunks
     const int ew = warp - 2;
-    uint8_t* stg = smem + C::kOffStage + ew * (C::kSlots * 4096);
+    uint8_t* stg = smem + C::kOffStage + ew * (SL * 4096);
     uint64_t* wld = ld_bar + 4 * ew;
     const int mode = epi.mode;
     const bool need_ld = mode == EPI_RESID_F32 || mode == EPI_DSILU;
     const uint32_t ld_bytes = epi_f32_out(mode) ? 4096u : 2048u;
     // SiLU' epilogue (bf16 operand in, bf16 out, in place): all NCH chunks' operands fit in the slots
-    const bool whole_tile_ld = mode == EPI_DSILU && NCH <= 4 && C::kSlots * 4096 >= NCH * 2048;
+    const bool whole_tile_ld = mode == EPI_DSILU && NCH <= 4 && SL * 4096 >= NCH * 2048;
     // residual epilogue (fp32 operand, 4 KB per chunk): two chunks loaded ahead, one per slot
-    const bool two_ahead = need_ld && !whole_tile_ld && C::kSlots == 2;
+    const bool two_ahead = need_ld && !whole_tile_ld && SL == 2;
     uint32_t gc = 0;        // chunks staged by this warp: slot = gc & 1
     bool pf = false;        // SiLU' operand chunks 0 .. NCH-2 of this tile were prefetched by the last one
     uint32_t ld_phase = 0;  // per-slot parity of the operand-load barriers
@@ -544,8 +570,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int m_blk, n_blk, kb0, kb1;
       tile_coords(t, m_blk, n_blk, kb0, kb1);
       const int row0 = m_blk * TM + static_cast<int>(rank) * BM + quad * 32;  // this warp's first row
-      const int n_base = n_blk * BN + half * 32;  // this warp's first chunk; chunk c at n_base + 64 c
-      auto chunk_ok = [&](int c) { return 2 * c + half < NCHT && n_base + 64 * c < N; };
+      const int n_base = n_blk * BN + grp * 32;  // this warp's first chunk; chunk c at n_base + CS c
+      auto chunk_ok = [&](int c) { return EG * c + grp < NCHT && n_base + CS * c < N; };
       if (whole_tile_ld) {
         // every chunk's bf16 operand (2 KB) gets its own quarter slot: all loads issued before the
         // accumulator wait (all but the last already at the end of the previous tile, see below)
@@ -555,7 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ch = 0; ch < NCH; ++ch)
             if ((!pf || ch == NCH - 1) && chunk_ok(ch)) {
               mbar_arrive_expect_tx(&wld[ch], 2048u);
-              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_base + 64 * ch, row0);
+              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_base + CS * ch, row0);
             }
         }
         __syncwarp();
@@ -568,15 +594,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (chunk_ok(k)) {
               const int sl = static_cast<int>((gc + k) & 1);
               mbar_arrive_expect_tx(&wld[sl], ld_bytes);
-              tma_load_2d(&tm_x, &wld[sl], stg + sl * 4096, n_base + 64 * k, row0);
+              tma_load_2d(&tm_x, &wld[sl], stg + sl * 4096, n_base + CS * k, row0);
             }
         }
         __syncwarp();
       } else if (need_ld && !ld_ahead && chunk_ok(0)) {
         // the tile's first epilogue operand chunk loads while its main loop still runs
-        const int slot = C::kSlots == 2 ? static_cast<int>(gc & 1) : 0;
+        const int slot = SL == 2 ? static_cast<int>(gc & 1) : 0;
         if (lane == 0) {
-          bulk_wait_read<C::kSlots - 1>();
+          bulk_wait_read<SL - 1>();
           mbar_arrive_expect_tx(&wld[slot], ld_bytes);
           tma_load_2d(&tm_x, &wld[slot], stg + slot * 4096, n_base, row0);
         }
@@ -587,14 +613,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       if (lane == 0) GT_TR(1, ti);
-      const uint32_t t_row = tmem_base + acc * C::kAccStride + half * 32 + (static_cast<uint32_t>(quad * 32) << 16);
+      const uint32_t t_row = tmem_base + acc * C::kAccStride + grp * 32 + (static_cast<uint32_t>(quad * 32) << 16);
       uint32_t rr[2][32];
       tmem_ld32(t_row, rr[0]);
 #pragma unroll
       for (int ch = 0; ch < NCH; ++ch) {
-        const int n0 = n_base + 64 * ch;
+        const int n0 = n_base + CS * ch;
         const bool active = chunk_ok(ch);  // warp-uniform
-        const int slot = whole_tile_ld ? ch : (C::kSlots == 2 ? static_cast<int>(gc & 1) : 0);
+        const int slot = whole_tile_ld ? ch : (SL == 2 ? static_cast<int>(gc & 1) : 0);
         uint8_t* buf = whole_tile_ld ? stg + ch * 2048 : stg + slot * 4096;
         int blk = 0, xc = n0;
         if (epi.split_w > 0) {
@@ -603,9 +629,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // the chunk's accumulator columns first (the last chunk hands the slot back to the MMA warp),
         // then the staging slot: a slow store drain does not hold the accumulator
+        long long gt0 = GT_CLK();
         tmem_ld_wait_regs(rr[ch & 1]);
+        if (lane == 0) GT_ADD(6, ti, GT_CLK() - gt0);
         if (ch + 1 < NCH) {
-          tmem_ld32(t_row + (ch + 1) * 64, rr[(ch + 1) & 1]);
+          tmem_ld32(t_row + (ch + 1) * CS, rr[(ch + 1) & 1]);
         } else {
           tc_fence_before();
           __syncwarp();
@@ -616,7 +644,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (active && !ld_ahead && !whole_tile_ld && !two_ahead) {
-          if (lane == 0) bulk_wait_read<C::kSlots - 1>();  // the store that last used this slot has read it
+          if (lane == 0) {
+            gt0 = GT_CLK();
+            bulk_wait_read<SL - 1>();  // the store that last used this slot has read it
+            GT_ADD(7, ti, GT_CLK() - gt0);
+          }
           __syncwarp();
           if (need_ld && lane == 0) {
             mbar_arrive_expect_tx(&wld[slot], ld_bytes);
@@ -626,10 +658,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         ld_ahead = false;
         if (active) {
           if (need_ld) {
+            gt0 = GT_CLK();
             mbar_wait(&wld[slot], (ld_phase >> slot) & 1);
             ld_phase ^= 1u << slot;
+            if (lane == 0) GT_ADD(4, ti, GT_CLK() - gt0);
           }
+          gt0 = GT_CLK();
           epi_stage(epi, rr[ch & 1], buf, lane, row0 + lane, M, n0, N);
+          if (lane == 0) GT_ADD(5, ti, GT_CLK() - gt0);
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -657,16 +693,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lane == 0) {
                 bulk_wait_read<0>();
                 mbar_arrive_expect_tx(&wld[ns], ld_bytes);
-                tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 128, row0);
+                tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 2 * CS, row0);
               }
               __syncwarp();
             }
-          } else if (C::kSlots == 2 && need_ld && !whole_tile_ld && ch + 1 < NCH && chunk_ok(ch + 1)) {
+          } else if (SL == 2 && need_ld && !whole_tile_ld && ch + 1 < NCH && chunk_ok(ch + 1)) {
             const int ns = static_cast<int>(gc & 1);
             if (lane == 0) {
               bulk_wait_read<1>();
               mbar_arrive_expect_tx(&wld[ns], ld_bytes);
-              tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + 64, row0);
+              tma_load_2d(&tm_x, &wld[ns], stg + ns * 4096, n0 + CS, row0);
             }
             __syncwarp();
             ld_ahead = true;
@@ -680,15 +716,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         int m2, n2, k0n, k1n;
         tile_coords(t + ncl, m2, n2, k0n, k1n);
         const int row0n = m2 * TM + static_cast<int>(rank) * BM + quad * 32;
-        const int n_basen = n2 * BN + half * 32;
+        const int n_basen = n2 * BN + grp * 32;
         if (lane == 0) {
           if (chunk_ok(NCH - 1)) bulk_wait_read<1>();  // the last group is chunk NCH-1's store
           else bulk_wait_read<0>();
 #pragma unroll
           for (int ch = 0; ch < NCH - 1; ++ch)
-            if (2 * ch + half < NCHT && n_basen + 64 * ch < N) {
+            if (EG * ch + grp < NCHT && n_basen + CS * ch < N) {
               mbar_arrive_expect_tx(&wld[ch], 2048u);
-              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_basen + 64 * ch, row0n);
+              tma_load_2d(&tm_x, &wld[ch], stg + ch * 2048, n_basen + CS * ch, row0n);
             }
         }
         __syncwarp();
@@ -789,16 +825,16 @@ void make_tmap_epi(CUtensorMap* map, const void* ptr, bool f32, uint64_t width, 
     throw std::runtime_error("cuTensorMapEncodeTiled (epilogue) failed (" + std::to_string(int(r)) + ")");
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN>
-void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
-            cudaStream_t stream) {
-  using C = Cfg<BN, CG>;
+template <int BN, int CG, bool A_MN, bool B_MN, int EPW>
+void launch_epw(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
+                cudaStream_t stream) {
+  using C = Cfg<BN, CG, EPW>;
   CUtensorMap ta, tb;
   if (!A_MN) make_tmap_bf16(&ta, A.ptr, K, M, A.ld, 64, BM);
   else make_tmap_bf16(&ta, A.ptr, M, K, A.ld, 64, 64);
   if (!B_MN) make_tmap_bf16(&tb, B.ptr, K, N, B.ld, 64, C::BNC);
   else make_tmap_bf16(&tb, B.ptr, N, K, B.ld, 64, 64);
-  ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<BN, CG, A_MN, B_MN>), C::kSmem);
+  ensure_smem_attr(reinterpret_cast<const void*>(gemm_kernel<BN, CG, A_MN, B_MN, EPW>), C::kSmem);
   const int g_num_sms = device_sm_count();
   const int kb_total = (K + BK - 1) / BK;
   if (splits < 1) splits = 1;
@@ -830,7 +866,7 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   if (e.mode == EPI_RESID_F32) make_tmap_epi(&tx, e.resid, true, N, M, e.ld_resid);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(threads_of(EPW));
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -840,8 +876,18 @@ void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, con
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  check_launch(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN>, ta, tb, to[0], to[1], to[2], tx, M, N, K, splits, e),
+  check_launch(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN, EPW>, ta, tb, to[0], to[1], to[2], tx, M, N, K,
+                                  splits, e),
                "gemm launch");
+}
+
+template <int BN, int CG, bool A_MN, bool B_MN>
+void launch(const GemmOperand& A, const GemmOperand& B, int M, int N, int K, const EpiParams& epi, int splits,
+            cudaStream_t stream) {
+  if constexpr (!(CG == 1 && BN == 256)) {
+    if (epi_warps(epi.mode, BN, CG) == 16) return launch_epw<BN, CG, A_MN, B_MN, 16>(A, B, M, N, K, epi, splits, stream);
+  }
+  launch_epw<BN, CG, A_MN, B_MN, 8>(A, B, M, N, K, epi, splits, stream);
 }
 
 }  // namespace

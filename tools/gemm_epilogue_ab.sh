@@ -14,6 +14,8 @@ OTHERS=$(ls ../../build/csrc_trace/*.o ../../build/csrc_trace/kernels/*.o | grep
 for v in ${EPI_VARIANTS:-ONESTORE NOSTORE}; do
   if [ "$v" = HEAD ]; then  # tools/_ab/gemm_head.cu: an older gemm_sm100.cu (untracked) for a same-box A/B
     nvcc $FL -Ikernels -c ../../tools/_ab/gemm_head.cu -o ../../build/exp/gemm_$v.o
+  elif [ "${v#EPI}" != "$v" ]; then  # EPI8 / EPI16: epilogue warps per CTA
+    nvcc $FL -DTT_GEMM_EPI_WARPS=${v#EPI} -c kernels/gemm_sm100.cu -o ../../build/exp/gemm_$v.o
   else
     nvcc $FL -DTT_EXP_SILU_$v -c kernels/gemm_sm100.cu -o ../../build/exp/gemm_$v.o
   fi

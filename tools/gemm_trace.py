@@ -1,8 +1,10 @@
 """Per-tile pipeline trace of the tcgen05 GEMM (debug library only: make -C paper_2602_00482_b200/csrc
 trace). Runs one GEMM shape of tools/gemm_shapes.py and prints, for the first CTAs, per tile in SM clocks:
   MMA warp (leader):  wait = waiting for a free accumulator slot (the epilogue), main = main loop
-  epilogue (8 warps): tf = waiting for the accumulator, rel = accumulator in -> slot released,
-                      st = accumulator in -> last store issued, sw = cycles in staging-slot waits
+  epilogue (draining warps): tf = waiting for the accumulator, rel = accumulator in -> slot released,
+                      st = accumulator in -> last store issued; summed over the tile's chunks:
+                      opw = operand-load waits, stg = staging (math + smem), tmw = TMEM-load waits,
+                      sw = staging-slot waits (bulk_wait_read)
 Usage: python tools/gemm_trace.py ["fwd mlp_in"]"""
 import ctypes
 import os
@@ -15,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from tools.gemm_shapes import SHAPES, EPI_STORE_F32, EPI_ADD_F32, EPI_RESID, EPI_STATS  # noqa: E402
 
-CT, NW, NT, NE = 4, 10, 48, 8
+CT, NW, NT, NE = 4, 18, 48, 8
 
 
 def main():
@@ -49,13 +51,14 @@ def main():
     lib.tt_debug_gemm_trace_read(buf.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)), ctypes.c_long(buf.size))
     tr = buf.reshape(CT, NW, NT, NE)
     print(f"{label}: M={M} N={N} K={K} epi={epi}")
-    agg = {k: [] for k in ("wait", "main", "tf", "rel", "st", "sw", "period")}
+    agg = {k: [] for k in ("wait", "main", "tf", "rel", "st", "opw", "stg", "tmw", "sw", "period")}
     for c in range(CT):
         print(f"-- CTA {c}")
         mma = tr[c, 1]
         for t in range(NT):
-            e = tr[c, 2:10, t]
-            if e[:, 1].max() == 0:
+            e = tr[c, 2:NW, t]
+            e = e[e[:, 1] != 0]  # the draining epilogue warps of this mode
+            if len(e) == 0:
                 break
             tf = e[:, 1] - e[:, 0]
             rel = e[:, 2] - e[:, 1]
@@ -70,12 +73,14 @@ def main():
                     agg["main"].append(mn)
                     agg["period"].append(per)
             line += (f" | epi tf {int(tf.mean()):6d} rel {int(rel.mean()):6d} (max {int(rel.max()):6d})"
-                     f" st {int(st.mean()):6d} (max {int(st.max()):6d}) sw {int(e[:, 5].mean()):6d}")
+                     f" st {int(st.mean()):6d} (max {int(st.max()):6d}) opw {int(e[:, 4].mean())} stg {int(e[:, 5].mean())}"
+                     f" tmw {int(e[:, 6].mean())} sw {int(e[:, 7].mean())}")
             if t >= 2:
                 agg["tf"].append(tf.mean())
                 agg["rel"].append(rel.max())
                 agg["st"].append(st.max())
-                agg["sw"].append(e[:, 5].mean())
+                for k, j in (("opw", 4), ("stg", 5), ("tmw", 6), ("sw", 7)):
+                    agg[k].append(e[:, j].mean())
             if t < 12:
                 print(line)
     print("median over tiles >= 2: " + "  ".join(f"{k} {int(np.median(v)) if v else 0}" for k, v in agg.items()))

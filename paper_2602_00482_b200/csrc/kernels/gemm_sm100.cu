@@ -909,11 +909,17 @@ bool gemm_use_2cta(int M, int N) {
 }
 
 // 2-CTA tile width: 256 unless its padding waste outweighs the halved per-CTA B traffic
-// 2-CTA tile width from a wave model: time ~ waves x per-tile cost, with a 128-wide pair tile ~25%
-// less efficient per column than a 256-wide one (twice the A re-reads per FLOP, shorter MMAs).
-// Measured (profiles/r1/gemm_shapes_bn2.log): N = 896 at M = 32768 runs 17-22% faster with 256-wide
-// tiles despite 12.5% padding; M = 4864 prefers 128 (76 vs 133 tiles on 74 CTA pairs).
+// 2-CTA tile width from a wave model: time ~ waves x per-tile cost, with a 128-wide pair tile ~60%
+// more expensive per column than a 256-wide one (twice the A re-reads per FLOP, shorter MMAs, half
+// the B staging per CTA). Measured (profiles/r1/gemm_shapes_bn2.log, profiles/r2/gemm_bn2.txt): N = 896
+// at M = 32768 runs 17-22% faster with 256-wide tiles despite 12.5% padding; the c3 QKV weight
+// gradient (1536 x 4608 x 8192) 911 -> 1373 TF/s with 256 (3 waves of 128-wide tiles modelled at
+// 1.25 had picked 128); M = 4864, N = 896 runs the same either way.
+int g_gemm_force_bn2 = 0;  // debug entry only (tt_debug_gemm_force_bn2): 0 = modelled
+void gemm_force_bn2(int bn) { g_gemm_force_bn2 = bn; }
+
 int gemm_pick_bn2(int M, int N) {
+  if (g_gemm_force_bn2 == 128 || g_gemm_force_bn2 == 256) return g_gemm_force_bn2;
   const int g_num_sms = device_sm_count();
   const long pairs = std::max(1, g_num_sms / 2);
   const long m_tiles = (M + 255) / 256;
@@ -921,7 +927,7 @@ int gemm_pick_bn2(int M, int N) {
     const long tiles = m_tiles * ((N + bn - 1) / bn);
     return static_cast<double>((tiles + pairs - 1) / pairs) * bn * f;
   };
-  return cost(256, 1.0) <= cost(128, 1.25) ? 256 : 128;
+  return cost(256, 1.0) <= cost(128, 1.6) ? 256 : 128;
 }
 
 int gemm_pick_bn(int N, bool b_mn_major) {
@@ -1032,7 +1038,7 @@ static double gemm_est_cost(int M, int N, int K) {
   const int g_num_sms = device_sm_count();
   const bool two = gemm_use_2cta(M, N);
   const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
-  const double f = two ? (bn == 256 ? 1.0 : 1.25) : (bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.10));
+  const double f = two ? (bn == 256 ? 1.0 : 1.6) : (bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.10));
   const long units = two ? g_num_sms / 2 : g_num_sms;
   const long tiles = (two ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM) * static_cast<long>((N + bn - 1) / bn);
   const int sp = gemm_choose_splits(M, N, K);

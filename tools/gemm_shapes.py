@@ -81,6 +81,12 @@ def main():
     vp = ctypes.c_void_p
     out = []
     shapes = list(SHAPES)
+    lib.tt_debug_gemm_force_bn2(int(os.environ.get("GEMM_BN2", "0")))  # 2-CTA tile width (0 = modelled)
+    for spec in filter(None, os.environ.get("GEMM_CUSTOM", "").split(";")):  # "M,N,K,a_mn,b_mn,epi;..."
+        M_, N_, K_, am_, bm_, ep_ = (int(x) for x in spec.split(","))
+        lab = f"custom {M_}x{N_}x{K_} a{am_} b{bm_} e{ep_}"
+        shapes.append((lab, M_, N_, K_, am_, bm_, ep_))
+        only = (only + "," if only else "") + lab
     if os.environ.get("GEMM_EXTRA"):  # "M,N,K" plain bf16-store GEMM (A K-major, B MN-major)
         M_, N_, K_ = (int(x) for x in os.environ["GEMM_EXTRA"].split(","))
         shapes.append(("extra", M_, N_, K_, 0, 1, EPI_STORE_BF16))

@@ -70,6 +70,7 @@ int tt_debug_rmsnorm_bwd(const float* gy, const float* x, const float* inv, cons
 void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
 void tt_debug_gemm_set_transpose(int mode) { ttb::gemm_set_transpose(mode); }
 void tt_debug_gemm_force_bn2(int bn) { ttb::gemm_force_bn2(bn); }
+void tt_debug_gemm_force_bn1(int bn) { ttb::gemm_force_bn1(bn); }
 
 static int g_attn_nseg = 1;
 // Timing tools: the n queries of tt_debug_attn form nseg equal sibling segments over the shared prefix

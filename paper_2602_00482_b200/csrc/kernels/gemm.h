@@ -57,10 +57,12 @@ bool gemm_prefer_transposed(int M, int N, int K);
 void gemm_set_transpose(int mode);  // 0 never, 1 modelled (default), 2 always
 int gemm_pick_bn(int N, bool b_mn_major);
 int gemm_pick_bn2(int M, int N);
-// 2-CTA (cta_group::2) tiles for M >= 256 (default on); 0 forces the single-CTA kernel.
+// 2-CTA (cta_group::2) tiles for M >= 256 (default 1: where the padding model allows); 0 forces the
+// single-CTA kernel, 2 forces pair tiles (measurement only).
 void gemm_set_2cta(int on);
 // Debug / measurement only: force the 2-CTA tile width (128 or 256; 0 = the wave model's choice).
 void gemm_force_bn2(int bn);
+void gemm_force_bn1(int bn);  // single-CTA tile width (128 / 192 / 256; 0 = modelled)
 // Per-device launch helpers (a process may drive engines on several GPUs; the current device is
 // whatever the calling engine selected): one-time MaxDynamicSharedMemorySize per (kernel, device),
 // the SM count of the current device, and a launch-status check that throws.

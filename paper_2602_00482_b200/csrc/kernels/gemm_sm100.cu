@@ -900,6 +900,7 @@ void gemm_set_2cta(int on) { g_gemm_2cta = on; }
 // pair's halved operand traffic outweighs the padding (profiles/r1: 0.556 -> 0.513 ms).
 bool gemm_use_2cta(int M, int N) {
   if (!g_gemm_2cta || M < 256) return false;
+  if (g_gemm_2cta == 2) return true;  // debug / measurement: always pair tiles
   constexpr int waste_pct = 5;  // allowed M padding in %
   const long padded = (M + 255) / 256 * 256;
   if ((padded - M) * 100 <= static_cast<long>(M) * waste_pct) return true;
@@ -930,13 +931,19 @@ int gemm_pick_bn2(int M, int N) {
   return cost(256, 1.0) <= cost(128, 1.6) ? 256 : 128;
 }
 
+int g_gemm_force_bn1 = 0;  // debug entry only (tt_debug_gemm_force_bn1): 0 = modelled
+void gemm_force_bn1(int bn) { g_gemm_force_bn1 = bn; }
+
 int gemm_pick_bn(int N, bool b_mn_major) {
   (void)b_mn_major;  // 128/192/256 are all multiples of the 64-element MN atom
-  // padded columns weighted by the per-tile overhead of narrower tiles (smem operand traffic)
+  if (g_gemm_force_bn1 == 128 || g_gemm_force_bn1 == 192 || g_gemm_force_bn1 == 256) return g_gemm_force_bn1;
+  // padded columns weighted by the per-tile overhead of narrower tiles (smem operand traffic); 128-wide
+  // at 1.25 (profiles/r2/gemm_bn2.txt: the c2 W_o weight gradient 896 x 896 x 32768 runs at 965 TF/s
+  // with 128-wide tiles, 1035 with 192, 1074 with 256)
   int best = 256;
   double best_cost = 0;
   for (int bn : {256, 192, 128}) {
-    const double f = bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.10);
+    const double f = bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.25);
     const double cost = static_cast<double>((N + bn - 1) / bn) * bn * f;
     if (bn == 256 || cost < best_cost) {
       best = bn;
@@ -1038,7 +1045,7 @@ static double gemm_est_cost(int M, int N, int K) {
   const int g_num_sms = device_sm_count();
   const bool two = gemm_use_2cta(M, N);
   const int bn = two ? gemm_pick_bn2(M, N) : gemm_pick_bn(N, true);
-  const double f = two ? (bn == 256 ? 1.0 : 1.6) : (bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.10));
+  const double f = two ? (bn == 256 ? 1.0 : 1.6) : (bn == 256 ? 1.0 : (bn == 192 ? 1.04 : 1.25));
   const long units = two ? g_num_sms / 2 : g_num_sms;
   const long tiles = (two ? (M + 2 * BM - 1) / (2 * BM) : (M + BM - 1) / BM) * static_cast<long>((N + bn - 1) / bn);
   const int sp = gemm_choose_splits(M, N, K);

@@ -82,6 +82,7 @@ def main():
     out = []
     shapes = list(SHAPES)
     lib.tt_debug_gemm_force_bn2(int(os.environ.get("GEMM_BN2", "0")))  # 2-CTA tile width (0 = modelled)
+    lib.tt_debug_gemm_force_bn1(int(os.environ.get("GEMM_BN1", "0")))  # single-CTA tile width
     for spec in filter(None, os.environ.get("GEMM_CUSTOM", "").split(";")):  # "M,N,K,a_mn,b_mn,epi;..."
         M_, N_, K_, am_, bm_, ep_ = (int(x) for x in spec.split(","))
         lab = f"custom {M_}x{N_}x{K_} a{am_} b{bm_} e{ep_}"

@@ -145,6 +145,50 @@ def test_gemm_silu_and_dsilu():
     assert _rel(gh, ref) < 1e-2
 
 
+@pytest.mark.parametrize("M,N,K", [(150, 1024, 256), (300, 4864, 896), (512, 4864, 896), (513, 1040, 256), (256, 576, 128)])
+def test_gemm_dsilu_epilogue_warp_variants(M, N, K):
+    """EPI_DSILU on shapes that launch the 16-epilogue-warp kernel (CTA-pair 256 / 128-wide tiles,
+    single-CTA 192-wide tiles) and the 8-warp one (single-CTA 256-wide), with M and N edges."""
+    torch.manual_seed(40 + M)
+    g = torch.randn(M, K, device="cuda").bfloat16()
+    w2 = torch.randn(N, K, device="cuda").bfloat16()
+    h = (2 * torch.randn(M, N, device="cuda")).bfloat16()
+    gh = torch.full((M, N), float("nan"), device="cuda").bfloat16()
+    _gemm(g, 0, w2, 0, M, N, K, EPI_DSILU, [gh], N, aux=h)
+    s = torch.sigmoid(h.float())
+    ref = (g.float() @ w2.float().t()) * s * (1 + h.float() * (1 - s))
+    assert torch.isfinite(gh.float()).all()
+    assert _rel(gh, ref) < 1e-2
+
+
+EPI_STORE_BF16_STATS = 8
+
+
+@pytest.mark.parametrize("M,N", [(256, 151936), (77, 1040), (300, 4864), (130, 1040), (512, 576)])
+def test_gemm_bf16_logits_with_group_stats(M, N):
+    """EPI_STORE_BF16_STATS (the engine's LM-head logits): bf16(l - m_g) with m_g the row's 32-column
+    group max, plus fp32 (m_g, sum exp(l - m_g)); 16- and 8-epilogue-warp launches, M / N edges."""
+    torch.manual_seed(7 + M)
+    K = 896
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = (0.05 * torch.randn(K, N, device="cuda")).bfloat16()
+    out = torch.full((M, N), float("nan"), device="cuda").bfloat16()
+    G = (N + 31) // 32
+    stats = torch.full((M, G, 2), float("nan"), device="cuda")
+    _gemm(x, 0, w, 1, M, N, K, EPI_STORE_BF16_STATS, [out], N, act=stats)
+    ref = x.float() @ w.float()
+    pad = torch.full((M, G * 32), float("-inf"), device="cuda")
+    pad[:, :N] = ref
+    grp = pad.view(M, G, 32)
+    mx = grp.max(-1).values
+    assert torch.allclose(stats[..., 0], mx, rtol=1e-4, atol=1e-4)
+    se = torch.exp(grp - mx[..., None]).sum(-1)
+    assert torch.allclose(stats[..., 1], se, rtol=1e-3)
+    rec = out.float() + stats[..., 0].repeat_interleave(32, dim=1)[:, :N]
+    assert _rel(rec, ref) < 1e-2
+    assert (out.float() <= 0).all()  # every entry is relative to its group's max
+
+
 def test_gemm_large_vocab_head():
     torch.manual_seed(5)
     M, K, N = 256, 896, 151936

@@ -188,7 +188,6 @@ int tt_debug_attn(int impl, int dir, const void* q, const void* k, const void* v
         }
         void *dk128 = up(k128), *dk128b = up(k128b);
         timed([&] {
-          cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d * 4, nullptr);  // fused kernels: dQ is added
           ttb::attn_bwd_sm100(a, rows_cap, static_cast<const int4*>(dk128), static_cast<const int2*>(dk128b),
                               static_cast<int>(k128.size() / 4), nullptr);
         });

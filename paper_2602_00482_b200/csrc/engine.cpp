@@ -187,6 +187,12 @@ void Engine::set_option(const std::string& key, int64_t value) {
     if (value < 1) throw std::invalid_argument("head_chunk_mb must be >= 1");
     head_chunk_bytes_ = value << 20;
     head_cap_rows_ = 0;
+  } else if (key == "pdl") {
+    // programmatic dependent launch (kernels/launch.cuh): 0 off, 1 every batch, 2 (default) batches of
+    // at most kPdlAutoElems activation elements, where launch latency and kernel prologues are a
+    // visible share of each kernel (tools/pdl_ab.py: c1 +4.4%; the c2 step -0.6% with PDL)
+    if (value < 0 || value > 2) throw std::invalid_argument("pdl must be 0, 1 or 2");
+    pdl_ = static_cast<int>(value);
   } else if (key == "cuda_graph") {
     cuda_graph_ = value != 0;
   } else if (key == "ce_stats") {
@@ -544,6 +550,7 @@ void Engine::gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int 
 // ----------------------------------------------------------------------------- push (forward_segment)
 void Engine::forward_batch(const Batch& b, size_t arena_off) {
   const int n = static_cast<int>(b.n);
+  set_pdl(pdl_ == 1 || (pdl_ == 2 && static_cast<double>(b.n) * d_ <= kPdlAutoElems));
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
   const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);
@@ -737,6 +744,7 @@ void Engine::head_backward_dense(const Batch& b, const bf16* nf, const float* ho
 // ----------------------------------------------------------------------------- pop (backward_segment)
 void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits, float* grad_prefix) {
   const int n = static_cast<int>(b.n);
+  set_pdl(pdl_ == 1 || (pdl_ == 2 && static_cast<double>(b.n) * d_ <= kPdlAutoElems));
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
   const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);
@@ -865,8 +873,8 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
         a.dkv16 = dqkv + d;
         a.lddkv16 = 3 * d;
       }
-      // fused kernels (dh 64 and 128): dQ partials (one per key block) reduced into the fp32 accumulator
-      ck(cudaMemsetAsync(dq, 0, static_cast<size_t>(n) * d_ * 4, stream_), "memset");
+      // fused kernels (dh 64 and 128): dQ partials (one per key block) reduced into the fp32 accumulator,
+      // which the D pre-pass zeroes (no memset node between the kernels)
       tag("attn_bwd_sm100");
       run(KC_ATTN_BWD, 8.0 * d_ * b.attn_ctx, 0, [&] {
         attn_bwd_sm100(a, rows_cap_, meta<int4>(b.o_kvit128), meta<int2>(b.o_kvit128_2),

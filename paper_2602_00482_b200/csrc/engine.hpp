@@ -292,6 +292,10 @@ class Engine {
   bool logits_bf16_ = true;
   bool plan_timing_ = false;  // LM-head logits stored bf16 relative to the 32-column group max
   int gemm_2cta_ = 1;
+  // programmatic dependent launch (engine option "pdl"): 0 off, 1 on, 2 auto = batches of at most
+  // kPdlAutoElems rows x d_model
+  int pdl_ = 2;
+  static constexpr double kPdlAutoElems = 2.0 * 1024 * 1024;
   uint64_t opt_epoch_ = 1;  // bumped by set_option: a plan's CUDA graph is re-captured after a change
   // multi-root batching: consecutive forest roots whose children are all short leaves are pushed as
   // ONE batch of up to this many tokens (0 = off); each root's leaves attend to its own rows

@@ -34,7 +34,7 @@ struct AttnBwdArgs {
   long ldkv = 0;
   const float* lse = nullptr;  // [H x n]
   float* D = nullptr;          // [H x n] scratch: rowsum(dO * O)
-  float* dq = nullptr;         // [n x lddq] fp32, accumulated (zeroed by the caller)
+  float* dq = nullptr;         // [n x lddq] fp32, overwritten (zeroed by the D pre-pass, then reduced into)
   long lddq = 0;
   float* dk = nullptr;  // fp32 dK/dV stack rows (absolute), accumulated
   float* dv = nullptr;

@@ -19,6 +19,7 @@
 
 #include "attention.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 // Resource experiments (tools/attn_bwd_ab.sh builds; the product and trace builds define none of
@@ -194,6 +195,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // predecessor grid complete (launch.cuh); TMEM held before the successor may start
+  pdl_trigger_early();
   const uint32_t t_S = tmem, t_dP = tmem + 256, t_dK = tmem + 384, t_dV = tmem + 448;
   const int wg = warp >> 2;
   if (threadIdx.x == 0) TT_TR(0, kTrBlocksLast);
@@ -472,6 +475,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       }
     }
   }
+  pdl_trigger_late();
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -587,6 +591,8 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // predecessor grid complete (launch.cuh); TMEM held before the successor may start
+  pdl_trigger_early();
   const uint32_t t_S = tmem, t_dP = tmem + 128, t_dQ = tmem + 192, t_dK = tmem + 256, t_dV = tmem + 384;
   const int wg = warp >> 2;
 
@@ -839,6 +845,7 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
       }
     }
   }
+  pdl_trigger_late();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 512);
@@ -846,8 +853,13 @@ __global__ void __launch_bounds__(kThreadsFused, 1)
 
 // D[h][r] = rowsum(dO * O) over head h's dh columns (the softmax-backward correction term): one
 // thread per 8 columns (16-byte loads), a group of dh/8 lanes per (row, head) reduces with shuffles.
+// The same thread zeroes its 8 columns of the fp32 dQ accumulator the fused kernel reduces into (no
+// separate memset between the two launches).
 __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
-                                    long ld, float* __restrict__ D, int n, int H, int dh) {
+                                    long ld, float* __restrict__ D, float* __restrict__ dq, long lddq, int n, int H,
+                                    int dh) {
+  pdl_wait();
+  pdl_trigger();
   const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int gpr = dh / 8;  // threads per (row, head): 8 or 16
   const int cols8 = H * gpr;
@@ -855,6 +867,9 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dO, const 
   const int j = static_cast<int>(t - r * cols8);
   float s = 0.f;
   if (r < n) {
+    float4* z = reinterpret_cast<float4*>(dq + r * lddq + j * 8);
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
     const uint4 x = *reinterpret_cast<const uint4*>(dO + r * ld + j * 8);
     const uint4 y = *reinterpret_cast<const uint4*>(O + r * ld + j * 8);
     const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&x);
@@ -869,7 +884,7 @@ __global__ void attn_bwd_pre_kernel(const __nv_bfloat16* __restrict__ dO, const 
   if (r < n && (j % gpr) == 0) D[static_cast<long>(j / gpr) * n + r] = s;
 }
 
-// dh = 64: the fused kernel; dQ partials are reduced into a.dq (fp32 [n x lddq], zeroed by the caller)
+// dh = 64: the fused kernel; dQ partials are reduced into a.dq (fp32 [n x lddq], zeroed by the D pre-pass)
 void launch_bwd_fused(const AttnBwdArgs& a, long rows_cap, const int4* kv_items, const int2* kv_items2, int n_kv,
                       cudaStream_t stream) {
 #ifndef TT_EXP_BWD_NS
@@ -890,10 +905,10 @@ void launch_bwd_fused(const AttnBwdArgs& a, long rows_cap, const int4* kv_items,
               a.dv_pre ? a.dv_pre : a.dv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, kv_items, kv_items2, a.scale,
               a.scale * kLog2e, a.dkv16, a.lddkv16};
   ensure_smem_attr(reinterpret_cast<const void*>(fa_bwd_fused_kernel<NS>), C::kSmem);
-  fa_bwd_fused_kernel<NS><<<dim3(n_kv, a.H), kThreadsFused, C::kSmem, stream>>>(tq, tdo, tk, tv, tdq, p);
+  launch_k(fa_bwd_fused_kernel<NS>, dim3(n_kv, a.H), dim3(kThreadsFused), C::kSmem, stream, tq, tdo, tk, tv, tdq, p);
 }
 
-// dh = 128: the fused kernel with 64-query blocks; dQ partials reduced into a.dq (fp32, zeroed by the caller)
+// dh = 128: the fused kernel with 64-query blocks; dQ partials reduced into a.dq (fp32, zeroed by the D pre-pass)
 void launch_bwd_fused128(const AttnBwdArgs& a, long rows_cap, const int4* kv_items, const int2* kv_items2, int n_kv,
                          cudaStream_t stream) {
   constexpr int NS = 3;
@@ -910,7 +925,7 @@ void launch_bwd_fused128(const AttnBwdArgs& a, long rows_cap, const int4* kv_ite
               a.dv_pre ? a.dv_pre : a.dv, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, kv_items, kv_items2, a.scale,
               a.scale * kLog2e, a.dkv16, a.lddkv16};
   ensure_smem_attr(reinterpret_cast<const void*>(fa_bwd_fused128_kernel<NS>), C::kSmem);
-  fa_bwd_fused128_kernel<NS><<<dim3(n_kv, a.H), kThreadsFused, C::kSmem, stream>>>(tq, tdo, tk, tv, tdq, p);
+  launch_k(fa_bwd_fused128_kernel<NS>, dim3(n_kv, a.H), dim3(kThreadsFused), C::kSmem, stream, tq, tdo, tk, tv, tdq, p);
 }
 
 }  // namespace
@@ -930,9 +945,11 @@ extern "C" int tt_debug_trace_clear() {
 void attn_bwd_pre(const AttnBwdArgs& a, cudaStream_t stream) {
   const long threads = static_cast<long>(a.n) * a.H * (a.dh / 8);
   if (a.ldq % 8 != 0) throw std::invalid_argument("attention backward: dO/O pitch must be a multiple of 8");
+  if (!a.dq || a.lddq % 4 != 0 || a.lddq < static_cast<long>(a.H) * a.dh)
+    throw std::invalid_argument("attention backward: dQ accumulator missing or its pitch not a multiple of 4");
   if (threads > 0)
-    attn_bwd_pre_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, stream>>>(a.dO, a.o, a.ldq, a.D, a.n,
-                                                                                         a.H, a.dh);
+    launch_k(attn_bwd_pre_kernel, dim3(static_cast<unsigned>((threads + 255) / 256)), dim3(256), 0, stream, a.dO, a.o,
+             a.ldq, a.D, a.dq, a.lddq, a.n, a.H, a.dh);
 }
 
 void attn_bwd_sm100(const AttnBwdArgs& a, long rows_cap, const int4* kv_items, const int2* kv_items2, int n_kv,

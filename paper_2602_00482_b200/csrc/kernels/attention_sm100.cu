@@ -21,6 +21,7 @@
 
 #include "attention.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 #ifndef TT_TRACE
@@ -172,6 +173,8 @@ __global__ void __launch_bounds__(FwdCfg<DH, BKV, NS, SPL>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // predecessor grid complete (launch.cuh); TMEM held before the successor may start
+  pdl_trigger_early();
   if (threadIdx.x == 0) TT_FCTA(1);
   constexpr int NB = C::NB;
   const uint32_t tmem_S = tmem;              // NB x BKV columns
@@ -427,6 +430,7 @@ __global__ void __launch_bounds__(FwdCfg<DH, BKV, NS, SPL>::kThreads, 1)
     }
     if (half == 0 && row_ok) p.lse[static_cast<long>(h) * p.n + row] = (m + log2f(lt)) * 0.6931471805599453f;
   }
+  pdl_trigger_late();
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TT_FCTA(3);
@@ -444,7 +448,7 @@ void launch_fwd(const AttnFwdArgs& a, long rows_cap, cudaStream_t stream) {
   ensure_smem_attr(reinterpret_cast<const void*>(fa_fwd_kernel<DH, BKV, NS, POLY, SPL>), C::kSmem);
   FwdParams p{a.o, a.ldo, a.lse, a.n, a.S, a.H, a.pbase, a.r0 < 0 ? a.S : a.r0, a.qblocks, a.scale * kLog2e};
   dim3 grid(a.nqb, a.H);
-  fa_fwd_kernel<DH, BKV, NS, POLY, SPL><<<grid, C::kThreads, C::kSmem, stream>>>(tq, tk, tv, p);
+  launch_k(fa_fwd_kernel<DH, BKV, NS, POLY, SPL>, grid, dim3(C::kThreads), C::kSmem, stream, tq, tk, tv, p);
 }
 
 }  // namespace

@@ -9,6 +9,7 @@
 
 #include "elementwise.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace ttb {
@@ -40,6 +41,8 @@ __device__ __forceinline__ float block_sum256(float v, float* red) {
 __global__ void embed_pe_kernel(const int32_t* __restrict__ tok, const int32_t* __restrict__ pos,
                                 const __nv_bfloat16* __restrict__ emb, const float* __restrict__ pe,
                                 float* __restrict__ x, int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const int r = blockIdx.x;
   const long e0 = static_cast<long>(tok[r]) * d, p0 = static_cast<long>(pos[r]) * d, x0 = static_cast<long>(r) * d;
   for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
@@ -59,6 +62,8 @@ template <int VPT, int WPR = 1>
 __global__ void __launch_bounds__(256) rmsnorm_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gain,
                                                           float* __restrict__ inv, __nv_bfloat16* __restrict__ y, int n,
                                                           int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   constexpr int STRIDE = 32 * WPR;
   __shared__ float red[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -113,6 +118,8 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(const float* __restric
                                                           const float* __restrict__ inv, const float* __restrict__ gain,
                                                           const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
                                                           float* __restrict__ ggain, int n, int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   constexpr int RPB = 8 / WPR;     // rows per block step
   constexpr int STRIDE = 32 * WPR;  // float4 column stride between a lane's groups
   extern __shared__ float gsum[];  // [d]
@@ -202,7 +209,7 @@ void launch_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const
     return std::max(1, b);
   }();
   const int blocks = std::min((n + RPB - 1) / RPB, 148 * per_sm);
-  rmsnorm_bwd_kernel<VPT, WPR><<<blocks, 256, d * sizeof(float), s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
+  launch_k(rmsnorm_bwd_kernel<VPT, WPR>, dim3(blocks), dim3(256), d * sizeof(float), s, gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
 }
 
 // rmsnorm_backward fed by TMA (rows up to 4096 columns): a persistent block per SM, one producer warp
@@ -230,6 +237,8 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
     rmsnorm_bwd_tma_kernel(const float* __restrict__ gy, const float* __restrict__ x, const float* __restrict__ inv,
                            const float* __restrict__ gain, const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
                            float* __restrict__ ggain, int n, int d, int nst, int ncw) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int nb = gres ? 3 : 2;  // row buffers per stage
   const int row_bytes = d * 4;
@@ -356,8 +365,7 @@ void launch_rmsnorm_bwd_tma(const float* gy, const float* x, const float* inv, c
   const int smem = ((nst * 16 + 2 * d * 4 + 127) / 128) * 128 + nst * stage_bytes;
   ensure_smem_attr(reinterpret_cast<const void*>(rmsnorm_bwd_tma_kernel<VPT, GS>), kSmemMax);
   const int blocks = std::min(n, device_sm_count());
-  rmsnorm_bwd_tma_kernel<VPT, GS><<<blocks, kNormTmaThreads, smem, s>>>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d,
-                                                                        nst, ncw);
+  launch_k(rmsnorm_bwd_tma_kernel<VPT, GS>, dim3(blocks), dim3(kNormTmaThreads), smem, s, gy, x, inv, gain, gres, gx, gxb, ggain, n, d, nst, ncw);
 }
 
 // Weighted NLL over one vocab row with several (target, weight) pairs (weighted_nll,
@@ -399,6 +407,8 @@ __global__ void __launch_bounds__(kCeThreads, 4) ce_kernel(const float* __restri
                                                   const int32_t* __restrict__ tgt, const double* __restrict__ w,
                                                   OutT* __restrict__ dl, double* __restrict__ loss,
                                                   const float2* __restrict__ stats, int n_groups) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   __shared__ float red[32];
   __shared__ float s_lse;
   uint64_t pol;
@@ -497,6 +507,8 @@ __global__ void __launch_bounds__(kCeThreads, 4)
     ce_bf16_kernel(const __nv_bfloat16* __restrict__ y, int m, long V, const int32_t* __restrict__ pair_off,
                    const int32_t* __restrict__ tgt, const double* __restrict__ w, __nv_bfloat16* __restrict__ dl,
                    double* __restrict__ loss, const float2* __restrict__ stats, int n_groups) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   __shared__ float red[32];
   __shared__ float s_lse;
   constexpr float kL2e = 1.4426950408889634f;
@@ -586,6 +598,8 @@ __global__ void __launch_bounds__(kCeThreads, 4)
 
 __global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, const int32_t* __restrict__ idx,
                                         __nv_bfloat16* __restrict__ dst, int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const int i = blockIdx.x;
   const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<long>(idx[i]) * d);
   uint4* o = reinterpret_cast<uint4*>(dst + static_cast<long>(i) * d);
@@ -594,6 +608,8 @@ __global__ void gather_rows_bf16_kernel(const __nv_bfloat16* __restrict__ src, c
 
 __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int32_t* __restrict__ idx,
                                         float* __restrict__ dst, int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const int i = blockIdx.x;
   const float4* s = reinterpret_cast<const float4*>(src + static_cast<long>(i) * d);
   float4* o = reinterpret_cast<float4*>(dst + static_cast<long>(idx[i]) * d);
@@ -604,6 +620,8 @@ __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int
 // dK/dV stack rows (KVGrad::add_rows consumer + frame release, model.hpp:193-206).
 __global__ void pack_dqkv_kernel(const float* __restrict__ dq, float* __restrict__ dk, float* __restrict__ dv,
                                  __nv_bfloat16* __restrict__ out, int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const int r = blockIdx.x;
   const long o = static_cast<long>(r) * d;
   __nv_bfloat16* orow = out + static_cast<long>(r) * 3 * d;
@@ -622,6 +640,8 @@ __global__ void pack_dqkv_kernel(const float* __restrict__ dq, float* __restrict
 
 __global__ void pack_dkv_kernel(float* __restrict__ dk, float* __restrict__ dv, __nv_bfloat16* __restrict__ out,
                                 int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const int r = blockIdx.x;
   const long o = static_cast<long>(r) * d;
   __nv_bfloat16* orow = out + static_cast<long>(r) * 3 * d;
@@ -638,6 +658,8 @@ __global__ void pack_dkv_kernel(float* __restrict__ dk, float* __restrict__ dv, 
 // dE[tok[r]] += gx[r]   (model.hpp:627-630)
 __global__ void embed_grad_kernel(const float* __restrict__ gx, const int32_t* __restrict__ tok,
                                   float* __restrict__ gemb, int d) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const int r = blockIdx.x;
   const float* s = gx + static_cast<long>(r) * d;
   float* o = gemb + static_cast<long>(tok[r]) * d;
@@ -650,6 +672,8 @@ __global__ void embed_grad_kernel(const float* __restrict__ gx, const int32_t* _
 // dst[c * ldd + r] = bf16(src[r * lds + c]) (parameter upload into a transposed device layout)
 __global__ void f32_to_bf16_2d_t_kernel(const float* __restrict__ src, long lds, __nv_bfloat16* __restrict__ dst,
                                         long ldd, int rows, int cols) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const long total = static_cast<long>(rows) * cols;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -660,6 +684,8 @@ __global__ void f32_to_bf16_2d_t_kernel(const float* __restrict__ src, long lds,
 
 __global__ void f32_to_bf16_2d_kernel(const float* __restrict__ src, long lds, __nv_bfloat16* __restrict__ dst,
                                       long ldd, int rows, int cols) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   const long total = static_cast<long>(rows) * cols;
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
@@ -676,6 +702,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 
 // N(0, std) via Box-Muller on a counter hash (seed, element index).
 __global__ void init_normal_kernel(float* __restrict__ out, long n, uint64_t seed, float stdv) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
     const uint64_t h = mix64(seed * 0x9E3779B97F4A7C15ULL + static_cast<uint64_t>(i));
@@ -686,6 +714,8 @@ __global__ void init_normal_kernel(float* __restrict__ out, long n, uint64_t see
 }
 
 __global__ void fill_kernel(float* __restrict__ out, long n, float v) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x)
     out[i] = v;
@@ -695,18 +725,18 @@ __global__ void fill_kernel(float* __restrict__ out, long n, float v) {
 
 void k_embed_pe(const int32_t* tok, const int32_t* pos, const __nv_bfloat16* emb, const float* pe, float* x, int n,
                 int d, cudaStream_t s) {
-  if (n > 0) embed_pe_kernel<<<n, 128, 0, s>>>(tok, pos, emb, pe, x, d);
+  if (n > 0) launch_k(embed_pe_kernel, dim3(n), dim3(128), 0, s, tok, pos, emb, pe, x, d);
 }
 void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16* y, int n, int d, cudaStream_t s) {
   if (n <= 0) return;
   const int vpt = (d + 127) / 128;
   const int blocks = (n + 7) / 8;
-  if (vpt <= 2) rmsnorm_fwd_kernel<2><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
-  else if (vpt <= 4) rmsnorm_fwd_kernel<4><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
-  else if (vpt <= 8) rmsnorm_fwd_kernel<8><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
-  else if (vpt <= 16) rmsnorm_fwd_kernel<16><<<blocks, 256, 0, s>>>(x, gain, inv, y, n, d);
-  else if (vpt <= 32) rmsnorm_fwd_kernel<16, 2><<<(n + 3) / 4, 256, 0, s>>>(x, gain, inv, y, n, d);
-  else if (vpt <= 64) rmsnorm_fwd_kernel<16, 4><<<(n + 1) / 2, 256, 0, s>>>(x, gain, inv, y, n, d);
+  if (vpt <= 2) launch_k(rmsnorm_fwd_kernel<2>, dim3(blocks), dim3(256), 0, s, x, gain, inv, y, n, d);
+  else if (vpt <= 4) launch_k(rmsnorm_fwd_kernel<4>, dim3(blocks), dim3(256), 0, s, x, gain, inv, y, n, d);
+  else if (vpt <= 8) launch_k(rmsnorm_fwd_kernel<8>, dim3(blocks), dim3(256), 0, s, x, gain, inv, y, n, d);
+  else if (vpt <= 16) launch_k(rmsnorm_fwd_kernel<16>, dim3(blocks), dim3(256), 0, s, x, gain, inv, y, n, d);
+  else if (vpt <= 32) launch_k(rmsnorm_fwd_kernel<16, 2>, dim3((n + 3) / 4), dim3(256), 0, s, x, gain, inv, y, n, d);
+  else if (vpt <= 64) launch_k(rmsnorm_fwd_kernel<16, 4>, dim3((n + 1) / 2), dim3(256), 0, s, x, gain, inv, y, n, d);
   else throw std::invalid_argument("rmsnorm: d_model > 8192");
 }
 void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
@@ -731,22 +761,23 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
           __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {
   if (m > 0)
-    ce_kernel<__nv_bfloat16><<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, stats,
-                                                                         n_groups);
+    launch_k(ce_kernel<__nv_bfloat16>, dim3(std::min(m, 148 * 4)), dim3(kCeThreads), 0, s, logits, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
 }
 void k_ce_bf16(const __nv_bfloat16* y, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
                __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {
   if (V % 8 != 0) throw std::invalid_argument("k_ce_bf16: vocab_size must be a multiple of 8");
   if (m > 0)
-    ce_bf16_kernel<<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(y, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
+    launch_k(ce_bf16_kernel, dim3(std::min(m, 148 * 4)), dim3(kCeThreads), 0, s, y, m, V, pair_off, tgt, w, dl, loss, stats, n_groups);
 }
 void k_ce_f32(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
               float* dl, double* loss, cudaStream_t s) {
   if (m > 0)
-    ce_kernel<float><<<std::min(m, 148 * 4), kCeThreads, 0, s>>>(logits, m, V, pair_off, tgt, w, dl, loss, nullptr, 0);
+    launch_k(ce_kernel<float>, dim3(std::min(m, 148 * 4)), dim3(kCeThreads), 0, s, logits, m, V, pair_off, tgt, w, dl, loss, nullptr, 0);
 }
 // dst[i] += src[i] (fp32, n % 4 == 0, 16-byte aligned)
 __global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict__ src, long n4) {
+  pdl_wait();  // launch.cuh: no global access before the predecessor completes
+  pdl_trigger();
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
     float4 a = reinterpret_cast<float4*>(dst)[i];
@@ -761,39 +792,38 @@ __global__ void add_f32_kernel(float* __restrict__ dst, const float* __restrict_
 void k_add_f32(float* dst, const float* src, long n, cudaStream_t s) {
   if (n % 4 != 0) throw std::invalid_argument("k_add_f32: n must be a multiple of 4");
   if (n > 0)
-    add_f32_kernel<<<static_cast<int>(std::min<long>((n / 4 + 255) / 256, 148 * 16)), 256, 0, s>>>(dst, src, n / 4);
+    launch_k(add_f32_kernel, dim3(static_cast<int>(std::min<long>((n / 4 + 255) / 256, 148 * 16))), dim3(256), 0, s, dst, src, n / 4);
 }
 void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloat16* dst, int m, int d,
                         cudaStream_t s) {
-  if (m > 0) gather_rows_bf16_kernel<<<m, 128, 0, s>>>(src, idx, dst, d);
+  if (m > 0) launch_k(gather_rows_bf16_kernel, dim3(m), dim3(128), 0, s, src, idx, dst, d);
 }
 void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m, int d, cudaStream_t s) {
-  if (m > 0) scatter_rows_f32_kernel<<<m, 128, 0, s>>>(src, idx, dst, d);
+  if (m > 0) launch_k(scatter_rows_f32_kernel, dim3(m), dim3(128), 0, s, src, idx, dst, d);
 }
 void k_pack_dqkv(const float* dq, float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s) {
-  if (n > 0) pack_dqkv_kernel<<<n, 128, 0, s>>>(dq, dk, dv, out, d);
+  if (n > 0) launch_k(pack_dqkv_kernel, dim3(n), dim3(128), 0, s, dq, dk, dv, out, d);
 }
 void k_pack_dkv(float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s) {
-  if (n > 0) pack_dkv_kernel<<<n, 128, 0, s>>>(dk, dv, out, d);
+  if (n > 0) launch_k(pack_dkv_kernel, dim3(n), dim3(128), 0, s, dk, dv, out, d);
 }
 void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s) {
-  if (n > 0) embed_grad_kernel<<<n, 128, 0, s>>>(gx, tok, gemb, d);
+  if (n > 0) launch_k(embed_grad_kernel, dim3(n), dim3(128), 0, s, gx, tok, gemb, d);
 }
 void k_f32_to_bf16_2d_t(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s) {
   const long total = static_cast<long>(rows) * cols;
   if (total > 0)
-    f32_to_bf16_2d_t_kernel<<<static_cast<int>(std::min<long>((total + 255) / 256, 148 * 32)), 256, 0, s>>>(src, lds, dst,
-                                                                                                          ldd, rows, cols);
+    launch_k(f32_to_bf16_2d_t_kernel, dim3(static_cast<int>(std::min<long>((total + 255) / 256, 148 * 32))), dim3(256), 0, s, src, lds, dst, ldd, rows, cols);
 }
 void k_f32_to_bf16_2d(const float* src, long lds, __nv_bfloat16* dst, long ldd, int rows, int cols, cudaStream_t s) {
   const long total = static_cast<long>(rows) * cols;
-  if (total > 0) f32_to_bf16_2d_kernel<<<static_cast<int>(std::min<long>((total + 255) / 256, 148 * 32)), 256, 0, s>>>(src, lds, dst, ldd, rows, cols);
+  if (total > 0) launch_k(f32_to_bf16_2d_kernel, dim3(static_cast<int>(std::min<long>((total + 255) / 256, 148 * 32))), dim3(256), 0, s, src, lds, dst, ldd, rows, cols);
 }
 void k_init_normal(float* out, long n, uint64_t seed, float stdv, cudaStream_t s) {
-  if (n > 0) init_normal_kernel<<<static_cast<int>(std::min<long>((n + 255) / 256, 148 * 32)), 256, 0, s>>>(out, n, seed, stdv);
+  if (n > 0) launch_k(init_normal_kernel, dim3(static_cast<int>(std::min<long>((n + 255) / 256, 148 * 32))), dim3(256), 0, s, out, n, seed, stdv);
 }
 void k_fill(float* out, long n, float v, cudaStream_t s) {
-  if (n > 0) fill_kernel<<<static_cast<int>(std::min<long>((n + 255) / 256, 148 * 32)), 256, 0, s>>>(out, n, v);
+  if (n > 0) launch_k(fill_kernel, dim3(static_cast<int>(std::min<long>((n + 255) / 256, 148 * 32))), dim3(256), 0, s, out, n, v);
 }
 
 }  // namespace ttb

@@ -60,6 +60,10 @@ int gemm_pick_bn2(int M, int N);
 // 2-CTA (cta_group::2) tiles for M >= 256 (default 1: where the padding model allows); 0 forces the
 // single-CTA kernel, 2 forces pair tiles (measurement only).
 void gemm_set_2cta(int on);
+// Programmatic dependent launch for every kernel (kernels/launch.cuh): 1 (default) launches with the
+// PDL attribute, 0 in plain stream order (A/B measurement; engine option "pdl").
+extern int g_pdl;
+void set_pdl(int on);
 // Debug / measurement only: force the 2-CTA tile width (128 or 256; 0 = the wave model's choice).
 void gemm_force_bn2(int bn);
 void gemm_force_bn1(int bn);  // single-CTA tile width (128 / 192 / 256; 0 = modelled)

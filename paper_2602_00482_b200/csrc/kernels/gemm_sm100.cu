@@ -30,6 +30,7 @@
 #include <type_traits>
 
 #include "gemm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace ttb {
@@ -404,6 +405,8 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
   if constexpr (CG == 2) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();     // predecessor grid complete: operands / epilogue inputs are final (launch.cuh)
+  pdl_trigger_early();  // TMEM held: the successor may start its prologue
 
   // Rasterisation: the concurrently running tiles should share the LARGER operand's panels so it
   // streams from HBM once while the smaller one stays L2-resident: n-fastest when A (M x K) is the
@@ -738,6 +741,7 @@ __global__ void __launch_bounds__(threads_of(EPW), 1)
     if (lane == 0) bulk_wait_all();  // stores complete before the CTA (and its smem) retires
   }
 
+  pdl_trigger_late();
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();  // the peer's MMAs into this CTA's TMEM are complete
@@ -869,13 +873,13 @@ void launch_epw(const GemmOperand& A, const GemmOperand& B, int M, int N, int K,
   cfg.blockDim = dim3(threads_of(EPW));
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_attr(attr, 1);
   check_launch(cudaLaunchKernelEx(&cfg, gemm_kernel<BN, CG, A_MN, B_MN, EPW>, ta, tb, to[0], to[1], to[2], tx, M, N, K,
                                   splits, e),
                "gemm launch");

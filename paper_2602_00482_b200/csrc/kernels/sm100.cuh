@@ -89,6 +89,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// (kernels/launch.cuh): block until the predecessor grid has completed and its writes are visible (a
+// no-op when launched without the PDL attribute); let the successor grid start its prologue.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// TMEM-holding kernels release their successor either right after the prologue (early) or when the
+// CTA's work is done (late, TT_PDL_LATE=1 experiment builds).
+#ifndef TT_PDL_LATE
+#define TT_PDL_LATE 0
+#endif
+__device__ __forceinline__ void pdl_trigger_early() {
+  if (!TT_PDL_LATE) pdl_trigger();
+}
+__device__ __forceinline__ void pdl_trigger_late() {
+  if (TT_PDL_LATE) pdl_trigger();
+}
+
 // ---------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

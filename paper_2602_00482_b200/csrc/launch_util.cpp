@@ -43,6 +43,9 @@ int device_sm_count() {
   return n;
 }
 
+int g_pdl = 1;
+void set_pdl(int on) { g_pdl = on ? 1 : 0; }
+
 void check_launch(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }

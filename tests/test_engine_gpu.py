@@ -382,6 +382,33 @@ def test_plan_cuda_graph_replay_matches_eager():
     assert abs(r.total_loss - outs[0][0]) <= 1e-9 * abs(outs[0][0]) and rel(eng.gradients(), outs[0][1]) <= 1e-5
 
 
+@pytest.mark.parametrize("spec", ["small", "dh128"])
+def test_programmatic_dependent_launch_matches_stream_order(spec):
+    # every kernel launched with PDL (option pdl=1: the successor's prologue overlaps the predecessor's
+    # tail, griddepcontrol.wait before any global access) must give the plain stream-ordered step
+    # (pdl=0) and the oracle, eager and graph-replayed
+    cfg, flat, eng = make(SMALL if spec == "small" else DH128, 47)
+    seqs = O.grouped_corpus(3, 4, 60, 50, cfg.vocab_size, 48, weight_jitter=True)
+    tree = tt.build_prefix_tree([tt.TokenSequence(s.seq_id, s.tokens, s.weights) for s in seqs])
+    plan = eng.plan(tree, tt.SchedulerConfig())
+    outs = {}
+    for mode in (0, 1, 2):
+        eng.set_option("pdl", mode)
+        for _ in range(3):  # eager, capture + launch, replay
+            eng.zero_gradients()
+            r = plan.execute()
+            outs.setdefault(mode, []).append((r.total_loss, eng.gradients().copy()))
+    l0, g0 = outs[0][0]
+    for mode in (1, 2):
+        for loss, g in outs[mode]:
+            assert abs(loss - l0) <= 1e-9 * abs(l0) and rel(g, g0) <= 1e-5
+    ref = O.tree_train_step(cfg, flat, O.order_children(O.build_prefix_tree(seqs), "subtree_tokens_desc"), seqs)
+    assert abs(outs[1][-1][0] - ref.total_loss) <= 5e-3 * abs(ref.total_loss)
+    assert rel(outs[1][-1][1], ref.grads) <= 2e-2
+    with pytest.raises(ValueError):
+        eng.set_option("pdl", 3)
+
+
 def test_plan_execute_async_overlapping_next_plan():
     # tt_plan_execute_async + tt_plan_wait: while step k runs, the next tree is built and planned
     # (its metadata goes over the copy stream); every step matches the synchronous execute, and a

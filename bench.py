@@ -374,6 +374,9 @@ def run_b200(args):
     else:
         seqs = all_seqs
     eng = tt.Engine(cfg, device=local)
+    for kv in args.option:  # engine execution options (A/B runs; recorded in config.engine_options)
+        k, v = kv.split("=")
+        eng.set_option(k, int(v))
     eng.init_params_random(7)
     sched = tt.SchedulerConfig(sibling_batch=not args.no_sibling_batch, batch_token_budget=args.batch_budget,
                                chunk_len=args.chunk_len)
@@ -486,7 +489,8 @@ def run_b200(args):
         "config": {"workload": f"{args.config}: {c['desc']}", "model": c["model"], "global_batch": len(all_seqs),
                    "seq_len": seq_len, "parallelism": f"dp{world}",
                    "trees_per_gpu": c["prompts"], "sibling_batch": not args.no_sibling_batch,
-                   "l2": "step working set (weights + activations) >> 126 MB L2; no flush needed", "env": env},
+                   "l2": "step working set (weights + activations) >> 126 MB L2; no flush needed", "env": env,
+                   **({"engine_options": dict(kv.split("=") for kv in args.option)} if args.option else {})},
         "e2e": {"value": roll_total / (e2e_ms / 1e3) if e2e_ms else None, "unit": "rollout tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms,
                 "includes": "per step: host tree build + schedule + metadata H2D (pinned, copy stream) + execute + loss "
@@ -575,6 +579,8 @@ def main():
     ap.add_argument("--prompts", type=int, default=0, help="override the config's prompts per GPU (quick profiling only)")
     ap.add_argument("--share", type=float, default=0.5, help="c5: shared-prefix fraction r of the 4096-token rollouts")
     ap.add_argument("--chunk-len", type=int, default=0, help="chunked backward (SPEC.md:234-251); 0 = off")
+    ap.add_argument("--option", action="append", default=[],
+                    help="engine option key=value (tt_engine_set_option; A/B runs only), repeatable")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

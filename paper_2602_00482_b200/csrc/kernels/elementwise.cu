@@ -618,40 +618,39 @@ __global__ void scatter_rows_f32_kernel(const float* __restrict__ src, const int
 
 // Stack pop of one layer: dqkv[r] = [dQ[r] | dK[r] | dV[r]] (bf16), then zero the consumed
 // dK/dV stack rows (KVGrad::add_rows consumer + frame release, model.hpp:193-206).
-__global__ void pack_dqkv_kernel(const float* __restrict__ dq, float* __restrict__ dk, float* __restrict__ dv,
-                                 __nv_bfloat16* __restrict__ out, int d) {
-  pdl_wait();  // launch.cuh: no global access before the predecessor completes
-  pdl_trigger();
-  const int r = blockIdx.x;
-  const long o = static_cast<long>(r) * d;
-  __nv_bfloat16* orow = out + static_cast<long>(r) * 3 * d;
-  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
-    const float4 a = *reinterpret_cast<const float4*>(dq + o + c);
-    *reinterpret_cast<uint2*>(orow + c) = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
-    if (dk == nullptr) continue;  // dK / dV written into the operand by the attention backward
-    const float4 b = *reinterpret_cast<float4*>(dk + o + c);
-    const float4 e = *reinterpret_cast<float4*>(dv + o + c);
-    *reinterpret_cast<uint2*>(orow + d + c) = make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
-    *reinterpret_cast<uint2*>(orow + 2 * d + c) = make_uint2(pack_bf16x2(e.x, e.y), pack_bf16x2(e.z, e.w));
-    *reinterpret_cast<float4*>(dk + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(dv + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+// Grid-stride over 8-column chunks (two 16-byte loads per fp32 stream, one 16-byte bf16 store): at
+// d = 896 a block-per-row layout left a quarter of the threads idle and paid one CTA per 3.5 KB row.
+// DQ: pack dQ (leaf batches: dK / dV were written into the operand by the attention backward);
+// KV: pack and consume dK / dV.
+__device__ __forceinline__ void zero8(float* p) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+  reinterpret_cast<float4*>(p)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
-
-__global__ void pack_dkv_kernel(float* __restrict__ dk, float* __restrict__ dv, __nv_bfloat16* __restrict__ out,
-                                int d) {
+__device__ __forceinline__ uint4 ld8_bf16(const float* p) {
+  const float4 a = __ldcs(reinterpret_cast<const float4*>(p)), b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+  return make_uint4(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w), pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
+}
+template <bool DQ, bool KV>
+__global__ void __launch_bounds__(256) pack_dqkv_kernel(const float* __restrict__ dq, float* __restrict__ dk,
+                                                        float* __restrict__ dv, __nv_bfloat16* __restrict__ out,
+                                                        long n, int d) {
   pdl_wait();  // launch.cuh: no global access before the predecessor completes
   pdl_trigger();
-  const int r = blockIdx.x;
-  const long o = static_cast<long>(r) * d;
-  __nv_bfloat16* orow = out + static_cast<long>(r) * 3 * d;
-  for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
-    const float4 b = *reinterpret_cast<float4*>(dk + o + c);
-    const float4 e = *reinterpret_cast<float4*>(dv + o + c);
-    *reinterpret_cast<uint2*>(orow + d + c) = make_uint2(pack_bf16x2(b.x, b.y), pack_bf16x2(b.z, b.w));
-    *reinterpret_cast<uint2*>(orow + 2 * d + c) = make_uint2(pack_bf16x2(e.x, e.y), pack_bf16x2(e.z, e.w));
-    *reinterpret_cast<float4*>(dk + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(dv + o + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int cpr = d / 8;
+  const long total = n * cpr;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long r = i / cpr;
+    const int c = static_cast<int>(i - r * cpr) * 8;
+    const long o = r * d + c;
+    __nv_bfloat16* orow = out + r * 3 * d + c;
+    if (DQ) *reinterpret_cast<uint4*>(orow) = ld8_bf16(dq + o);
+    if (KV) {
+      *reinterpret_cast<uint4*>(orow + d) = ld8_bf16(dk + o);
+      *reinterpret_cast<uint4*>(orow + 2 * d) = ld8_bf16(dv + o);
+      zero8(dk + o);
+      zero8(dv + o);
+    }
   }
 }
 
@@ -801,11 +800,23 @@ void k_gather_rows_bf16(const __nv_bfloat16* src, const int32_t* idx, __nv_bfloa
 void k_scatter_rows_f32(const float* src, const int32_t* idx, float* dst, int m, int d, cudaStream_t s) {
   if (m > 0) launch_k(scatter_rows_f32_kernel, dim3(m), dim3(128), 0, s, src, idx, dst, d);
 }
+static unsigned pack_grid(long n, int d) {
+  const long chunks = n * (d / 8);
+  return static_cast<unsigned>(std::min<long>((chunks + 255) / 256, static_cast<long>(device_sm_count()) * 8));
+}
 void k_pack_dqkv(const float* dq, float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s) {
-  if (n > 0) launch_k(pack_dqkv_kernel, dim3(n), dim3(128), 0, s, dq, dk, dv, out, d);
+  if (d % 8 != 0) throw std::invalid_argument("pack_dqkv: d_model must be a multiple of 8");
+  if (n <= 0) return;
+  if (dk == nullptr)
+    launch_k(pack_dqkv_kernel<true, false>, dim3(pack_grid(n, d)), dim3(256), 0, s, dq, dk, dv, out, static_cast<long>(n), d);
+  else
+    launch_k(pack_dqkv_kernel<true, true>, dim3(pack_grid(n, d)), dim3(256), 0, s, dq, dk, dv, out, static_cast<long>(n), d);
 }
 void k_pack_dkv(float* dk, float* dv, __nv_bfloat16* out, int n, int d, cudaStream_t s) {
-  if (n > 0) launch_k(pack_dkv_kernel, dim3(n), dim3(128), 0, s, dk, dv, out, d);
+  if (d % 8 != 0) throw std::invalid_argument("pack_dkv: d_model must be a multiple of 8");
+  if (n > 0)
+    launch_k(pack_dqkv_kernel<false, true>, dim3(pack_grid(n, d)), dim3(256), 0, s, nullptr, dk, dv, out,
+             static_cast<long>(n), d);
 }
 void k_embed_grad(const float* gx, const int32_t* tok, float* gemb, int n, int d, cudaStream_t s) {
   if (n > 0) launch_k(embed_grad_kernel, dim3(n), dim3(128), 0, s, gx, tok, gemb, d);

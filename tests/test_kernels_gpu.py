@@ -57,6 +57,21 @@ def test_gemm_fwd_kmajor_mnmajor(M, N, K):
     assert _rel(out, ref) < 1e-5
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 896, 896), (129, 4864, 896), (77, 448, 512), (1000, 896, 4864), (64, 256, 128),
+                                   (4096, 896, 896)])
+def test_gemm_residual_epilogue(M, N, K):
+    # x_mid = x + attn W_o / x_out = x_mid + act W_out (model.hpp:427-428,447-448): fp32 residual in, fp32 out
+    torch.manual_seed(5)
+    a = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(K, N, device="cuda").bfloat16()
+    res = torch.randn(M, N, device="cuda")
+    out = torch.full((M, N), float("nan"), device="cuda")
+    _gemm(a, 0, w, 1, M, N, K, EPI_RESID_F32, [out], N, aux=res)
+    ref = res + a.float() @ w.float()
+    assert torch.isfinite(out).all()
+    assert _rel(out, ref) < 1e-5
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 128, 256), (77, 896, 4864), (513, 256, 896), (100, 2688, 256),
                                    (512, 896, 256), (4096, 896, 2688), (300, 448, 512), (1000, 672, 896)])
 def test_gemm_dx_kmajor_kmajor(M, N, K):

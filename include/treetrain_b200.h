@@ -227,6 +227,8 @@ int tt_engine_set_profiling(tt_engine* eng, int32_t on);
  *                        ce_stats), 0 = fp32 logits (loss / gradients then differ by bf16 rounding only)
  *   "head_chunk_mb"      LM-head / CE scratch budget per loss-row chunk (default 6144, >= 1; capped by free HBM)
  *   "plan_timing"        1 = print the host phases of tt_plan_create (schedule, memory plan, metadata) to stderr
+ *   "gn_bf16"            1 = the grad_normed outputs of the dX GEMMs stored bf16 for the RMSNorm backward (default,
+ *                        d_model % 8 == 0 and <= 4096), 0 = fp32 (loss unchanged; gradients differ by bf16 rounding)
  *   "pdl"                programmatic dependent launch of every kernel: 0 = off, 1 = on, 2 = segment batches of
  *                        at most 2^21 rows x d_model elements (default; launch-bound batches gain, large ones not)
  * Unknown keys and out-of-range values return TT_ERR_INVALID_ARGUMENT. */

@@ -106,6 +106,7 @@ EXPORTS = {
     "tt_debug_gemm_force_bn1": [c.c_int],
     "tt_debug_attn_set_segments": [c.c_int],
     "tt_debug_rmsnorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, c.c_int, c.c_int],
+    "tt_debug_rmsnorm_bwd16": [vp, vp, vp, vp, vp, vp, vp, vp, c.c_int, c.c_int],
 }
 
 

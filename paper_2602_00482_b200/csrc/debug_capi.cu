@@ -67,6 +67,16 @@ int tt_debug_rmsnorm_bwd(const float* gy, const float* x, const float* inv, cons
     ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_rmsnorm_bwd sync");
   });
 }
+// The same with a bf16 gy (the engine's grad_normed path; d_model % 8 == 0, <= 4096).
+int tt_debug_rmsnorm_bwd16(const void* gy, const float* x, const float* inv, const float* gain, const float* gres,
+                           float* gx, void* gxb, float* ggain, int n, int d) {
+  return ttb::guarded([&] {
+    ttb::k_rmsnorm_bwd(static_cast<const __nv_bfloat16*>(gy), x, inv, gain, gres, gx, static_cast<__nv_bfloat16*>(gxb),
+                       ggain, n, d, nullptr);
+    ttb::check_cuda(cudaGetLastError(), "tt_debug_rmsnorm_bwd16 launch");
+    ttb::check_cuda(cudaDeviceSynchronize(), "tt_debug_rmsnorm_bwd16 sync");
+  });
+}
 void tt_debug_gemm_set_2cta(int on) { ttb::gemm_set_2cta(on); }
 void tt_debug_gemm_set_transpose(int mode) { ttb::gemm_set_transpose(mode); }
 void tt_debug_gemm_force_bn2(int bn) { ttb::gemm_force_bn2(bn); }

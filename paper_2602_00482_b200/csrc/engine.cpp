@@ -187,6 +187,9 @@ void Engine::set_option(const std::string& key, int64_t value) {
     if (value < 1) throw std::invalid_argument("head_chunk_mb must be >= 1");
     head_chunk_bytes_ = value << 20;
     head_cap_rows_ = 0;
+  } else if (key == "gn_bf16") {
+    // 1: grad_normed (dX GEMM -> RMSNorm backward) in bf16 where supported (default); 0: fp32
+    gn_bf16_ = value != 0;
   } else if (key == "pdl") {
     // programmatic dependent launch (kernels/launch.cuh): 0 off, 1 every batch, 2 (default) batches of
     // at most kPdlAutoElems activation elements, where launch latency and kernel prologues are a
@@ -758,6 +761,15 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
   bf16* gxb = sc_gxb_.as<bf16>();
   float* gxf = sc_gxf_.as<float>();
   float* gn = sc_gn_.as<float>();
+  // grad_normed (the dX GEMM output the RMSNorm backward consumes once) in bf16 where the TMA-fed
+  // RMSNorm backward takes it (d % 8 == 0, d <= 4096): 16 instead of 18 bytes per element there and
+  // half the GEMM's store; the residual gradient it is added into stays fp32
+  const bool gn16 = gn_bf16_ && rmsnorm_bwd_bf16_gy_ok(d);
+  bf16* gnb = sc_gn_.as<bf16>();
+  auto norm_bwd = [&](const float* x, const float* inv, const float* gain, float* ggain) {
+    if (gn16) k_rmsnorm_bwd(gnb, x, inv, gain, gx, gx, gxb, ggain, n, d, stream_);
+    else k_rmsnorm_bwd(gn, x, inv, gain, gx, gx, gxb, ggain, n, d, stream_);
+  };
   bf16* gh = sc_gh_.as<bf16>();
   bf16* dO = sc_dO_.as<bf16>();
   float* dq = sc_dq_.as<float>();
@@ -818,14 +830,14 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
     }
     {  // grad_normed2 = grad_hidden W_in^T  (model.hpp:535)
       EpiParams e;
-      e.mode = EPI_STORE_F32;
+      e.mode = gn16 ? EPI_STORE_BF16 : EPI_STORE_F32;
       e.out[0] = gn;
       e.ldo[0] = d;
       gemm(op(gh, F, false), op(win_[l], F, false), n, d, F, e, 1);
     }
     tag("k_rmsnorm_bwd");
-    run(KC_ELEMWISE, 0, nd * 18, [&] {  // gx_mid = gx + rmsnorm_bwd (model.hpp:536-539)
-      k_rmsnorm_bwd(gn, xmid, inv2, mlp_g_[l], gx, gx, gxb, g_mlp_g_[l], n, d, stream_);
+    run(KC_ELEMWISE, 0, nd * (gn16 ? 16 : 18), [&] {  // gx_mid = gx + rmsnorm_bwd (model.hpp:536-539)
+      norm_bwd(xmid, inv2, mlp_g_[l], g_mlp_g_[l]);
     });
     {  // dW_o += attn^T gx_mid  (model.hpp:542)
       EpiParams e;
@@ -902,14 +914,14 @@ void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_
     }
     {  // grad_normed1 = dq W_q^T + dk W_k^T + dv W_v^T  (model.hpp:613-618)
       EpiParams e;
-      e.mode = EPI_STORE_F32;
+      e.mode = gn16 ? EPI_STORE_BF16 : EPI_STORE_F32;
       e.out[0] = gn;
       e.ldo[0] = d;
       gemm(op(dqkv, 3 * d, false), op(wqkv_[l], 3 * d, false), n, d, 3 * d, e, 1);
     }
     tag("k_rmsnorm_bwd");
-    run(KC_ELEMWISE, 0, nd * 18, [&] {  // gx = gx_mid + rmsnorm_bwd (model.hpp:620-624)
-      k_rmsnorm_bwd(gn, X(l), inv1, attn_g_[l], gx, gx, gxb, g_attn_g_[l], n, d, stream_);
+    run(KC_ELEMWISE, 0, nd * (gn16 ? 16 : 18), [&] {  // gx = gx_mid + rmsnorm_bwd (model.hpp:620-624)
+      norm_bwd(X(l), inv1, attn_g_[l], g_attn_g_[l]);
     });
   }
   tag("k_embed_grad");

@@ -295,6 +295,7 @@ class Engine {
   // programmatic dependent launch (engine option "pdl"): 0 off, 1 on, 2 auto = batches of at most
   // kPdlAutoElems rows x d_model
   int pdl_ = 2;
+  bool gn_bf16_ = true;  // engine option "gn_bf16"
   static constexpr double kPdlAutoElems = 2.0 * 1024 * 1024;
   uint64_t opt_epoch_ = 1;  // bumped by set_option: a plan's CUDA graph is re-captured after a change
   // multi-root batching: consecutive forest roots whose children are all short leaves are pushed as

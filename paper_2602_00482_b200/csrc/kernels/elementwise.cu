@@ -232,16 +232,18 @@ __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, ui
 
 constexpr int kNormTmaThreads = 288;  // up to 8 consumer warps + 1 producer warp (warp 8)
 
-template <int VPT, bool GS>
+// GyT: fp32 gy, or bf16 gy (the grad_normed outputs of the dX GEMMs: 2 of the 18 bytes per element)
+template <int VPT, bool GS, typename GyT = float>
 __global__ void __launch_bounds__(kNormTmaThreads, 1)
-    rmsnorm_bwd_tma_kernel(const float* __restrict__ gy, const float* __restrict__ x, const float* __restrict__ inv,
+    rmsnorm_bwd_tma_kernel(const GyT* __restrict__ gy, const float* __restrict__ x, const float* __restrict__ inv,
                            const float* __restrict__ gain, const float* gres, float* gx, __nv_bfloat16* __restrict__ gxb,
                            float* __restrict__ ggain, int n, int d, int nst, int ncw) {
   pdl_wait();  // launch.cuh: no global access before the predecessor completes
   pdl_trigger();
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  const int nb = gres ? 3 : 2;  // row buffers per stage
   const int row_bytes = d * 4;
+  const int gy_bytes = d * static_cast<int>(sizeof(GyT));
+  const int stage_bytes = gy_bytes + (gres ? 2 : 1) * row_bytes;  // [gy | x | gres]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + nst;
   float* gsum = reinterpret_cast<float*>(empty + nst);  // [d]
@@ -267,11 +269,11 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
         const int st = k % nst;
         const long r = blockIdx.x + static_cast<long>(k) * gridDim.x;
         mbar_wait(&empty[st], ((k / nst) & 1) ^ 1);
-        uint8_t* b = ring + static_cast<long>(st) * nb * row_bytes;
-        mbar_arrive_expect_tx(&full[st], nb * row_bytes);
-        bulk_load_1d(b, gy + r * d, row_bytes, &full[st]);
-        bulk_load_1d(b + row_bytes, x + r * d, row_bytes, &full[st]);
-        if (gres) bulk_load_1d(b + 2 * row_bytes, gres + r * d, row_bytes, &full[st]);
+        uint8_t* b = ring + static_cast<long>(st) * stage_bytes;
+        mbar_arrive_expect_tx(&full[st], stage_bytes);
+        bulk_load_1d(b, gy + r * d, gy_bytes, &full[st]);
+        bulk_load_1d(b + gy_bytes, x + r * d, row_bytes, &full[st]);
+        if (gres) bulk_load_1d(b + gy_bytes + row_bytes, gres + r * d, row_bytes, &full[st]);
       }
     }
   } else if (warp < ncw) {
@@ -291,15 +293,25 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
       const long r = blockIdx.x + static_cast<long>(k) * gridDim.x;
       const float iv = inv[r];  // issued before the wait: its latency overlaps the ring
       mbar_wait(&full[st], (k / nst) & 1);
-      const float* sgy = reinterpret_cast<const float*>(ring + static_cast<long>(st) * nb * row_bytes);
-      const float* sx = sgy + d;
-      const float* sres = sgy + 2 * d;
+      const uint8_t* stage = ring + static_cast<long>(st) * stage_bytes;
+      const GyT* sgy = reinterpret_cast<const GyT*>(stage);
+      const float* sx = reinterpret_cast<const float*>(stage + gy_bytes);
+      const float* sres = sx + d;
+      auto gy4 = [&](int c) {
+        if constexpr (sizeof(GyT) == 4) {
+          return *reinterpret_cast<const float4*>(sgy + c);
+        } else {
+          const uint2 w = *reinterpret_cast<const uint2*>(sgy + c);
+          return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xffff0000u), __uint_as_float(w.y << 16),
+                             __uint_as_float(w.y & 0xffff0000u));
+        }
+      };
       float dot = 0.f;
 #pragma unroll
       for (int q = 0; q < VPT; ++q) {
         const int c = (lane + 32 * q) * 4;
         if (c < d) {
-          const float4 a = *reinterpret_cast<const float4*>(sgy + c);
+          const float4 a = gy4(c);
           const float4 b = *reinterpret_cast<const float4*>(sx + c);
           const float4 gq = gain4(q, c);
           dot += a.x * gq.x * b.x + a.y * gq.y * b.y + a.z * gq.z * b.z + a.w * gq.w * b.w;
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
       for (int q = 0; q < VPT; ++q) {
         const int c = (lane + 32 * q) * 4;
         if (c < d) {
-          const float4 a = *reinterpret_cast<const float4*>(sgy + c);
+          const float4 a = gy4(c);
           const float4 b = *reinterpret_cast<const float4*>(sx + c);
           const float4 gq = gain4(q, c);
           float4 res = gres ? *reinterpret_cast<const float4*>(sres + c) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -351,11 +363,11 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
     red_add_v4_f32(ggain + c, gsum[c], gsum[c + 1], gsum[c + 2], gsum[c + 3]);
 }
 
-template <int VPT, bool GS>
-void launch_rmsnorm_bwd_tma(const float* gy, const float* x, const float* inv, const float* gain, const float* gres,
+template <int VPT, bool GS, typename GyT = float>
+void launch_rmsnorm_bwd_tma(const GyT* gy, const float* x, const float* inv, const float* gain, const float* gres,
                             float* gx, __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
   constexpr int kSmemMax = 227 * 1024;
-  const int stage_bytes = (gres ? 3 : 2) * d * 4;
+  const int stage_bytes = d * static_cast<int>(sizeof(GyT)) + (gres ? 2 : 1) * d * 4;
   const int head = ((16 * 32 + 2 * d * 4 + 127) / 128) * 128;  // barriers (<= 32 stages) + gsum + gain copy
   const int fit = std::min(32, (kSmemMax - head - 1024) / stage_bytes);
   // consumer warps: 8 when 8 stages fit, else 4 / 2 (stage k % nst must belong to warp k % ncw)
@@ -363,9 +375,9 @@ void launch_rmsnorm_bwd_tma(const float* gy, const float* x, const float* inv, c
   const int nst = fit / ncw * ncw;
   if (nst < 2) throw std::invalid_argument("rmsnorm backward: row too wide for the TMA ring");
   const int smem = ((nst * 16 + 2 * d * 4 + 127) / 128) * 128 + nst * stage_bytes;
-  ensure_smem_attr(reinterpret_cast<const void*>(rmsnorm_bwd_tma_kernel<VPT, GS>), kSmemMax);
+  ensure_smem_attr(reinterpret_cast<const void*>(rmsnorm_bwd_tma_kernel<VPT, GS, GyT>), kSmemMax);
   const int blocks = std::min(n, device_sm_count());
-  launch_k(rmsnorm_bwd_tma_kernel<VPT, GS>, dim3(blocks), dim3(kNormTmaThreads), smem, s, gy, x, inv, gain, gres, gx, gxb, ggain, n, d, nst, ncw);
+  launch_k(rmsnorm_bwd_tma_kernel<VPT, GS, GyT>, dim3(blocks), dim3(kNormTmaThreads), smem, s, gy, x, inv, gain, gres, gx, gxb, ggain, n, d, nst, ncw);
 }
 
 // Weighted NLL over one vocab row with several (target, weight) pairs (weighted_nll,
@@ -756,6 +768,18 @@ void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const floa
   else if (vpt <= 28) launch_rmsnorm_bwd<7, 4>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else if (vpt <= 64) launch_rmsnorm_bwd<8, 8>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
   else throw std::invalid_argument("rmsnorm backward: d_model > 8192");
+}
+bool rmsnorm_bwd_bf16_gy_ok(int d) { return d % 8 == 0 && d <= 4096; }
+void k_rmsnorm_bwd(const __nv_bfloat16* gy, const float* x, const float* inv, const float* gain, const float* gres,
+                   float* gx, __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s) {
+  if (!rmsnorm_bwd_bf16_gy_ok(d)) throw std::invalid_argument("rmsnorm backward (bf16 gy): d_model must be a multiple of 8, <= 4096");
+  if (n <= 0) return;
+  const int vpt = (d + 127) / 128;
+  if (vpt <= 2) launch_rmsnorm_bwd_tma<2, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 4) launch_rmsnorm_bwd_tma<4, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 8) launch_rmsnorm_bwd_tma<8, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else if (vpt <= 16) launch_rmsnorm_bwd_tma<16, false>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
+  else launch_rmsnorm_bwd_tma<32, true>(gy, x, inv, gain, gres, gx, gxb, ggain, n, d, s);
 }
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,
           __nv_bfloat16* dl, double* loss, cudaStream_t s, const float2* stats, int n_groups) {

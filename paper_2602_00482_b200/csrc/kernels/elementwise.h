@@ -14,6 +14,11 @@ void k_rmsnorm_fwd(const float* x, const float* gain, float* inv, __nv_bfloat16*
 // gx = gres + d(rmsnorm)/dx (gres may be null; gx may alias gres), bf16 copy into gxb, gain grad into ggain.
 void k_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const float* gain, const float* gres, float* gx,
                    __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s);
+// The same with a bf16 gy (the grad_normed GEMM outputs; 16 instead of 18 bytes per element), TMA-fed
+// kernel only: d_model a multiple of 8 and <= 4096 (rmsnorm_bwd_bf16_gy_ok).
+bool rmsnorm_bwd_bf16_gy_ok(int d);
+void k_rmsnorm_bwd(const __nv_bfloat16* gy, const float* x, const float* inv, const float* gain, const float* gres,
+                   float* gx, __nv_bfloat16* gxb, float* ggain, int n, int d, cudaStream_t s);
 // stats: optional per-row (max, sum exp) of 32-column groups from the LM-head GEMM epilogue
 // (EPI_STORE_F32_STATS, n_groups = ceil(V/32) per row); NULL = two passes over the logits row.
 void k_ce(const float* logits, int m, long V, const int32_t* pair_off, const int32_t* tgt, const double* w,

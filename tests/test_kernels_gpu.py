@@ -272,6 +272,43 @@ def test_rmsnorm_bwd_matches_torch(n, d, inplace):
     assert _rel(gg, gg0 + gr.grad) < 1e-5
 
 
+@pytest.mark.parametrize("n,d", [(1, 256), (37, 896), (4099, 896), (32768, 896), (300, 1536), (1001, 3584), (77, 4096),
+                                 (150, 448)])
+def test_rmsnorm_bwd_bf16_gy_matches_torch(n, d):
+    # the engine's grad_normed path: gy (a dX GEMM output) in bf16, residual gradient in place (fp32)
+    torch.manual_seed(8)
+    lib = _lib()
+    vp = ctypes.c_void_p
+    gy = torch.randn(n, d, device="cuda").bfloat16()
+    x = torch.randn(n, d, device="cuda")
+    g = torch.rand(d, device="cuda") + 0.5
+    inv = 1.0 / torch.sqrt((x * x).mean(-1) + 1e-6)
+    gres = torch.randn(n, d, device="cuda")
+    gx = gres.clone()
+    gxb = torch.empty(n, d, device="cuda", dtype=torch.bfloat16)
+    gg = torch.randn(d, device="cuda")
+    gg0 = gg.clone()
+    rc = lib.tt_debug_rmsnorm_bwd16(vp(gy.data_ptr()), vp(x.data_ptr()), vp(inv.data_ptr()), vp(g.data_ptr()),
+                                    vp(gx.data_ptr()), vp(gx.data_ptr()), vp(gxb.data_ptr()), vp(gg.data_ptr()), n, d)
+    assert rc == 0, lib.tt_last_error().decode()
+    xr = x.clone().requires_grad_(True)
+    gr = g.clone().requires_grad_(True)
+    y = xr * torch.rsqrt((xr * xr).mean(-1, keepdim=True) + 1e-6) * gr
+    y.backward(gy.float())
+    assert _rel(gx, gres + xr.grad) < 1e-5
+    assert _rel(gxb, gres + xr.grad) < 1e-2
+    assert _rel(gg, gg0 + gr.grad) < 1e-5
+
+
+def test_rmsnorm_bwd_bf16_gy_rejects_unsupported_width():
+    lib = _lib()
+    t = torch.zeros(8, 8200, device="cuda")
+    vp = ctypes.c_void_p
+    rc = lib.tt_debug_rmsnorm_bwd16(vp(t.data_ptr()), vp(t.data_ptr()), vp(t.data_ptr()), vp(t.data_ptr()), vp(0),
+                                    vp(t.data_ptr()), vp(t.data_ptr()), vp(t.data_ptr()), 8, 8200)
+    assert rc != 0
+
+
 # ----------------------------------------------------------------------------- segment attention
 def _attn_ref(q, K, V, S, H, dh):
     """fp32 reference of one segment's attention over stack rows [0,S) + own rows (causal)."""

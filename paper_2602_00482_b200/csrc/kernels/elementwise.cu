@@ -212,11 +212,15 @@ void launch_rmsnorm_bwd(const float* gy, const float* x, const float* inv, const
   launch_k(rmsnorm_bwd_kernel<VPT, WPR>, dim3(blocks), dim3(256), d * sizeof(float), s, gy, x, inv, gain, gres, gx, gxb, ggain, n, d);
 }
 
-// rmsnorm_backward fed by TMA (rows up to 4096 columns): a persistent block per SM, one producer warp
-// streams each of its rows' gy / x / gres (3 x d fp32) into an NST-deep shared-memory ring with
-// cp.async.bulk (mbarrier complete_tx), NCW consumer warps take the rows round-robin (warp w: the
-// block's rows k = w (mod NCW); NST is a multiple of NCW, so stage k % NST belongs to warp k % NCW and
-// is used in order — no warp can wait on a stage's next phase while its current one is pending). The
+// rmsnorm_backward fed by TMA (rows up to 4096 columns): a persistent block per SM streams each of its
+// rows' gy / x / gres into an NST-deep shared-memory ring with cp.async.bulk (mbarrier complete_tx);
+// NCW consumer warps take the rows round-robin (warp w: the block's rows k = w (mod NCW); NST is a
+// multiple of NCW, so stage k % NST belongs to warp k % NCW and is used in order — no warp can wait on
+// a stage's next phase while its current one is pending). Each consumer warp refills the stage it just
+// read with its row k + NST (TT_NORM_SELFLOAD): the single producer thread of the first version spent
+// an empty-barrier wait and three bulk copies per row for all ~221 rows of an SM, which at the
+// power-capped in-step clock (~1.46 GHz) held the c2 kernel at 4.1-4.7 TB/s; self-refilling runs it
+// at 5.5 TB/s in-step (profiles/r2/rmsnorm_selfload_ab.txt). The
 // ring keeps ~170 KB of rows in flight per SM independently of the consumers' reduce-then-store
 // latency, which is what bounded the register version (one HBM round trip for gy / x, a second for
 // gres, 16 warps per SM: 4.1-4.5 TB/s). Each consumer reads its row from shared memory twice (dot
@@ -230,6 +234,10 @@ __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, ui
                : "memory");
 }
 
+#ifndef TT_NORM_SELFLOAD
+#define TT_NORM_SELFLOAD 1  // consumer warps refill their own ring stages (0: one producer thread; A/B)
+#endif
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 constexpr int kNormTmaThreads = 288;  // up to 8 consumer warps + 1 producer warp (warp 8)
 
 // GyT: fp32 gy, or bf16 gy (the grad_normed outputs of the dX GEMMs: 2 of the 18 bytes per element)
@@ -263,20 +271,33 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
   }
   __syncthreads();
   const int rows_mine = n > static_cast<int>(blockIdx.x) ? (n - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // row k's gy / x / gres into stage k % nst (one thread)
+  auto issue = [&](int k) {
+    const int st = k % nst;
+    const long r = blockIdx.x + static_cast<long>(k) * gridDim.x;
+    uint8_t* b = ring + static_cast<long>(st) * stage_bytes;
+    mbar_arrive_expect_tx(&full[st], stage_bytes);
+    bulk_load_1d(b, gy + r * d, gy_bytes, &full[st]);
+    bulk_load_1d(b + gy_bytes, x + r * d, row_bytes, &full[st]);
+    if (gres) bulk_load_1d(b + gy_bytes + row_bytes, gres + r * d, row_bytes, &full[st]);
+  };
+#if TT_NORM_SELFLOAD
+  // every consumer warp refills its own stages (stage k % nst belongs to warp k % ncw): no producer
+  // thread serialising ~221 rows x (empty wait + 3 bulk copies) per launch, no empty barriers
+  if (warp < ncw && lane == 0)
+    for (int k = warp; k < rows_mine && k < nst; k += ncw) issue(k);
+  if (warp == 8) {
+  } else if (warp < ncw) {
+#else
   if (warp == 8) {
     if (lane == 0) {
       for (int k = 0; k < rows_mine; ++k) {
-        const int st = k % nst;
-        const long r = blockIdx.x + static_cast<long>(k) * gridDim.x;
-        mbar_wait(&empty[st], ((k / nst) & 1) ^ 1);
-        uint8_t* b = ring + static_cast<long>(st) * stage_bytes;
-        mbar_arrive_expect_tx(&full[st], stage_bytes);
-        bulk_load_1d(b, gy + r * d, gy_bytes, &full[st]);
-        bulk_load_1d(b + gy_bytes, x + r * d, row_bytes, &full[st]);
-        if (gres) bulk_load_1d(b + gy_bytes + row_bytes, gres + r * d, row_bytes, &full[st]);
+        mbar_wait(&empty[k % nst], ((k / nst) & 1) ^ 1);
+        issue(k);
       }
     }
   } else if (warp < ncw) {
+#endif
     float4 g[GS ? 1 : VPT], gacc[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
@@ -344,8 +365,16 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
           gacc[q].w += a.w * b.w * iv;
         }
       }
+#if TT_NORM_SELFLOAD
+      // this warp's reads of the stage are done: refill it with row k + nst (generic-proxy reads
+      // ordered before the async-proxy writes)
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0 && k + nst < rows_mine) issue(k + nst);
+#else
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
+#endif
     }
 #pragma unroll
     for (int q = 0; q < VPT; ++q) {

@@ -13,6 +13,8 @@ from paper_2602_00482_b200 import _native  # noqa: E402
 
 def main():
     n, d = (int(a) for a in sys.argv[1:3]) if len(sys.argv) > 2 else (32768, 896)
+    if os.environ.get("EW_LIB"):  # experiment builds
+        _native.LIB_PATH = os.path.abspath(os.environ["EW_LIB"])
     lib = _native.lib()
     vp = ctypes.c_void_p
     gy, x, gres = (torch.randn(n, d, device="cuda") for _ in range(3))

@@ -227,6 +227,7 @@ int tt_engine_set_profiling(tt_engine* eng, int32_t on);
  *                        ce_stats), 0 = fp32 logits (loss / gradients then differ by bf16 rounding only)
  *   "head_chunk_mb"      LM-head / CE scratch budget per loss-row chunk (default 6144, >= 1; capped by free HBM)
  *   "plan_timing"        1 = print the host phases of tt_plan_create (schedule, memory plan, metadata) to stderr
+ *   "pdl_auto_elems"     the batch size (rows x d_model elements) up to which pdl = 2 enables PDL (default 2^21)
  *   "gn_bf16"            1 = the grad_normed outputs of the dX GEMMs stored bf16 for the RMSNorm backward (default,
  *                        d_model % 8 == 0 and <= 4096), 0 = fp32 (loss unchanged; gradients differ by bf16 rounding)
  *   "pdl"                programmatic dependent launch of every kernel: 0 = off, 1 = on, 2 = segment batches of

@@ -187,12 +187,15 @@ void Engine::set_option(const std::string& key, int64_t value) {
     if (value < 1) throw std::invalid_argument("head_chunk_mb must be >= 1");
     head_chunk_bytes_ = value << 20;
     head_cap_rows_ = 0;
+  } else if (key == "pdl_auto_elems") {
+    if (value < 0) throw std::invalid_argument("pdl_auto_elems must be >= 0");
+    pdl_auto_elems_ = static_cast<double>(value);
   } else if (key == "gn_bf16") {
     // 1: grad_normed (dX GEMM -> RMSNorm backward) in bf16 where supported (default); 0: fp32
     gn_bf16_ = value != 0;
   } else if (key == "pdl") {
     // programmatic dependent launch (kernels/launch.cuh): 0 off, 1 every batch, 2 (default) batches of
-    // at most kPdlAutoElems activation elements, where launch latency and kernel prologues are a
+    // at most pdl_auto_elems activation elements (rows x d_model), where launch latency and kernel prologues are a
     // visible share of each kernel (tools/pdl_ab.py: c1 +4.4%; the c2 step -0.6% with PDL)
     if (value < 0 || value > 2) throw std::invalid_argument("pdl must be 0, 1 or 2");
     pdl_ = static_cast<int>(value);
@@ -553,7 +556,7 @@ void Engine::gemm(const GemmOperand& A, const GemmOperand& B, int M, int N, int 
 // ----------------------------------------------------------------------------- push (forward_segment)
 void Engine::forward_batch(const Batch& b, size_t arena_off) {
   const int n = static_cast<int>(b.n);
-  set_pdl(pdl_ == 1 || (pdl_ == 2 && static_cast<double>(b.n) * d_ <= kPdlAutoElems));
+  set_pdl(pdl_ == 1 || (pdl_ == 2 && static_cast<double>(b.n) * d_ <= pdl_auto_elems_));
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
   const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);
@@ -747,7 +750,7 @@ void Engine::head_backward_dense(const Batch& b, const bf16* nf, const float* ho
 // ----------------------------------------------------------------------------- pop (backward_segment)
 void Engine::backward_batch(const Batch& b, size_t arena_off, const float* host_grad_logits, float* grad_prefix) {
   const int n = static_cast<int>(b.n);
-  set_pdl(pdl_ == 1 || (pdl_ == 2 && static_cast<double>(b.n) * d_ <= kPdlAutoElems));
+  set_pdl(pdl_ == 1 || (pdl_ == 2 && static_cast<double>(b.n) * d_ <= pdl_auto_elems_));
   const int d = static_cast<int>(d_), F = static_cast<int>(F_);
   const double nd = double(n) * d_;
   const ActLayout lay = layout(b.n);

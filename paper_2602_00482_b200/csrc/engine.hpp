@@ -296,7 +296,7 @@ class Engine {
   // kPdlAutoElems rows x d_model
   int pdl_ = 2;
   bool gn_bf16_ = true;  // engine option "gn_bf16"
-  static constexpr double kPdlAutoElems = 2.0 * 1024 * 1024;
+  double pdl_auto_elems_ = 2.0 * 1024 * 1024;  // engine option "pdl_auto_elems"
   uint64_t opt_epoch_ = 1;  // bumped by set_option: a plan's CUDA graph is re-captured after a change
   // multi-root batching: consecutive forest roots whose children are all short leaves are pushed as
   // ONE batch of up to this many tokens (0 = off); each root's leaves attend to its own rows

@@ -238,7 +238,7 @@ __device__ __forceinline__ void bulk_load_1d(void* smem_dst, const void* src, ui
 #define TT_NORM_SELFLOAD 1  // consumer warps refill their own ring stages (0: one producer thread; A/B)
 #endif
 __device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-constexpr int kNormTmaThreads = 288;  // up to 8 consumer warps + 1 producer warp (warp 8)
+constexpr int kNormTmaThreads = 288;  // up to 8 consumer warps + warp 8 (the producer of TT_NORM_SELFLOAD=0 builds)
 
 // GyT: fp32 gy, or bf16 gy (the grad_normed outputs of the dX GEMMs: 2 of the 18 bytes per element)
 template <int VPT, bool GS, typename GyT = float>
@@ -283,21 +283,19 @@ __global__ void __launch_bounds__(kNormTmaThreads, 1)
   };
 #if TT_NORM_SELFLOAD
   // every consumer warp refills its own stages (stage k % nst belongs to warp k % ncw): no producer
-  // thread serialising ~221 rows x (empty wait + 3 bulk copies) per launch, no empty barriers
+  // thread serialising ~221 rows x (empty wait + 3 bulk copies) per launch, no empty barriers; warp 8
+  // idles
   if (warp < ncw && lane == 0)
     for (int k = warp; k < rows_mine && k < nst; k += ncw) issue(k);
-  if (warp == 8) {
-  } else if (warp < ncw) {
 #else
-  if (warp == 8) {
-    if (lane == 0) {
-      for (int k = 0; k < rows_mine; ++k) {
-        mbar_wait(&empty[k % nst], ((k / nst) & 1) ^ 1);
-        issue(k);
-      }
+  if (warp == 8 && lane == 0) {  // the single producer (A/B builds)
+    for (int k = 0; k < rows_mine; ++k) {
+      mbar_wait(&empty[k % nst], ((k / nst) & 1) ^ 1);
+      issue(k);
     }
-  } else if (warp < ncw) {
+  }
 #endif
+  if (warp < ncw) {
     float4 g[GS ? 1 : VPT], gacc[VPT];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
